@@ -1,0 +1,425 @@
+"""fp64 CPU oracle for the distributed K-FAC hot path (arXiv 1811.12019).
+
+TEST INFRASTRUCTURE ONLY -- only tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / ``--impl reference`` legs may import this package.  It shares no
+code with the CUDA path (paper_1811_12019_b200/) and neither imports the other;
+the only common module is ``synth`` (shape tables + seeded inputs, no K-FAC
+arithmetic).
+
+Arithmetic lives in ``kfac_oracle.c`` (plain fp64 loops, built with gcc by
+``build()``); this module marshals arguments and implements the host-side
+parts of the method in plain Python:
+
+* ``plan``             layer ownership + wire layout (
+                       readings R-15, R-16) -- an implementation independent
+                       of the library's plan.cpp, compared bit-exactly.
+* ``reduce_scatter``   ReduceScatterV(mean) simulated in-process, summation in
+                       ascending rank order then x 1/P (R-11).
+* ``all_gather``       AllGatherV of the primary owners' 𝒢.
+* ``damping_schedule`` warmup damping recurrence (reading R-2).
+* ``kfac_step``        Algorithm 1's body minus fwd/bwd/update.
+
+Parity status: every function here is pinned by tests/test_oracle_*.py (see
+DESIGN.md §Oracle pins); none is "parity unpinned".
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "kfac_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+FMT = {"bf16": 0, "fp16": 1}
+
+
+def build(force: bool = False) -> str:
+    """Compile kfac_oracle.c -> liboracle.so with gcc (fp64, OpenMP, no FP contraction)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        cmd = ["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fopenmp",
+               "-fPIC", "-shared", "-o", _LIB + ".tmp", _SRC, "-lm"]
+        subprocess.check_call(cmd)
+        os.replace(_LIB + ".tmp", _LIB)
+    return _LIB
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_LIB)
+        i32, i64, f64 = ctypes.c_int, ctypes.c_int64, ctypes.c_double
+        P = ctypes.c_void_p
+        L.or_decode_half.argtypes = [ctypes.c_uint16, i32]
+        L.or_decode_half.restype = f64
+        L.or_factor_A.argtypes = [i32] * 11 + [P, i32, f64, P, i32]
+        L.or_factor_A_entries.argtypes = [i32] * 11 + [P, i32, f64, P, i64, P, i32]
+        L.or_factor_G.argtypes = [i64, i32, P, i32, f64, P, i32]
+        L.or_factor_G_entries.argtypes = [i64, i32, P, i32, f64, P, i64, P, i32]
+        L.or_pack_upper.argtypes = [P, i32, P]
+        L.or_unpack_upper.argtypes = [P, i32, P]
+        L.or_damp.argtypes = [P, i32, P, i32, f64, P]
+        L.or_cholesky.argtypes = [P, i32, P, i32]
+        L.or_tri_inv_lower.argtypes = [P, i32, P, i32]
+        L.or_inverse_spd.argtypes = [P, i32, P, i32]
+        L.or_precondition.argtypes = [P, i32, P, i32, P, P, i32]
+        L.or_precondition_entries.argtypes = [P, i32, P, i32, P, P, i64, P, i32]
+        _lib = L
+    return _lib
+
+
+def max_threads() -> int:
+    return int(lib().or_max_threads())
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _c(a, dtype):
+    return np.ascontiguousarray(a, dtype=dtype)
+
+
+# --------------------------------------------------------------------------
+# geometry (plain definitions, written here independently of the library)
+# --------------------------------------------------------------------------
+def out_hw(layer):
+    if layer["kind"] == 1:
+        return 1, 1
+    ho = (layer["h_in"] + 2 * layer["pad_h"] - layer["kh"]) // layer["stride_h"] + 1
+    wo = (layer["w_in"] + 2 * layer["pad_w"] - layer["kw"]) // layer["stride_w"] + 1
+    return ho, wo
+
+
+def dims(layer):
+    return layer["c_in"] * layer["kh"] * layer["kw"] + (1 if layer["has_bias"] else 0), layer["c_out"]
+
+
+def rows(layer, n):
+    ho, wo = out_hw(layer)
+    return n * ho * wo
+
+
+def _geom(layer):
+    if layer["kind"] == 1:
+        return (1, 1, layer["c_in"], 1, 1, 1, 1, 0, 0)
+    return (layer["h_in"], layer["w_in"], layer["c_in"], layer["kh"], layer["kw"],
+            layer["stride_h"], layer["stride_w"], layer["pad_h"], layer["pad_w"])
+
+
+# --------------------------------------------------------------------------
+# stages 1-2: Kronecker factors
+# --------------------------------------------------------------------------
+def factor_A(layer, x_bits, n, alpha=None, fmt="bf16", threads=0):
+    """A = alpha * Σ_rows ã ãᵀ (full, fp64). Default alpha = 1/rows (R-3)."""
+    d_a, _ = dims(layer)
+    if alpha is None:
+        alpha = 1.0 / rows(layer, n)
+    x = _c(x_bits, np.uint16)
+    A = np.empty((d_a, d_a), dtype=np.float64)
+    st = lib().or_factor_A(n, *_geom(layer), int(layer["has_bias"]), _p(x), FMT[fmt],
+                           float(alpha), _p(A), threads)
+    if st:
+        raise ValueError("empty capture (S:201)")
+    return A
+
+
+def factor_A_entries(layer, x_bits, n, ij, alpha=None, fmt="bf16", threads=0):
+    if alpha is None:
+        alpha = 1.0 / rows(layer, n)
+    x = _c(x_bits, np.uint16)
+    ij = _c(ij, np.int64).reshape(-1, 2)
+    out = np.empty(len(ij), dtype=np.float64)
+    lib().or_factor_A_entries(n, *_geom(layer), int(layer["has_bias"]), _p(x), FMT[fmt],
+                              float(alpha), _p(ij), len(ij), _p(out), threads)
+    return out
+
+
+def factor_G(gy_bits, n_rows, c, alpha=None, fmt="bf16", threads=0):
+    """G = alpha * Σ_rows g gᵀ (full, fp64). Default alpha = 1/rows (R-3, R-4)."""
+    if alpha is None:
+        alpha = 1.0 / n_rows
+    g = _c(gy_bits, np.uint16)
+    G = np.empty((c, c), dtype=np.float64)
+    if lib().or_factor_G(n_rows, c, _p(g), FMT[fmt], float(alpha), _p(G), threads):
+        raise ValueError("empty capture (S:201)")
+    return G
+
+
+def factor_G_entries(gy_bits, n_rows, c, ij, alpha=None, fmt="bf16", threads=0):
+    if alpha is None:
+        alpha = 1.0 / n_rows
+    g = _c(gy_bits, np.uint16)
+    ij = _c(ij, np.int64).reshape(-1, 2)
+    out = np.empty(len(ij), dtype=np.float64)
+    lib().or_factor_G_entries(n_rows, c, _p(g), FMT[fmt], float(alpha), _p(ij), len(ij), _p(out), threads)
+    return out
+
+
+# --------------------------------------------------------------------------
+# symmetric packing (R-10)
+# --------------------------------------------------------------------------
+def packed_len(d):
+    return d * (d + 1) // 2
+
+
+def pack(M):
+    M = _c(M, np.float64)
+    n = M.shape[0]
+    if M.shape != (n, n):
+        raise ValueError("pack: non-square input")
+    if n and np.max(np.abs(M - M.T)) > 1e-12 * max(np.max(np.abs(M)), 1e-300):
+        raise ValueError("pack: asymmetric input (S:36)")
+    p = np.empty(packed_len(n), dtype=np.float64)
+    lib().or_pack_upper(_p(M), n, _p(p))
+    return p
+
+
+def unpack(p):
+    p = _c(p, np.float64)
+    n = int((math.isqrt(8 * len(p) + 1) - 1) // 2)
+    if packed_len(n) != len(p):
+        raise ValueError("unpack: length is not d(d+1)/2")
+    M = np.empty((n, n), dtype=np.float64)
+    lib().or_unpack_upper(_p(p), n, _p(M))
+    return M
+
+
+# --------------------------------------------------------------------------
+# stage 4: damping + inverse (P:466-473 R-1; P:247-260, P:328 R-12)
+# --------------------------------------------------------------------------
+def damp(A, G, gamma):
+    A = _c(A, np.float64).copy()
+    G = _c(G, np.float64).copy()
+    pi = np.zeros(1)
+    if lib().or_damp(_p(A), A.shape[0], _p(G), G.shape[0], float(gamma), _p(pi)):
+        raise ValueError("damping requires gamma > 0 (S:217)")
+    return A, G, float(pi[0])
+
+
+def cholesky(M, threads=0):
+    M = _c(M, np.float64)
+    L = np.empty_like(M)
+    st = lib().or_cholesky(_p(M), M.shape[0], _p(L), threads)
+    return L, int(st)
+
+
+def inverse(M, threads=0):
+    """(X, status): X = M⁻¹ via Cholesky; status = 0 or failing pivot + 1."""
+    M = _c(M, np.float64)
+    X = np.zeros_like(M)
+    st = lib().or_inverse_spd(_p(M), M.shape[0], _p(X), threads)
+    return X, int(st)
+
+
+# --------------------------------------------------------------------------
+# stage 5: preconditioning (R-14)
+# --------------------------------------------------------------------------
+def precondition(Ginv, Ainv, dW, threads=0):
+    Ginv, Ainv, dW = _c(Ginv, np.float64), _c(Ainv, np.float64), _c(dW, np.float64)
+    dg, da = dW.shape
+    if Ginv.shape != (dg, dg) or Ainv.shape != (da, da):
+        raise ValueError("precondition: shape mismatch (S:72)")
+    out = np.empty((dg, da), dtype=np.float64)
+    lib().or_precondition(_p(Ginv), dg, _p(Ainv), da, _p(dW), _p(out), threads)
+    return out
+
+
+def precondition_entries(Ginv, Ainv, dW, ij, threads=0):
+    Ginv, Ainv, dW = _c(Ginv, np.float64), _c(Ainv, np.float64), _c(dW, np.float64)
+    dg, da = dW.shape
+    ij = _c(ij, np.int64).reshape(-1, 2)
+    out = np.empty(len(ij), dtype=np.float64)
+    lib().or_precondition_entries(_p(Ginv), dg, _p(Ainv), da, _p(dW), _p(ij), len(ij), _p(out), threads)
+    return out
+
+
+# --------------------------------------------------------------------------
+# schedules (Table 3; reading R-2)
+# --------------------------------------------------------------------------
+def damping_alpha(gamma0, gamma_target, t_warmup):
+    """α = 2·log10(γ⁽⁰⁾/γ_target) / t_warmup."""
+    if t_warmup <= 0:
+        raise ValueError("t_warmup must be > 0")
+    return 2.0 * math.log10(gamma0 / gamma_target) / t_warmup
+
+
+def damping_schedule(gamma0, gamma_target, t_warmup, steps):
+    """[γ⁽⁰⁾, γ⁽¹⁾, ...]: γ⁽ᵗ⁺¹⁾ = (1−α)γ⁽ᵗ⁾ + α·γ_target."""
+    a = damping_alpha(gamma0, gamma_target, t_warmup)
+    g = [float(gamma0)]
+    for _ in range(steps):
+        g.append((1.0 - a) * g[-1] + a * gamma_target)
+    return g
+
+
+# --------------------------------------------------------------------------
+# a0: ownership + wire layout (R-15, R-16)
+# --------------------------------------------------------------------------
+POLICY_RR, POLICY_LPT = 0, 1
+ALIGN = 16  # elements (64 B) per segment start
+
+
+def _align(v):
+    return (v + ALIGN - 1) // ALIGN * ALIGN
+
+
+def layer_cost(layer):
+    """Stage-4/5 cost model (R-15): dA³ + dG³ + 2dG²dA + 2dGdA²."""
+    a, g = dims(layer)
+    return a ** 3 + g ** 3 + 2 * g * g * a + 2 * g * a * a
+
+
+def plan(layers, world, policy=POLICY_RR):
+    """Owner map and owner-major segment layout.
+
+    owner[l]: primary owner.  RR: l mod P.  LPT: layers by (-cost, l), each to
+    argmin (load, rank).  If P > L, rank r >= L also owns layer r mod L
+    (redundant copy).  Rank r's chunk lists its owned layers ascending,
+    each with segments [∇W (dG·dA), A packed, G packed], every segment start
+    aligned to 16 elements; rs_chunk = max chunk.  AG: each rank's chunk holds
+    its primary layers' 𝒢 (dG·dA) ascending, aligned; ag_chunk = max.
+    """
+    L, P = len(layers), int(world)
+    if L < 1 or P < 1:
+        raise ValueError("plan: L, P >= 1")
+    if policy == POLICY_RR:
+        owner = [l % P for l in range(L)]
+    elif policy == POLICY_LPT:
+        owner = [0] * L
+        load = [0] * P
+        for l in sorted(range(L), key=lambda l: (-layer_cost(layers[l]), l)):
+            r = min(range(P), key=lambda r: (load[r], r))
+            owner[l] = r
+            load[r] += layer_cost(layers[l])
+    else:
+        raise ValueError("unknown policy")
+    owned = [sorted([l for l in range(L) if owner[l] == r] + ([r % L] if r >= L else []))
+             for r in range(P)]
+    local = []  # per rank: {layer: (off_dw, off_a, off_g)} relative to the chunk
+    chunk = []
+    for r in range(P):
+        off, m = 0, {}
+        for l in owned[r]:
+            a, g = dims(layers[l])
+            o_w = off
+            off = _align(off + g * a)
+            o_a = off
+            off = _align(off + packed_len(a))
+            o_g = off
+            off = _align(off + packed_len(g))
+            m[l] = (o_w, o_a, o_g)
+        local.append(m)
+        chunk.append(off)
+    rs_chunk = max(chunk)
+    seg_off = np.zeros((L, 3), dtype=np.int64)
+    for l in range(L):
+        r = owner[l]
+        seg_off[l] = [r * rs_chunk + v for v in local[r][l]]
+    ag_local, ag_chunks = [], []
+    for r in range(P):
+        off, m = 0, {}
+        for l in range(L):
+            if owner[l] == r:
+                a, g = dims(layers[l])
+                m[l] = off
+                off = _align(off + g * a)
+        ag_local.append(m)
+        ag_chunks.append(off)
+    ag_chunk = max(ag_chunks)
+    ag_off = np.array([owner[l] * ag_chunk + ag_local[owner[l]][l] for l in range(L)], dtype=np.int64)
+    return dict(owner=np.array(owner, dtype=np.int32), owned=owned, local=local,
+                seg_off=seg_off, rs_chunk=int(rs_chunk), ag_off=ag_off, ag_chunk=int(ag_chunk),
+                world=P, L=L)
+
+
+# --------------------------------------------------------------------------
+# a4 / a8: simulated collectives (R-11, R-16)
+# --------------------------------------------------------------------------
+def reduce_scatter(sends, pl):
+    """ReduceScatterV(mean): rank r receives chunk r of Σ_{q=0..P-1} send_q (ascending), × 1/P."""
+    P, c = pl["world"], pl["rs_chunk"]
+    acc = np.zeros(P * c, dtype=np.float64)
+    for q in range(P):
+        acc += np.asarray(sends[q], dtype=np.float64)
+    acc *= 1.0 / P
+    return [acc[r * c:(r + 1) * c].copy() for r in range(P)]
+
+
+def all_gather(slots, pl):
+    """AllGatherV: every rank receives the concatenation of every rank's AG chunk."""
+    full = np.concatenate([np.asarray(s) for s in slots])
+    return [full.copy() for _ in range(pl["world"])]
+
+
+# --------------------------------------------------------------------------
+# Algorithm 1 body: factors -> RS -> damp+invert -> precondition -> AG
+# --------------------------------------------------------------------------
+def build_send(layers, pl, rank, factors, dws):
+    """Rank `rank`'s RS send buffer: (∇W, A packed, G packed) of every layer at every owner copy."""
+    P, c = pl["world"], pl["rs_chunk"]
+    send = np.zeros(P * c, dtype=np.float64)
+    for r in range(P):
+        for l, (o_w, o_a, o_g) in pl["local"][r].items():
+            A, G = factors[l]
+            a, g = dims(layers[l])
+            base = r * c
+            send[base + o_w: base + o_w + g * a] = np.asarray(dws[l], dtype=np.float64).reshape(-1)
+            send[base + o_a: base + o_a + packed_len(a)] = pack(A)
+            send[base + o_g: base + o_g + packed_len(g)] = pack(G)
+    return send
+
+
+def owned_results(layers, pl, rank, recv, gamma, threads=0):
+    """Stages 4-5 on one rank: {layer: dict(A_d, G_d, pi, Ainv, Ginv, precond, status)}."""
+    out = {}
+    for l, (o_w, o_a, o_g) in pl["local"][rank].items():
+        a, g = dims(layers[l])
+        dW = recv[o_w:o_w + g * a].reshape(g, a)
+        A = unpack(recv[o_a:o_a + packed_len(a)])
+        G = unpack(recv[o_g:o_g + packed_len(g)])
+        A_d, G_d, pi = damp(A, G, gamma)
+        Ainv, sa = inverse(A_d, threads)
+        Ginv, sg = inverse(G_d, threads)
+        pre = precondition(Ginv, Ainv, dW, threads) if (sa == 0 and sg == 0) else None
+        out[l] = dict(A=A, G=G, dW=dW, A_d=A_d, G_d=G_d, pi=pi, Ainv=Ainv, Ginv=Ginv,
+                      precond=pre, status=(sa, sg))
+    return out
+
+
+def kfac_step(layers, rank_inputs, world, gamma, policy=POLICY_RR, fmt="bf16", threads=0):
+    """Simulate all P ranks.  rank_inputs[r] = (x_bits list, gy_bits list, dW list, n_local).
+
+    Returns dict(plan, sends, recvs, results (per rank), gathered (per rank AG buffer)).
+    """
+    pl = plan(layers, world, policy)
+    sends = []
+    for r in range(world):
+        xs, gys, dws, n = rank_inputs[r]
+        factors = []
+        for l, layer in enumerate(layers):
+            A = factor_A(layer, xs[l], n, fmt=fmt, threads=threads)
+            rws = rows(layer, n)
+            G = factor_G(gys[l], rws, layer["c_out"], fmt=fmt, threads=threads)
+            factors.append((A, G))
+        sends.append(build_send(layers, pl, r, factors, dws))
+    recvs = reduce_scatter(sends, pl)
+    results = [owned_results(layers, pl, r, recvs[r], gamma, threads) for r in range(world)]
+    slots = []
+    for r in range(world):
+        slot = np.zeros(pl["ag_chunk"], dtype=np.float64)
+        for l in range(len(layers)):
+            if pl["owner"][l] == r:
+                a, g = dims(layers[l])
+                o = pl["ag_off"][l] - r * pl["ag_chunk"]
+                slot[o:o + g * a] = results[r][l]["precond"].reshape(-1)
+        slots.append(slot)
+    gathered = all_gather(slots, pl)
+    return dict(plan=pl, sends=sends, recvs=recvs, results=results, gathered=gathered)
