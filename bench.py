@@ -1,0 +1,389 @@
+#!/usr/bin/env python
+"""K-FAC hot-path benchmark (BASELINE.json metric: "ResNet-50 K-FAC step ms & factor
+TFLOP/s at 1/2/4/8 B200, % roofline").
+
+A step is one pass of the whole hot path -- factors (A, G) + ReduceScatterV +
+damped inverse + precondition + AllGatherV (Alg. 1) -- for
+every layer of the configuration, on synthetic inputs of the paper's shapes
+(ResNet-50/ImageNet, batch 32 per GPU).  One process per GPU; launched with
+torchrun for N > 1.  Prints ONE JSON line on rank 0.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config resnet50] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from synth import inputs, shapes  # noqa: E402
+
+METRIC = "ResNet-50 K-FAC step ms & factor TFLOP/s at 1/2/4/8 B200, % roofline"
+# derived peaks: 148 SM x lanes x 2 flop x 1.965 GHz
+FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # 37.2 (DFMA)
+FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # 74.4 (FFMA)
+NVLINK_GBS = 770.0                                   # measured peer copy per direction (B200_PROFILING.md)
+
+
+def peaks():
+    p = dict(hbm_gbs=6650.0, bf16_tflops=1590.0, bf16_tflops_sustained=1400.0, src="fallback (B200_PROFILING.md)")
+    f = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(f):
+        m = json.load(open(f))
+        p = dict(hbm_gbs=m["hbm_gbs"], bf16_tflops=m["bf16_tflops"], bf16_tflops_sustained=m["bf16_tflops_sustained"],
+                 src="measured (MEASURED_PEAKS.json)")
+    return p
+
+
+def work(layers, n, plan_q=None, rank_layers=None):
+    """Algorithmic work of one step on one rank."""
+    fac_flops = fac_bytes = 0
+    for l in layers:
+        da, dg = shapes.dims(l)
+        rows = shapes.rows(l, n)
+        fac_flops += rows * (da * (da + 1) + dg * (dg + 1))  # upper triangle, 2 flop / MAC
+        ho, wo = shapes.out_hw(l)
+        fac_bytes += n * l["h_in"] * l["w_in"] * l["c_in"] * 2 + n * ho * wo * dg * 2  # x, gy read once
+        fac_bytes += 4 * (da * (da + 1) // 2 + dg * (dg + 1) // 2)  # packed fp32 out
+    inv_flops = prec_flops = 0
+    owned = rank_layers if rank_layers is not None else range(len(layers))
+    for li in owned:
+        da, dg = shapes.dims(layers[li])
+        inv_flops += da ** 3 + dg ** 3
+        prec_flops += 2 * dg * dg * da + 2 * dg * da * da
+    return dict(factor_flops=fac_flops, factor_bytes=fac_bytes, inverse_flops=inv_flops, precond_flops=prec_flops)
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu):
+        self.gpu, self.lines, self.proc = gpu, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.t.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_sample(layers, n, small_dim, threads=0):
+    """Bounded oracle sample, scaled to one full step (ms).  Factors: 1 image of n (rows scale
+    linearly); inverse + precondition: layers with max(dA, dG) <= small_dim, scaled by flops."""
+    import numpy as np
+
+    import oracle
+    oracle.build()
+    t_fac = 0.0
+    for i, l in enumerate(layers):
+        x = inputs.half_bits(inputs.layer_x(l, i, 1))
+        gy = inputs.half_bits(inputs.layer_gy(l, i, 1))
+        t0 = time.perf_counter()
+        oracle.factor_A(l, x, 1, threads=threads)
+        oracle.factor_G(gy, shapes.rows(l, 1), l["c_out"], threads=threads)
+        t_fac += time.perf_counter() - t0
+    t_inv = 0.0
+    f_s = f_all = 0
+    rng = np.random.default_rng(0)
+    for i, l in enumerate(layers):
+        da, dg = shapes.dims(l)
+        f = da ** 3 + dg ** 3 + 2 * dg * dg * da + 2 * dg * da * da
+        f_all += f
+        if max(da, dg) > small_dim:
+            continue
+        f_s += f
+        Ba = rng.standard_normal((da, da)) / da
+        Bg = rng.standard_normal((dg, dg)) / dg
+        A = Ba @ Ba.T + np.eye(da)
+        G = Bg @ Bg.T + np.eye(dg)
+        dW = rng.standard_normal((dg, da))
+        t0 = time.perf_counter()
+        Ad, Gd, _ = oracle.damp(A, G, 2.5e-2)
+        Ai, _ = oracle.inverse(Ad, threads)
+        Gi, _ = oracle.inverse(Gd, threads)
+        oracle.precondition(Gi, Ai, dW, threads)
+        t_inv += time.perf_counter() - t0
+    scaled = (t_fac * n + t_inv * (f_all / max(f_s, 1))) * 1e3
+    desc = (f"oracle factors on 1 of {n} images (x{n}) + damp/inverse/precondition of layers with dim <= {small_dim} "
+            f"({100.0 * f_s / f_all:.1f}% of stage-4/5 flops, scaled by flops); measured {t_fac + t_inv:.1f} s")
+    return scaled, desc, oracle.max_threads(), t_fac + t_inv
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    layers, n = shapes.config(args.config)
+    small = 576 if args.config in ("resnet50", "resnet18_cifar") else 10 ** 9
+    if args.config == "stress":
+        small = 1000
+    for _ in range(args.warmup):
+        cpu_sample(layers[:1], 1, 64)  # cheap warm-up (library load, page-in)
+    vals = []
+    desc = cores = None
+    for _ in range(args.steps):
+        v, desc, cores, _ = cpu_sample(layers, n, small)
+        vals.append(v)
+    ms = statistics.mean(vals)
+    out = {"metric": METRIC, "value": round(ms, 3), "unit": "ms", "impl": "reference", "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": False,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": args.config, "global_batch": n * args.gpus, "per_gpu_batch": n},
+           "cpu_baseline": {"value": round(ms, 3), "unit": "ms", "cores": cores, "kind": "oracle", "sample": desc},
+           "e2e": {"value": round(ms, 3), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        if world == 1 and args.gpus > 1:
+            print(json.dumps({"error": "--gpus N>1 must be launched with torchrun"}), flush=True)
+            return 2
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_1811_12019_b200 as K
+
+    comm = None
+    if world > 1:
+        uid = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(K.comm_unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, 0)
+        comm = K.Comm(bytes(uid.cpu().numpy().tobytes()), rank, world, local)
+
+    layers, n = shapes.config(args.config)
+    policy = K.LPT if args.policy == "lpt" else K.RR
+    st = K.KfacStep(layers, n, rank=rank, world=world, policy=policy, comm=comm, device=dev)
+    # synthetic inputs of this rank (global-sample seeded), pinned host copies for the e2e leg
+    t0 = time.time()
+    xs_h = [inputs.layer_x(l, i, n, rank, args.seed).pin_memory() for i, l in enumerate(layers)]
+    gys_h = [inputs.layer_gy(l, i, n, rank, args.seed).pin_memory() for i, l in enumerate(layers)]
+    dws_h = [inputs.layer_dw(l, i, rank, args.seed).pin_memory() for i, l in enumerate(layers)]
+    gen_s = time.time() - t0
+    xs = [x.to(dev) for x in xs_h]
+    gys = [g.to(dev) for g in gys_h]
+    st.set_dw([d.to(dev) for d in dws_h])
+    in_bytes = sum(x.numel() * 2 for x in xs) + sum(g.numel() * 2 for g in gys)
+    dw_bytes = sum(d.numel() * 4 for d in dws_h)
+    l2_bytes = 126 * 2 ** 20
+    flush = torch.empty(0, device=dev)
+    if in_bytes < 2 * l2_bytes:
+        flush = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    nst = 5
+    names = ["factors", "reduce_scatter", "inverse", "precondition", "allgather"]
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        st.run(xs, gys, args.gamma, stream)
+    torch.cuda.synchronize()
+    status = st.dev_status.cpu().tolist()
+
+    # ---- device-timed region: inputs resident in HBM
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(nst + 1)] for _ in range(args.steps)]
+    barrier()
+    l0 = K.kfac.launch_count()
+    with ClockSampler(local) as clk:
+        for s in range(args.steps):
+            if flush.numel():
+                flush.fill_(s & 0xFF)
+            ev[s][0].record(stream)
+            st.run(xs, gys, args.gamma, stream, events=ev[s][1:])
+        barrier()
+    launches = K.kfac.launch_count() - l0
+    step_ms = [e[0].elapsed_time(e[nst]) for e in ev]
+    stage_ms = [[e[i].elapsed_time(e[i + 1]) for e in ev] for i in range(nst)]
+    mine = torch.tensor([sum(step_ms)] + [sum(x) for x in stage_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(mine, op=dist.ReduceOp.MAX)
+    tot = mine.cpu().tolist()
+    ms = tot[0] / args.steps
+    st_ms = {nm: tot[1 + i] / args.steps for i, nm in enumerate(names)}
+
+    # ---- end-to-end through the public API with host buffers (H2D inputs, D2H result)
+    e2e = None
+    if not args.no_e2e:
+        out_h = torch.empty(st.ag_buf.numel(), dtype=torch.float32).pin_memory()
+        dwv = [st.dw_view(l) for l in range(len(layers))]
+        for _ in range(2):
+            for x, xh in zip(xs, xs_h):
+                x.copy_(xh, non_blocking=True)
+            st.run(xs, gys, args.gamma, stream)
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        ke = max(1, min(args.steps, 5))
+        for _ in range(ke):
+            for x, xh in zip(xs, xs_h):
+                x.copy_(xh, non_blocking=True)
+            for g, gh in zip(gys, gys_h):
+                g.copy_(gh, non_blocking=True)
+            for d, dh in zip(dwv, dws_h):
+                d.copy_(dh, non_blocking=True)
+            st.run(xs, gys, args.gamma, stream)
+            out_h.copy_(st.ag_buf, non_blocking=True)
+        e1.record(stream)
+        barrier()
+        em = torch.tensor([e0.elapsed_time(e1) / ke], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(em, op=dist.ReduceOp.MAX)
+        e2e = {"value": round(em.item(), 3), "unit": "ms", "h2d_bytes_per_step": in_bytes + dw_bytes,
+               "d2h_bytes_per_step": out_h.numel() * 4, "steps": ke}
+
+    # ---- roofline of the dominant stage (+ the factor kernel, the north-star contraction)
+    pk = peaks()
+    w = work(layers, n, rank_layers=st.rl["layers"])
+    wmax = torch.tensor([w["inverse_flops"], w["precond_flops"]], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(wmax, op=dist.ReduceOp.MAX)
+    fac_s = st_ms["factors"] / 1e3
+    fac_tflops = w["factor_flops"] / fac_s / 1e12
+    fac_roof = {"bound": "tensor", "achieved": round(fac_tflops, 2), "peak": pk["bf16_tflops_sustained"],
+                "unit": "TFLOP/s", "frac": round(fac_tflops / pk["bf16_tflops_sustained"], 4), "traffic": None,
+                "kernel": "factor_syrk_kernel (+fixup, bias)", "flops_counting": "upper triangle, rows*d*(d+1)",
+                "hbm_gbs": round(w["factor_bytes"] / fac_s / 1e9, 1), "peak_src": pk["src"] + " sustained"}
+    inv_tf = w["inverse_flops"] / (st_ms["inverse"] / 1e3) / 1e12
+    prec_tf = w["precond_flops"] / (st_ms["precondition"] / 1e3) / 1e12
+    rs_bytes = st.q["rs_chunk"] * 4 * (world - 1)
+    roofs = {
+        "factors": fac_roof,
+        "inverse": {"bound": "alu", "achieved": round(inv_tf, 3), "peak": round(FP64_PEAK_TFLOPS, 1),
+                    "unit": "TFLOP/s", "frac": round(inv_tf / FP64_PEAK_TFLOPS, 4), "traffic": None,
+                    "kernel": "damped_inverse (pivot/panel/update_kernel, fp64)",
+                    "flops_counting": "n^3 per matrix", "peak_src": "derived fp64 148x64x2x1.965GHz"},
+        "precondition": {"bound": "alu", "achieved": round(prec_tf, 3), "peak": round(FP32_PEAK_TFLOPS, 1),
+                         "unit": "TFLOP/s", "frac": round(prec_tf / FP32_PEAK_TFLOPS, 4), "traffic": None,
+                         "kernel": "sgemm_grouped_kernel (fp32 FFMA)", "peak_src": "derived fp32 148x128x2x1.965GHz"},
+    }
+    if world > 1:
+        for nm in ("reduce_scatter", "allgather"):
+            b = rs_bytes if nm == "reduce_scatter" else st.q["ag_chunk"] * 4 * (world - 1)
+            gbs = b / (st_ms[nm] / 1e3) / 1e9
+            roofs[nm] = {"bound": "nvlink", "achieved": round(gbs, 1), "peak": NVLINK_GBS, "unit": "GB/s",
+                         "frac": round(gbs / NVLINK_GBS, 4), "traffic": None, "kernel": "NCCL"}
+    dom = max((k for k in roofs), key=lambda k: st_ms[k])
+    # committed ncu traffic per kernel, if a profile summary exists
+    tf = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tf):
+        tr = json.load(open(tf))
+        for k, r in roofs.items():
+            if k in tr:
+                r["traffic"] = tr[k]
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        small = 576 if args.config in ("resnet50", "resnet18_cifar") else (1000 if args.config == "stress" else 10 ** 9)
+        v, desc, cores, _ = cpu_sample(layers, n, small)
+        cpu = {"value": round(v, 1), "unit": "ms", "cores": cores, "kind": "oracle", "sample": desc}
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": round(ms, 3), "unit": "ms", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": args.config, "global_batch": n * world, "per_gpu_batch": n,
+                       "parallelism": f"dp{world}+layer-sharded inverse/precondition ({args.policy})",
+                       "gamma": args.gamma, "l2": ("inputs %.2f GB > 126 MB L2" % (in_bytes / 1e9)) if not flush.numel()
+                       else "L2 flushed (256 MB write) between steps"},
+            "factor_tflops": round(fac_tflops, 2),
+            "images_per_s": round(n * world / (ms / 1e3), 1),
+            "stage_ms": {k: round(v, 3) for k, v in st_ms.items()},
+            "roofline": dict(roofs[dom], stage=dom),
+            "roofline_factors": fac_roof,
+            "roofline_stages": roofs,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+            "dev_status_ok": all(v == 0 for v in status),
+            "input_gen_s": round(gen_s, 1),
+        }
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier(device_ids=[local])
+        del comm
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="resnet50", choices=list(shapes.CONFIGS))
+    ap.add_argument("--policy", default="lpt", choices=["lpt", "rr"])
+    ap.add_argument("--gamma", type=float, default=2.5e-2)  # gamma^(0), Table 3
+    ap.add_argument("--seed", type=int, default=1811)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

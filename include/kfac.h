@@ -1,0 +1,224 @@
+/*
+ * kfac.h -- C-ABI of the B200-native distributed K-FAC hot path
+ * (Osawa et al., "Large-Scale Distributed Second-Order Optimization Using
+ * Kronecker-Factored Approximate Curvature for Deep CNNs", arXiv 1811.12019).
+ *
+ * The calls follow the paper's statement of one K-FAC iteration (PAPER.md
+ * §3.3, Fig. 1 and Algorithm 1), minus forward/backward and the
+ * weight update:
+ *
+ *   stage 1-2  kfac_factor_A / kfac_factor_G / kfac_factor_all
+ *              A_{l-1} = alpha * sum_rows a a^T over im2col patches (+bias 1),
+ *              G_l     = alpha * sum_rows g g^T over output-gradient pixels
+ *              (P:237-245 Eq. kf), written as the packed upper
+ *              triangle (P:407-411 symmetry-aware communication).
+ *   stage 3    kfac_reduce_scatter_factors: ReduceScatterV(mean) of
+ *              (dW, A, G) to the layer owners (Alg. 1 line
+ *              "Reduce+ScatterV").
+ *   stage 4    kfac_damped_inverse: factored Tikhonov damping
+ *              and the inverses A_d^-1, G_d^-1 (P:247-260 Eq. inv_fim).
+ *   stage 5    kfac_precondition: G_d^-1 * dW * A_d^-1.
+ *   stage 6    kfac_allgather_precond: AllGatherV of the preconditioned
+ *              gradients.
+ *
+ * Conventions for every call
+ *   - Pointers are CUDA device pointers unless marked "host".
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *     Every call only ENQUEUES work on `stream`; none synchronises the device
+ *     and none allocates device memory, except kfac_plan_create /
+ *     kfac_comm_create (setup-time allocation of small metadata).
+ *   - The caller owns every buffer.  The library owns only the opaque plan
+ *     and communicator handles.
+ *   - Errors are returned synchronously as kfac_status; kfac_last_error()
+ *     gives a thread-local message.  Numeric failures found on the device
+ *     (a non-positive pivot) are written to `dev_status`, never silently
+ *     regularised (damping is the caller's gamma).
+ *   - Calls on different streams / ranks may run concurrently; calls sharing
+ *     a workspace must be stream-ordered.
+ *
+ * Data layouts
+ *   x   layer input, NHWC [n, h_in, w_in, c_in] for conv2d, [n, c_in] for
+ *       linear; bf16 or fp16.
+ *   gy  gradient w.r.t. the layer output, NHWC [n, h_out, w_out, c_out]
+ *       ([n, c_out] for linear); bf16 or fp16.
+ *   dW  weight gradient [c_out, dA] row-major fp32, dA = c_in*kh*kw (+1 bias
+ *       column, last); the patch feature order is (kh, kw, c), c fastest,
+ *       i.e. channels-last weights (R-5, R-6).
+ *   packed factor of dimension d: d(d+1)/2 fp32, upper triangle, row-major:
+ *       element (i, j), j >= i, at i*d - i*(i-1)/2 + (j - i)  (R-10).
+ *   inverse: full d x d fp32 row-major (symmetric).
+ */
+#ifndef KFAC_H
+#define KFAC_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define KFAC_API __attribute__((visibility("default")))
+#else
+#define KFAC_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    KFAC_OK = 0,
+    KFAC_ERR_ARG = 1,         /* bad argument: NULL pointer, n < 1, gamma <= 0, ... */
+    KFAC_ERR_SHAPE = 2,       /* inconsistent shapes */
+    KFAC_ERR_UNSUPPORTED = 3, /* geometry the kernels do not support */
+    KFAC_ERR_CUDA = 4,        /* a CUDA runtime/driver call failed */
+    KFAC_ERR_NCCL = 5,        /* an NCCL call failed */
+    KFAC_ERR_NOT_PD = 6,      /* reserved: host-side report of a non-PD factor */
+    KFAC_ERR_STATE = 7        /* plan/communicator mismatch, wrong world size, ... */
+} kfac_status;
+
+typedef enum { KFAC_BF16 = 0, KFAC_FP16 = 1 } kfac_dtype;
+
+/* Layer ownership policy for the model-parallel stages (R-15).
+ * ROUND_ROBIN: owner(l) = l mod world.  LPT: layers by descending stage-4/5
+ * cost dA^3 + dG^3 + 2 dG^2 dA + 2 dG dA^2 (ties by index) to the least
+ * loaded rank (ties by rank).  If world > L, rank r >= L also owns layer
+ * r mod L redundantly ("some layers will be calculated
+ * redundantly"; R-16).                                                      */
+typedef enum { KFAC_OWN_ROUND_ROBIN = 0, KFAC_OWN_LPT = 1 } kfac_policy;
+
+typedef struct {
+    int32_t kind; /* 0 = conv2d, 1 = linear */
+    int32_t c_in, c_out;
+    int32_t kh, kw;             /* 1, 1 for linear */
+    int32_t stride_h, stride_w; /* 1, 1 for linear */
+    int32_t pad_h, pad_w;       /* 0, 0 for linear */
+    int32_t h_in, w_in;         /* 1, 1 for linear */
+    int32_t has_bias;           /* appends the homogeneous coordinate 1 to the patch */
+} kfac_layer_desc;
+
+typedef struct kfac_plan *kfac_plan_t;
+typedef struct kfac_comm *kfac_comm_t;
+
+/* Thread-local message describing the last non-OK status of this thread. */
+KFAC_API const char *kfac_last_error(void);
+/* Library version string, e.g. "kfac-b200 0.1 sm_100a". */
+KFAC_API const char *kfac_version(void);
+/* Instrumentation: number of CUDA kernels this library has launched in this
+ * process so far (NCCL's own kernels are not counted).  Host-only, no sync. */
+KFAC_API int64_t kfac_launch_count(void);
+
+/* ------------------------------------------------------------------ plan
+ * kfac_plan_create: ownership map + wire layout for L layers over `world`
+ * ranks with `n_local` samples per rank.  host
+ * `layers` is copied.  Rank r's ReduceScatter chunk lists its owned layers
+ * in ascending order, each with the segments [dW (dG*dA), A packed, G
+ * packed]; every segment starts on a 16-element (64 B) boundary and every
+ * chunk is padded to rs_chunk = max chunk (NCCL has no V variant).  The
+ * AllGather chunk of rank r holds the preconditioned gradient of each layer
+ * whose PRIMARY owner is r, ascending, 16-aligned, padded to ag_chunk.
+ * Errors: KFAC_ERR_ARG (NULL, L < 1, world < 1, n_local < 1, bad policy),
+ * KFAC_ERR_SHAPE (a non-positive dimension, kind not 0/1).                 */
+KFAC_API kfac_status kfac_plan_create(const kfac_layer_desc *layers /* host [L] */, int32_t L, int32_t world,
+                             int32_t n_local, kfac_policy policy, kfac_plan_t *out /* host */);
+
+/* Host outputs (each may be NULL):
+ *   owner[L]     primary owner of each layer
+ *   seg_off[3L]  element offsets into the world*rs_chunk send buffer of the
+ *                PRIMARY copy of (dW, A packed, G packed) of each layer
+ *   rs_chunk     elements per rank of the ReduceScatter buffers
+ *   ag_off[L]    element offset of each layer's preconditioned gradient in
+ *                the world*ag_chunk AllGather buffer
+ *   ag_chunk     elements per rank of the AllGather buffer
+ *   ws_bytes     workspace bytes needed by any stage on any rank           */
+KFAC_API kfac_status kfac_plan_query(kfac_plan_t plan, int32_t *owner, int64_t *seg_off, int64_t *rs_chunk,
+                            int64_t *ag_off, int64_t *ag_chunk, int64_t *ws_bytes);
+
+/* Layers owned by `rank` (primary and redundant), ascending.  Host outputs
+ * (each may be NULL): n_owned; layers[n_owned]; local_off[3*n_owned] =
+ * offsets of (dW, A, G) inside the rank's recv chunk; inv_off[2*n_owned] =
+ * offsets (floats) of A_d^-1 and G_d^-1 inside inv_ws; inv_floats = size of
+ * inv_ws in floats for this rank.                                           */
+KFAC_API kfac_status kfac_plan_rank_layers(kfac_plan_t plan, int32_t rank, int32_t *n_owned, int32_t *layers,
+                                  int64_t *local_off, int64_t *inv_off, int64_t *inv_floats);
+
+KFAC_API void kfac_plan_destroy(kfac_plan_t plan);
+
+/* ------------------------------------------------------------------ comm
+ * NCCL communicator over NVLink/NVSwitch (one process per GPU).  Rank 0 calls
+ * kfac_comm_unique_id and broadcasts the 128 host bytes (e.g. with
+ * torch.distributed); every rank then calls kfac_comm_create on its device.
+ * Errors: KFAC_ERR_NCCL, KFAC_ERR_CUDA, KFAC_ERR_ARG.                       */
+KFAC_API kfac_status kfac_comm_unique_id(uint8_t id[128] /* host */);
+KFAC_API kfac_status kfac_comm_create(const uint8_t id[128] /* host */, int32_t rank, int32_t world, int32_t device,
+                             kfac_comm_t *out /* host */);
+KFAC_API void kfac_comm_destroy(kfac_comm_t comm);
+
+/* ------------------------------------------------------------------ stage 1-2
+ * kfac_factor_A: out_packed[dA(dA+1)/2] = alpha * sum over the n*h_out*w_out
+ * patches ã of ã ã^T (patch extraction fused into the
+ * kernel's shared-memory staging, zero padding, (kh,kw,c) order, bias 1
+ * last).  Inputs are half precision, products are accumulated in fp32 on the
+ * tensor cores.  alpha = 1/rows is the paper's mean (R-3).
+ * `ws` is scratch of at least kfac_factor_ws_bytes(..., which=0) bytes (split-K
+ * partials); it may be NULL when that size is 0.
+ * Errors: KFAC_ERR_ARG, KFAC_ERR_UNSUPPORTED (e.g. dilation-like geometry the
+ * descriptor cannot express), KFAC_ERR_CUDA.                                */
+KFAC_API kfac_status kfac_factor_A(const kfac_layer_desc *layer /* host */, const void *x, kfac_dtype dtype, int32_t n,
+                          float alpha, float *out_packed, void *ws, int64_t ws_bytes, void *stream);
+
+/* kfac_factor_G: out_packed[dG(dG+1)/2] = alpha * sum over the n*h_out*w_out
+ * pixels g = gy[pixel, :] of g g^T (the caller folds any per-sample
+ * loss scale into gy or alpha, R-4).                                        */
+KFAC_API kfac_status kfac_factor_G(const kfac_layer_desc *layer /* host */, const void *gy, kfac_dtype dtype, int32_t n,
+                          float alpha, float *out_packed, void *ws, int64_t ws_bytes, void *stream);
+
+/* Scratch bytes kfac_factor_A (which = 0) / kfac_factor_G (which = 1) need. */
+KFAC_API kfac_status kfac_factor_ws_bytes(const kfac_layer_desc *layer /* host */, int32_t n, int32_t which,
+                                 int64_t *bytes /* host */);
+
+/* All factors of one rank in ONE grouped launch (plus a split-K fix-up):
+ * A and G of every layer l are written packed into rs_send at every owner
+ * copy of layer l (primary seg_off and redundant copies); the dW segment of
+ * each redundant copy is refreshed from the primary copy (the caller writes
+ * dW into the primary segments).  xs / gys: host arrays of L device
+ * pointers; alphaA / alphaG: host arrays of L scales, or NULL for 1/rows.
+ * ws: at least ws_bytes from kfac_plan_query.                               */
+KFAC_API kfac_status kfac_factor_all(kfac_plan_t plan, const void *const *xs /* host [L] */,
+                            const void *const *gys /* host [L] */, kfac_dtype dtype,
+                            const float *alphaA /* host [L] or NULL */, const float *alphaG /* host [L] or NULL */,
+                            float *rs_send /* [world*rs_chunk] */, void *ws, void *stream);
+
+/* ------------------------------------------------------------------ stage 3
+ * ReduceScatterV(mean): rs_recv[0:rs_chunk] of rank r = mean over ranks of
+ * rs_send[r*rs_chunk : (r+1)*rs_chunk] (R-11).  One NCCL
+ * ReduceScatter(ncclAvg) over the owner-major padded buffer.  comm may be NULL
+ * only when world == 1 (then a device copy, or nothing if send == recv).   */
+KFAC_API kfac_status kfac_reduce_scatter_factors(kfac_comm_t comm, kfac_plan_t plan, const float *rs_send,
+                                        float *rs_recv, void *stream);
+
+/* ------------------------------------------------------------------ stage 4
+ * For every layer owned by `rank` (kfac_plan_rank_layers order, k-th layer):
+ *   pi = sqrt((tr A / dA) / (tr G / dG)), pi = 1 if a trace is 0;
+ *   A_d = A + pi*sqrt(gamma) I,  G_d = G + sqrt(gamma)/pi I   (R-1)
+ * and writes A_d^-1, G_d^-1 (full fp32) at inv_off into inv_ws (R-12:
+ * fp64 arithmetic).  dev_status[2k+0 / 2k+1] = 0 on success, else the failing
+ * pivot index + 1 for A_d / G_d.  pi_out (device, may be NULL) receives pi per
+ * owned layer.  Errors: KFAC_ERR_ARG (gamma <= 0, NULL), KFAC_ERR_STATE.    */
+KFAC_API kfac_status kfac_damped_inverse(kfac_plan_t plan, int32_t rank, const float *rs_recv, float gamma, float *inv_ws,
+                                int32_t *dev_status, float *pi_out, void *ws, void *stream);
+
+/* ------------------------------------------------------------------ stage 5
+ * For every layer owned by `rank`: P = G_d^-1 * dW * A_d^-1, dW
+ * read from rs_recv.  The primary owner writes P into ag_buf at ag_off[l]
+ * (its own AllGather slot); a redundant owner writes into `ws`.             */
+KFAC_API kfac_status kfac_precondition(kfac_plan_t plan, int32_t rank, const float *rs_recv, const float *inv_ws,
+                              float *ag_buf /* [world*ag_chunk] */, void *ws, void *stream);
+
+/* ------------------------------------------------------------------ stage 6
+ * In-place AllGatherV: afterwards every rank's ag_buf holds every layer's
+ * preconditioned gradient at ag_off[l].  comm may be NULL when
+ * world == 1 (no-op).                                                        */
+KFAC_API kfac_status kfac_allgather_precond(kfac_comm_t comm, kfac_plan_t plan, float *ag_buf, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KFAC_H */

@@ -1,0 +1,266 @@
+// api.cpp -- the C-ABI entry points of the K-FAC hot path (include/kfac.h):
+// argument validation, marshalling into the grouped kernel launchers, and the
+// NCCL collectives.  Every step of the path runs in this library's kernels or
+// in NCCL; nothing here computes on the host.
+#include <dlfcn.h>
+
+#include <cstring>
+#include <string>
+
+#include <nccl.h>
+
+#include "kfac_plan.hpp"
+
+using namespace kfac;
+
+struct kfac_comm {
+    ncclComm_t comm = nullptr;
+    int rank = 0, world = 1, device = 0;
+};
+
+#define KFAC_NCCL_TRY(expr)                                                                   \
+    do {                                                                                      \
+        ncclResult_t _r = (expr);                                                             \
+        if (_r != ncclSuccess)                                                                \
+            return set_error(KFAC_ERR_NCCL, std::string(#expr) + ": " + ncclGetErrorString(_r)); \
+    } while (0)
+
+static cudaStream_t S(void *s) { return static_cast<cudaStream_t>(s); }
+
+static kfac_status one_factor(const kfac_layer_desc *layer, const void *src, kfac_dtype dt, int32_t n, float alpha,
+                              float *out, void *ws, int64_t ws_bytes, void *stream, bool is_A) {
+    if (!layer || !src || !out) return set_error(KFAC_ERR_ARG, "kfac_factor: NULL argument");
+    if (n < 1) return set_error(KFAC_ERR_ARG, "kfac_factor: n must be >= 1 (empty capture)");
+    if (dt != KFAC_BF16 && dt != KFAC_FP16) return set_error(KFAC_ERR_ARG, "kfac_factor: dtype");
+    FactorJob j{};
+    kfac_status s = make_geom(*layer, &j.g);
+    if (s) return s;
+    j.is_A = is_A;
+    j.src = src;
+    j.out = out;
+    j.alpha = alpha;
+    j.n = n;
+    std::vector<FactorJob> jobs{j};
+    FactorLaunch fl;
+    s = factor_prepare(jobs, dt, ws, ws ? ws_bytes : 0, false, &fl);
+    if (s) return s;
+    return factor_launch(fl, jobs, S(stream));
+}
+
+extern "C" {
+
+kfac_status kfac_factor_A(const kfac_layer_desc *layer, const void *x, kfac_dtype dt, int32_t n, float alpha,
+                          float *out_packed, void *ws, int64_t ws_bytes, void *stream) {
+    return one_factor(layer, x, dt, n, alpha, out_packed, ws, ws_bytes, stream, true);
+}
+
+kfac_status kfac_factor_G(const kfac_layer_desc *layer, const void *gy, kfac_dtype dt, int32_t n, float alpha,
+                          float *out_packed, void *ws, int64_t ws_bytes, void *stream) {
+    return one_factor(layer, gy, dt, n, alpha, out_packed, ws, ws_bytes, stream, false);
+}
+
+kfac_status kfac_factor_ws_bytes(const kfac_layer_desc *layer, int32_t n, int32_t which, int64_t *bytes) {
+    if (!layer || !bytes || n < 1 || (which != 0 && which != 1)) return set_error(KFAC_ERR_ARG, "kfac_factor_ws_bytes");
+    FactorJob j{};
+    kfac_status s = make_geom(*layer, &j.g);
+    if (s) return s;
+    j.is_A = which == 0;
+    j.n = n;
+    std::vector<FactorJob> jobs{j};
+    FactorLaunch fl;
+    s = factor_prepare(jobs, KFAC_BF16, nullptr, 0, true, &fl);
+    if (s) return s;
+    *bytes = fl.ws_bytes;
+    return KFAC_OK;
+}
+
+kfac_status kfac_factor_all(kfac_plan_t p, const void *const *xs, const void *const *gys, kfac_dtype dt,
+                            const float *alphaA, const float *alphaG, float *rs_send, void *ws, void *stream) {
+    if (!p || !xs || !gys || !rs_send) return set_error(KFAC_ERR_ARG, "kfac_factor_all: NULL argument");
+    if (dt != KFAC_BF16 && dt != KFAC_FP16) return set_error(KFAC_ERR_ARG, "kfac_factor_all: dtype");
+    if (p->factor_ws > 0 && !ws) return set_error(KFAC_ERR_ARG, "kfac_factor_all: workspace required");
+    const int L = p->L;
+    std::vector<float> aA(L), aG(L);
+    for (int l = 0; l < L; l++) {
+        const Geom &g = p->geoms[l];
+        const double rows = (double)p->n_local * g.ho * g.wo;
+        aA[l] = alphaA ? alphaA[l] : (float)(1.0 / rows);
+        aG[l] = alphaG ? alphaG[l] : (float)(1.0 / rows);
+        if (!xs[l] || !gys[l]) return set_error(KFAC_ERR_ARG, "kfac_factor_all: NULL input pointer");
+    }
+    const bool same = p->c_dt == (int)dt && p->c_send == rs_send && p->c_ws == ws &&
+                      p->c_xs == std::vector<const void *>(xs, xs + L) &&
+                      p->c_gys == std::vector<const void *>(gys, gys + L) && p->c_aA == aA && p->c_aG == aG;
+    if (!same) {
+        p->c_jobs.clear();
+        for (int l = 0; l < L; l++) {
+            FactorJob a{};
+            a.g = p->geoms[l];
+            a.n = p->n_local;
+            a.is_A = true;
+            a.src = xs[l];
+            a.out = rs_send + p->seg_off[3 * l + 1];
+            a.alpha = aA[l];
+            p->c_jobs.push_back(a);
+            FactorJob b = a;
+            b.is_A = false;
+            b.src = gys[l];
+            b.out = rs_send + p->seg_off[3 * l + 2];
+            b.alpha = aG[l];
+            p->c_jobs.push_back(b);
+        }
+        kfac_status s = factor_prepare(p->c_jobs, dt, ws, p->ws_bytes, false, &p->c_fl);
+        if (s) {
+            p->c_dt = -1;
+            return s;
+        }
+        p->c_dt = (int)dt;
+        p->c_send = rs_send;
+        p->c_ws = ws;
+        p->c_xs.assign(xs, xs + L);
+        p->c_gys.assign(gys, gys + L);
+        p->c_aA = aA;
+        p->c_aG = aG;
+    }
+    kfac_status s = factor_launch(p->c_fl, p->c_jobs, S(stream));
+    if (s) return s;
+    // redundant owners: copy the primary (dW, A, G) segments into their chunks
+    std::vector<std::pair<const float *, float *>> sd;
+    std::vector<int64_t> cnt;
+    for (int r = 0; r < p->world; r++) {
+        for (size_t k = 0; k < p->owned[r].size(); k++) {
+            const int l = p->owned[r][k];
+            if (p->owner[l] == r) continue;
+            const Geom &g = p->geoms[l];
+            const int64_t n3[3] = {(int64_t)g.dG * g.dA, packed_len(g.dA), packed_len(g.dG)};
+            for (int s3 = 0; s3 < 3; s3++) {
+                sd.push_back({rs_send + p->seg_off[3 * l + s3], rs_send + (int64_t)r * p->rs_chunk + p->local[r][k][s3]});
+                cnt.push_back(n3[s3]);
+            }
+        }
+    }
+    if (!sd.empty()) return replicate_launch(sd, cnt, S(stream));
+    return KFAC_OK;
+}
+
+// ------------------------------------------------------------------ comm
+kfac_status kfac_comm_unique_id(uint8_t id[128]) {
+    if (!id) return set_error(KFAC_ERR_ARG, "kfac_comm_unique_id: NULL");
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    ncclUniqueId u;
+    KFAC_NCCL_TRY(ncclGetUniqueId(&u));
+    memcpy(id, &u, 128);
+    return KFAC_OK;
+}
+
+kfac_status kfac_comm_create(const uint8_t id[128], int32_t rank, int32_t world, int32_t device, kfac_comm_t *out) {
+    if (!id || !out || world < 1 || rank < 0 || rank >= world) return set_error(KFAC_ERR_ARG, "kfac_comm_create");
+    KFAC_CUDA_TRY(cudaSetDevice(device));
+    ncclUniqueId u;
+    memcpy(&u, id, 128);
+    kfac_comm *c = new kfac_comm();
+    ncclResult_t r = ncclCommInitRank(&c->comm, world, u, rank);
+    if (r != ncclSuccess) {
+        delete c;
+        return set_error(KFAC_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    }
+    c->rank = rank;
+    c->world = world;
+    c->device = device;
+    *out = c;
+    return KFAC_OK;
+}
+
+void kfac_comm_destroy(kfac_comm_t c) {
+    if (!c) return;
+    if (c->comm) ncclCommDestroy(c->comm);
+    delete c;
+}
+
+// ------------------------------------------------------------------ stage 3
+kfac_status kfac_reduce_scatter_factors(kfac_comm_t c, kfac_plan_t p, const float *send, float *recv, void *stream) {
+    if (!p || !send || !recv) return set_error(KFAC_ERR_ARG, "kfac_reduce_scatter_factors: NULL argument");
+    if (p->world == 1) {
+        if (send != recv)
+            KFAC_CUDA_TRY(cudaMemcpyAsync(recv, send, p->rs_chunk * sizeof(float), cudaMemcpyDeviceToDevice, S(stream)));
+        return KFAC_OK;
+    }
+    if (!c || c->world != p->world) return set_error(KFAC_ERR_STATE, "kfac_reduce_scatter_factors: comm/plan world mismatch");
+    KFAC_NCCL_TRY(ncclReduceScatter(send, recv, (size_t)p->rs_chunk, ncclFloat32, ncclAvg, c->comm, S(stream)));
+    return KFAC_OK;
+}
+
+// ------------------------------------------------------------------ stage 4
+kfac_status kfac_damped_inverse(kfac_plan_t p, int32_t rank, const float *recv, float gamma, float *inv_ws,
+                                int32_t *dev_status, float *pi_out, void *ws, void *stream) {
+    if (!p || !recv || !inv_ws || !dev_status || !ws) return set_error(KFAC_ERR_ARG, "kfac_damped_inverse: NULL argument");
+    if (!(gamma > 0.f)) return set_error(KFAC_ERR_ARG, "kfac_damped_inverse: gamma must be > 0");
+    if (rank < 0 || rank >= p->world) return set_error(KFAC_ERR_STATE, "kfac_damped_inverse: rank out of range");
+    const auto &ow = p->owned[rank];
+    uint8_t *w = static_cast<uint8_t *>(ws);
+    double *pair_scratch = reinterpret_cast<double *>(w);
+    int64_t off = align16(4 * (int64_t)ow.size()) * 8 + 1024;
+    std::vector<InvMat> mats;
+    for (size_t k = 0; k < ow.size(); k++) {
+        const Geom &g = p->geoms[ow[k]];
+        for (int which = 0; which < 2; which++) {
+            InvMat m{};
+            m.n = which == 0 ? g.dA : g.dG;
+            m.packed = recv + p->local[rank][k][1 + which];
+            m.inv = inv_ws + p->inv_off[rank][2 * k + which];
+            m.work = reinterpret_cast<double *>(w + off);
+            m.panel = m.work + (int64_t)m.n * m.n;
+            off += align16((int64_t)m.n * m.n + 2 * (int64_t)kPanel * m.n + kPanel * kPanel) * 8;
+            m.status = dev_status + 2 * k + which;
+            m.pair = (int)k;
+            m.is_A = which == 0;
+            mats.push_back(m);
+        }
+    }
+    if (off > p->ws_bytes) return set_error(KFAC_ERR_STATE, "kfac_damped_inverse: workspace layout exceeds ws_bytes");
+    return inverse_launch(mats, (int)ow.size(), gamma, pair_scratch, pi_out, S(stream));
+}
+
+// ------------------------------------------------------------------ stage 5
+kfac_status kfac_precondition(kfac_plan_t p, int32_t rank, const float *recv, const float *inv_ws, float *ag_buf,
+                              void *ws, void *stream) {
+    if (!p || !recv || !inv_ws || !ag_buf || !ws) return set_error(KFAC_ERR_ARG, "kfac_precondition: NULL argument");
+    if (rank < 0 || rank >= p->world) return set_error(KFAC_ERR_STATE, "kfac_precondition: rank out of range");
+    const auto &ow = p->owned[rank];
+    float *w = static_cast<float *>(ws);
+    int64_t off = 0;
+    std::vector<PrecJob> jobs;
+    for (size_t k = 0; k < ow.size(); k++) {
+        const int l = ow[k];
+        const Geom &g = p->geoms[l];
+        PrecJob j{};
+        j.dG = g.dG;
+        j.dA = g.dA;
+        j.dW = recv + p->local[rank][k][0];
+        j.Ainv = inv_ws + p->inv_off[rank][2 * k];
+        j.Ginv = inv_ws + p->inv_off[rank][2 * k + 1];
+        j.tmp = w + off;
+        off += align16((int64_t)g.dG * g.dA);
+        if (p->owner[l] == rank) {
+            j.out = ag_buf + p->ag_off[l];
+        } else {
+            j.out = w + off;
+        }
+        off += align16((int64_t)g.dG * g.dA);
+        jobs.push_back(j);
+    }
+    if (off * 4 > p->ws_bytes) return set_error(KFAC_ERR_STATE, "kfac_precondition: workspace layout exceeds ws_bytes");
+    return precond_launch(jobs, S(stream));
+}
+
+// ------------------------------------------------------------------ stage 6
+kfac_status kfac_allgather_precond(kfac_comm_t c, kfac_plan_t p, float *ag_buf, void *stream) {
+    if (!p || !ag_buf) return set_error(KFAC_ERR_ARG, "kfac_allgather_precond: NULL argument");
+    if (p->world == 1) return KFAC_OK;
+    if (!c || c->world != p->world) return set_error(KFAC_ERR_STATE, "kfac_allgather_precond: comm/plan world mismatch");
+    float *mine = ag_buf + (int64_t)c->rank * p->ag_chunk;
+    KFAC_NCCL_TRY(ncclAllGather(mine, ag_buf, (size_t)p->ag_chunk, ncclFloat32, c->comm, S(stream)));
+    return KFAC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,108 @@
+// kfac_internal.hpp -- shared host/device declarations of the K-FAC library
+// (not part of the C-ABI; see include/kfac.h for the public contract).
+#pragma once
+#include <atomic>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "../../include/kfac.h"
+
+namespace kfac {
+
+// ---------------------------------------------------------------- errors
+kfac_status set_error(kfac_status st, const std::string &msg);
+extern std::atomic<int64_t> g_launches;  // kernels launched (kfac_launch_count)
+#define KFAC_LAUNCHED() (::kfac::g_launches.fetch_add(1, std::memory_order_relaxed))
+#define KFAC_CUDA_TRY(expr)                                                                     \
+    do {                                                                                        \
+        cudaError_t _e = (expr);                                                                \
+        if (_e != cudaSuccess)                                                                  \
+            return ::kfac::set_error(KFAC_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+    } while (0)
+
+inline int64_t packed_len(int64_t d) { return d * (d + 1) / 2; }
+inline int64_t align16(int64_t v) { return (v + 15) / 16 * 16; }
+
+struct Geom {  // derived geometry of one layer
+    int c_in, c_out, kh, kw, sh, sw, ph, pw, h, w, ho, wo, bias, kind;
+    int dF;  // c_in*kh*kw (patch features)
+    int dA, dG;
+};
+kfac_status make_geom(const kfac_layer_desc &d, Geom *g);
+
+// ---------------------------------------------------------------- factor kernel
+constexpr int kMaxProbs = 112;   // factor problems per grouped launch
+constexpr int kTile = 128;       // feature tile (M = N = 128)
+constexpr int kBK = 64;          // rows (K) per pipeline stage
+
+enum FactorMode : int32_t { MODE_TILED2D = 0, MODE_IM2COL = 1, MODE_GATHER = 2 };
+
+struct alignas(64) FactorProb {
+    CUtensorMap tmap;       // 128 B, used by MODE_TILED2D / MODE_IM2COL
+    const uint16_t *src;    // NHWC half input (MODE_GATHER and bias column sums)
+    float *out;             // packed upper output, dimension d_out
+    float *partial;         // split-K partial tiles (splits > 1)
+    float alpha;
+    int32_t mode, d, d_out, nt, splits, kchunks, chunks_per_split;
+    int32_t cb;             // channels per TMA box / swizzle atom (16, 32, 64)
+    int32_t item_begin;     // first global work item of this problem
+    int32_t c, h, w, kh, kw, sh, sw, ph, pw, ho, wo;
+    int64_t rows;
+};
+
+struct FactorParams {
+    int32_t nprobs, total_items, ab_fmt, pad;
+    FactorProb probs[kMaxProbs];
+};
+
+// one factor problem (a layer's A or G) as seen by the host planner
+struct FactorJob {
+    Geom g;
+    bool is_A;            // A over im2col patches, else G over gy pixels
+    const void *src;      // x or gy
+    float *out;           // packed output (dimension dA or dG)
+    float alpha;
+    int64_t n;            // samples
+};
+
+// host planning of a list of jobs: item counts, splits, workspace bytes
+struct FactorLaunch {
+    std::vector<FactorParams> params;  // one per grouped launch (<= kMaxProbs problems)
+    int64_t ws_bytes = 0;
+};
+kfac_status factor_prepare(const std::vector<FactorJob> &jobs, kfac_dtype dt, void *ws, int64_t ws_cap,
+                           bool dry_run, FactorLaunch *out);
+kfac_status factor_launch(const FactorLaunch &fl, const std::vector<FactorJob> &jobs, cudaStream_t st);
+
+// ---------------------------------------------------------------- inverse / precondition
+struct InvMat {        // one damped factor to invert
+    const float *packed;  // packed upper fp32 (from rs_recv)
+    float *inv;           // full fp32 output
+    double *work;         // n*n fp64 working matrix
+    double *panel;        // 2 * kPanel * n fp64 (row panel R and W = P R)
+    int32_t *status;      // device status word
+    int32_t n;
+    int32_t pair;         // index of the (A, G) pair this matrix belongs to
+    int32_t is_A;
+};
+struct PrecJob {
+    const float *dW;      // [dG, dA]
+    const float *Ainv;    // [dA, dA]
+    const float *Ginv;    // [dG, dG]
+    float *tmp;           // [dG, dA] scratch  T = dW * Ainv
+    float *out;           // [dG, dA]
+    int32_t dG, dA;
+};
+kfac_status inverse_launch(const std::vector<InvMat> &mats, int npairs, float gamma, double *pair_scratch,
+                           float *pi_out, cudaStream_t st);
+kfac_status precond_launch(const std::vector<PrecJob> &jobs, cudaStream_t st);
+kfac_status replicate_launch(const std::vector<std::pair<const float *, float *>> &src_dst,
+                             const std::vector<int64_t> &counts, cudaStream_t st);
+
+constexpr int kPanel = 64;  // sweep block size of the inverse
+
+}  // namespace kfac

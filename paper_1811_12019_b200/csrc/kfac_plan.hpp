@@ -1,0 +1,32 @@
+// kfac_plan.hpp -- the opaque plan / communicator objects behind the C-ABI.
+#pragma once
+#include <array>
+#include <vector>
+
+#include "kfac_internal.hpp"
+
+struct kfac_plan {
+    std::vector<kfac_layer_desc> layers;
+    std::vector<kfac::Geom> geoms;
+    int L = 0, world = 1, n_local = 1;
+    kfac_policy policy = KFAC_OWN_ROUND_ROBIN;
+    std::vector<int32_t> owner;
+    std::vector<std::vector<int>> owned;                          // per rank, ascending
+    std::vector<std::vector<std::array<int64_t, 3>>> local;       // per rank, per owned layer
+    std::vector<int64_t> seg_off, ag_off;
+    int64_t rs_chunk = 0, ag_chunk = 0, ws_bytes = 0, factor_ws = 0;
+    std::vector<std::vector<int64_t>> inv_off;  // per rank: 2 per owned layer
+    std::vector<int64_t> inv_floats;
+    // cached grouped factor launch (re-encoded when the pointers change)
+    std::vector<const void *> c_xs, c_gys;
+    std::vector<float> c_aA, c_aG;
+    float *c_send = nullptr;
+    void *c_ws = nullptr;
+    int c_dt = -1;
+    kfac::FactorLaunch c_fl;
+    std::vector<kfac::FactorJob> c_jobs;
+};
+
+namespace kfac {
+kfac_status plan_build(kfac_plan *p);
+}

@@ -1,0 +1,236 @@
+"""ctypes binding of libkfac.so (include/kfac.h) -- argument marshalling only.
+
+Every function here has the name of the C entry point it wraps (without the
+``kfac_`` prefix) and forwards device pointers of torch CUDA tensors plus the
+current CUDA stream; all computation happens in the library's kernels / NCCL.
+There is no fallback: if libkfac.so is missing, importing this module fails.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libkfac.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_1811_12019_b200.build` "
+                      "(there is no CPU fallback for the K-FAC hot path)")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+BF16, FP16 = 0, 1
+RR, LPT = 0, 1
+_DT = {torch.bfloat16: BF16, torch.float16: FP16}
+
+STATUS = {0: "OK", 1: "ERR_ARG", 2: "ERR_SHAPE", 3: "ERR_UNSUPPORTED", 4: "ERR_CUDA", 5: "ERR_NCCL",
+          6: "ERR_NOT_PD", 7: "ERR_STATE"}
+
+
+class KfacError(RuntimeError):
+    def __init__(self, status, where):
+        self.status = status
+        msg = _lib.kfac_last_error().decode(errors="replace")
+        super().__init__(f"{where}: {STATUS.get(status, status)}: {msg}")
+
+
+class LayerDesc(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in
+                ("kind", "c_in", "c_out", "kh", "kw", "stride_h", "stride_w", "pad_h", "pad_w", "h_in", "w_in",
+                 "has_bias")]
+
+
+def layer_desc(d: dict) -> LayerDesc:
+    return LayerDesc(*(int(d[k]) for k, _ in LayerDesc._fields_))
+
+
+_P = ctypes.c_void_p
+_i32, _i64, _f32 = ctypes.c_int32, ctypes.c_int64, ctypes.c_float
+_pi32, _pi64 = ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int64)
+_pf32 = ctypes.POINTER(ctypes.c_float)
+
+
+def _sig(name, args):
+    f = getattr(_lib, name)
+    f.argtypes = args
+    f.restype = ctypes.c_int
+    return f
+
+
+_lib.kfac_last_error.restype = ctypes.c_char_p
+_lib.kfac_version.restype = ctypes.c_char_p
+_lib.kfac_launch_count.restype = ctypes.c_int64
+_lib.kfac_launch_count.argtypes = []
+_lib.kfac_plan_destroy.argtypes = [_P]
+_lib.kfac_plan_destroy.restype = None
+_lib.kfac_comm_destroy.argtypes = [_P]
+_lib.kfac_comm_destroy.restype = None
+_plan_create = _sig("kfac_plan_create", [ctypes.POINTER(LayerDesc), _i32, _i32, _i32, ctypes.c_int, ctypes.POINTER(_P)])
+_plan_query = _sig("kfac_plan_query", [_P, _pi32, _pi64, _pi64, _pi64, _pi64, _pi64])
+_plan_rank_layers = _sig("kfac_plan_rank_layers", [_P, _i32, _pi32, _pi32, _pi64, _pi64, _pi64])
+_comm_unique_id = _sig("kfac_comm_unique_id", [ctypes.c_char_p])
+_comm_create = _sig("kfac_comm_create", [ctypes.c_char_p, _i32, _i32, _i32, ctypes.POINTER(_P)])
+_factor_A = _sig("kfac_factor_A", [ctypes.POINTER(LayerDesc), _P, ctypes.c_int, _i32, _f32, _P, _P, _i64, _P])
+_factor_G = _sig("kfac_factor_G", [ctypes.POINTER(LayerDesc), _P, ctypes.c_int, _i32, _f32, _P, _P, _i64, _P])
+_factor_ws_bytes = _sig("kfac_factor_ws_bytes", [ctypes.POINTER(LayerDesc), _i32, _i32, _pi64])
+_factor_all = _sig("kfac_factor_all", [_P, ctypes.POINTER(_P), ctypes.POINTER(_P), ctypes.c_int, _pf32, _pf32, _P, _P, _P])
+_reduce_scatter = _sig("kfac_reduce_scatter_factors", [_P, _P, _P, _P, _P])
+_damped_inverse = _sig("kfac_damped_inverse", [_P, _i32, _P, _f32, _P, _P, _P, _P, _P])
+_precondition = _sig("kfac_precondition", [_P, _i32, _P, _P, _P, _P, _P])
+_allgather = _sig("kfac_allgather_precond", [_P, _P, _P, _P])
+
+EXPORTS = ["kfac_last_error", "kfac_version", "kfac_launch_count", "kfac_plan_create", "kfac_plan_query", "kfac_plan_rank_layers",
+           "kfac_plan_destroy", "kfac_comm_unique_id", "kfac_comm_create", "kfac_comm_destroy", "kfac_factor_A",
+           "kfac_factor_G", "kfac_factor_ws_bytes", "kfac_factor_all", "kfac_reduce_scatter_factors",
+           "kfac_damped_inverse", "kfac_precondition", "kfac_allgather_precond"]
+
+
+def _check(st, where):
+    if st != 0:
+        raise KfacError(st, where)
+
+
+def version() -> str:
+    return _lib.kfac_version().decode()
+
+
+def launch_count() -> int:
+    """Kernels launched by libkfac.so in this process (instrumentation)."""
+    return int(_lib.kfac_launch_count())
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if not isinstance(t, torch.Tensor):
+        return t
+    if not t.is_cuda:
+        raise ValueError("expected a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError("expected a contiguous tensor")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+# ------------------------------------------------------------------ plan
+class Plan:
+    """kfac_plan_create / _query / _rank_layers / _destroy."""
+
+    def __init__(self, layers, world, n_local, policy=RR):
+        self.layers = list(layers)
+        arr = (LayerDesc * len(layers))(*[layer_desc(l) for l in layers])
+        h = _P()
+        _check(_plan_create(arr, len(layers), int(world), int(n_local), int(policy), ctypes.byref(h)),
+               "kfac_plan_create")
+        self.h = h
+        self.world, self.n_local, self.L = int(world), int(n_local), len(layers)
+        self._q = None
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and h.value:
+            _lib.kfac_plan_destroy(h)
+            self.h = None
+
+    def query(self):
+        if self._q is None:
+            L = self.L
+            owner = (ctypes.c_int32 * L)()
+            seg = (ctypes.c_int64 * (3 * L))()
+            ag = (ctypes.c_int64 * L)()
+            rs_chunk, ag_chunk, ws = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+            _check(_plan_query(self.h, owner, seg, ctypes.byref(rs_chunk), ag, ctypes.byref(ag_chunk),
+                               ctypes.byref(ws)), "kfac_plan_query")
+            self._q = dict(owner=list(owner), seg_off=[list(seg[3 * l:3 * l + 3]) for l in range(L)],
+                           rs_chunk=rs_chunk.value, ag_off=list(ag), ag_chunk=ag_chunk.value, ws_bytes=ws.value)
+        return self._q
+
+    def rank_layers(self, rank):
+        L = self.L
+        n = ctypes.c_int32()
+        layers = (ctypes.c_int32 * L)()
+        loc = (ctypes.c_int64 * (3 * L))()
+        inv = (ctypes.c_int64 * (2 * L))()
+        nf = ctypes.c_int64()
+        _check(_plan_rank_layers(self.h, int(rank), ctypes.byref(n), layers, loc, inv, ctypes.byref(nf)),
+               "kfac_plan_rank_layers")
+        k = n.value
+        return dict(layers=list(layers[:k]), local_off=[list(loc[3 * i:3 * i + 3]) for i in range(k)],
+                    inv_off=[list(inv[2 * i:2 * i + 2]) for i in range(k)], inv_floats=nf.value)
+
+
+# ------------------------------------------------------------------ comm
+class Comm:
+    def __init__(self, uid: bytes, rank: int, world: int, device: int):
+        h = _P()
+        _check(_comm_create(uid, int(rank), int(world), int(device), ctypes.byref(h)), "kfac_comm_create")
+        self.h, self.rank, self.world = h, rank, world
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and h.value:
+            _lib.kfac_comm_destroy(h)
+            self.h = None
+
+
+def comm_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(_comm_unique_id(buf), "kfac_comm_unique_id")
+    return buf.raw
+
+
+# ------------------------------------------------------------------ stages
+def factor_ws_bytes(layer, n, which):
+    b = ctypes.c_int64()
+    _check(_factor_ws_bytes(ctypes.byref(layer_desc(layer)), int(n), int(which), ctypes.byref(b)),
+           "kfac_factor_ws_bytes")
+    return b.value
+
+
+def factor_A(layer, x, n, alpha, out, ws=None, stream=None):
+    _check(_factor_A(ctypes.byref(layer_desc(layer)), _ptr(x), _DT[x.dtype], int(n), float(alpha), _ptr(out),
+                     _ptr(ws), ws.numel() * ws.element_size() if ws is not None else 0, _stream(stream)),
+           "kfac_factor_A")
+
+
+def factor_G(layer, gy, n, alpha, out, ws=None, stream=None):
+    _check(_factor_G(ctypes.byref(layer_desc(layer)), _ptr(gy), _DT[gy.dtype], int(n), float(alpha), _ptr(out),
+                     _ptr(ws), ws.numel() * ws.element_size() if ws is not None else 0, _stream(stream)),
+           "kfac_factor_G")
+
+
+def factor_all(plan, xs, gys, rs_send, ws, alphaA=None, alphaG=None, stream=None):
+    L = plan.L
+    xa = (_P * L)(*[x.data_ptr() for x in xs])
+    ga = (_P * L)(*[g.data_ptr() for g in gys])
+    aA = (ctypes.c_float * L)(*alphaA) if alphaA is not None else None
+    aG = (ctypes.c_float * L)(*alphaG) if alphaG is not None else None
+    _check(_factor_all(plan.h, xa, ga, _DT[xs[0].dtype], aA, aG, _ptr(rs_send), _ptr(ws), _stream(stream)),
+           "kfac_factor_all")
+
+
+def reduce_scatter_factors(comm, plan, rs_send, rs_recv, stream=None):
+    _check(_reduce_scatter(comm.h if comm is not None else None, plan.h, _ptr(rs_send), _ptr(rs_recv),
+                           _stream(stream)), "kfac_reduce_scatter_factors")
+
+
+def damped_inverse(plan, rank, rs_recv, gamma, inv_ws, dev_status, pi_out, ws, stream=None):
+    _check(_damped_inverse(plan.h, int(rank), _ptr(rs_recv), float(gamma), _ptr(inv_ws), _ptr(dev_status),
+                           _ptr(pi_out), _ptr(ws), _stream(stream)), "kfac_damped_inverse")
+
+
+def precondition(plan, rank, rs_recv, inv_ws, ag_buf, ws, stream=None):
+    _check(_precondition(plan.h, int(rank), _ptr(rs_recv), _ptr(inv_ws), _ptr(ag_buf), _ptr(ws), _stream(stream)),
+           "kfac_precondition")
+
+
+def allgather_precond(comm, plan, ag_buf, stream=None):
+    _check(_allgather(comm.h if comm is not None else None, plan.h, _ptr(ag_buf), _stream(stream)),
+           "kfac_allgather_precond")

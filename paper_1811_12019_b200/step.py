@@ -1,0 +1,99 @@
+"""One distributed K-FAC step (Algorithm 1 body, minus
+forward/backward and the update) driven through the C-ABI.
+
+Plumbing only: torch allocates the caller-owned buffers the C-ABI asks for
+(kfac_plan_query sizes) and supplies the stream; every stage runs in
+libkfac.so kernels / NCCL.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import kfac
+
+
+class KfacStep:
+    def __init__(self, layers, n_local, rank=0, world=1, policy=kfac.RR, comm=None, device=None):
+        self.layers = list(layers)
+        self.rank, self.world, self.n_local = int(rank), int(world), int(n_local)
+        self.comm = comm
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.plan = kfac.Plan(self.layers, world, n_local, policy)
+        q = self.plan.query()
+        self.q = q
+        self.rl = self.plan.rank_layers(rank)
+        dev = self.device
+        self.rs_send = torch.zeros(world * q["rs_chunk"], dtype=torch.float32, device=dev)
+        self.rs_recv = torch.zeros(q["rs_chunk"], dtype=torch.float32, device=dev)
+        self.ag_buf = torch.zeros(world * q["ag_chunk"], dtype=torch.float32, device=dev)
+        self.inv_ws = torch.zeros(max(self.rl["inv_floats"], 1), dtype=torch.float32, device=dev)
+        self.ws = torch.zeros(max(q["ws_bytes"], 16), dtype=torch.uint8, device=dev)
+        n_owned = len(self.rl["layers"])
+        self.dev_status = torch.zeros(max(2 * n_owned, 1), dtype=torch.int32, device=dev)
+        self.pi = torch.zeros(max(n_owned, 1), dtype=torch.float32, device=dev)
+
+    # ---- views (zero-copy: the caller's dW lives in the send buffer)
+    def dims(self, l):
+        L = self.layers[l]
+        return L["c_in"] * L["kh"] * L["kw"] + (1 if L["has_bias"] else 0), L["c_out"]
+
+    def dw_view(self, l):
+        da, dg = self.dims(l)
+        o = self.q["seg_off"][l][0]
+        return self.rs_send[o:o + dg * da].view(dg, da)
+
+    def set_dw(self, dws):
+        for l, d in enumerate(dws):
+            self.dw_view(l).copy_(d, non_blocking=True)
+
+    def send_factor_view(self, l, which):
+        da, dg = self.dims(l)
+        o = self.q["seg_off"][l][1 + which]
+        n = da if which == 0 else dg
+        return self.rs_send[o:o + n * (n + 1) // 2]
+
+    def recv_views(self, k):
+        """(dW, A packed, G packed) of the k-th owned layer in rs_recv."""
+        l = self.rl["layers"][k]
+        da, dg = self.dims(l)
+        o = self.rl["local_off"][k]
+        return (self.rs_recv[o[0]:o[0] + dg * da].view(dg, da), self.rs_recv[o[1]:o[1] + da * (da + 1) // 2],
+                self.rs_recv[o[2]:o[2] + dg * (dg + 1) // 2])
+
+    def inv_views(self, k):
+        l = self.rl["layers"][k]
+        da, dg = self.dims(l)
+        a, g = self.rl["inv_off"][k]
+        return self.inv_ws[a:a + da * da].view(da, da), self.inv_ws[g:g + dg * dg].view(dg, dg)
+
+    def result(self, l):
+        da, dg = self.dims(l)
+        o = self.q["ag_off"][l]
+        return self.ag_buf[o:o + dg * da].view(dg, da)
+
+    # ---- the six stages
+    def factors(self, xs, gys, alphaA=None, alphaG=None, stream=None):
+        kfac.factor_all(self.plan, xs, gys, self.rs_send, self.ws, alphaA, alphaG, stream)
+
+    def reduce_scatter(self, stream=None):
+        kfac.reduce_scatter_factors(self.comm, self.plan, self.rs_send, self.rs_recv, stream)
+
+    def inverse(self, gamma, stream=None):
+        kfac.damped_inverse(self.plan, self.rank, self.rs_recv, gamma, self.inv_ws, self.dev_status, self.pi,
+                            self.ws, stream)
+
+    def precondition(self, stream=None):
+        kfac.precondition(self.plan, self.rank, self.rs_recv, self.inv_ws, self.ag_buf, self.ws, stream)
+
+    def allgather(self, stream=None):
+        kfac.allgather_precond(self.comm, self.plan, self.ag_buf, stream)
+
+    def run(self, xs, gys, gamma, stream=None, events=None):
+        """Stages 1-6.  `events`: optional list of 6 torch.cuda.Event recorded after each stage."""
+        stages = (lambda: self.factors(xs, gys, stream=stream), lambda: self.reduce_scatter(stream),
+                  lambda: self.inverse(gamma, stream), lambda: self.precondition(stream),
+                  lambda: self.allgather(stream))
+        for i, f in enumerate(stages):
+            f()
+            if events is not None:
+                events[i].record(stream)

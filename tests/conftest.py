@@ -18,3 +18,12 @@ def orc():
     import oracle
     oracle.build()
     return oracle
+
+
+def build_lib():
+    """Build libkfac.so without importing the package (its import needs the library)."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("_kfac_build", os.path.join(ROOT, "paper_1811_12019_b200", "build.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod.build()

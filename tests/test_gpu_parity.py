@@ -1,0 +1,255 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the fp64 oracle on the
+same seeded inputs.
+
+Tolerances (BASELINE.json north_star): relative Frobenius error vs fp64
+  factors (half inputs, fp32 accumulate)      <= 2e-3
+  damped inverse (vs fp64 inverse of the same fp32 damped matrix) <= 1e-5
+  preconditioned gradient                     <= 2e-3
+Layouts / ownership are bit-exact (tests/test_abi.py).
+"""
+import numpy as np
+import pytest
+import torch
+
+from synth import inputs, shapes
+
+pytestmark = pytest.mark.gpu
+
+TOL_FACTOR, TOL_INV, TOL_PREC = 2e-3, 1e-5, 2e-3
+
+
+@pytest.fixture(scope="module")
+def K():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU test run without a GPU")
+    from conftest import build_lib
+    build_lib()
+    import paper_1811_12019_b200 as K
+    return K
+
+
+def relerr(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def unpack_f32(p, d):
+    M = np.zeros((d, d))
+    iu = np.triu_indices(d)
+    M[iu] = p
+    M = M + M.T - np.diag(np.diag(M))
+    return M
+
+
+def gpu_factor(K, layer, t, n, which, alpha):
+    d_a, d_g = shapes.dims(layer)
+    d = d_a if which == 0 else d_g
+    out = torch.full((d * (d + 1) // 2,), float("nan"), dtype=torch.float32, device="cuda")
+    wsb = K.factor_ws_bytes(layer, n, which)
+    ws = torch.empty(max(wsb, 16), dtype=torch.uint8, device="cuda")
+    f = K.factor_A if which == 0 else K.factor_G
+    f(layer, t.cuda(), n, alpha, out, ws)
+    torch.cuda.synchronize()
+    return out.cpu().double().numpy()
+
+
+GEOMS = {  # name: (layer, n) -- each exercises one staging path / edge case
+    "config1_im2col_c16_bias": (shapes.single_conv()[0], 32),
+    "im2col_c64_3x3": (shapes.conv("c", 64, 64, 3, 1, 1, 9), 3),
+    "im2col_c32_3x3_s2": (shapes.conv("c", 32, 48, 3, 2, 1, 11), 4),
+    "im2col_c128_1x1_s2": (shapes.conv("c", 128, 256, 1, 2, 0, 14), 2),
+    "tiled_1x1_multitile_splitk": (shapes.conv("c", 256, 64, 1, 1, 0, 28), 16),
+    "gather_stem_c3_7x7_s2": (shapes.conv("c", 3, 64, 7, 2, 3, 30), 2),
+    "fc_bias_c1000": (shapes.linear("fc", 1000, 1000), 8),
+    "fc_c10_gather": (shapes.linear("fc", 200, 10), 5),
+    "ragged_rows_d_not_128": (shapes.conv("c", 48, 40, 3, 1, 1, 5), 3),
+}
+
+
+@pytest.mark.parametrize("name", list(GEOMS))
+@pytest.mark.parametrize("dtype", ["bf16", "fp16"])
+def test_factor_parity(K, orc, name, dtype):
+    layer, n = GEOMS[name]
+    x = inputs.layer_x(layer, 0, n, dtype=dtype, stem=layer["c_in"] == 3)
+    gy = inputs.layer_gy(layer, 0, n, dtype=dtype)
+    rows = shapes.rows(layer, n)
+    d_a, d_g = shapes.dims(layer)
+    A = orc.factor_A(layer, inputs.half_bits(x), n, fmt=dtype)
+    G = orc.factor_G(inputs.half_bits(gy), rows, d_g, fmt=dtype)
+    pa = gpu_factor(K, layer, x, n, 0, 1.0 / rows)
+    pg = gpu_factor(K, layer, gy, n, 1, 1.0 / rows)
+    assert np.all(np.isfinite(pa)) and np.all(np.isfinite(pg))
+    ea = relerr(unpack_f32(pa, d_a), A)
+    eg = relerr(unpack_f32(pg, d_g), G)
+    print(f"{name} {dtype}: A err {ea:.2e}  G err {eg:.2e}")
+    assert ea <= TOL_FACTOR and eg <= TOL_FACTOR
+    assert ea <= 1e-5 and eg <= 1e-5  # fp32 accumulation of exact half products
+
+
+def test_factor_gather_matches_tma(K, monkeypatch):
+    """The generic gather producer and the TMA im2col producer give the same bits."""
+    layer, n = GEOMS["im2col_c64_3x3"]
+    x = inputs.layer_x(layer, 0, n)
+    rows = shapes.rows(layer, n)
+    a = gpu_factor(K, layer, x, n, 0, 1.0 / rows)
+    monkeypatch.setenv("KFAC_FORCE_GATHER", "1")
+    b = gpu_factor(K, layer, x, n, 0, 1.0 / rows)
+    assert np.array_equal(a, b)
+
+
+def test_factor_deterministic(K):
+    layer, n = GEOMS["tiled_1x1_multitile_splitk"]
+    x = inputs.layer_x(layer, 0, n)
+    rows = shapes.rows(layer, n)
+    a = gpu_factor(K, layer, x, n, 0, 1.0 / rows)
+    b = gpu_factor(K, layer, x, n, 0, 1.0 / rows)
+    assert np.array_equal(a, b)
+
+
+# --------------------------------------------------------------- full step
+def _run_step(K, layers, n, gamma, world=1, rank=0, policy=0, dws=None, seed=1811):
+    st = K.KfacStep(layers, n, rank=rank, world=world, policy=policy)
+    xs = [inputs.layer_x(l, i, n, rank, seed).cuda() for i, l in enumerate(layers)]
+    gys = [inputs.layer_gy(l, i, n, rank, seed).cuda() for i, l in enumerate(layers)]
+    if dws is None:
+        dws = [inputs.layer_dw(l, i, rank, seed) for i, l in enumerate(layers)]
+    st.set_dw([d.cuda() for d in dws])
+    st.run(xs, gys, gamma)
+    torch.cuda.synchronize()
+    return st, xs, gys, dws
+
+
+@pytest.mark.parametrize("gamma", [2.5e-2, 2.5e-4])
+def test_step_config1_end_to_end(K, orc, gamma):
+    layers, n = shapes.config("single_conv")
+    st, xs, gys, dws = _run_step(K, layers, n, gamma)
+    rin = [([inputs.half_bits(x.cpu()) for x in xs], [inputs.half_bits(g.cpu()) for g in gys],
+            [d.numpy() for d in dws], n)]
+    ref = orc.kfac_step(layers, rin, 1, gamma)
+    res = ref["results"][0][0]
+    # stage-wise: RS result (world 1 = copy of the send buffer)
+    dW, pa, pg = st.recv_views(0)
+    d_a, d_g = shapes.dims(layers[0])
+    assert relerr(unpack_f32(pa.cpu().double().numpy(), d_a), res["A"]) <= TOL_FACTOR
+    assert relerr(unpack_f32(pg.cpu().double().numpy(), d_g), res["G"]) <= TOL_FACTOR
+    assert np.array_equal(dW.cpu().numpy(), dws[0].numpy())
+    assert st.dev_status.cpu().tolist() == [0, 0]
+    assert abs(st.pi[0].item() - res["pi"]) <= 1e-6 * res["pi"]
+    # inverse vs fp64 inverse of the SAME fp32 damped matrix the GPU saw
+    Ai, Gi = st.inv_views(0)
+    A32 = unpack_f32(pa.cpu().double().numpy(), d_a)
+    G32 = unpack_f32(pg.cpu().double().numpy(), d_g)
+    Ad, Gd, _ = orc.damp(A32, G32, gamma)
+    ea = relerr(Ai.cpu().double().numpy(), orc.inverse(Ad)[0])
+    eg = relerr(Gi.cpu().double().numpy(), orc.inverse(Gd)[0])
+    print(f"inverse err A {ea:.2e} G {eg:.2e}")
+    assert ea <= TOL_INV and eg <= TOL_INV
+    # precondition vs oracle on the same fp32 inverses
+    pre_ref = orc.precondition(Gi.cpu().double().numpy(), Ai.cpu().double().numpy(), dW.cpu().double().numpy())
+    ep = relerr(st.result(0).cpu().double().numpy(), pre_ref)
+    assert ep <= TOL_PREC and ep <= 1e-5
+    # end to end vs the all-fp64 oracle from the same half inputs
+    e2e = relerr(st.result(0).cpu().double().numpy(), res["precond"])
+    print(f"precond err {ep:.2e} e2e {e2e:.2e}")
+    assert e2e <= TOL_PREC
+
+
+def test_step_multilayer_end_to_end(K, orc):
+    """A small multi-layer network touching every staging path, world 1."""
+    layers = [shapes.conv("stem", 3, 16, 7, 2, 3, 20), shapes.conv("a", 16, 32, 3, 1, 1, 10, bias=1),
+              shapes.conv("b", 32, 64, 1, 2, 0, 10), shapes.conv("c", 64, 64, 3, 1, 1, 5),
+              shapes.linear("fc", 64, 10)]
+    n, gamma = 4, 2.5e-2
+    st, xs, gys, dws = _run_step(K, layers, n, gamma)
+    rin = [([inputs.half_bits(x.cpu()) for x in xs], [inputs.half_bits(g.cpu()) for g in gys],
+            [d.numpy() for d in dws], n)]
+    ref = orc.kfac_step(layers, rin, 1, gamma)
+    assert st.dev_status.cpu().abs().sum().item() == 0
+    for l in range(len(layers)):
+        e = relerr(st.result(l).cpu().double().numpy(), ref["results"][0][l]["precond"])
+        print(f"layer {l}: e2e {e:.2e}")
+        assert e <= TOL_PREC
+
+
+def test_inverse_reports_not_pd(K, orc):
+    layers = [shapes.linear("fc", 7, 5, bias=0)]
+    st = K.KfacStep(layers, 1)
+    dW, pa, pg = None, None, None
+    # hand-made recv: A = -I (not PD after damping 0.1*pi), G = I
+    d_a, d_g = 7, 5
+    A = np.eye(d_a)
+    A[0, 0], A[1, 1] = 5.0, -1.0  # positive trace (pi real), not PD at pivot 1
+    G = np.eye(d_g)
+    _, pa, pg = st.recv_views(0)
+    pa.copy_(torch.as_tensor(orc.pack(A), dtype=torch.float32))
+    pg.copy_(torch.as_tensor(orc.pack(G), dtype=torch.float32))
+    st.inverse(1e-2)
+    torch.cuda.synchronize()
+    _, want = orc.inverse(orc.damp(A, G, 1e-2)[0])
+    assert st.dev_status.cpu().tolist() == [want, 0]
+    assert want == 2
+
+
+@pytest.mark.parametrize("n", [64, 65, 130, 300])
+def test_inverse_ill_conditioned(K, orc, n):
+    """Rank-deficient ReLU-like factors at small damping (kappa ~ 1e4): fp64 sweep meets 1e-5."""
+    rng = np.random.default_rng(n)
+    X = np.maximum(rng.standard_normal((n // 3, n)), 0)
+    A = (X.T @ X / X.shape[0]).astype(np.float32).astype(np.float64)
+    G = np.eye(4)
+    layers = [shapes.linear("fc", n, 4, bias=0)]
+    st = K.KfacStep(layers, 1)
+    _, pa, pg = st.recv_views(0)
+    pa.copy_(torch.as_tensor(orc.pack(A), dtype=torch.float32))
+    pg.copy_(torch.as_tensor(orc.pack(G), dtype=torch.float32))
+    st.inverse(2.5e-4)
+    torch.cuda.synchronize()
+    Ad, _, _ = orc.damp(A, G, 2.5e-4)
+    ref, s = orc.inverse(Ad)
+    Ai, _ = st.inv_views(0)
+    e = relerr(Ai.cpu().double().numpy(), ref)
+    print(f"n={n} cond={np.linalg.cond(Ad):.1e} err={e:.2e}")
+    assert s == 0 and st.dev_status.cpu().tolist() == [0, 0]
+    assert e <= TOL_INV
+
+
+# --------------------------------------------------------------- full-size, sampled
+@pytest.mark.parametrize("cfg", ["resnet50"])
+def test_fullsize_factors_sampled(K, orc, cfg):
+    """BASELINE config 3 at full size, in the bench's launch configuration (kfac_factor_all):
+    sampled packed entries vs the oracle's entries, one by one."""
+    layers, n = shapes.config(cfg)
+    st = K.KfacStep(layers, n)
+    xs = [inputs.layer_x(l, i, n) for i, l in enumerate(layers)]
+    gys = [inputs.layer_gy(l, i, n) for i, l in enumerate(layers)]
+    st.factors([x.cuda() for x in xs], [g.cuda() for g in gys])
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(0)
+    worst = 0.0
+    for l, layer in enumerate(layers):
+        d_a, d_g = shapes.dims(layer)
+        rows = shapes.rows(layer, n)
+        for which, d in ((0, d_a), (1, d_g)):
+            m = 24
+            ij = np.stack([rng.integers(0, d, m), rng.integers(0, d, m)], 1)
+            ij[:4] = [[0, 0], [d - 1, d - 1], [0, d - 1], [d // 2, d // 2]]
+            ij = np.sort(ij, 1)
+            got = st.send_factor_view(l, which).cpu().double().numpy()
+            g = got[ij[:, 0] * d - ij[:, 0] * (ij[:, 0] - 1) // 2 + (ij[:, 1] - ij[:, 0])]
+            if which == 0:
+                ref = orc.factor_A_entries(layer, inputs.half_bits(xs[l]), n, ij)
+                scale = np.sqrt(np.abs(orc.factor_A_entries(layer, inputs.half_bits(xs[l]), n,
+                                                            np.stack([ij[:, 0], ij[:, 0]], 1)) *
+                                       orc.factor_A_entries(layer, inputs.half_bits(xs[l]), n,
+                                                            np.stack([ij[:, 1], ij[:, 1]], 1))))
+            else:
+                ref = orc.factor_G_entries(inputs.half_bits(gys[l]), rows, d, ij)
+                scale = np.sqrt(np.abs(orc.factor_G_entries(inputs.half_bits(gys[l]), rows, d,
+                                                            np.stack([ij[:, 0], ij[:, 0]], 1)) *
+                                       orc.factor_G_entries(inputs.half_bits(gys[l]), rows, d,
+                                                            np.stack([ij[:, 1], ij[:, 1]], 1))))
+            # entry error relative to sqrt(A_ii A_jj) (Cauchy-Schwarz scale of the entry)
+            err = np.max(np.abs(g - ref) / np.maximum(scale, 1e-30))
+            worst = max(worst, err)
+            assert err <= 1e-5, (layer["name"], which, err)
+    print(f"{cfg}: worst sampled entry error {worst:.2e}")
