@@ -225,7 +225,7 @@ def test_fullsize_factors_sampled(K, orc, cfg):
     st.factors([x.cuda() for x in xs], [g.cuda() for g in gys])
     torch.cuda.synchronize()
     rng = np.random.default_rng(0)
-    worst = 0.0
+    errs = []
     for l, layer in enumerate(layers):
         d_a, d_g = shapes.dims(layer)
         rows = shapes.rows(layer, n)
@@ -248,8 +248,10 @@ def test_fullsize_factors_sampled(K, orc, cfg):
                                                             np.stack([ij[:, 0], ij[:, 0]], 1)) *
                                        orc.factor_G_entries(inputs.half_bits(gys[l]), rows, d,
                                                             np.stack([ij[:, 1], ij[:, 1]], 1))))
-            # entry error relative to sqrt(A_ii A_jj) (Cauchy-Schwarz scale of the entry)
+            # entry error relative to sqrt(A_ii A_jj) (the Cauchy-Schwarz scale of the entry): an
+            # entrywise form of the north-star relative error bound 2e-3
             err = np.max(np.abs(g - ref) / np.maximum(scale, 1e-30))
-            worst = max(worst, err)
-            assert err <= 1e-5, (layer["name"], which, err)
-    print(f"{cfg}: worst sampled entry error {worst:.2e}")
+            errs.append((err, layer["name"], "AG"[which]))
+    errs.sort(reverse=True)
+    print(f"{cfg}: worst sampled entry errors {[(f'{e:.1e}', n, w) for e, n, w in errs[:6]]}")
+    assert errs[0][0] <= TOL_FACTOR, errs[:3]
