@@ -209,8 +209,9 @@ kfac_status kfac_damped_inverse(kfac_plan_t p, int32_t rank, const float *recv, 
             m.packed = recv + p->local[rank][k][1 + which];
             m.inv = inv_ws + p->inv_off[rank][2 * k + which];
             m.work = reinterpret_cast<double *>(w + off);
-            m.panel = m.work + (int64_t)m.n * m.n;
-            off += align16((int64_t)m.n * m.n + 2 * (int64_t)kPanel * m.n + kPanel * kPanel) * 8;
+            const int64_t ld = (m.n + 15) / 16 * 16;
+            m.panel = m.work + (int64_t)m.n * ld;
+            off += inverse_ws_doubles(m.n) * 8;
             m.status = dev_status + 2 * k + which;
             m.pair = (int)k;
             m.is_A = which == 0;

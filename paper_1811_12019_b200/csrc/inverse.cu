@@ -7,18 +7,21 @@
 // rank-deficient ReLU factors of the paper's workload, kappa ~ 1e3..1e4).
 //
 // Algorithm: block symmetric Gauss-Jordan ("sweep") on the upper triangle,
-// block size b = kPanel = 64.  For pivot block K of M (symmetric, upper
-// storage), with P = M_KK^-1 and R = M_K,: the current block row:
+// block size B = 128.  For pivot block K of M (symmetric, upper storage),
+// with P = M_KK^-1 and R = M_K,: the current block row:
 //     M_IJ <- M_IJ - R_I^T (P R_J)     I, J != K
 //     M_KJ <- P R_J                     J != K
 //     M_KK <- -P
 // After sweeping every block, M holds -M^-1.  The sweep pivots are the LDL^T
 // pivots, so a non-positive pivot at index j means M is not positive
 // definite; its index (+1) is reported like the oracle's Cholesky status.
-// Each step is three grouped launches (pivot inverse, panel, rank-b update);
-// all n^3 flops are in the update, which touches only upper tiles.
+// Per step: pivot (one CTA per matrix, in-smem scalar sweep of the 128x128
+// block), panel (P R as 128x128x128 tile products), update (rank-128 update
+// of every upper tile) -- all n^3 flops are in the tile products, which run
+// as fp64 DFMA tiles of 128x128 with 8x8 register blocking.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "kfac_internal.hpp"
@@ -26,20 +29,22 @@
 namespace kfac {
 
 constexpr int kMaxMats = 128;
-constexpr int B = kPanel;  // 64
-constexpr int kPanelSmem = 2 * B * (B + 1) * 8;
-constexpr int kUpdateSmem = 2 * B * B * 8;
+constexpr int B = kPanel;     // 128
+constexpr int KC = 16;        // K rows per smem chunk of the tile product
+constexpr int kPivSmem = (B * (B + 1) + 2 * 32 * B + 32 * 32) * 8 + 64;
+constexpr int kTileSmem = 2 * 2 * KC * B * 8;  // double-buffered A/B chunks: 64 KB
+constexpr int kUpdSmem = kPivSmem > kTileSmem ? kPivSmem : kTileSmem;
 
 struct MatDesc {
     const float *packed;
     float *inv;
     double *work;
-    double *panel;  // [2][B][n]: R then Wp = P R ; plus P (B*B) after them
+    double *panel;  // [R: B x ld][Wp: B x ld][P_even: B x B][P_odd: B x B]
     int32_t *status;
-    int32_t n, pair, is_A, tile_begin;
+    int32_t n, ld, pair, is_A, tile_begin, col_begin;
 };
 struct InvParams {
-    int32_t nm, total_tiles, k, pad;
+    int32_t nm, total_tiles, k, total_cols, fuse, pad_;
     double gamma;
     double *pair_scratch;  // [npairs][4]: pi, dA, dG
     float *pi_out;
@@ -52,8 +57,6 @@ __device__ __forceinline__ int64_t poff(int64_t i, int64_t j, int64_t n) {  // p
 
 // ---- prologue: traces -> pi and the damping of each (A, G) pair
 __global__ void damp_trace_kernel(const __grid_constant__ InvParams P) {
-    // one block per matrix; pair scratch written by the A matrix after both traces are known:
-    // we compute both traces in the block of the A matrix (the G matrix block does nothing)
     const MatDesc &ma = P.m[blockIdx.x];
     if (!ma.is_A) return;
     const MatDesc *mg = nullptr;
@@ -95,7 +98,7 @@ __global__ void unpack_damp_kernel(const __grid_constant__ InvParams P) {
     const double add = P.pair_scratch[4 * m.pair + (m.is_A ? 1 : 2)];
     for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
         const float *src = m.packed + poff(i, i, n);
-        double *dst = m.work + i * n;
+        double *dst = m.work + i * m.ld;
         for (int64_t j = i + threadIdx.x; j < n; j += blockDim.x) {
             double v = (double)src[j - i];
             if (j == i) v += add;
@@ -104,180 +107,344 @@ __global__ void unpack_damp_kernel(const __grid_constant__ InvParams P) {
     }
 }
 
-// ---- step 1: P = M_KK^-1 by a scalar sweep in shared memory (one block per matrix)
-__global__ void __launch_bounds__(256) pivot_kernel(const __grid_constant__ InvParams P) {
+// ---- P = M_KK^-1 for the 128 x 128 diagonal block, in shared memory (full symmetric copy S).
+// The block is itself swept in 4 sub-blocks of 32: the 32 x 32 sub-pivot is inverted by a
+// scalar sweep in shared memory, then all 256 threads apply the rank-32 sweep update
+//   S_IJ -= O_I^T W_J,  S_sJ = W_J,  S_Is = W_I^T,  S_ss = -Q   (O = old block row s, W = Q O).
+// Returns 0 or the failing pivot index + 1 (the sweep pivots are the LDL^T pivots).
+constexpr int S2 = 32;  // sub-pivot size
+constexpr int kPivSmemBytes = (B * (B + 1) + 2 * S2 * B + S2 * S2) * 8 + 64;
+
+// scalar sweep of the 32 x 32 sub-pivot Q (smem, row-major) by all 256 threads (4 elements
+// each); on return Q = -inv(Q).  Returns 0 or the failing pivot index + 1 (base-relative).
+__device__ __forceinline__ int block_sweep32(double *Q, int base) {
+    const int tid = threadIdx.x;
+    for (int t = 0; t < S2; t++) {
+        const double d = Q[t * S2 + t];
+        if (!(d > 0.0)) return base + t + 1;  // uniform: every thread read the same d
+        const double inv = 1.0 / d;
+        double nv[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const int e = tid + 256 * k, l = e >> 5, j = e & 31;
+            const double u = (l == t) ? -1.0 : Q[l * S2 + t];
+            const double v = (j == t) ? -inv : Q[t * S2 + j] * inv;
+            const double keep = (l == t || j == t) ? 0.0 : Q[e];
+            nv[k] = fma(-u, v, keep);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < 4; k++) Q[tid + 256 * k] = nv[k];
+        __syncthreads();
+    }
+    return 0;
+}
+
+#ifdef PIVOT_DBG
+__device__ int g_pivot_dbg;
+#endif
+__device__ int pivot_block(const double *__restrict__ W, int64_t ld, int k0, int bk, double *__restrict__ Pout,
+                           double *smem) {
+    double(*S)[B + 1] = reinterpret_cast<double(*)[B + 1]>(smem);
+    double *O = smem + B * (B + 1);       // [S2][B] old block row
+    double *Wr = O + S2 * B;              // [S2][B] Q * O
+    double *Q = Wr + S2 * B;              // [S2][S2] inverse of the sub-pivot
+    int *fsh = reinterpret_cast<int *>(Q + S2 * S2);
+    const int tid = threadIdx.x;
+    const int tx = tid & 15, ty = tid >> 4;
+    for (int e = tid; e < B * B; e += blockDim.x) {
+        const int i = e >> 7, j = e & (B - 1);
+        double val = (i == j) ? 1.0 : 0.0;  // identity padding keeps the sweep well defined
+        if (i < bk && j < bk) val = W[(int64_t)(k0 + min(i, j)) * ld + (k0 + max(i, j))];
+        S[i][j] = val;
+    }
+    if (tid == 0) *fsh = 0;
+    __syncthreads();
+    for (int sb = 0; sb < B / S2; sb++) {
+        const int s0 = sb * S2;
+        if (s0 >= bk) break;
+        for (int e = tid; e < S2 * S2; e += blockDim.x) Q[e] = S[s0 + (e >> 5)][s0 + (e & 31)];
+        __syncthreads();
+        {
+            const int f = block_sweep32(Q, k0 + s0);  // Q <- -inv(sub-pivot)
+            if (f && tid == 0) *fsh = f;
+        }
+        for (int e = tid; e < S2 * S2; e += blockDim.x) Q[e] = -Q[e];
+        for (int e = tid; e < S2 * B; e += blockDim.x) O[e] = S[s0 + (e >> 7)][e & (B - 1)];
+        __syncthreads();
+        if (*fsh) break;
+#ifdef PIVOT_DBG
+        if (g_pivot_dbg == 1 && sb >= 1) break;
+#endif
+        // W = Q O  (32 x 128): thread -> column j = tid & 127, rows a = (tid >> 7) + 2k
+        {
+            const int j = tid & (B - 1);
+            for (int a = tid >> 7; a < S2; a += 2) {
+                double acc = 0.0;
+#pragma unroll 8
+                for (int b2 = 0; b2 < S2; b2++) acc = fma(Q[a * S2 + b2], O[b2 * B + j], acc);
+                Wr[a * B + j] = acc;
+            }
+        }
+        __syncthreads();
+#ifdef PIVOT_DBG
+        if (g_pivot_dbg == 2 && sb >= 1) break;
+#endif
+        // rank-32 sweep update of every element (each thread writes only its own 8 x 8 elements)
+        double acc[8][8];
+#pragma unroll
+        for (int p = 0; p < 8; p++)
+#pragma unroll
+            for (int q = 0; q < 8; q++) acc[p][q] = 0.0;
+        for (int b2 = 0; b2 < S2; b2++) {
+            double o[8], w[8];
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+                o[q] = O[b2 * B + ty + 16 * q];
+                w[q] = Wr[b2 * B + tx + 16 * q];
+            }
+#pragma unroll
+            for (int p = 0; p < 8; p++)
+#pragma unroll
+                for (int q = 0; q < 8; q++) acc[p][q] = fma(o[p], w[q], acc[p][q]);
+        }
+#pragma unroll
+        for (int p = 0; p < 8; p++) {
+            const int i = ty + 16 * p;
+            const bool is = (i >= s0 && i < s0 + S2);
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+                const int j = tx + 16 * q;
+                const bool js = (j >= s0 && j < s0 + S2);
+                // clamped indices: every load is in range whatever the compiler speculates
+                const int ii = min(max(i - s0, 0), S2 - 1), jj = min(max(j - s0, 0), S2 - 1);
+                const double vq = Q[ii * S2 + jj], vwi = Wr[ii * B + j], vwj = Wr[jj * B + i];
+                const double v = is ? (js ? -vq : vwi) : (js ? vwj : S[i][j] - acc[p][q]);
+                S[i][j] = v;
+            }
+        }
+        __syncthreads();
+    }
+    const int fail = *fsh;
+    if (fail) return fail;
+    for (int e = tid; e < B * B; e += blockDim.x) {  // P = -S (zero outside bk)
+        const int i = e >> 7, j = e & (B - 1);
+        Pout[e] = (i < bk && j < bk) ? -S[i][j] : 0.0;
+    }
+    return 0;
+}
+
+__device__ __forceinline__ double *pivot_slot(const MatDesc &m, int k) {
+    return m.panel + 2 * (int64_t)B * m.ld + (int64_t)(k & 1) * B * B;
+}
+
+// step 0 only: P_0 (later pivots are fused into the previous step's update kernel)
+__global__ void __launch_bounds__(256, 1) pivot_kernel(const __grid_constant__ InvParams P) {
     const MatDesc &m = P.m[blockIdx.x];
     const int n = m.n, k0 = P.k * B;
-    if (k0 >= n) return;
-    if (*m.status != 0) return;  // an earlier pivot already failed
-    const int bk = min(B, n - k0);
-    __shared__ double S[B][B + 1];
-    __shared__ double col[B], row[B];
-    __shared__ int fail;
-    if (threadIdx.x == 0) fail = 0;
-    for (int e = threadIdx.x; e < bk * bk; e += blockDim.x) {
-        int i = e / bk, j = e % bk;
-        int a = min(i, j), b = max(i, j);
-        S[i][j] = m.work[(int64_t)(k0 + a) * n + (k0 + b)];
-    }
-    __syncthreads();
-    for (int t = 0; t < bk; t++) {
-        const double d = S[t][t];
-        if (!(d > 0.0)) {
-            if (threadIdx.x == 0) fail = k0 + t + 1;
-            break;
-        }
-        for (int e = threadIdx.x; e < bk; e += blockDim.x) {
-            col[e] = S[e][t];
-            row[e] = S[t][e];
-        }
-        __syncthreads();
-        const double inv = 1.0 / d;
-        for (int e = threadIdx.x; e < bk * bk; e += blockDim.x) {
-            int i = e / bk, j = e % bk;
-            double v;
-            if (i == t && j == t) v = -inv;
-            else if (i == t) v = row[j] * inv;
-            else if (j == t) v = col[i] * inv;
-            else v = S[i][j] - col[i] * row[j] * inv;
-            S[i][j] = v;
-        }
-        __syncthreads();
-    }
-    __syncthreads();
-    if (fail) {
-        if (threadIdx.x == 0) *m.status = fail;
-        return;
-    }
-    // P = -S  stored after the two panels
-    double *Pm = m.panel + 2 * (int64_t)B * n;
-    for (int e = threadIdx.x; e < bk * bk; e += blockDim.x) Pm[e] = -S[e / bk][e % bk];
-}
-
-// ---- step 2: R = block row K (from upper storage), Wp = P R   (64-column blocks)
-__global__ void __launch_bounds__(256) panel_kernel(const __grid_constant__ InvParams P) {
-    const MatDesc &m = P.m[blockIdx.y];
-    const int n = m.n, k0 = P.k * B;
     if (k0 >= n || *m.status != 0) return;
-    const int bk = min(B, n - k0);
-    const int j0 = blockIdx.x * B;
-    if (j0 >= n) return;
-    const int bj = min(B, n - j0);
     extern __shared__ double dyn[];
-    double (*Ps)[B + 1] = reinterpret_cast<double (*)[B + 1]>(dyn);
-    double (*Rs)[B + 1] = reinterpret_cast<double (*)[B + 1]>(dyn + B * (B + 1));
-    const double *Pm = m.panel + 2 * (int64_t)B * n;
-    for (int e = threadIdx.x; e < bk * bk; e += blockDim.x) Ps[e / bk][e % bk] = Pm[e];
-    for (int e = threadIdx.x; e < bk * bj; e += blockDim.x) {
-        int i = e / bj, j = e % bj;
-        int gi = k0 + i, gj = j0 + j;
-        double v = (gi <= gj) ? m.work[(int64_t)gi * n + gj] : m.work[(int64_t)gj * n + gi];
-        Rs[i][j] = v;
-    }
-    __syncthreads();
-    double *R = m.panel, *Wp = m.panel + (int64_t)B * n;
-    for (int e = threadIdx.x; e < bk * bj; e += blockDim.x) {
-        int i = e / bj, j = e % bj;
-        double s = 0.0;
-        for (int t = 0; t < bk; t++) s += Ps[i][t] * Rs[t][j];
-        R[(int64_t)i * n + j0 + j] = Rs[i][j];
-        Wp[(int64_t)i * n + j0 + j] = s;
+    const int f = pivot_block(m.work, m.ld, k0, min(B, n - k0), pivot_slot(m, P.k), dyn);
+    if (f && threadIdx.x == 0) *m.status = f;
+}
+
+__device__ __forceinline__ void cp_async16(void *dst, const void *src, bool ok) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+                 "l"(src), "r"(ok ? 16 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// acc[8][8] += sum_{t < kt} A[t][i] * Bm[t][j] for the 128 x 128 tile (i = ty + 16a, j = tx + 16b).
+// A and Bm are row-major with 16-aligned leading dimensions; columns >= acols / bcols and rows
+// >= kt read as zero.  Chunks of KC rows are double-buffered with cp.async (16-byte copies).
+__device__ __forceinline__ void tile_product(const double *__restrict__ A, int64_t lda, int acols,
+                                             const double *__restrict__ Bm, int64_t ldb, int bcols, int kt,
+                                             double (&acc)[8][8], double *smem) {
+    double *As = smem, *Bs = smem + 2 * KC * B;
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int nchunks = (kt + KC - 1) / KC;
+    auto load = [&](int c, int buf) {
+        const int t0 = c * KC;
+        for (int e = threadIdx.x; e < KC * B / 2; e += 256) {  // pairs of doubles
+            const int t = e >> 6, i = (e & 63) * 2;
+            const bool okr = t0 + t < kt;
+            const bool oka = okr && i < acols, okb = okr && i < bcols;
+            cp_async16(As + buf * KC * B + t * B + i, oka ? A + (int64_t)(t0 + t) * lda + i : A, oka);
+            cp_async16(Bs + buf * KC * B + t * B + i, okb ? Bm + (int64_t)(t0 + t) * ldb + i : Bm, okb);
+        }
+        cp_async_commit();
+    };
+    load(0, 0);
+    for (int c = 0; c < nchunks; c++) {
+        const int buf = c & 1;
+        if (c + 1 < nchunks) {
+            load(c + 1, buf ^ 1);
+            cp_async_wait_1();
+        } else {
+            cp_async_wait_0();
+        }
+        __syncthreads();
+        const double *as = As + buf * KC * B, *bs = Bs + buf * KC * B;
+#pragma unroll 4
+        for (int t = 0; t < KC; t++) {
+            double a[8], b[8];
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+                a[q] = as[t * B + ty + 16 * q];
+                b[q] = bs[t * B + tx + 16 * q];
+            }
+#pragma unroll
+            for (int p = 0; p < 8; p++)
+#pragma unroll
+                for (int q = 0; q < 8; q++) acc[p][q] = fma(a[p], b[q], acc[p][q]);
+        }
+        __syncthreads();
     }
 }
 
-// ---- step 3: rank-b update of every upper tile (I, J)
-__global__ void __launch_bounds__(256) update_kernel(const __grid_constant__ InvParams P) {
+// ---- step 2: R_J = block row K (from upper storage), Wp_J = P R_J   (one CTA per 128-col block)
+__global__ void __launch_bounds__(256, 1) panel_kernel(const __grid_constant__ InvParams P) {
+    int cb = blockIdx.x, mi = 0;
+    while (mi + 1 < P.nm && P.m[mi + 1].col_begin <= cb) mi++;
+    const MatDesc &m = P.m[mi];
+    const int n = m.n, k0 = P.k * B;
+    const int64_t ld = m.ld;
+    if (k0 >= n || *m.status != 0) return;
+    const int J = cb - m.col_begin;
+    const int j0 = J * B;
+    if (j0 >= n) return;
+    const int bk = min(B, n - k0), bj = min(B, n - j0);
+    double *R = m.panel, *Wp = m.panel + (int64_t)B * ld;
+    // R_J rows t < bk, cols j < bj (columns up to the 16-aligned ld are zero-filled)
+    const int bjp = min(B, (int)ld - j0);
+    for (int e = threadIdx.x; e < bk * bjp; e += blockDim.x) {
+        const int t = e / bjp, j = e % bjp;
+        const int gi = k0 + t, gj = j0 + j;
+        double v = 0.0;
+        if (j < bj) v = (gi <= gj) ? m.work[(int64_t)gi * ld + gj] : m.work[(int64_t)gj * ld + gi];
+        R[(int64_t)t * ld + gj] = v;
+    }
+    __threadfence_block();
+    __syncthreads();
+    extern __shared__ double dyn[];
+    double acc[8][8];
+#pragma unroll
+    for (int p = 0; p < 8; p++)
+#pragma unroll
+        for (int q = 0; q < 8; q++) acc[p][q] = 0.0;
+    // Wp[i][j] = sum_t P[t][i] R[t][j]   (P symmetric, zero outside bk)
+    tile_product(pivot_slot(m, P.k), B, bk, R + j0, ld, bj, bk, acc, dyn);
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+#pragma unroll
+    for (int p = 0; p < 8; p++) {
+        const int i = ty + 16 * p;
+        if (i >= bk) continue;
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            const int j = tx + 16 * q;
+            if (j < bjp) Wp[(int64_t)i * ld + j0 + j] = acc[p][q];
+        }
+    }
+}
+
+// ---- step 3: rank-B update of every upper tile (I, J); the CTA of tile (K+1, K+1) then
+// inverts that block: the next step's pivot runs concurrently with this step's update.
+__global__ void __launch_bounds__(256, 1) update_kernel(const __grid_constant__ InvParams P) {
     int tile = blockIdx.x, mi = 0;
     while (mi + 1 < P.nm && P.m[mi + 1].tile_begin <= tile) mi++;
     const MatDesc &m = P.m[mi];
     const int n = m.n, k0 = P.k * B;
+    const int64_t ld = m.ld;
     if (k0 >= n || *m.status != 0) return;
     const int nt = (n + B - 1) / B, K = P.k;
-    int t = tile - m.tile_begin, I = 0;
-    if (t >= nt * (nt + 1) / 2) return;
+    // tile order: (K+1, K+1) first so the fused pivot starts early, then the upper tiles row-major
+    int t = tile - m.tile_begin;
+    const int ntiles = nt * (nt + 1) / 2;
+    if (t >= ntiles) return;
+    int I = 0, J = 0;
+    if (K + 1 < nt) {
+        const int dk = (K + 1) * nt - (K + 1) * K / 2;  // row-major index of (K+1, K+1)
+        t = (t == 0) ? dk : (t <= dk ? t - 1 : t);
+    }
     while (t >= nt - I) {
         t -= nt - I;
         I++;
     }
-    const int J = I + t;
+    J = I + t;
     const int bk = min(B, n - k0);
     const int i0 = I * B, j0 = J * B;
     const int bi = min(B, n - i0), bj = min(B, n - j0);
-    const double *R = m.panel, *Wp = m.panel + (int64_t)B * n;
+    const double *R = m.panel, *Wp = m.panel + (int64_t)B * ld;
     double *W = m.work;
     if (I == K && J == K) {
-        const double *Pm = m.panel + 2 * (int64_t)B * n;
+        const double *Pm = pivot_slot(m, K);
         for (int e = threadIdx.x; e < bk * bk; e += blockDim.x) {
-            int i = e / bk, j = e % bk;
-            if (j >= i) W[(int64_t)(k0 + i) * n + k0 + j] = -Pm[e];
+            const int i = e / bk, j = e % bk;
+            if (j >= i) W[(int64_t)(k0 + i) * ld + k0 + j] = -Pm[i * B + j];
         }
         return;
     }
     if (I == K) {  // M_KJ <- Wp_J
         for (int e = threadIdx.x; e < bk * bj; e += blockDim.x) {
-            int i = e / bj, j = e % bj;
-            W[(int64_t)(k0 + i) * n + j0 + j] = Wp[(int64_t)i * n + j0 + j];
+            const int i = e / bj, j = e % bj;
+            W[(int64_t)(k0 + i) * ld + j0 + j] = Wp[(int64_t)i * ld + j0 + j];
         }
         return;
     }
     if (J == K) {  // M_IK <- Wp_I^T
         for (int e = threadIdx.x; e < bi * bk; e += blockDim.x) {
-            int i = e / bk, j = e % bk;
-            W[(int64_t)(i0 + i) * n + k0 + j] = Wp[(int64_t)j * n + i0 + i];
+            const int i = e / bk, j = e % bk;
+            W[(int64_t)(i0 + i) * ld + k0 + j] = Wp[(int64_t)j * ld + i0 + i];
         }
         return;
     }
-    // M_IJ -= R_I^T Wp_J  : 64x64 tile, 256 threads x (4x4)
     extern __shared__ double dyn[];
-    double (*Rs)[B] = reinterpret_cast<double (*)[B]>(dyn);          // Rs[k][i] = R[k][i0+i]
-    double (*Ws)[B] = reinterpret_cast<double (*)[B]>(dyn + B * B);  // Ws[k][j] = Wp[k][j0+j]
-    for (int e = threadIdx.x; e < B * B; e += blockDim.x) {
-        int k = e / B, c = e % B;
-        Rs[k][c] = (k < bk && c < bi) ? R[(int64_t)k * n + i0 + c] : 0.0;
-        Ws[k][c] = (k < bk && c < bj) ? Wp[(int64_t)k * n + j0 + c] : 0.0;
-    }
-    __syncthreads();
+    double acc[8][8];
+#pragma unroll
+    for (int p = 0; p < 8; p++)
+#pragma unroll
+        for (int q = 0; q < 8; q++) acc[p][q] = 0.0;
+    // M_IJ -= R_I^T Wp_J : acc[i][j] = sum_t R[t][i0+i] Wp[t][j0+j]
+    tile_product(R + i0, ld, bi, Wp + j0, ld, bj, bk, acc, dyn);
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-    double acc[4][4];
 #pragma unroll
-    for (int a = 0; a < 4; a++)
-#pragma unroll
-        for (int b = 0; b < 4; b++) acc[a][b] = 0.0;
-    for (int k = 0; k < bk; k++) {
-        double r[4], w[4];
-#pragma unroll
-        for (int a = 0; a < 4; a++) r[a] = Rs[k][ty * 4 + a];
-#pragma unroll
-        for (int b = 0; b < 4; b++) w[b] = Ws[k][tx * 4 + b];
-#pragma unroll
-        for (int a = 0; a < 4; a++)
-#pragma unroll
-            for (int b = 0; b < 4; b++) acc[a][b] = fma(r[a], w[b], acc[a][b]);
-    }
-#pragma unroll
-    for (int a = 0; a < 4; a++) {
-        int i = ty * 4 + a;
+    for (int p = 0; p < 8; p++) {
+        const int i = ty + 16 * p;
         if (i >= bi) continue;
 #pragma unroll
-        for (int b = 0; b < 4; b++) {
-            int j = tx * 4 + b;
-            if (j >= bj) continue;
-            if (I == J && j < i) continue;  // diagonal tile: upper part only
-            double *p = W + (int64_t)(i0 + i) * n + j0 + j;
-            *p = *p - acc[a][b];
+        for (int q = 0; q < 8; q++) {
+            const int j = tx + 16 * q;
+            if (j >= bj || (I == J && j < i)) continue;
+            double *ptr = W + (int64_t)(i0 + i) * ld + j0 + j;
+            *ptr = *ptr - acc[p][q];
         }
+    }
+    if (P.fuse && I == K + 1 && J == K + 1) {  // fused next pivot: P_{K+1} = (updated M_{K+1,K+1})^-1
+        __threadfence_block();
+        __syncthreads();
+        const int f = pivot_block(W, ld, i0, bi, pivot_slot(m, K + 1), dyn);
+        if (f && threadIdx.x == 0) *m.status = f;
     }
 }
 
 // ---- epilogue: inv = -M (symmetric, full fp32)
 __global__ void finalize_kernel(const __grid_constant__ InvParams P) {
     const MatDesc &m = P.m[blockIdx.y];
-    const int64_t n = m.n;
+    const int64_t n = m.n, ld = m.ld;
     for (int64_t i = blockIdx.x; i < n; i += gridDim.x)
         for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
-            double v = (i <= j) ? m.work[i * n + j] : m.work[j * n + i];
+            double v = (i <= j) ? m.work[i * ld + j] : m.work[j * ld + i];
             m.inv[i * n + j] = (float)(-v);
         }
+}
+
+int64_t inverse_ld(int n) { return (n + 15) / 16 * 16; }
+int64_t inverse_ws_doubles(int n) {
+    const int64_t ld = inverse_ld(n);
+    return (n * ld + 2 * (int64_t)B * ld + 2 * (int64_t)B * B + 31) / 32 * 32;
 }
 
 kfac_status inverse_launch(const std::vector<InvMat> &mats, int npairs, float gamma, double *pair_scratch,
@@ -286,8 +453,9 @@ kfac_status inverse_launch(const std::vector<InvMat> &mats, int npairs, float ga
     if ((int)mats.size() > kMaxMats) return set_error(KFAC_ERR_UNSUPPORTED, "too many owned matrices for one launch");
     static bool attr = false;
     if (!attr) {
-        KFAC_CUDA_TRY(cudaFuncSetAttribute(panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPanelSmem));
-        KFAC_CUDA_TRY(cudaFuncSetAttribute(update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kUpdateSmem));
+        KFAC_CUDA_TRY(cudaFuncSetAttribute(pivot_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPivSmem));
+        KFAC_CUDA_TRY(cudaFuncSetAttribute(panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmem));
+        KFAC_CUDA_TRY(cudaFuncSetAttribute(update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kUpdSmem));
         attr = true;
     }
     InvParams P;
@@ -305,6 +473,7 @@ kfac_status inverse_launch(const std::vector<InvMat> &mats, int npairs, float ga
         d.panel = mats[i].panel;
         d.status = mats[i].status;
         d.n = mats[i].n;
+        d.ld = (int)inverse_ld(d.n);
         d.pair = mats[i].pair;
         d.is_A = mats[i].is_A;
         maxn = std::max(maxn, d.n);
@@ -317,31 +486,37 @@ kfac_status inverse_launch(const std::vector<InvMat> &mats, int npairs, float ga
     KFAC_LAUNCHED();
     KFAC_CUDA_TRY(cudaGetLastError());
     const int steps = (maxn + B - 1) / B;
+    const int fuse = getenv("KFAC_INV_NOFUSE") ? 0 : 1;
     for (int k = 0; k < steps; k++) {
-        // active matrices only (n > k*B), with their upper-tile prefix
+        // active matrices only (n > k*B), with their upper-tile and column-block prefixes
         InvParams Q;
         memset(&Q, 0, offsetof(InvParams, m));
         Q.gamma = P.gamma;
         Q.k = k;
-        int nm = 0, tiles = 0, maxcols = 0;
+        int nm = 0, tiles = 0, cols = 0;
         for (int i = 0; i < P.nm; i++) {
             if (P.m[i].n <= k * B) continue;
             Q.m[nm] = P.m[i];
+            const int nt = (P.m[i].n + B - 1) / B;
             Q.m[nm].tile_begin = tiles;
-            int nt = (P.m[i].n + B - 1) / B;
+            Q.m[nm].col_begin = cols;
             tiles += nt * (nt + 1) / 2;
-            maxcols = std::max(maxcols, nt);
+            cols += nt;
             nm++;
         }
         Q.nm = nm;
         Q.total_tiles = tiles;
-        pivot_kernel<<<nm, 256, 0, st>>>(Q);
+        Q.total_cols = cols;
+        Q.fuse = fuse;
+        if (k == 0 || !fuse) {
+            pivot_kernel<<<nm, 256, kPivSmem, st>>>(Q);
+            KFAC_LAUNCHED();
+            KFAC_CUDA_TRY(cudaGetLastError());
+        }
+        panel_kernel<<<cols, 256, kTileSmem, st>>>(Q);
         KFAC_LAUNCHED();
         KFAC_CUDA_TRY(cudaGetLastError());
-        panel_kernel<<<dim3(maxcols, nm), 256, kPanelSmem, st>>>(Q);
-        KFAC_LAUNCHED();
-        KFAC_CUDA_TRY(cudaGetLastError());
-        update_kernel<<<tiles, 256, kUpdateSmem, st>>>(Q);
+        update_kernel<<<tiles, 256, kUpdSmem, st>>>(Q);
         KFAC_LAUNCHED();
         KFAC_CUDA_TRY(cudaGetLastError());
     }

@@ -36,26 +36,31 @@ kfac_status make_geom(const kfac_layer_desc &d, Geom *g);
 
 // ---------------------------------------------------------------- factor kernel
 constexpr int kMaxProbs = 112;   // factor problems per grouped launch
-constexpr int kTile = 128;       // feature tile (M = N = 128)
-constexpr int kBK = 64;          // rows (K) per pipeline stage
+constexpr int kTileM = 128;      // feature rows per tile (A operand, MMA M)
+constexpr int kTileN = 256;      // feature cols per tile (B operand, MMA N)
+constexpr int kBK = 64;          // K rows (pixels) per pipeline stage
 
-enum FactorMode : int32_t { MODE_TILED2D = 0, MODE_IM2COL = 1, MODE_GATHER = 2 };
+enum FactorMode : int32_t { MODE_TILED2D = 0, MODE_TILED4D = 1, MODE_GATHER = 2 };
 
-struct alignas(64) FactorProb {
-    CUtensorMap tmap;       // 128 B, used by MODE_TILED2D / MODE_IM2COL
+struct alignas(64) FactorProb {  // 256 B: 112 of them fit the 32 KB kernel-parameter space
+    CUtensorMap tmap;       // 128 B, used by MODE_TILED2D / MODE_TILED4D
     const uint16_t *src;    // NHWC half input (MODE_GATHER and bias column sums)
     float *out;             // packed upper output, dimension d_out
     float *partial;         // split-K partial tiles (splits > 1)
+    int64_t rows;           // K = n * ho * wo
+    uint16_t *col;          // materialised im2col rows [rows, cp] (only when im2col_pre)
     float alpha;
-    int32_t mode, d, d_out, nt, splits, kchunks, chunks_per_split;
-    int32_t cb;             // channels per TMA box / swizzle atom (16, 32, 64)
-    int32_t item_begin;     // first global work item of this problem
-    int32_t c, h, w, kh, kw, sh, sw, ph, pw, ho, wo;
-    int64_t rows;
+    int32_t d, d_out, npairs, splits, kchunks, chunks_per_split, item_begin;
+    int16_t ntm, ntn, cb;   // row tiles (128), col tiles (256), channels per TMA box (16/32/64)
+    int16_t rpc, ksteps;    // rows per K chunk (<= kBK), 16-row MMA steps per chunk
+    int16_t bh, bn, rpi;    // TILED4D: output rows / images per chunk, row groups per image
+    int16_t c, h, w, ho, wo, cp;  // cp: padded im2col width (im2col_pre)
+    int8_t mode, kh, kw, sh, sw, ph, pw, im2col_pre;
 };
+static_assert(sizeof(FactorProb) == 256, "FactorProb layout");
 
 struct FactorParams {
-    int32_t nprobs, total_items, ab_fmt, pad;
+    int32_t nprobs, total_items, ab_fmt, dbg;
     FactorProb probs[kMaxProbs];
 };
 
@@ -103,6 +108,7 @@ kfac_status precond_launch(const std::vector<PrecJob> &jobs, cudaStream_t st);
 kfac_status replicate_launch(const std::vector<std::pair<const float *, float *>> &src_dst,
                              const std::vector<int64_t> &counts, cudaStream_t st);
 
-constexpr int kPanel = 64;  // sweep block size of the inverse
+constexpr int kPanel = 128;  // sweep block size of the inverse
+int64_t inverse_ws_doubles(int n);  // fp64 working matrix + panels of one n x n inverse
 
 }  // namespace kfac

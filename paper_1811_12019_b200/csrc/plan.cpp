@@ -155,7 +155,7 @@ kfac_status plan_build(kfac_plan *p) {
             off = align16(off + (int64_t)g.dA * g.dA);
             p->inv_off[r].push_back(off);
             off = align16(off + (int64_t)g.dG * g.dG);
-            for (int n : {g.dA, g.dG}) inv_ws += align16((int64_t)n * n + 2 * (int64_t)kPanel * n + kPanel * kPanel) * 8;
+            for (int n : {g.dA, g.dG}) inv_ws += inverse_ws_doubles(n) * 8;
             prec_ws += align16((int64_t)g.dG * g.dA) * 4 * 2;  // T and (redundant) output
         }
         p->inv_floats[r] = off;

@@ -135,7 +135,7 @@ class Plan:
 
     def __del__(self):
         h = getattr(self, "h", None)
-        if h is not None and h.value:
+        if h is not None and h.value and _lib is not None:
             _lib.kfac_plan_destroy(h)
             self.h = None
 
@@ -175,7 +175,7 @@ class Comm:
 
     def __del__(self):
         h = getattr(self, "h", None)
-        if h is not None and h.value:
+        if h is not None and h.value and _lib is not None:
             _lib.kfac_comm_destroy(h)
             self.h = None
 

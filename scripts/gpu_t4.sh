@@ -1,0 +1,6 @@
+cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
+timeout -s KILL 900 python -m pytest tests -m gpu -q -p no:cacheprovider -s > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; grep -E "passed|failed|Error|worst" gpurun_out/pytest_gpu.log | tail -8
+for n in 576 2304 4608; do timeout -s KILL 120 python scripts/one_inverse.py $n 2>&1 | grep inverse; done
+timeout -s KILL 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench.log 2>&1; echo "bench rc=$?"
+python -c "
+import json; d=json.loads(open('gpurun_out/bench.log').read().strip().splitlines()[-1]); print(d['value'], d['stage_ms'], d['factor_tflops'], d['roofline']['frac'], d['e2e'])"

@@ -86,15 +86,20 @@ def test_factor_parity(K, orc, name, dtype):
     assert ea <= 1e-5 and eg <= 1e-5  # fp32 accumulation of exact half products
 
 
-def test_factor_gather_matches_tma(K, monkeypatch):
-    """The generic gather producer and the TMA im2col producer give the same bits."""
-    layer, n = GEOMS["im2col_c64_3x3"]
+@pytest.mark.parametrize("name", ["im2col_c64_3x3", "im2col_c32_3x3_s2", "tiled_1x1_multitile_splitk"])
+def test_factor_gather_matches_tma(K, orc, monkeypatch, name):
+    """The generic gather producer and the TMA producers agree (their K chunking differs, so the
+    fp32 accumulation order differs: agreement to accumulation rounding, and both match the oracle)."""
+    layer, n = GEOMS[name]
     x = inputs.layer_x(layer, 0, n)
     rows = shapes.rows(layer, n)
+    d_a, _ = shapes.dims(layer)
     a = gpu_factor(K, layer, x, n, 0, 1.0 / rows)
     monkeypatch.setenv("KFAC_FORCE_GATHER", "1")
     b = gpu_factor(K, layer, x, n, 0, 1.0 / rows)
-    assert np.array_equal(a, b)
+    A = orc.factor_A(layer, inputs.half_bits(x), n)
+    assert relerr(unpack_f32(a, d_a), unpack_f32(b, d_a)) <= 1e-6
+    assert relerr(unpack_f32(b, d_a), A) <= 1e-5
 
 
 def test_factor_deterministic(K):
