@@ -33,7 +33,8 @@ constexpr int B = kPanel;     // 128
 constexpr int KC = 16;        // K rows per smem chunk of the tile product
 constexpr int kPivSmem = (B * (B + 1) + 2 * 32 * B + 32 * 32) * 8 + 64;
 constexpr int kTileSmem = 2 * 2 * KC * B * 8;  // double-buffered A/B chunks: 64 KB
-constexpr int kUpdSmem = kPivSmem > kTileSmem ? kPivSmem : kTileSmem;
+constexpr int kUpdSmem = kPivSmem > kTileSmem + B * B * 8 ? kPivSmem : kTileSmem + B * B * 8;
+constexpr int kPanelSmem = B * (B + 1) * 8 > kTileSmem ? B * (B + 1) * 8 : kTileSmem;
 
 struct MatDesc {
     const float *packed;
@@ -115,33 +116,39 @@ __global__ void unpack_damp_kernel(const __grid_constant__ InvParams P) {
 constexpr int S2 = 32;  // sub-pivot size
 constexpr int kPivSmemBytes = (B * (B + 1) + 2 * S2 * B + S2 * S2) * 8 + 64;
 
-// scalar sweep of the 32 x 32 sub-pivot Q (smem, row-major) by all 256 threads (4 elements
-// each); on return Q = -inv(Q).  Returns 0 or the failing pivot index + 1 (base-relative).
-__device__ __forceinline__ int block_sweep32(double *Q, int base) {
+// scalar sweep of the 32 x 32 sub-pivot (smem, row-major, ping-pong buffers Q / Q2) by all 256
+// threads (4 elements each), one barrier per pivot; the result -inv(sub-pivot) ends in Q (an even
+// number of swaps).  Returns 0 or the failing pivot index + 1 (base-relative).
+__device__ __forceinline__ int block_sweep32(double *Q, double *Q2, int base) {
     const int tid = threadIdx.x;
+    double *src = Q, *dst = Q2;
     for (int t = 0; t < S2; t++) {
-        const double d = Q[t * S2 + t];
+        const double d = src[t * S2 + t];
         if (!(d > 0.0)) return base + t + 1;  // uniform: every thread read the same d
-        const double inv = 1.0 / d;
-        double nv[4];
+        const double inv = __drcp_rn(d);
 #pragma unroll
         for (int k = 0; k < 4; k++) {
             const int e = tid + 256 * k, l = e >> 5, j = e & 31;
-            const double u = (l == t) ? -1.0 : Q[l * S2 + t];
-            const double v = (j == t) ? -inv : Q[t * S2 + j] * inv;
-            const double keep = (l == t || j == t) ? 0.0 : Q[e];
-            nv[k] = fma(-u, v, keep);
+            const double u = (l == t) ? -1.0 : src[l * S2 + t];
+            const double v = (j == t) ? -inv : src[t * S2 + j] * inv;
+            const double keep = (l == t || j == t) ? 0.0 : src[e];
+            dst[e] = fma(-u, v, keep);
         }
         __syncthreads();
-#pragma unroll
-        for (int k = 0; k < 4; k++) Q[tid + 256 * k] = nv[k];
-        __syncthreads();
+        double *tmp = src;
+        src = dst;
+        dst = tmp;
     }
     return 0;
 }
+static_assert(S2 % 2 == 0, "block_sweep32 leaves its result in Q after an even number of swaps");
 
 #ifdef PIVOT_DBG
 __device__ int g_pivot_dbg;
+__device__ long long g_pclk[64];
+#define PCLK(k) if (threadIdx.x == 0) g_pclk[k] = clock64();
+#else
+#define PCLK(k)
 #endif
 __device__ int pivot_block(const double *__restrict__ W, int64_t ld, int k0, int bk, double *__restrict__ Pout,
                            double *smem) {
@@ -160,33 +167,41 @@ __device__ int pivot_block(const double *__restrict__ W, int64_t ld, int k0, int
     }
     if (tid == 0) *fsh = 0;
     __syncthreads();
+    PCLK(0)
     for (int sb = 0; sb < B / S2; sb++) {
         const int s0 = sb * S2;
         if (s0 >= bk) break;
         for (int e = tid; e < S2 * S2; e += blockDim.x) Q[e] = S[s0 + (e >> 5)][s0 + (e & 31)];
         __syncthreads();
         {
-            const int f = block_sweep32(Q, k0 + s0);  // Q <- -inv(sub-pivot)
+            const int f = block_sweep32(Q, Wr, k0 + s0);  // Q <- -inv(sub-pivot) (Wr: ping-pong scratch)
             if (f && tid == 0) *fsh = f;
+            for (int e = tid; e < S2 * S2; e += blockDim.x) Q[e] = -Q[e];
         }
-        for (int e = tid; e < S2 * S2; e += blockDim.x) Q[e] = -Q[e];
+        PCLK(1 + 4 * sb)
         for (int e = tid; e < S2 * B; e += blockDim.x) O[e] = S[s0 + (e >> 7)][e & (B - 1)];
         __syncthreads();
         if (*fsh) break;
+        PCLK(2 + 4 * sb)
 #ifdef PIVOT_DBG
         if (g_pivot_dbg == 1 && sb >= 1) break;
 #endif
-        // W = Q O  (32 x 128): thread -> column j = tid & 127, rows a = (tid >> 7) + 2k
+        // W = Q O  (32 x 128): thread -> column j = tid & 127, rows a = (tid >> 7) + 2k (16 chains)
         {
-            const int j = tid & (B - 1);
-            for (int a = tid >> 7; a < S2; a += 2) {
-                double acc = 0.0;
-#pragma unroll 8
-                for (int b2 = 0; b2 < S2; b2++) acc = fma(Q[a * S2 + b2], O[b2 * B + j], acc);
-                Wr[a * B + j] = acc;
+            const int j = tid & (B - 1), a0 = tid >> 7;
+            double w[S2 / 2];
+#pragma unroll
+            for (int k = 0; k < S2 / 2; k++) w[k] = 0.0;
+            for (int b2 = 0; b2 < S2; b2++) {
+                const double o = O[b2 * B + j];
+#pragma unroll
+                for (int k = 0; k < S2 / 2; k++) w[k] = fma(Q[(a0 + 2 * k) * S2 + b2], o, w[k]);
             }
+#pragma unroll
+            for (int k = 0; k < S2 / 2; k++) Wr[(a0 + 2 * k) * B + j] = w[k];
         }
         __syncthreads();
+        PCLK(3 + 4 * sb)
 #ifdef PIVOT_DBG
         if (g_pivot_dbg == 2 && sb >= 1) break;
 #endif
@@ -225,6 +240,7 @@ __device__ int pivot_block(const double *__restrict__ W, int64_t ld, int k0, int
         }
         __syncthreads();
     }
+    PCLK(20)
     const int fail = *fsh;
     if (fail) return fail;
     for (int e = tid; e < B * B; e += blockDim.x) {  // P = -S (zero outside bk)
@@ -313,23 +329,34 @@ __global__ void __launch_bounds__(256, 1) panel_kernel(const __grid_constant__ I
     const int n = m.n, k0 = P.k * B;
     const int64_t ld = m.ld;
     if (k0 >= n || *m.status != 0) return;
-    const int J = cb - m.col_begin;
+    const int J = cb - m.col_begin, K = P.k;
     const int j0 = J * B;
     if (j0 >= n) return;
     const int bk = min(B, n - k0), bj = min(B, n - j0);
     double *R = m.panel, *Wp = m.panel + (int64_t)B * ld;
-    // R_J rows t < bk, cols j < bj (columns up to the 16-aligned ld are zero-filled)
+    // R_J (rows t < bk, cols j < bj; zero up to the 16-aligned ld) staged through shared memory so
+    // that both the read of W (upper storage, possibly transposed) and the write of R coalesce.
+    extern __shared__ double dyn[];
+    double(*T)[B + 1] = reinterpret_cast<double(*)[B + 1]>(dyn);
     const int bjp = min(B, (int)ld - j0);
-    for (int e = threadIdx.x; e < bk * bjp; e += blockDim.x) {
-        const int t = e / bjp, j = e % bjp;
-        const int gi = k0 + t, gj = j0 + j;
-        double v = 0.0;
-        if (j < bj) v = (gi <= gj) ? m.work[(int64_t)gi * ld + gj] : m.work[(int64_t)gj * ld + gi];
-        R[(int64_t)t * ld + gj] = v;
+    const bool trans = J < K;  // block row K left of the diagonal lives in column K of the upper storage
+    const int r0 = trans ? j0 : k0, c0 = trans ? k0 : j0, nr = trans ? bj : bk, nc = trans ? bk : bj;
+    for (int e = threadIdx.x; e < B * B; e += blockDim.x) {
+        const int r = e >> 7, c = e & (B - 1);
+        T[r][c] = (r < nr && c < nc && (J != K || c >= r)) ? m.work[(int64_t)(r0 + r) * ld + c0 + c] : 0.0;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < bk * B; e += blockDim.x) {
+        const int t = e >> 7, j = e & (B - 1);
+        if (j >= bjp) continue;
+        double v;
+        if (trans) v = T[j][t];
+        else if (J == K) v = (j >= t) ? T[t][j] : T[j][t];
+        else v = T[t][j];
+        R[(int64_t)t * ld + j0 + j] = v;
     }
     __threadfence_block();
     __syncthreads();
-    extern __shared__ double dyn[];
     double acc[8][8];
 #pragma unroll
     for (int p = 0; p < 8; p++)
@@ -407,6 +434,14 @@ __global__ void __launch_bounds__(256, 1) update_kernel(const __grid_constant__ 
     for (int p = 0; p < 8; p++)
 #pragma unroll
         for (int q = 0; q < 8; q++) acc[p][q] = 0.0;
+    // prefetch the C tile M_IJ into shared memory (its own cp.async group, overlapped with the product)
+    double *Cs = dyn + kTileSmem / 8;
+    for (int e = threadIdx.x; e < B * B / 2; e += 256) {
+        const int i = e >> 6, j = (e & 63) * 2;
+        const bool ok = i < bi && j < bj;
+        cp_async16(Cs + i * B + j, ok ? W + (int64_t)(i0 + i) * ld + j0 + j : W, ok);
+    }
+    cp_async_commit();
     // M_IJ -= R_I^T Wp_J : acc[i][j] = sum_t R[t][i0+i] Wp[t][j0+j]
     tile_product(R + i0, ld, bi, Wp + j0, ld, bj, bk, acc, dyn);
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
@@ -418,8 +453,7 @@ __global__ void __launch_bounds__(256, 1) update_kernel(const __grid_constant__ 
         for (int q = 0; q < 8; q++) {
             const int j = tx + 16 * q;
             if (j >= bj || (I == J && j < i)) continue;
-            double *ptr = W + (int64_t)(i0 + i) * ld + j0 + j;
-            *ptr = *ptr - acc[p][q];
+            W[(int64_t)(i0 + i) * ld + j0 + j] = Cs[i * B + j] - acc[p][q];
         }
     }
     if (P.fuse && I == K + 1 && J == K + 1) {  // fused next pivot: P_{K+1} = (updated M_{K+1,K+1})^-1
@@ -454,7 +488,7 @@ kfac_status inverse_launch(const std::vector<InvMat> &mats, int npairs, float ga
     static bool attr = false;
     if (!attr) {
         KFAC_CUDA_TRY(cudaFuncSetAttribute(pivot_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPivSmem));
-        KFAC_CUDA_TRY(cudaFuncSetAttribute(panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmem));
+        KFAC_CUDA_TRY(cudaFuncSetAttribute(panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPanelSmem));
         KFAC_CUDA_TRY(cudaFuncSetAttribute(update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kUpdSmem));
         attr = true;
     }
@@ -513,7 +547,7 @@ kfac_status inverse_launch(const std::vector<InvMat> &mats, int npairs, float ga
             KFAC_LAUNCHED();
             KFAC_CUDA_TRY(cudaGetLastError());
         }
-        panel_kernel<<<cols, 256, kTileSmem, st>>>(Q);
+        panel_kernel<<<cols, 256, kPanelSmem, st>>>(Q);
         KFAC_LAUNCHED();
         KFAC_CUDA_TRY(cudaGetLastError());
         update_kernel<<<tiles, 256, kUpdSmem, st>>>(Q);

@@ -50,5 +50,7 @@ int main(int argc, char **argv) {
             err = fmax(err, fabs(s - (i == j)));
         }
     printf("status %d  max|M P - I| = %.3e\n", st, err);
+    long long clk[64]; cudaMemcpyFromSymbol(clk, g_pclk, sizeof(clk));
+    for (int k = 1; k <= 20; k++) if (clk[k]) printf("phase %2d: +%lld cycles\n", k, clk[k] - clk[0]);
     return 0;
 }
