@@ -1,0 +1,115 @@
+"""Multi-GPU parity of the full K-FAC step (launched with torchrun, one rank per GPU).
+
+  torchrun --nproc-per-node P tests/mp_parity.py [config] [policy]
+
+Every rank runs stages 1-6 through the C-ABI on its own shard (NCCL
+ReduceScatter / AllGather over NVLink); rank 0 then checks, against the fp64
+oracle simulating the same P ranks (oracle.kfac_step):
+  * the reduced factors each owner received (stage 3),
+  * every layer's preconditioned gradient in the gathered buffer (stage 6),
+  * that the AllGather buffers of all ranks are bitwise identical (replica consistency).
+Exit code 0 on success.
+"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+from synth import inputs, shapes  # noqa: E402
+
+NETS = {
+    "small": lambda: ([shapes.conv("stem", 3, 16, 7, 2, 3, 20), shapes.conv("a", 16, 32, 3, 1, 1, 10, bias=1),
+                       shapes.conv("b", 32, 64, 1, 2, 0, 10), shapes.conv("c", 64, 64, 3, 1, 1, 5),
+                       shapes.linear("fc", 64, 10)], 4),
+    "one_layer": lambda: ([shapes.conv("a", 16, 32, 3, 1, 1, 8, bias=1)], 4),  # L < P: redundant owners
+    "single_conv": lambda: shapes.config("single_conv"),
+}
+
+
+def relerr(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(np.asarray(b)), 1e-300))
+
+
+def unpack(p, d):
+    M = np.zeros((d, d))
+    M[np.triu_indices(d)] = p
+    return M + M.T - np.diag(np.diag(M))
+
+
+def main():
+    cfg = sys.argv[1] if len(sys.argv) > 1 else "small"
+    policy = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    import paper_1811_12019_b200 as K
+
+    uid = torch.zeros(128, dtype=torch.uint8, device=dev)
+    if rank == 0:
+        uid.copy_(torch.frombuffer(bytearray(K.comm_unique_id()), dtype=torch.uint8))
+    dist.broadcast(uid, 0)
+    comm = K.Comm(bytes(uid.cpu().numpy().tobytes()), rank, world, local)
+    layers, n = NETS[cfg]()
+    gamma = 2.5e-2
+    st = K.KfacStep(layers, n, rank=rank, world=world, policy=policy, comm=comm, device=dev)
+    xs = [inputs.layer_x(l, i, n, rank) for i, l in enumerate(layers)]
+    gys = [inputs.layer_gy(l, i, n, rank) for i, l in enumerate(layers)]
+    dws = [inputs.layer_dw(l, i, rank) for i, l in enumerate(layers)]
+    st.set_dw([d.to(dev) for d in dws])
+    st.run([x.to(dev) for x in xs], [g.to(dev) for g in gys], gamma)
+    torch.cuda.synchronize()
+    ok = st.dev_status.abs().sum().item() == 0
+    # replica consistency of the gathered buffer
+    bufs = [torch.empty_like(st.ag_buf) for _ in range(world)]
+    dist.all_gather(bufs, st.ag_buf)
+    recvs = [torch.empty_like(st.rs_recv) for _ in range(world)]
+    dist.all_gather(recvs, st.rs_recv)
+    # every rank ships its inputs to rank 0 for the oracle
+    payload = ([inputs.half_bits(x) for x in xs], [inputs.half_bits(g) for g in gys], [d.numpy() for d in dws], n)
+    allin = [None] * world
+    dist.all_gather_object(allin, payload)
+    err = 0.0
+    if rank == 0:
+        import oracle
+        for b in bufs[1:]:
+            ok &= torch.equal(b, bufs[0])
+        ref = oracle.kfac_step(layers, allin, world, gamma, policy=policy)
+        pl = ref["plan"]
+        for r in range(world):
+            rl = st.plan.rank_layers(r)
+            for k, l in enumerate(rl["layers"]):
+                da, dg = shapes.dims(layers[l])
+                o = rl["local_off"][k]
+                got = recvs[r].cpu().double().numpy()
+                res = ref["results"][r][l]
+                err = max(err, relerr(unpack(got[o[1]:o[1] + da * (da + 1) // 2], da), res["A"]),
+                          relerr(unpack(got[o[2]:o[2] + dg * (dg + 1) // 2], dg), res["G"]),
+                          relerr(got[o[0]:o[0] + dg * da], res["dW"].reshape(-1)))
+        stage3 = err
+        g = bufs[0].cpu().double().numpy()
+        for l in range(len(layers)):
+            da, dg = shapes.dims(layers[l])
+            off = pl["ag_off"][l]
+            owner = pl["owner"][l]
+            e = relerr(g[off:off + dg * da], ref["results"][owner][l]["precond"].reshape(-1))
+            err = max(err, e)
+        print(f"mp_parity {cfg} P={world} policy={policy}: stage3 err {stage3:.2e}, end-to-end max err {err:.2e}, "
+              f"replicas identical {ok}", flush=True)
+        ok &= err <= 2e-3
+    flag = torch.tensor([1 if ok else 0], device=dev)
+    dist.broadcast(flag, 0)
+    dist.barrier(device_ids=[local])
+    del st, comm
+    dist.destroy_process_group()
+    sys.exit(0 if flag.item() == 1 else 1)
+
+
+if __name__ == "__main__":
+    main()
