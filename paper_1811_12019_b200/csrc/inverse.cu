@@ -42,12 +42,13 @@ struct MatDesc {
     double *work;
     double *panel;  // [R: B x ld][Wp: B x ld][P_even: B x B][P_odd: B x B]
     int32_t *status;
-    int32_t n, ld, pair, is_A, tile_begin, col_begin;
+    int32_t n, ld, pair, is_A, tile_begin, col_begin, piv_idx, pad_;
 };
 struct InvParams {
-    int32_t nm, total_tiles, k, total_cols, fuse, pad_;
+    int32_t nm, total_tiles, k, total_cols, fuse, npiv;
     double gamma;
     double *pair_scratch;  // [npairs][4]: pi, dA, dG
+    int *counter;          // this step's tile counter (zeroed per inverse call)
     float *pi_out;
     MatDesc m[kMaxMats];
 };
@@ -379,16 +380,21 @@ __global__ void __launch_bounds__(256, 1) panel_kernel(const __grid_constant__ I
 
 // ---- step 3: rank-B update of every upper tile (I, J); the CTA of tile (K+1, K+1) then
 // inverts that block: the next step's pivot runs concurrently with this step's update.
-__global__ void __launch_bounds__(256, 1) update_kernel(const __grid_constant__ InvParams P) {
-    int tile = blockIdx.x, mi = 0;
-    while (mi + 1 < P.nm && P.m[mi + 1].tile_begin <= tile) mi++;
+// Global tile order: first every matrix's (K+1, K+1) tile (so the fused pivots start at once),
+// then the remaining upper tiles matrix by matrix, row-major.  Persistent CTAs stride over it.
+__device__ __forceinline__ void update_tile(const InvParams &P, int g, double *dyn) {
+    int mi = 0, t = 0;
+    if (g < P.npiv) {
+        while (P.m[mi].piv_idx != g) mi++;
+    } else {
+        while (mi + 1 < P.nm && P.m[mi + 1].tile_begin <= g) mi++;
+        t = g - P.m[mi].tile_begin + (P.m[mi].piv_idx >= 0 ? 1 : 0);
+    }
     const MatDesc &m = P.m[mi];
     const int n = m.n, k0 = P.k * B;
     const int64_t ld = m.ld;
     if (k0 >= n || *m.status != 0) return;
     const int nt = (n + B - 1) / B, K = P.k;
-    // tile order: (K+1, K+1) first so the fused pivot starts early, then the upper tiles row-major
-    int t = tile - m.tile_begin;
     const int ntiles = nt * (nt + 1) / 2;
     if (t >= ntiles) return;
     int I = 0, J = 0;
@@ -428,7 +434,6 @@ __global__ void __launch_bounds__(256, 1) update_kernel(const __grid_constant__ 
         }
         return;
     }
-    extern __shared__ double dyn[];
     double acc[8][8];
 #pragma unroll
     for (int p = 0; p < 8; p++)
@@ -464,6 +469,21 @@ __global__ void __launch_bounds__(256, 1) update_kernel(const __grid_constant__ 
     }
 }
 
+// persistent CTAs take tiles from an atomic counter: the CTA that runs a fused pivot simply takes
+// fewer tiles, so the pivot hides behind the other CTAs' updates
+__global__ void __launch_bounds__(256, 1) update_kernel(const __grid_constant__ InvParams P) {
+    extern __shared__ double dyn[];
+    __shared__ int next;
+    for (;;) {
+        __syncthreads();  // the previous tile's epilogue / pivot is done with shared memory and `next`
+        if (threadIdx.x == 0) next = atomicAdd(P.counter, 1);
+        __syncthreads();
+        const int g = next;
+        if (g >= P.total_tiles) break;
+        update_tile(P, g, dyn);
+    }
+}
+
 // ---- epilogue: inv = -M (symmetric, full fp32)
 __global__ void finalize_kernel(const __grid_constant__ InvParams P) {
     const MatDesc &m = P.m[blockIdx.y];
@@ -474,6 +494,8 @@ __global__ void finalize_kernel(const __grid_constant__ InvParams P) {
             m.inv[i * n + j] = (float)(-v);
         }
 }
+
+static int g_inv_sms = 0;
 
 int64_t inverse_ld(int n) { return (n + 15) / 16 * 16; }
 int64_t inverse_ws_doubles(int n) {
@@ -486,6 +508,11 @@ kfac_status inverse_launch(const std::vector<InvMat> &mats, int npairs, float ga
     if (mats.empty()) return KFAC_OK;
     if ((int)mats.size() > kMaxMats) return set_error(KFAC_ERR_UNSUPPORTED, "too many owned matrices for one launch");
     static bool attr = false;
+    if (!g_inv_sms) {
+        int dev = 0;
+        KFAC_CUDA_TRY(cudaGetDevice(&dev));
+        KFAC_CUDA_TRY(cudaDeviceGetAttribute(&g_inv_sms, cudaDevAttrMultiProcessorCount, dev));
+    }
     if (!attr) {
         KFAC_CUDA_TRY(cudaFuncSetAttribute(pivot_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPivSmem));
         KFAC_CUDA_TRY(cudaFuncSetAttribute(panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPanelSmem));
@@ -512,7 +539,6 @@ kfac_status inverse_launch(const std::vector<InvMat> &mats, int npairs, float ga
         d.is_A = mats[i].is_A;
         maxn = std::max(maxn, d.n);
     }
-    (void)npairs;
     damp_trace_kernel<<<P.nm, 256, 0, st>>>(P);
     KFAC_LAUNCHED();
     KFAC_CUDA_TRY(cudaGetLastError());
@@ -521,23 +547,34 @@ kfac_status inverse_launch(const std::vector<InvMat> &mats, int npairs, float ga
     KFAC_CUDA_TRY(cudaGetLastError());
     const int steps = (maxn + B - 1) / B;
     const int fuse = getenv("KFAC_INV_NOFUSE") ? 0 : 1;
+    // per-step tile counters live in the scratch after the pair data (plan reserves 1 KB)
+    int *counters = reinterpret_cast<int *>(pair_scratch + ((4 * (int64_t)npairs + 15) / 16) * 16);
+    if (steps > 256) return set_error(KFAC_ERR_UNSUPPORTED, "inverse: matrix too large for the step counters");
+    KFAC_CUDA_TRY(cudaMemsetAsync(counters, 0, steps * sizeof(int), st));
     for (int k = 0; k < steps; k++) {
         // active matrices only (n > k*B), with their upper-tile and column-block prefixes
         InvParams Q;
         memset(&Q, 0, offsetof(InvParams, m));
         Q.gamma = P.gamma;
         Q.k = k;
-        int nm = 0, tiles = 0, cols = 0;
+        int nm = 0, tiles = 0, cols = 0, npiv = 0;
         for (int i = 0; i < P.nm; i++) {
             if (P.m[i].n <= k * B) continue;
             Q.m[nm] = P.m[i];
             const int nt = (P.m[i].n + B - 1) / B;
-            Q.m[nm].tile_begin = tiles;
+            Q.m[nm].piv_idx = (fuse && k + 1 < nt) ? npiv++ : -1;
             Q.m[nm].col_begin = cols;
-            tiles += nt * (nt + 1) / 2;
             cols += nt;
             nm++;
         }
+        tiles = npiv;
+        for (int i = 0; i < nm; i++) {
+            const int nt = (Q.m[i].n + B - 1) / B;
+            Q.m[i].tile_begin = tiles;
+            tiles += nt * (nt + 1) / 2 - (Q.m[i].piv_idx >= 0 ? 1 : 0);
+        }
+        Q.npiv = npiv;
+        Q.counter = counters + k;
         Q.nm = nm;
         Q.total_tiles = tiles;
         Q.total_cols = cols;
@@ -550,7 +587,7 @@ kfac_status inverse_launch(const std::vector<InvMat> &mats, int npairs, float ga
         panel_kernel<<<cols, 256, kPanelSmem, st>>>(Q);
         KFAC_LAUNCHED();
         KFAC_CUDA_TRY(cudaGetLastError());
-        update_kernel<<<tiles, 256, kUpdSmem, st>>>(Q);
+        update_kernel<<<std::min(tiles, g_inv_sms), 256, kUpdSmem, st>>>(Q);
         KFAC_LAUNCHED();
         KFAC_CUDA_TRY(cudaGetLastError());
     }
