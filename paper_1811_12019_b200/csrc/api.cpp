@@ -241,7 +241,7 @@ kfac_status kfac_precondition(kfac_plan_t p, int32_t rank, const float *recv, co
         j.Ainv = inv_ws + p->inv_off[rank][2 * k];
         j.Ginv = inv_ws + p->inv_off[rank][2 * k + 1];
         j.tmp = w + off;
-        off += align16((int64_t)g.dG * g.dA);
+        off += align16(precond_ws_floats(g.dG, g.dA));
         if (p->owner[l] == rank) {
             j.out = ag_buf + p->ag_off[l];
         } else {

@@ -98,13 +98,14 @@ struct PrecJob {
     const float *dW;      // [dG, dA]
     const float *Ainv;    // [dA, dA]
     const float *Ginv;    // [dG, dG]
-    float *tmp;           // [dG, dA] scratch  T = dW * Ainv
+    float *tmp;           // precond_ws_floats(dG, dA) scratch (3xTF32 split operands, T^T)
     float *out;           // [dG, dA]
     int32_t dG, dA;
 };
 kfac_status inverse_launch(const std::vector<InvMat> &mats, int npairs, float gamma, double *pair_scratch,
                            float *pi_out, cudaStream_t st);
 kfac_status precond_launch(const std::vector<PrecJob> &jobs, cudaStream_t st);
+int64_t precond_ws_floats(int dG, int dA);  // split operands of one layer's two products
 kfac_status replicate_launch(const std::vector<std::pair<const float *, float *>> &src_dst,
                              const std::vector<int64_t> &counts, cudaStream_t st);
 

@@ -156,7 +156,7 @@ kfac_status plan_build(kfac_plan *p) {
             p->inv_off[r].push_back(off);
             off = align16(off + (int64_t)g.dG * g.dG);
             for (int n : {g.dA, g.dG}) inv_ws += inverse_ws_doubles(n) * 8;
-            prec_ws += align16((int64_t)g.dG * g.dA) * 4 * 2;  // T and (redundant) output
+            prec_ws += (align16(precond_ws_floats(g.dG, g.dA)) + align16((int64_t)g.dG * g.dA)) * 4;  // split operands + (redundant) output
         }
         p->inv_floats[r] = off;
         inv_ws += align16(4 * (int64_t)p->owned[r].size()) * 8 + 1024;  // pair scratch

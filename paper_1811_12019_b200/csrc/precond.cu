@@ -1,125 +1,325 @@
 // precond.cu -- stage 5 of distributed K-FAC (PAPER.md P:264-282 Eqs. K-FAC
 // update): the preconditioned gradient of every owned layer
 //     𝒢 = G_d^-1 * dW * A_d^-1        (row-major vec, reading R-14)
-// as two grouped fp32 GEMM launches over all owned layers:
-//     T = dW * A_d^-1   then   𝒢 = G_d^-1 * T.
-// fp32 FFMA arithmetic (single-pass bf16/TF32 misses the
-// 2e-3 bound on activation-consistent gradients); 128x128 output tiles,
-// 256 threads x (8x8) register tiles, double-buffered shared memory.
+// as two grouped tcgen05 GEMM launches over all owned layers, both with
+// K-major operands only (the inverses are symmetric):
+//     T^T = A_d^-1 * dW^T      (A-op A_d^-1 [dA x dA], B-op dW [dG x dA])
+//     𝒢   = G_d^-1 * T         (A-op G_d^-1 [dG x dG], B-op T^T [dA x dG])
+// Precision: single-pass TF32 / bf16 miss the 2e-3 bound on
+// activation-consistent gradients, so every product is a 3xTF32 split
+//     a*b ~ hi(a)hi(b) + hi(a)lo(b) + lo(a)hi(b),  lo(x) = x - tf32(x)
+// on tcgen05.mma kind::tf32 with fp32 accumulation in TMEM (fp32-class error).
+// The operands are staged as [2][rows][K] (hi, lo) by a split kernel (the
+// first GEMM's epilogue writes T^T already split); TMA loads 32-element K
+// boxes (SW128, K-major) of hi and lo for both operands.
 #include <algorithm>
 #include <cstring>
 
 #include "kfac_internal.hpp"
+#include "sm100.cuh"
 
 namespace kfac {
 
-constexpr int kMaxGemm = 128;
-constexpr int GBM = 128, GBN = 128, GBK = 8;
+constexpr int GM = 128, GN = 128, GK = 32;  // tile M, N; K elements per stage (128 B rows)
+constexpr int GStages = 3;
+constexpr int GThreads = 192;               // warps 0-3 epilogue, 4 MMA, 5 TMA
+constexpr int kMaxG = 96;
+constexpr int GOp = GM * GK * 4;            // 16 KB per operand half per stage
+constexpr int GStageBytes = 4 * GOp;        // A hi, A lo, B hi, B lo
+constexpr int GLd = 33;                     // epilogue staging stride
+constexpr size_t GSmem = 1024 + (size_t)GStages * GStageBytes + (size_t)GM * GLd * 4 + 256;
 
-struct GemmDesc {
-    const float *A;  // [M, K] row-major
-    const float *B;  // [K, N] row-major
-    float *C;        // [M, N] row-major
-    int32_t M, N, K, tile_begin, tiles_n;
+struct alignas(64) GemmProb {
+    CUtensorMap tA;        // [2][M][Kp] fp32 (hi, lo)
+    CUtensorMap tB;        // [2][N][Kp] fp32
+    float *C;              // output, row-major ldc
+    float *Clo;            // if non-null: write split output: C = hi copy, Clo = lo part
+    int32_t M, N, K, ldc, tiles_n, item_begin, pad0, pad1;
 };
 struct GemmParams {
-    int32_t ng, total;
-    GemmDesc g[kMaxGemm];
+    int32_t np, total, dbg, pad;
+    GemmProb p[kMaxG];
 };
 
-__global__ void __launch_bounds__(256) sgemm_grouped_kernel(const __grid_constant__ GemmParams P) {
-    int tile = blockIdx.x, gi = 0;
-    while (gi + 1 < P.ng && P.g[gi + 1].tile_begin <= tile) gi++;
-    const GemmDesc &g = P.g[gi];
-    const int local = tile - g.tile_begin;
-    const int m0 = (local / g.tiles_n) * GBM, n0 = (local % g.tiles_n) * GBN;
-    if (m0 >= g.M) return;
-    __shared__ float As[2][GBK][GBM];  // transposed A tile: As[k][m]
-    __shared__ float Bs[2][GBK][GBN];
-    const int tid = threadIdx.x;
-    const int tx = tid & 15, ty = tid >> 4;
-    // loaders: A tile 128x8 -> each thread 4 elements (rows tid/2, k 4*(tid&1)..+3)
-    const int a_r = tid >> 1, a_k = (tid & 1) * 4;
-    // B tile 8x128 -> each thread 4 elements (k = tid/32, n = 4*(tid%32)..+3)
-    const int b_k = tid >> 5, b_n = (tid & 31) * 4;
-    float acc[8][8];
-#pragma unroll
-    for (int i = 0; i < 8; i++)
-#pragma unroll
-        for (int j = 0; j < 8; j++) acc[i][j] = 0.f;
-    const int ktiles = (g.K + GBK - 1) / GBK;
-    float ra[4], rb[4];
-    auto load = [&](int kt) {
-        const int k0 = kt * GBK;
-#pragma unroll
-        for (int e = 0; e < 4; e++) {
-            int r = m0 + a_r, k = k0 + a_k + e;
-            ra[e] = (r < g.M && k < g.K) ? __ldg(g.A + (int64_t)r * g.K + k) : 0.f;
-            int kk = k0 + b_k, c = n0 + b_n + e;
-            rb[e] = (kk < g.K && c < g.N) ? __ldg(g.B + (int64_t)kk * g.N + c) : 0.f;
+__device__ __forceinline__ float tf32_trunc(float x) {
+    return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+}
+
+__device__ __forceinline__ void mma_tf32_ss(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *m, uint64_t *bar, int32_t c0, int32_t c1,
+                                            int32_t c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+
+// idesc kind::tf32: D fp32 (1), A/B TF32 (2), both K-major
+constexpr uint32_t kIdescTF32 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(GN >> 3) << 17) | ((uint32_t)(GM >> 4) << 24);
+
+__device__ __forceinline__ void gdecode(const GemmParams &P, int item, int &pi, int &m0, int &n0) {
+    int p = 0;
+    while (p + 1 < P.np && P.p[p + 1].item_begin <= item) p++;
+    const int local = item - P.p[p].item_begin;
+    pi = p;
+    m0 = (local / P.p[p].tiles_n) * GM;
+    n0 = (local % P.p[p].tiles_n) * GN;
+}
+
+__global__ void __launch_bounds__(GThreads, 1) gemm_3xtf32_kernel(const __grid_constant__ GemmParams P) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    float *stage_buf = reinterpret_cast<float *>(smem + (size_t)GStages * GStageBytes);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + (size_t)GStages * GStageBytes + (size_t)GM * GLd * 4);
+    uint64_t *full = bars, *empty = bars + GStages, *tfull = bars + 2 * GStages, *tempty = bars + 2 * GStages + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * GStages + 4);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < GStages; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
         }
-    };
-    auto store = [&](int buf) {
-#pragma unroll
-        for (int e = 0; e < 4; e++) {
-            As[buf][a_k + e][a_r] = ra[e];
-            Bs[buf][b_k][b_n + e] = rb[e];
+        for (int b = 0; b < 2; b++) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], 128);
         }
-    };
-    load(0);
-    store(0);
-    __syncthreads();
-    for (int kt = 0; kt < ktiles; kt++) {
-        const int buf = kt & 1;
-        if (kt + 1 < ktiles) load(kt + 1);
-#pragma unroll
-        for (int k = 0; k < GBK; k++) {
-            float a[8], b[8];
-#pragma unroll
-            for (int i = 0; i < 4; i++) {
-                a[i] = As[buf][k][ty * 4 + i];
-                a[i + 4] = As[buf][k][64 + ty * 4 + i];
-                b[i] = Bs[buf][k][tx * 4 + i];
-                b[i + 4] = Bs[buf][k][64 + tx * 4 + i];
-            }
-#pragma unroll
-            for (int i = 0; i < 8; i++)
-#pragma unroll
-                for (int j = 0; j < 8; j++) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
-        }
-        if (kt + 1 < ktiles) {
-            store(buf ^ 1);
-        }
-        __syncthreads();
+        fence_barrier_init();
     }
-#pragma unroll
-    for (int i = 0; i < 8; i++) {
-        const int r = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
-        if (r >= g.M) continue;
-#pragma unroll
-        for (int j = 0; j < 8; j++) {
-            const int c = n0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4));
-            if (c < g.N) g.C[(int64_t)r * g.N + c] = acc[i][j];
+    if (warp == 4) tmem_alloc(tmem_slot, 2 * GN);
+    if (warp == 5)
+        for (int p = lane; p < P.np; p += 32) {
+            tma_prefetch(&P.p[p].tA);
+            tma_prefetch(&P.p[p].tB);
         }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const int total = P.total;
+
+    if (warp == 5) {
+        if (lane == 0) {  // TMA producer
+            uint32_t stage = 0, phase = 0;
+            for (int item = blockIdx.x; item < total; item += gridDim.x) {
+                int pi, m0, n0;
+                gdecode(P, item, pi, m0, n0);
+                const GemmProb &g = P.p[pi];
+                const int kch = (g.K + GK - 1) / GK;
+                for (int kc = 0; kc < kch; kc++) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    uint8_t *s = smem + (size_t)stage * GStageBytes;
+                    mbar_arrive_expect_tx(&full[stage], GStageBytes);
+                    tma_load_3d(s, &g.tA, &full[stage], kc * GK, m0, 0);
+                    tma_load_3d(s + GOp, &g.tA, &full[stage], kc * GK, m0, 1);
+                    tma_load_3d(s + 2 * GOp, &g.tB, &full[stage], kc * GK, n0, 0);
+                    tma_load_3d(s + 3 * GOp, &g.tB, &full[stage], kc * GK, n0, 1);
+                    if (++stage == GStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 4) {
+        uint32_t stage = 0, phase = 0, tph0 = 0, tph1 = 0;
+        int buf = 0;
+        for (int item = blockIdx.x; item < total; item += gridDim.x) {
+            int pi, m0, n0;
+            gdecode(P, item, pi, m0, n0);
+            const int kch = (P.p[pi].K + GK - 1) / GK;
+            const uint32_t tacc = tmem_base + buf * GN;
+            if (lane == 0) {
+                mbar_wait(&tempty[buf], (buf ? tph1 : tph0) ^ 1);
+                tc_fence_after();
+                for (int kc = 0; kc < kch; kc++) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t s = smem_u32(smem + (size_t)stage * GStageBytes);
+                    const uint32_t ah = s, al = s + GOp, bh = s + 2 * GOp, bl = s + 3 * GOp;
+#pragma unroll
+                    for (int k = 0; k < GK / 8; k++) {  // K = 8 tf32 per MMA = 32 bytes within the SW128 atom
+                        const uint32_t ko = k * 32;
+                        const uint64_t dah = umma_desc(ah + ko, 16, 1024, UMMA_SW128);
+                        const uint64_t dal = umma_desc(al + ko, 16, 1024, UMMA_SW128);
+                        const uint64_t dbh = umma_desc(bh + ko, 16, 1024, UMMA_SW128);
+                        const uint64_t dbl = umma_desc(bl + ko, 16, 1024, UMMA_SW128);
+                        const uint32_t acc0 = (kc > 0 || k > 0) ? 1u : 0u;
+                        mma_tf32_ss(tacc, dal, dbh, kIdescTF32, acc0);  // small terms first
+                        mma_tf32_ss(tacc, dah, dbl, kIdescTF32, 1u);
+                        mma_tf32_ss(tacc, dah, dbh, kIdescTF32, 1u);
+                    }
+                    mma_commit(&empty[stage]);
+                    if (++stage == GStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                mma_commit(&tfull[buf]);
+            }
+            __syncwarp();
+            if (buf) tph1 ^= 1; else tph0 ^= 1;
+            buf ^= 1;
+        }
+    } else {  // epilogue warps 0-3
+        uint32_t tph0 = 0, tph1 = 0;
+        int buf = 0;
+        const int row = warp * 32 + lane;
+        for (int item = blockIdx.x; item < total; item += gridDim.x) {
+            int pi, m0, n0;
+            gdecode(P, item, pi, m0, n0);
+            const GemmProb &g = P.p[pi];
+            float *C = g.C, *Clo = g.Clo;
+            const int M = g.M, N = g.N, ldc = g.ldc;
+            mbar_wait(&tfull[buf], buf ? tph1 : tph0);
+            tc_fence_after();
+            const uint32_t tacc = tmem_base + buf * GN + ((uint32_t)(warp * 32) << 16);
+            for (int q = 0; q < GN / 32; q++) {
+                uint32_t r[32];
+                tmem_ld_32x32b_x32(tacc + q * 32, r);
+                tmem_ld_wait();
+#pragma unroll
+                for (int i = 0; i < 32; i++) stage_buf[row * GLd + i] = __uint_as_float(r[i]);
+                if (q == GN / 32 - 1) {
+                    tc_fence_before();
+                    mbar_arrive(&tempty[buf]);
+                }
+                named_bar_sync(2, 128);
+                const int j = n0 + q * 32 + lane;
+                for (int rr = warp; rr < GM; rr += 4) {
+                    const int i = m0 + rr;
+                    if (i >= M) break;
+                    if (j < N) {
+                        const float v = stage_buf[rr * GLd + lane];
+                        if (Clo) {  // split output for the next product: hi = tf32(v), lo = v - hi
+                            const float hi = tf32_trunc(v);
+                            C[(int64_t)i * ldc + j] = hi;
+                            Clo[(int64_t)i * ldc + j] = v - hi;
+                        } else {
+                            C[(int64_t)i * ldc + j] = v;
+                        }
+                    } else if (Clo && j < ldc) {  // zero the K padding the next product reads
+                        C[(int64_t)i * ldc + j] = 0.f;
+                        Clo[(int64_t)i * ldc + j] = 0.f;
+                    }
+                }
+                named_bar_sync(2, 128);
+            }
+            if (buf) tph1 ^= 1; else tph0 ^= 1;
+            buf ^= 1;
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 4) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, 2 * GN);
     }
 }
 
-static kfac_status gemm_grouped(const std::vector<GemmDesc> &gs, cudaStream_t st) {
-    for (size_t b = 0; b < gs.size(); b += kMaxGemm) {
+// split fp32 rows [rows][K] (row stride ld_src) into [2][rows][Kp]: hi = x, lo = x - tf32(x)
+struct SplitJob {
+    const float *src;
+    float *dst;
+    int32_t rows, K, ld_src, Kp;
+};
+struct SplitParams {
+    int32_t n, pad;
+    SplitJob j[kMaxG];
+};
+__global__ void split_kernel(const __grid_constant__ SplitParams P) {
+    const SplitJob &J = P.j[blockIdx.y];
+    const int64_t tot = (int64_t)J.rows * J.Kp;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = e / J.Kp;
+        const int k = (int)(e - r * J.Kp);
+        const float x = k < J.K ? J.src[r * J.ld_src + k] : 0.f;
+        const float hi = tf32_trunc(x);  // exact tf32 value, whatever rounding the MMA applies
+        J.dst[e] = hi;
+        J.dst[tot + e] = x - hi;
+    }
+}
+
+// ---------------------------------------------------------------- host side
+typedef CUresult (*PFN_encTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                 const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static PFN_encTiled g_enc = nullptr;
+static int g_gsms = 0;
+
+static kfac_status split_map(CUtensorMap *m, float *base, int rows, int Kp) {
+    if (!g_enc) {
+        cudaDriverEntryPointQueryResult q;
+        void *f = nullptr;
+        KFAC_CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q));
+        if (!f) return set_error(KFAC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+        g_enc = (PFN_encTiled)f;
+    }
+    cuuint64_t dims[3] = {(cuuint64_t)Kp, (cuuint64_t)rows, 2};
+    cuuint64_t strides[2] = {(cuuint64_t)Kp * 4, (cuuint64_t)Kp * 4 * rows};
+    cuuint32_t box[3] = {GK, GM, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = g_enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                       CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_error(KFAC_ERR_UNSUPPORTED, "cuTensorMapEncodeTiled (split operand) failed");
+    return KFAC_OK;
+}
+
+static int64_t kpad(int k) { return (k + 3) / 4 * 4; }
+
+int64_t precond_ws_floats(int dG, int dA) {
+    // A_d^-1 split, G_d^-1 split, dW split, T^T split (all [2][rows][Kp]) + output staging
+    return 2 * ((int64_t)dA * kpad(dA) + (int64_t)dG * kpad(dG) + (int64_t)dG * kpad(dA) + (int64_t)dA * kpad(dG)) + 64;
+}
+
+static kfac_status launch_splits(const std::vector<SplitJob> &js, cudaStream_t st) {
+    for (size_t b = 0; b < js.size(); b += kMaxG) {
+        SplitParams P;
+        memset(&P, 0, sizeof(P));
+        P.n = (int)std::min<size_t>(kMaxG, js.size() - b);
+        for (int i = 0; i < P.n; i++) P.j[i] = js[b + i];
+        split_kernel<<<dim3(64, P.n), 256, 0, st>>>(P);
+        KFAC_LAUNCHED();
+        KFAC_CUDA_TRY(cudaGetLastError());
+    }
+    return KFAC_OK;
+}
+
+static kfac_status launch_gemms(std::vector<GemmProb> &gs, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        KFAC_CUDA_TRY(cudaFuncSetAttribute(gemm_3xtf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GSmem));
+        int dev = 0;
+        KFAC_CUDA_TRY(cudaGetDevice(&dev));
+        KFAC_CUDA_TRY(cudaDeviceGetAttribute(&g_gsms, cudaDevAttrMultiProcessorCount, dev));
+        attr = true;
+    }
+    // heaviest problems first (static striding)
+    std::stable_sort(gs.begin(), gs.end(), [](const GemmProb &a, const GemmProb &b) {
+        return (int64_t)a.M * a.N * a.K > (int64_t)b.M * b.N * b.K;
+    });
+    for (size_t b = 0; b < gs.size(); b += kMaxG) {
         GemmParams P;
         memset(&P, 0, sizeof(P));
-        int tiles = 0;
-        P.ng = (int)std::min<size_t>(kMaxGemm, gs.size() - b);
-        for (int i = 0; i < P.ng; i++) {
-            GemmDesc d = gs[b + i];
-            d.tiles_n = (d.N + GBN - 1) / GBN;
-            d.tile_begin = tiles;
-            tiles += ((d.M + GBM - 1) / GBM) * d.tiles_n;
-            P.g[i] = d;
+        P.np = (int)std::min<size_t>(kMaxG, gs.size() - b);
+        int items = 0;
+        for (int i = 0; i < P.np; i++) {
+            P.p[i] = gs[b + i];
+            P.p[i].tiles_n = (P.p[i].N + GN - 1) / GN;
+            P.p[i].item_begin = items;
+            items += ((P.p[i].M + GM - 1) / GM) * P.p[i].tiles_n;
         }
-        P.total = tiles;
-        if (!tiles) continue;
-        sgemm_grouped_kernel<<<tiles, 256, 0, st>>>(P);
+        P.total = items;
+        if (!items) continue;
+        gemm_3xtf32_kernel<<<std::min(items, g_gsms), GThreads, GSmem, st>>>(P);
         KFAC_LAUNCHED();
         KFAC_CUDA_TRY(cudaGetLastError());
     }
@@ -127,28 +327,52 @@ static kfac_status gemm_grouped(const std::vector<GemmDesc> &gs, cudaStream_t st
 }
 
 kfac_status precond_launch(const std::vector<PrecJob> &jobs, cudaStream_t st) {
-    std::vector<GemmDesc> g1, g2;
+    // workspace per job: [Ainv split][Ginv split][dW split][T^T split]
+    std::vector<SplitJob> sj;
+    std::vector<GemmProb> g1, g2;
     for (const PrecJob &j : jobs) {
-        GemmDesc a{};
-        a.A = j.dW;
-        a.B = j.Ainv;
-        a.C = j.tmp;
-        a.M = j.dG;
-        a.N = j.dA;
-        a.K = j.dA;
+        float *w = j.tmp;
+        const int dA = j.dA, dG = j.dG;
+        float *sA = w;
+        w += 2 * (int64_t)dA * kpad(dA);
+        float *sG = w;
+        w += 2 * (int64_t)dG * kpad(dG);
+        float *sW = w;
+        w += 2 * (int64_t)dG * kpad(dA);
+        float *sT = w;
+        sj.push_back({j.Ainv, sA, dA, dA, dA, (int32_t)kpad(dA)});
+        sj.push_back({j.Ginv, sG, dG, dG, dG, (int32_t)kpad(dG)});
+        sj.push_back({j.dW, sW, dG, dA, dA, (int32_t)kpad(dA)});
+        GemmProb a{};
+        kfac_status s = split_map(&a.tA, sA, dA, (int)kpad(dA));
+        if (s) return s;
+        s = split_map(&a.tB, sW, dG, (int)kpad(dA));
+        if (s) return s;
+        a.M = dA;
+        a.N = dG;
+        a.K = dA;
+        a.C = sT;  // T^T hi [dA][kpad(dG)], lo right after
+        a.ldc = (int)kpad(dG);
+        a.Clo = sT + (int64_t)dA * kpad(dG);
         g1.push_back(a);
-        GemmDesc b{};
-        b.A = j.Ginv;
-        b.B = j.tmp;
+        GemmProb b{};
+        s = split_map(&b.tA, sG, dG, (int)kpad(dG));
+        if (s) return s;
+        s = split_map(&b.tB, sT, dA, (int)kpad(dG));
+        if (s) return s;
+        b.M = dG;
+        b.N = dA;
+        b.K = dG;
         b.C = j.out;
-        b.M = j.dG;
-        b.N = j.dA;
-        b.K = j.dG;
+        b.ldc = dA;
+        b.Clo = nullptr;
         g2.push_back(b);
     }
-    kfac_status s = gemm_grouped(g1, st);
+    kfac_status s = launch_splits(sj, st);
     if (s) return s;
-    return gemm_grouped(g2, st);
+    s = launch_gemms(g1, st);
+    if (s) return s;
+    return launch_gemms(g2, st);
 }
 
 }  // namespace kfac
