@@ -32,8 +32,8 @@ constexpr int kMaxMats = 128;
 constexpr int B = kPanel;     // 128
 constexpr int KC = 16;        // K rows per smem chunk of the tile product
 constexpr int kPivSmem = (B * (B + 1) + 2 * 32 * B + 32 * 32) * 8 + 64;
-constexpr int kTileSmem = 2 * 2 * KC * B * 8;  // double-buffered A/B chunks: 64 KB
-constexpr int kUpdSmem = kPivSmem > kTileSmem + B * B * 8 ? kPivSmem : kTileSmem + B * B * 8;
+constexpr int kTileSmem = 2 * 2 * KC * (B + 4) * 8;  // double-buffered A/B chunks (padded rows): 66 KB
+constexpr int kUpdSmem = kPivSmem > kTileSmem + B * (B + 4) * 8 ? kPivSmem : kTileSmem + B * (B + 4) * 8;
 constexpr int kPanelSmem = B * (B + 1) * 8 > kTileSmem ? B * (B + 1) * 8 : kTileSmem;
 
 struct MatDesc {
@@ -274,14 +274,36 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
-// acc[8][8] += sum_{t < kt} A[t][i] * Bm[t][j] for the 128 x 128 tile (i = ty + 16a, j = tx + 16b).
-// A and Bm are row-major with 16-aligned leading dimensions; columns >= acols / bcols and rows
-// >= kt read as zero.  Chunks of KC rows are double-buffered with cp.async (16-byte copies).
+// acc += sum_{t < kt} A[t][i] * Bm[t][j] for the 128 x 128 tile on the fp64 tensor cores
+// (mma.sync m8n8k4 f64, DMMA: 256 FMAs per warp instruction).  Warp w owns rows
+// 64*(w>>2) + [0, 64) and columns 32*(w&3) + [0, 32) as 8 x 4 m8n8 blocks; acc[p][q] is the
+// element (tile_row(p), tile_col(q)) below.  A and Bm are row-major with 16-aligned leading
+// dimensions; columns >= acols / bcols and rows >= kt read as zero.  Chunks of KC rows are
+// double-buffered with cp.async; shared rows are padded to 132 doubles (conflict-free fragments).
+constexpr int SLD = B + 4;
+__device__ __forceinline__ int tile_row(int p) {
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    return 64 * (w >> 2) + 8 * p + (lane >> 2);
+}
+__device__ __forceinline__ int tile_col(int q) {
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    return 32 * (w & 3) + 8 * (q >> 1) + 2 * (lane & 3) + (q & 1);
+}
+__device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+struct NoExtra {
+    __device__ __forceinline__ void operator()(int, int) const {}
+};
+template <typename Extra = NoExtra>
 __device__ __forceinline__ void tile_product(const double *__restrict__ A, int64_t lda, int acols,
                                              const double *__restrict__ Bm, int64_t ldb, int bcols, int kt,
-                                             double (&acc)[8][8], double *smem) {
-    double *As = smem, *Bs = smem + 2 * KC * B;
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+                                             double (&acc)[8][8], double *smem, Extra extra = Extra()) {
+    double *As = smem, *Bs = smem + 2 * KC * SLD;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int arow = 64 * (w >> 2) + (lane >> 2), bcol = 32 * (w & 3) + (lane >> 2), kl = lane & 3;
     const int nchunks = (kt + KC - 1) / KC;
     auto load = [&](int c, int buf) {
         const int t0 = c * KC;
@@ -289,9 +311,10 @@ __device__ __forceinline__ void tile_product(const double *__restrict__ A, int64
             const int t = e >> 6, i = (e & 63) * 2;
             const bool okr = t0 + t < kt;
             const bool oka = okr && i < acols, okb = okr && i < bcols;
-            cp_async16(As + buf * KC * B + t * B + i, oka ? A + (int64_t)(t0 + t) * lda + i : A, oka);
-            cp_async16(Bs + buf * KC * B + t * B + i, okb ? Bm + (int64_t)(t0 + t) * ldb + i : Bm, okb);
+            cp_async16(As + buf * KC * SLD + t * SLD + i, oka ? A + (int64_t)(t0 + t) * lda + i : A, oka);
+            cp_async16(Bs + buf * KC * SLD + t * SLD + i, okb ? Bm + (int64_t)(t0 + t) * ldb + i : Bm, okb);
         }
+        extra(c, nchunks);  // e.g. a slice of the C tile, in the same cp.async group
         cp_async_commit();
     };
     load(0, 0);
@@ -304,19 +327,19 @@ __device__ __forceinline__ void tile_product(const double *__restrict__ A, int64
             cp_async_wait_0();
         }
         __syncthreads();
-        const double *as = As + buf * KC * B, *bs = Bs + buf * KC * B;
-#pragma unroll 4
-        for (int t = 0; t < KC; t++) {
-            double a[8], b[8];
+        const double *as = As + buf * KC * SLD, *bs = Bs + buf * KC * SLD;
 #pragma unroll
-            for (int q = 0; q < 8; q++) {
-                a[q] = as[t * B + ty + 16 * q];
-                b[q] = bs[t * B + tx + 16 * q];
-            }
+        for (int kk = 0; kk < KC / 4; kk++) {
+            const int t = kk * 4 + kl;
+            double a[8], b[4];
+#pragma unroll
+            for (int p = 0; p < 8; p++) a[p] = as[t * SLD + arow + 8 * p];
+#pragma unroll
+            for (int q = 0; q < 4; q++) b[q] = bs[t * SLD + bcol + 8 * q];
 #pragma unroll
             for (int p = 0; p < 8; p++)
 #pragma unroll
-                for (int q = 0; q < 8; q++) acc[p][q] = fma(a[p], b[q], acc[p][q]);
+                for (int q = 0; q < 4; q++) dmma(acc[p][2 * q], acc[p][2 * q + 1], a[p], b[q]);
         }
         __syncthreads();
     }
@@ -365,14 +388,13 @@ __global__ void __launch_bounds__(256, 1) panel_kernel(const __grid_constant__ I
         for (int q = 0; q < 8; q++) acc[p][q] = 0.0;
     // Wp[i][j] = sum_t P[t][i] R[t][j]   (P symmetric, zero outside bk)
     tile_product(pivot_slot(m, P.k), B, bk, R + j0, ld, bj, bk, acc, dyn);
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
 #pragma unroll
     for (int p = 0; p < 8; p++) {
-        const int i = ty + 16 * p;
+        const int i = tile_row(p);
         if (i >= bk) continue;
 #pragma unroll
         for (int q = 0; q < 8; q++) {
-            const int j = tx + 16 * q;
+            const int j = tile_col(q);
             if (j < bjp) Wp[(int64_t)i * ld + j0 + j] = acc[p][q];
         }
     }
@@ -439,26 +461,28 @@ __device__ __forceinline__ void update_tile(const InvParams &P, int g, double *d
     for (int p = 0; p < 8; p++)
 #pragma unroll
         for (int q = 0; q < 8; q++) acc[p][q] = 0.0;
-    // prefetch the C tile M_IJ into shared memory (its own cp.async group, overlapped with the product)
+    // the C tile M_IJ streams into shared memory in slices, one per K chunk of the product
+    // (its HBM latency hides behind the tensor-core work instead of preceding it)
     double *Cs = dyn + kTileSmem / 8;
-    for (int e = threadIdx.x; e < B * B / 2; e += 256) {
-        const int i = e >> 6, j = (e & 63) * 2;
-        const bool ok = i < bi && j < bj;
-        cp_async16(Cs + i * B + j, ok ? W + (int64_t)(i0 + i) * ld + j0 + j : W, ok);
-    }
-    cp_async_commit();
+    auto cslice = [&](int c, int nch) {
+        const int r0 = c * B / nch, r1 = (c + 1) * B / nch;  // rows of this slice
+        for (int e = threadIdx.x; e < (r1 - r0) * (B / 2); e += 256) {
+            const int i = r0 + e / (B / 2), j = (e % (B / 2)) * 2;
+            const bool ok = i < bi && j < bj;
+            cp_async16(Cs + i * SLD + j, ok ? W + (int64_t)(i0 + i) * ld + j0 + j : W, ok);
+        }
+    };
     // M_IJ -= R_I^T Wp_J : acc[i][j] = sum_t R[t][i0+i] Wp[t][j0+j]
-    tile_product(R + i0, ld, bi, Wp + j0, ld, bj, bk, acc, dyn);
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    tile_product(R + i0, ld, bi, Wp + j0, ld, bj, bk, acc, dyn, cslice);
 #pragma unroll
     for (int p = 0; p < 8; p++) {
-        const int i = ty + 16 * p;
+        const int i = tile_row(p);
         if (i >= bi) continue;
 #pragma unroll
         for (int q = 0; q < 8; q++) {
-            const int j = tx + 16 * q;
+            const int j = tile_col(q);
             if (j >= bj || (I == J && j < i)) continue;
-            W[(int64_t)(i0 + i) * ld + j0 + j] = Cs[i * B + j] - acc[p][q];
+            W[(int64_t)(i0 + i) * ld + j0 + j] = Cs[i * SLD + j] - acc[p][q];  // padded rows: conflict-free
         }
     }
     if (P.fuse && I == K + 1 && J == K + 1) {  // fused next pivot: P_{K+1} = (updated M_{K+1,K+1})^-1
