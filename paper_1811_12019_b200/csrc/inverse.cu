@@ -31,7 +31,7 @@ namespace kfac {
 constexpr int kMaxMats = 128;
 constexpr int B = kPanel;     // 128
 constexpr int KC = 16;        // K rows per smem chunk of the tile product
-constexpr int kPivSmem = (B * (B + 1) + 2 * 32 * B + 32 * 32) * 8 + 64;
+constexpr int kPivSmem = (B * (B + 1) + 2 * 32 * (B + 4) + 32 * 32) * 8 + 64;
 constexpr int kTileSmem = 2 * 2 * KC * (B + 4) * 8;  // double-buffered A/B chunks (padded rows): 66 KB
 constexpr int kUpdSmem = kPivSmem > kTileSmem + B * (B + 4) * 8 ? kPivSmem : kTileSmem + B * (B + 4) * 8;
 constexpr int kPanelSmem = B * (B + 1) * 8 > kTileSmem ? B * (B + 1) * 8 : kTileSmem;
@@ -55,6 +55,23 @@ struct InvParams {
 
 __device__ __forceinline__ int64_t poff(int64_t i, int64_t j, int64_t n) {  // packed upper (i <= j)
     return i * n - i * (i - 1) / 2 + (j - i);
+}
+
+// DMMA (mma.sync m8n8k4 f64) 128 x 128 tile fragment mapping: warp w owns rows
+// 64*(w>>2) + [0, 64) and columns 32*(w&3) + [0, 32) as 8 x 4 m8n8 blocks.
+constexpr int SLD = B + 4;
+__device__ __forceinline__ int tile_row(int p) {
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    return 64 * (w >> 2) + 8 * p + (lane >> 2);
+}
+__device__ __forceinline__ int tile_col(int q) {
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    return 32 * (w & 3) + 8 * (q >> 1) + 2 * (lane & 3) + (q & 1);
+}
+__device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
 }
 
 // ---- prologue: traces -> pi and the damping of each (A, G) pair
@@ -115,7 +132,6 @@ __global__ void unpack_damp_kernel(const __grid_constant__ InvParams P) {
 //   S_IJ -= O_I^T W_J,  S_sJ = W_J,  S_Is = W_I^T,  S_ss = -Q   (O = old block row s, W = Q O).
 // Returns 0 or the failing pivot index + 1 (the sweep pivots are the LDL^T pivots).
 constexpr int S2 = 32;  // sub-pivot size
-constexpr int kPivSmemBytes = (B * (B + 1) + 2 * S2 * B + S2 * S2) * 8 + 64;
 
 // scalar sweep of the 32 x 32 sub-pivot (smem, row-major, ping-pong buffers Q / Q2) by all 256
 // threads (4 elements each), one barrier per pivot; the result -inv(sub-pivot) ends in Q (an even
@@ -154,12 +170,11 @@ __device__ long long g_pclk[64];
 __device__ int pivot_block(const double *__restrict__ W, int64_t ld, int k0, int bk, double *__restrict__ Pout,
                            double *smem) {
     double(*S)[B + 1] = reinterpret_cast<double(*)[B + 1]>(smem);
-    double *O = smem + B * (B + 1);       // [S2][B] old block row
-    double *Wr = O + S2 * B;              // [S2][B] Q * O
-    double *Q = Wr + S2 * B;              // [S2][S2] inverse of the sub-pivot
+    double *O = smem + B * (B + 1);       // [S2][SLD] old block row
+    double *Wr = O + S2 * SLD;            // [S2][SLD] Q * O
+    double *Q = Wr + S2 * SLD;            // [S2][S2] inverse of the sub-pivot
     int *fsh = reinterpret_cast<int *>(Q + S2 * S2);
     const int tid = threadIdx.x;
-    const int tx = tid & 15, ty = tid >> 4;
     for (int e = tid; e < B * B; e += blockDim.x) {
         const int i = e >> 7, j = e & (B - 1);
         double val = (i == j) ? 1.0 : 0.0;  // identity padding keeps the sweep well defined
@@ -180,7 +195,7 @@ __device__ int pivot_block(const double *__restrict__ W, int64_t ld, int k0, int
             for (int e = tid; e < S2 * S2; e += blockDim.x) Q[e] = -Q[e];
         }
         PCLK(1 + 4 * sb)
-        for (int e = tid; e < S2 * B; e += blockDim.x) O[e] = S[s0 + (e >> 7)][e & (B - 1)];
+        for (int e = tid; e < S2 * B; e += blockDim.x) O[(e >> 7) * SLD + (e & (B - 1))] = S[s0 + (e >> 7)][e & (B - 1)];
         __syncthreads();
         if (*fsh) break;
         PCLK(2 + 4 * sb)
@@ -194,47 +209,53 @@ __device__ int pivot_block(const double *__restrict__ W, int64_t ld, int k0, int
 #pragma unroll
             for (int k = 0; k < S2 / 2; k++) w[k] = 0.0;
             for (int b2 = 0; b2 < S2; b2++) {
-                const double o = O[b2 * B + j];
+                const double o = O[b2 * SLD + j];
 #pragma unroll
                 for (int k = 0; k < S2 / 2; k++) w[k] = fma(Q[(a0 + 2 * k) * S2 + b2], o, w[k]);
             }
 #pragma unroll
-            for (int k = 0; k < S2 / 2; k++) Wr[(a0 + 2 * k) * B + j] = w[k];
+            for (int k = 0; k < S2 / 2; k++) Wr[(a0 + 2 * k) * SLD + j] = w[k];
         }
         __syncthreads();
         PCLK(3 + 4 * sb)
 #ifdef PIVOT_DBG
         if (g_pivot_dbg == 2 && sb >= 1) break;
 #endif
-        // rank-32 sweep update of every element (each thread writes only its own 8 x 8 elements)
+        // rank-32 sweep update of every element on the fp64 tensor cores (DMMA); each thread then
+        // writes only its own elements
         double acc[8][8];
 #pragma unroll
         for (int p = 0; p < 8; p++)
 #pragma unroll
             for (int q = 0; q < 8; q++) acc[p][q] = 0.0;
-        for (int b2 = 0; b2 < S2; b2++) {
-            double o[8], w[8];
+        {
+            const int w = tid >> 5, lane = tid & 31;
+            const int arow = 64 * (w >> 2) + (lane >> 2), bcol = 32 * (w & 3) + (lane >> 2), kl = lane & 3;
 #pragma unroll
-            for (int q = 0; q < 8; q++) {
-                o[q] = O[b2 * B + ty + 16 * q];
-                w[q] = Wr[b2 * B + tx + 16 * q];
+            for (int kk = 0; kk < S2 / 4; kk++) {
+                const int t = kk * 4 + kl;
+                double a[8], b[4];
+#pragma unroll
+                for (int p = 0; p < 8; p++) a[p] = O[t * SLD + arow + 8 * p];
+#pragma unroll
+                for (int q = 0; q < 4; q++) b[q] = Wr[t * SLD + bcol + 8 * q];
+#pragma unroll
+                for (int p = 0; p < 8; p++)
+#pragma unroll
+                    for (int q = 0; q < 4; q++) dmma(acc[p][2 * q], acc[p][2 * q + 1], a[p], b[q]);
             }
-#pragma unroll
-            for (int p = 0; p < 8; p++)
-#pragma unroll
-                for (int q = 0; q < 8; q++) acc[p][q] = fma(o[p], w[q], acc[p][q]);
         }
 #pragma unroll
         for (int p = 0; p < 8; p++) {
-            const int i = ty + 16 * p;
+            const int i = tile_row(p);
             const bool is = (i >= s0 && i < s0 + S2);
 #pragma unroll
             for (int q = 0; q < 8; q++) {
-                const int j = tx + 16 * q;
+                const int j = tile_col(q);
                 const bool js = (j >= s0 && j < s0 + S2);
                 // clamped indices: every load is in range whatever the compiler speculates
                 const int ii = min(max(i - s0, 0), S2 - 1), jj = min(max(j - s0, 0), S2 - 1);
-                const double vq = Q[ii * S2 + jj], vwi = Wr[ii * B + j], vwj = Wr[jj * B + i];
+                const double vq = Q[ii * S2 + jj], vwi = Wr[ii * SLD + j], vwj = Wr[jj * SLD + i];
                 const double v = is ? (js ? -vq : vwi) : (js ? vwj : S[i][j] - acc[p][q]);
                 S[i][j] = v;
             }
@@ -280,20 +301,6 @@ __device__ __forceinline__ void cp_async_wait_0() { asm volatile("cp.async.wait_
 // element (tile_row(p), tile_col(q)) below.  A and Bm are row-major with 16-aligned leading
 // dimensions; columns >= acols / bcols and rows >= kt read as zero.  Chunks of KC rows are
 // double-buffered with cp.async; shared rows are padded to 132 doubles (conflict-free fragments).
-constexpr int SLD = B + 4;
-__device__ __forceinline__ int tile_row(int p) {
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    return 64 * (w >> 2) + 8 * p + (lane >> 2);
-}
-__device__ __forceinline__ int tile_col(int q) {
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    return 32 * (w & 3) + 8 * (q >> 1) + 2 * (lane & 3) + (q & 1);
-}
-__device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                 : "+d"(c0), "+d"(c1)
-                 : "d"(a), "d"(b));
-}
 struct NoExtra {
     __device__ __forceinline__ void operator()(int, int) const {}
 };
@@ -404,13 +411,19 @@ __global__ void __launch_bounds__(256, 1) panel_kernel(const __grid_constant__ I
 // inverts that block: the next step's pivot runs concurrently with this step's update.
 // Global tile order: first every matrix's (K+1, K+1) tile (so the fused pivots start at once),
 // then the remaining upper tiles matrix by matrix, row-major.  Persistent CTAs stride over it.
-__device__ __forceinline__ void update_tile(const InvParams &P, int g, double *dyn) {
+__device__ __forceinline__ void update_tile(const InvParams &P, int g, double *dyn, const int *sbeg,
+                                            const int *spiv) {
     int mi = 0, t = 0;
     if (g < P.npiv) {
-        while (P.m[mi].piv_idx != g) mi++;
-    } else {
-        while (mi + 1 < P.nm && P.m[mi + 1].tile_begin <= g) mi++;
-        t = g - P.m[mi].tile_begin + (P.m[mi].piv_idx >= 0 ? 1 : 0);
+        while (spiv[mi] != g) mi++;
+    } else {  // binary search of the (shared-memory copy of the) tile prefix
+        int lo = 0, hi = P.nm - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (sbeg[mid] <= g) lo = mid; else hi = mid - 1;
+        }
+        mi = lo;
+        t = g - sbeg[mi] + (spiv[mi] >= 0 ? 1 : 0);
     }
     const MatDesc &m = P.m[mi];
     const int n = m.n, k0 = P.k * B;
@@ -498,13 +511,18 @@ __device__ __forceinline__ void update_tile(const InvParams &P, int g, double *d
 __global__ void __launch_bounds__(256, 1) update_kernel(const __grid_constant__ InvParams P) {
     extern __shared__ double dyn[];
     __shared__ int next;
+    __shared__ int sbeg[kMaxMats], spiv[kMaxMats];  // decode tables (dynamic param indexing is slow)
+    for (int i = threadIdx.x; i < P.nm; i += blockDim.x) {
+        sbeg[i] = P.m[i].tile_begin;
+        spiv[i] = P.m[i].piv_idx;
+    }
     for (;;) {
         __syncthreads();  // the previous tile's epilogue / pivot is done with shared memory and `next`
         if (threadIdx.x == 0) next = atomicAdd(P.counter, 1);
         __syncthreads();
         const int g = next;
         if (g >= P.total_tiles) break;
-        update_tile(P, g, dyn);
+        update_tile(P, g, dyn, sbeg, spiv);
     }
 }
 
