@@ -158,7 +158,8 @@ KFAC_API void kfac_comm_destroy(kfac_comm_t comm);
  * last).  Inputs are half precision, products are accumulated in fp32 on the
  * tensor cores.  alpha = 1/rows is the paper's mean (R-3).
  * `ws` is scratch of at least kfac_factor_ws_bytes(..., which=0) bytes (split-K
- * partials); it may be NULL when that size is 0.
+ * partials + the work-item counter of the dynamic tile schedule, zeroed by the
+ * call on `stream`); it may be NULL (no split-K, static tile schedule).
  * Errors: KFAC_ERR_ARG, KFAC_ERR_UNSUPPORTED (e.g. dilation-like geometry the
  * descriptor cannot express), KFAC_ERR_CUDA.                                */
 KFAC_API kfac_status kfac_factor_A(const kfac_layer_desc *layer /* host */, const void *x, kfac_dtype dtype, int32_t n,

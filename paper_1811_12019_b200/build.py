@@ -53,6 +53,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objs = []
     common = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-fvisibility=hidden", "-I", CSRC,
               "-I", os.path.join(ROOT, "include"), "-I", inc]
+    common += os.environ.get("KFAC_NVCC_EXTRA", "").split()  # experiments only (e.g. -DKFAC_MBAR_MODE=1)
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
         cmd = ["nvcc", *ARCH, *common, "-c", src, "-o", obj]

@@ -4,23 +4,31 @@
 //     G = alpha * sum_rows g gᵀ   over output-gradient pixels g
 // as ONE grouped, persistent tcgen05 SYRK launch over every (layer, factor):
 //
-//   * operands are staged by TMA straight from the NHWC activation tensor:
-//     2-D tiled boxes for G / 1x1 convs / FC, im2col boxes (cuTensorMapEncode-
-//     Im2col) for k>1 or strided convs -- patch extraction is fused into the
-//     shared-memory staging, no im2col matrix is materialised;
+//   * output tiles are 256 x 256 (upper tiles ti <= tj only): per 16-row K step
+//     two tcgen05.mma kind::f16 M=128 x N=256 (bf16/fp16 in, fp32 accumulate in
+//     TMEM, "mixed precision") share one B operand, so a stage of
+//     64 pixel rows x (256 + 256) features feeds 2 x 128 x 256 x 64 MACs; on a
+//     diagonal tile A == B (loaded once) and the lower half's MMA is N = 128;
+//   * operands are staged by TMA straight from the NHWC activation tensor, in
+//     slots of cb (64) channels, MN-major SW128, K = pixels.  One TMA box
+//     carries S (up to 4) consecutive channel slots of one filter tap
+//     (3-D map {cb, rows, C/cb} for G / 1x1 convs / FC, 5-D map
+//     {cb, W, H, N, C/cb} for k>1 or strided convs): patch extraction is fused
+//     into the shared-memory staging, no im2col matrix is materialised.  Every
+//     chunk is exactly 64 pixel rows: the box width is the output width rounded
+//     up to a power of two and the phantom columns are zero-filled by the TMA
+//     out-of-bounds rule (one descriptor per distinct right edge, i.e. per
+//     filter column), so the 16-row MMA steps never read past a slot;
 //     a gather producer (plain loads) covers the geometries TMA cannot
-//     express (channel stride not a multiple of 16 B, e.g. the RGB stem);
-//   * the MMA is tcgen05.mma kind::f16 (bf16/fp16 in, fp32 accumulate in
-//     TMEM, "mixed precision"), M = N = 128, both operands
-//     MN-major (the channel dimension is contiguous in NHWC; K = pixels);
-//   * only upper tiles (ti <= tj) are computed and each output element is
-//     written once, packed upper row-major, straight into the
-//     ReduceScatter send buffer;
+//     express; the RGB stem (3 channels, 6 B pixels) is materialised once;
+//   * each output element is written once, packed upper row-major
+//     (P:407-411), straight into the ReduceScatter send buffer;
 //   * large-K/small-d problems are split along K with a deterministic,
 //     ordered fix-up (reading R-18).
 //
-// Warp roles (288 threads): warps 0-3 epilogue (TMEM -> smem -> packed
-// global), warp 4 TMEM allocator + MMA issuer, warps 5-8 producers.
+// Warp roles (416 threads): warps 0-7 epilogue (TMEM -> smem -> packed
+// global; warp w drains rows 32*(w%4).. of accumulator half w/4), warp 8 TMEM
+// allocator + MMA issuer, warps 9-12 TMA producers (lane 0 issues).
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -34,26 +42,35 @@
 
 namespace kfac {
 
-constexpr int kStages = 4;
-constexpr int kEpiThreads = 128;
-constexpr int kMmaWarp = 4;
-constexpr int kProdWarp0 = 5;
-constexpr int kProdThreads = 128;
-constexpr int kThreads = kEpiThreads + 32 + kProdThreads;  // 288
-constexpr int kOpA = kTileM * kBK * 2;                      // 16 KB A operand per stage
-constexpr int kOpB = kTileN * kBK * 2;                      // 32 KB B operand per stage
-constexpr int kStageBytes = kOpA + kOpB;
-constexpr int kQ = 32;                                      // epilogue column group (one tcgen05.ld x32)
-constexpr int kStageLd = kQ + 1;                            // staging row stride (floats, conflict-free)
-constexpr int kTmemCols = 2 * kTileN;                       // double-buffered 128 x 256 fp32 accumulator
+constexpr int kStages = 3;
+constexpr int kHalf = 128;                                  // MMA M
+constexpr int kEpiWarps = 8;
+constexpr int kEpiThreads = kEpiWarps * 32;
+constexpr int kMmaWarp = kEpiWarps;
+constexpr int kProdWarp0 = kEpiWarps + 1;
+#ifndef KFAC_PROD_WARPS
+#define KFAC_PROD_WARPS 4
+#endif
+constexpr int kProdWarps = KFAC_PROD_WARPS;
+constexpr int kProdThreads = kProdWarps * 32;
+#ifndef KFAC_ISSUE_LANES
+#define KFAC_ISSUE_LANES 1
+#endif
+constexpr int kIssueLanes = KFAC_ISSUE_LANES;                              // TMA-issuing lanes per producer warp
+constexpr int kIssuers = kProdWarps * kIssueLanes;
+constexpr int kThreads = kEpiThreads + 32 + kProdThreads;  // 416
+constexpr int kOp = kTile * kBK * 2;                        // 32 KB operand (256 features x 64 rows)
+constexpr int kStageBytes = 2 * kOp;
+constexpr int kQ = 16;                                      // epilogue column group (one tcgen05.ld x16)
+constexpr int kStageLd = 20;                                // staging row stride (floats; v4 stores conflict-free)
+constexpr int kTmemCols = 2 * kTile;                        // two 128 x 256 fp32 accumulators
 constexpr size_t kSmemOps = (size_t)kStages * kStageBytes;
-constexpr size_t kSmemStage = (size_t)kTileM * kStageLd * 4;
+constexpr size_t kSmemStage = (size_t)kEpiWarps * 32 * kStageLd * 4;
 constexpr size_t kSmemHdr = (size_t)kMaxProbs * 24;         // per-problem decode table
-constexpr size_t kSmemBytes = 1024 + kSmemOps + kSmemStage + kSmemHdr + 256;
+constexpr int kQueue = 4;                                   // work-item queue depth (items the producers may run ahead)
+constexpr int kConsumerWarps = kProdWarps + 1 + kEpiWarps;  // warps that read every queue entry
+constexpr size_t kSmemBytes = 1024 + kSmemOps + kSmemStage + kSmemHdr + 512;
 static_assert(kSmemBytes <= 232448, "shared memory budget");
-
-// zero rows for the K tail of short chunks, copied by the async proxy (cp.async.bulk)
-__device__ __align__(128) uint4 g_zero_rows[kBK * 8];  // 64 rows x 128 B
 
 __device__ __forceinline__ float dec_half(uint16_t b, int fmt) {
     if (fmt == 1) return __half2float(__ushort_as_half(b));
@@ -64,23 +81,22 @@ struct ItemInfo {
     int p, ti, tj, split, tp, k0, k1;
 };
 
-// tile pair tp -> (ti, tj): row tiles of 128, column tiles of 256, tj >= ti/2 (touches the upper triangle)
-__device__ __forceinline__ void decode_pair(int tp, int ntm, int ntn, int &ti, int &tj) {
+// tile pair tp -> (ti, tj), ti <= tj, row-major over the upper triangle of an nt x nt tile grid
+__device__ __forceinline__ void decode_pair(int tp, int nt, int &ti, int &tj) {
     int t = 0, rem = tp;
-    while (rem >= ntn - t / 2) {
-        rem -= ntn - t / 2;
+    while (rem >= nt - t) {
+        rem -= nt - t;
         t++;
     }
     ti = t;
-    tj = t / 2 + rem;
+    tj = t + rem;
 }
 
 // per-problem decode fields, copied to shared memory once per CTA (dynamic indexing of the
 // kernel-parameter array goes through the constant cache and is slow)
 struct ProbHdr {
     int32_t item_begin, npairs, kchunks, cps;
-    int16_t ntm, ntn;
-    int32_t pad;
+    int32_t nt, pad;
 };
 static_assert(sizeof(ProbHdr) == 24, "ProbHdr");
 
@@ -96,7 +112,7 @@ __device__ __forceinline__ ItemInfo decode_item(const ProbHdr *hdr, int nprobs, 
     // split-major: concurrently running CTAs share the same K rows (L2 reuse)
     it.split = local / h.npairs;
     it.tp = local - it.split * h.npairs;
-    decode_pair(it.tp, h.ntm, h.ntn, it.ti, it.tj);
+    decode_pair(it.tp, h.nt, it.ti, it.tj);
     it.p = lo;
     it.k0 = it.split * h.cps;
     it.k1 = min(h.kchunks, it.k0 + h.cps);
@@ -105,7 +121,8 @@ __device__ __forceinline__ ItemInfo decode_item(const ProbHdr *hdr, int nprobs, 
 
 // register copy of the fields a role needs for one work item
 struct ProbRegs {
-    int mode, d, d_out, cb, rpc, ksteps, bh, bn, rpi, c, h, w, ho, wo, kh, kw, sh, sw, ph, pw, splits, npairs;
+    int mode, d, d_out, cb, S, ksteps, bh, bn, rpi, c, h, w, ho, wo, kh, kw, sh, sw, ph, pw, splits, npairs, map0;
+    uint64_t mapj;
     float alpha;
     float *out, *partial;
     const uint16_t *src;
@@ -113,10 +130,11 @@ struct ProbRegs {
 };
 __device__ __forceinline__ ProbRegs load_prob(const FactorProb &g) {
     ProbRegs r;
-    r.mode = g.mode; r.d = g.d; r.d_out = g.d_out; r.cb = g.cb; r.rpc = g.rpc; r.ksteps = g.ksteps;
+    r.mode = g.mode; r.d = g.d; r.d_out = g.d_out; r.cb = g.cb; r.S = g.S; r.ksteps = g.ksteps;
     r.bh = g.bh; r.bn = g.bn; r.rpi = g.rpi; r.c = g.c; r.h = g.h; r.w = g.w; r.ho = g.ho; r.wo = g.wo;
     r.kh = g.kh; r.kw = g.kw; r.sh = g.sh; r.sw = g.sw; r.ph = g.ph; r.pw = g.pw; r.splits = g.splits;
-    r.npairs = g.npairs; r.alpha = g.alpha; r.out = g.out; r.partial = g.partial; r.src = g.src; r.rows = g.rows;
+    r.npairs = g.npairs; r.map0 = g.map0; r.mapj = g.mapj; r.alpha = g.alpha; r.out = g.out;
+    r.partial = g.partial; r.src = g.src; r.rows = g.rows;
     return r;
 }
 
@@ -137,10 +155,10 @@ __device__ __forceinline__ float gather_elem(const ProbRegs &pr, int fmt, int64_
     return dec_half(__ldg(pr.src + (((n * pr.h + h) * pr.w + w) * pr.c + c)), fmt);
 }
 
-// gather producer: fill `nfeat` features (from f_base) x 64 rows in the SW128 MN-major layout
-__device__ __forceinline__ void gather_tile(const ProbRegs &pr, int fmt, uint8_t *dst, int f_base, int nfeat,
-                                            int kc, int tid) {
-    const int nq = nfeat / 8;  // 16-byte chunks per row
+// gather producer: fill 256 features (from f_base) x 64 rows in the SW128 MN-major slot layout
+// (cb = 64), zero outside the matrix
+__device__ __forceinline__ void gather_tile(const ProbRegs &pr, uint8_t *dst, int f_base, int kc, int tid) {
+    constexpr int nq = kTile / 8;  // 16-byte chunks per row
     const int hw = pr.ho * pr.wo;
     for (int u = tid; u < kBK * nq; u += kProdThreads) {
         const int r = u / nq, q = u - r * nq;
@@ -171,74 +189,93 @@ __device__ __forceinline__ void gather_tile(const ProbRegs &pr, int fmt, uint8_t
                 }
             }
         }
-        (void)fmt;
         const int box = q >> 3, cq = q & 7;
         uint8_t *p = dst + box * (kBK * 128) + r * 128 + ((cq ^ (r & 7)) << 4);
         *reinterpret_cast<uint4 *>(p) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
     }
 }
 
-// chunk -> (image, first output row) for MODE_TILED4D
-__device__ __forceinline__ void chunk_origin(const ProbRegs &pr, int kc, int &n, int &oh0) {
-    if (pr.bh < pr.ho) {
-        n = kc / pr.rpi;
-        oh0 = (kc - n * pr.rpi) * pr.bh;
-    } else {
-        n = kc * pr.bn;
-        oh0 = 0;
-    }
-}
-
-// The TMA boxes of one chunk: first the B operand (256 features at fb), then -- unless A is
-// contained in B -- the A operand (128 features at fa); one box per cb-channel slot.  Issuer w
-// (of kIssuers producer warps) issues boxes k = w, w + kIssuers, ...  Returns the bytes it
-// asked for (for its expect_tx).
-constexpr int kIssuers = 4;
-__device__ __forceinline__ uint32_t issue_boxes(const ProbRegs &pr, const CUtensorMap *tmap, uint8_t *a, uint8_t *b,
-                                                uint64_t *bar, int fa, int fb, bool a_in_b, int kc, int w, bool go) {
-    const int cb = pr.cb;
-    const uint32_t slot = kBK * cb * 2;
-    const uint32_t box_bytes = (uint32_t)pr.rpc * cb * 2;
-    int n = 0, oh0 = 0;
-    if (pr.mode == MODE_TILED4D) chunk_origin(pr, kc, n, oh0);
-    const int nbb = kTileN / cb, nba = a_in_b ? 0 : kTileM / cb;
-    uint32_t bytes = 0;
-    for (int k = w; k < nbb + nba; k += kIssuers) {
-        const bool isB = k < nbb;
-        const int slot_i = isB ? k : k - nbb;
-        const int f0 = (isB ? fb : fa) + slot_i * cb;
-        if (f0 >= pr.d) continue;
-        bytes += box_bytes;
-        if (!go) continue;
-        uint8_t *dst = (isB ? b : a) + slot_i * slot;
-        if (pr.mode == MODE_TILED2D) {
-            tma_load_2d(dst, tmap, bar, f0, kc * kBK);
-        } else {
-            const int kk = f0 / pr.c, c0 = f0 - kk * pr.c;
-            const int i = kk / pr.kw, j = kk - i * pr.kw;
-            tma_load_4d(dst, tmap, bar, c0, j - pr.pw, oh0 * pr.sh - pr.ph + i, n);
+// The TMA boxes of one stage: operand B (256 features from fb), then -- off the diagonal --
+// operand A (from fa); box b of an operand carries features [f_base + b*cb*S, +cb*S) = S channel
+// slots of one filter tap.  Issuer w owns boxes k = w, w + kIssuers, ... of the stage; the
+// chunk-independent part of each owned box (destination, descriptor, tap offsets, slot) is
+// decoded once per work item, so the per-chunk issue loop is a handful of integer ops.
+constexpr int kMaxOwned = 8;  // 2 operands x <= 16 boxes (cb * S >= 16) / kIssuers
+static_assert(2 * kTile / 16 <= kMaxOwned * kIssuers, "owned box list");
+struct OwnedBoxes {
+    uint32_t dst[kMaxOwned];   // byte offset in the stage
+    uint32_t tap[kMaxOwned];   // map index | (dw + 128) << 8 | (dh + 128) << 16 | slot << 24 (TILED4D)
+    int n, bytes;
+};
+__device__ __forceinline__ void own_boxes(const ProbRegs &pr, int fa, int fb, bool diag, int w, OwnedBoxes &ob) {
+    const int fpb = pr.cb * pr.S;
+    const uint32_t box_bytes = (uint32_t)kBK * fpb * 2;  // S slots of kBK rows
+    ob.n = 0;
+    ob.bytes = 0;
+    int k = 0;
+    for (int op = 0; op < (diag ? 1 : 2); op++) {
+        const int f_base = op == 0 ? fb : fa;
+        const uint32_t base = op == 0 ? kOp : 0;
+        const int nbox = (min(kTile, pr.d - f_base) + fpb - 1) / fpb;
+        for (int b = 0; b < nbox; b++, k++) {
+            if (k % kIssuers != w || ob.n >= kMaxOwned) continue;
+            const int f0 = f_base + b * fpb;
+            uint32_t tap;
+            if (pr.mode == MODE_TILED2D) {
+                tap = (uint32_t)pr.map0 | ((uint32_t)(f0 / pr.cb) << 24);
+            } else {
+                const int kk = f0 / pr.c, c0 = f0 - kk * pr.c;
+                const int i = kk / pr.kw, j = kk - i * pr.kw;
+                const int mi = pr.map0 + (int)((pr.mapj >> (8 * j)) & 0xff);
+                tap = (uint32_t)mi | ((uint32_t)(j - pr.pw + 128) << 8) | ((uint32_t)(i - pr.ph + 128) << 16) |
+                      ((uint32_t)(c0 / pr.cb) << 24);
+            }
+            ob.dst[ob.n] = base + b * box_bytes;
+            ob.tap[ob.n] = tap;
+            ob.n++;
+            ob.bytes += box_bytes;
         }
     }
-    return bytes;
 }
 
-// zero rows [from, kBK) of every slot of one operand region (async proxy, completes on bar)
-__device__ __forceinline__ uint32_t zero_tail(uint8_t *region, int nslots, int cb, int from, uint64_t *bar, bool go) {
-    const uint32_t slot = kBK * cb * 2, bytes = (uint32_t)(kBK - from) * cb * 2;
-    if (go)
-        for (int s = 0; s < nslots; s++) bulk_load(region + s * slot + from * cb * 2, g_zero_rows, bytes, bar);
-    return bytes * nslots;
+// Work distribution: items are handed out in order (heaviest first) by a global atomic counter,
+// one at a time, to whichever CTA asks -- a dynamic longest-processing-time schedule.  Producer
+// warp 0 fetches item s on demand into a kQueue-deep shared-memory queue; every role reads the
+// same sequence.  Without a counter the CTA takes items blockIdx.x + s * gridDim.x.
+__device__ __forceinline__ int next_item(uint32_t s, const FactorParams &P, int *qitem, uint64_t *qfull,
+                                         uint64_t *qempty, bool scheduler, int lane) {
+    const int slot = (int)(s % kQueue);
+    const uint32_t ph = (s / kQueue) & 1;
+    if (scheduler && lane == 0) {
+        mbar_wait(&qempty[slot], ph ^ 1);
+        qitem[slot] = P.counter ? atomicAdd(P.counter, 1) : (int)(blockIdx.x + s * gridDim.x);
+        mbar_arrive(&qfull[slot]);
+    }
+    mbar_wait(&qfull[slot], ph);
+    const int item = qitem[slot];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&qempty[slot]);
+    return item;
 }
+
+#ifdef KFAC_FACTOR_PROF  // experiment build only: per-role cycle accounting printed by CTAs 0 and 100
+#define FPROF(...) __VA_ARGS__
+#else
+#define FPROF(...)
+#endif
 
 __global__ void __launch_bounds__(kThreads, 1) factor_syrk_kernel(const __grid_constant__ FactorParams P) {
+    FPROF(long long pf_start = clock64(); long long pf_a = 0, pf_b = 0, pf_c = 0; int pf_n = 0;)
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t *ops = smem;
     float *stage_buf = reinterpret_cast<float *>(smem + kSmemOps);
     ProbHdr *hdr = reinterpret_cast<ProbHdr *>(smem + kSmemOps + kSmemStage);
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + kSmemOps + kSmemStage + kSmemHdr);
-    uint64_t *full = bars, *empty = bars + kStages, *tfull = bars + 2 * kStages, *tempty = bars + 2 * kStages + 2;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * kStages + 4);
+    uint64_t *full = bars, *empty = bars + kStages, *tfull = bars + 2 * kStages, *tempty = bars + 2 * kStages + 1;
+    uint64_t *qfull = bars + 2 * kStages + 3, *qempty = qfull + kQueue;
+    int *qitem = reinterpret_cast<int *>(qempty + kQueue);
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(qitem + kQueue);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nprobs = P.nprobs;
@@ -248,90 +285,98 @@ __global__ void __launch_bounds__(kThreads, 1) factor_syrk_kernel(const __grid_c
         h.npairs = P.probs[p].npairs;
         h.kchunks = P.probs[p].kchunks;
         h.cps = P.probs[p].chunks_per_split;
-        h.ntm = P.probs[p].ntm;
-        h.ntn = P.probs[p].ntn;
+        h.nt = P.probs[p].nt;
         h.pad = 0;
         hdr[p] = h;
     }
-    // operand stages start zeroed: the K tail rows of short chunks then stay zero until a
-    // longer chunk dirties them (tracked by the issuer, re-zeroed with bulk copies)
-    for (size_t i = threadIdx.x; i < kSmemOps / 16; i += blockDim.x)
-        reinterpret_cast<uint4 *>(ops)[i] = make_uint4(0u, 0u, 0u, 0u);
-    fence_proxy_async_smem();
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; s++) {
             mbar_init(&full[s], kIssuers);
             mbar_init(&empty[s], 1);
         }
-        for (int b = 0; b < 2; b++) {
-            mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], kEpiThreads);
+        mbar_init(tfull, 1);
+        mbar_init(&tempty[0], kEpiThreads / 2);
+        mbar_init(&tempty[1], kEpiThreads / 2);
+        for (int q = 0; q < kQueue; q++) {
+            mbar_init(&qfull[q], 1);
+            mbar_init(&qempty[q], kConsumerWarps);
         }
         fence_barrier_init();
     }
     if (warp == kMmaWarp) tmem_alloc(tmem_slot, kTmemCols);
     if (warp == kProdWarp0) {
-        for (int p = lane; p < nprobs; p += 32)
-            if (P.probs[p].mode != MODE_GATHER) tma_prefetch(&P.probs[p].tmap);
+        for (int m = lane; m < P.nmaps; m += 32) tma_prefetch(&P.maps[m]);
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     const int mma_fmt = P.ab_fmt == 1 ? 0 : 1;  // kind::f16 A/B format: 0 fp16, 1 bf16
-    const int dec_fmt = P.ab_fmt;                // kfac_dtype: 0 bf16, 1 fp16
     const int dbg = P.dbg;
+    const bool no_mma = dbg == 1 || dbg == 4, no_tma = dbg >= 2, no_store = dbg == 5;
     const int total = P.total_items;
 
     if (warp >= kProdWarp0) {
         // ============================ producers ============================
-        // 4 warps; lane 0 of each issues a quarter of the TMA boxes of every stage (the TMA engine
-        // overlaps boxes from different issuers); all 128 threads gather in MODE_GATHER.
+        // lanes 0..kIssueLanes-1 of each warp issue a share of the TMA boxes of every stage (the
+        // TMA engine overlaps boxes from different issuers); all 128 threads gather in MODE_GATHER.
         const int ptid = threadIdx.x - kProdWarp0 * 32;
-        const int pw = warp - kProdWarp0;
+        const int wid = (warp - kProdWarp0) * kIssueLanes + lane;
+        const bool issuer = lane < kIssueLanes;
         uint32_t stage = 0, phase = 0;
-        int cleanA[kStages], cleanB[kStages];  // rows >= clean*[s] of that operand region are zero
-#pragma unroll
-        for (int s = 0; s < kStages; s++) cleanA[s] = cleanB[s] = 0;
-        for (int item = blockIdx.x; item < total; item += gridDim.x) {
+        for (uint32_t s = 0;; s++) {
+            const int item = next_item(s, P, qitem, qfull, qempty, warp == kProdWarp0, lane);
+            if (item >= total) break;
             const ItemInfo it = decode_item(hdr, nprobs, item);
             const ProbRegs pr = load_prob(P.probs[it.p]);
-            const CUtensorMap *tmap = &P.probs[it.p].tmap;
-            // A (128 features at ti*128) is contained in B (256 features at tj*256) when tj == ti/2
-            const bool a_in_b = it.tj == it.ti / 2;
-            const int fa = it.ti * kTileM, fb = it.tj * kTileN;
-            const int written = pr.mode == MODE_TILED4D ? pr.rpc : kBK;   // rows each slot receives
-            const int needed = pr.ksteps * 16;                              // rows the MMA reads
+            const bool diag = it.ti == it.tj;
+            const int fa = it.ti * kTile, fb = it.tj * kTile;
+            OwnedBoxes ob;
+            if (pr.mode != MODE_GATHER && issuer) own_boxes(pr, fa, fb, diag, wid, ob);
+            // TILED4D chunk origin (image n, first output row oh0), advanced incrementally
+            int ig = it.k0 / pr.rpi, rg = it.k0 - ig * pr.rpi;
             for (int kc = it.k0; kc < it.k1; kc++) {
                 uint8_t *a = ops + (size_t)stage * kStageBytes;
-                uint8_t *b = a + kOpA;
+                uint8_t *b = a + kOp;
                 if (pr.mode == MODE_GATHER) {
                     mbar_wait(&empty[stage], phase ^ 1);
-                    gather_tile(pr, dec_fmt, b, fb, kTileN, kc, ptid);
-                    if (!a_in_b) gather_tile(pr, dec_fmt, a, fa, kTileM, kc, ptid);
+                    gather_tile(pr, b, fb, kc, ptid);
+                    if (!diag) gather_tile(pr, a, fa, kc, ptid);
                     fence_proxy_async_smem();
                     named_bar_sync(1, kProdThreads);
-                    if (lane == 0) mbar_arrive(&full[stage]);
-                } else if (lane == 0) {
+                    if (issuer) mbar_arrive(&full[stage]);
+                } else if (issuer) {
+                    FPROF(long long t0 = clock64();)
                     mbar_wait(&empty[stage], phase ^ 1);
-                    if (dbg >= 2) {  // debug: no TMA (measures the MMA pipeline alone)
+                    FPROF(pf_a += clock64() - t0; pf_n++; t0 = clock64();)
+                    if (no_tma) {
                         mbar_arrive(&full[stage]);
                     } else {
-                        uint32_t bytes = issue_boxes(pr, tmap, a, b, &full[stage], fa, fb, a_in_b, kc, pw, false);
-                        const bool zb = pw == 0 && cleanB[stage] > written && needed > written;
-                        const bool za = pw == 0 && !a_in_b && cleanA[stage] > written && needed > written;
-                        if (zb) bytes += zero_tail(b, kTileN / pr.cb, pr.cb, written, &full[stage], false);
-                        if (za) bytes += zero_tail(a, kTileM / pr.cb, pr.cb, written, &full[stage], false);
-                        mbar_arrive_expect_tx(&full[stage], bytes);
-                        issue_boxes(pr, tmap, a, b, &full[stage], fa, fb, a_in_b, kc, pw, true);
-                        if (zb) zero_tail(b, kTileN / pr.cb, pr.cb, written, &full[stage], true);
-                        if (za) zero_tail(a, kTileM / pr.cb, pr.cb, written, &full[stage], true);
+                        mbar_arrive_expect_tx(&full[stage], ob.bytes);
+                        const int n = ig * pr.bn, h0 = rg * pr.bh * pr.sh;
+#pragma unroll
+                        for (int q = 0; q < kMaxOwned; q++) {
+                            if (q < ob.n) {
+                                const uint32_t t = ob.tap[q];
+                                const CUtensorMap *m = &P.maps[t & 0xff];
+                                if (pr.mode == MODE_TILED2D)
+                                    tma_load_3d(a + ob.dst[q], m, &full[stage], 0, kc * kBK, (int)(t >> 24));
+                                else
+                                    tma_load_5d(a + ob.dst[q], m, &full[stage], 0, (int)((t >> 8) & 0xff) - 128,
+                                                h0 + (int)((t >> 16) & 0xff) - 128, n, (int)(t >> 24));
+                            }
+                        }
                     }
+                    FPROF(pf_c += clock64() - t0;)
                 }
-                // every producer thread tracks the same tail state (only issuer 0 acts on it)
-                cleanB[stage] = (cleanB[stage] > written && needed > written) ? written : max(cleanB[stage], written);
-                if (!a_in_b) cleanA[stage] = (cleanA[stage] > written && needed > written) ? written : max(cleanA[stage], written);
-                if (pr.mode == MODE_GATHER) cleanA[stage] = cleanB[stage] = kBK;
+                if (++rg == pr.rpi) {
+                    rg = 0;
+                    ig++;
+                }
+                // keep the non-issuing lanes in step with the issuers: an mbarrier parity wait
+                // cannot tell phases apart that are two or more apart, so a lane that ran ahead
+                // into a later gather item would see a stale "empty" phase as free
+                __syncwarp();
                 if (++stage == kStages) {
                     stage = 0;
                     phase ^= 1;
@@ -340,34 +385,48 @@ __global__ void __launch_bounds__(kThreads, 1) factor_syrk_kernel(const __grid_c
         }
     } else if (warp == kMmaWarp) {
         // ============================ MMA issuer ============================
-        uint32_t stage = 0, phase = 0;
-        uint32_t tph0 = 0, tph1 = 0;
-        int buf = 0;
-        const uint32_t idesc = idesc_f16(mma_fmt, kTileM, kTileN, 1, 1);
-        for (int item = blockIdx.x; item < total; item += gridDim.x) {
+        uint32_t stage = 0, phase = 0, tph = 0;
+        for (uint32_t s = 0;; s++) {
+            const int item = next_item(s, P, qitem, qfull, qempty, false, lane);
+            if (item >= total) break;
             const ItemInfo it = decode_item(hdr, nprobs, item);
-            const int cb = P.probs[it.p].cb, ksteps = P.probs[it.p].ksteps;
-            const bool a_in_b = it.tj == it.ti / 2;
+            const int cb = P.probs[it.p].cb, ksteps = P.probs[it.p].ksteps, d = P.probs[it.p].d;
+            const bool diag = it.ti == it.tj;
+            const int nr = min(kTile, d - it.ti * kTile), nc = min(kTile, d - it.tj * kTile);
+            const int n0 = (nc + 15) / 16 * 16;          // N of the upper-half MMA
+            const bool h1 = nr > kHalf;                   // lower half has valid rows
+            const int n1 = diag ? n0 - kHalf : n0;        // diagonal: only columns >= 128 reach the upper triangle
             const uint32_t slot = kBK * cb * 2;
             const uint32_t lbo = slot, sbo = 8 * cb * 2, lay = layout_of(cb);
             const uint32_t kstep = 16 * cb * 2;  // bytes per K=16 slice
-            const uint32_t tacc = tmem_base + buf * kTileN;
+            const uint32_t half_off = (kHalf / cb) * slot;  // features 128.. of an operand
+            const uint32_t idesc0 = idesc_f16(mma_fmt, kHalf, n0, 1, 1);
+            const uint32_t idesc1 = idesc_f16(mma_fmt, kHalf, h1 ? n1 : 16, 1, 1);
+            const uint32_t t0 = tmem_base, t1 = tmem_base + kTile + (diag ? kHalf : 0);
             if (lane == 0) {
-                mbar_wait(&tempty[buf], (buf ? tph1 : tph0) ^ 1);
+                FPROF(long long t00 = clock64();)
+                mbar_wait(&tempty[0], tph ^ 1);
+                mbar_wait(&tempty[1], tph ^ 1);
+                FPROF(pf_b += clock64() - t00;)
                 tc_fence_after();
                 for (int kc = it.k0; kc < it.k1; kc++) {
+                    FPROF(long long t1c = clock64();)
                     mbar_wait(&full[stage], phase);
+                    FPROF(pf_a += clock64() - t1c; pf_n++;)
                     tc_fence_after();
-                    const uint32_t b_base = smem_u32(ops + (size_t)stage * kStageBytes + kOpA);
-                    const uint32_t a_base = a_in_b ? b_base + (it.ti & 1) * (kTileM / cb) * slot
-                                                   : smem_u32(ops + (size_t)stage * kStageBytes);
-                    if (dbg == 1 || dbg == 4) {  // debug: no MMA (measures the TMA pipeline alone)
+                    const uint32_t b_base = smem_u32(ops + (size_t)stage * kStageBytes + kOp);
+                    const uint32_t a_base = diag ? b_base : smem_u32(ops + (size_t)stage * kStageBytes);
+                    const uint32_t b1_base = diag ? b_base + half_off : b_base;
+                    if (no_mma) {
                         mbar_arrive(&empty[stage]);
                     } else {
                         for (int k = 0; k < ksteps; k++) {
-                            uint64_t ad = umma_desc(a_base + k * kstep, lbo, sbo, lay);
-                            uint64_t bd = umma_desc(b_base + k * kstep, lbo, sbo, lay);
-                            mma_f16_ss(tacc, ad, bd, idesc, (kc > it.k0 || k > 0) ? 1u : 0u);
+                            const uint32_t acc = (kc > it.k0 || k > 0) ? 1u : 0u;
+                            mma_f16_ss(t0, umma_desc(a_base + k * kstep, lbo, sbo, lay),
+                                       umma_desc(b_base + k * kstep, lbo, sbo, lay), idesc0, acc);
+                            if (h1)
+                                mma_f16_ss(t1, umma_desc(a_base + half_off + k * kstep, lbo, sbo, lay),
+                                           umma_desc(b1_base + k * kstep, lbo, sbo, lay), idesc1, acc);
                         }
                         mma_commit(&empty[stage]);
                     }
@@ -376,66 +435,80 @@ __global__ void __launch_bounds__(kThreads, 1) factor_syrk_kernel(const __grid_c
                         phase ^= 1;
                     }
                 }
-                if (dbg == 1 || dbg == 4) mbar_arrive(&tfull[buf]);
-                else mma_commit(&tfull[buf]);
+                if (no_mma) mbar_arrive(tfull);
+                else mma_commit(tfull);
             }
             __syncwarp();
-            if (buf) tph1 ^= 1; else tph0 ^= 1;
-            buf ^= 1;
+            tph ^= 1;
         }
     } else {
         // ============================ epilogue ============================
-        uint32_t tph0 = 0, tph1 = 0;
-        int buf = 0;
-        const int row = warp * 32 + lane;
-        for (int item = blockIdx.x; item < total; item += gridDim.x) {
+        // warp w drains tile rows h*128 + 32*(w%4) + lane of accumulator half h = w/4 (a warp may
+        // only address its own 32-lane quarter of TMEM), 16 columns at a time: TMEM -> registers
+        // -> per-warp staging -> 2 rows x 64 B coalesced stores.
+        const int h = warp >> 2, quarter = warp & 3;
+        float *stg = stage_buf + warp * 32 * kStageLd;
+        const int rbase = h * kHalf + quarter * 32;  // tile row of lane 0
+        uint32_t tph = 0;
+        for (uint32_t s = 0;; s++) {
+            const int item = next_item(s, P, qitem, qfull, qempty, false, lane);
+            if (item >= total) break;
             const ItemInfo it = decode_item(hdr, nprobs, item);
             const ProbRegs pr = load_prob(P.probs[it.p]);
-            mbar_wait(&tfull[buf], buf ? tph1 : tph0);
+            FPROF(long long t0 = clock64();)
+            mbar_wait(tfull, tph);
+            FPROF(pf_a += clock64() - t0; pf_n++; t0 = clock64();)
             tc_fence_after();
-            const uint32_t tacc = tmem_base + buf * kTileN + ((uint32_t)(warp * 32) << 16);
-            const int gi0 = it.ti * kTileM, gj0 = it.tj * kTileN;
+            const bool diag = it.ti == it.tj;
+            const int nr = min(kTile, pr.d - it.ti * kTile), nc = min(kTile, pr.d - it.tj * kTile);
+            const uint32_t tacc = tmem_base + ((uint32_t)(quarter * 32) << 16) + h * kTile;
             float *part = pr.splits > 1
-                              ? pr.partial + ((size_t)it.split * pr.npairs + it.tp) * (size_t)(kTileM * kTileN)
+                              ? pr.partial + ((size_t)it.split * pr.npairs + it.tp) * (size_t)(kTile * kTile)
                               : nullptr;
             const int64_t dd = pr.d_out;
-            for (int q = 0; q < kTileN / kQ; q++) {
-                const int gq = gj0 + q * kQ;
-                const bool any = gq < pr.d && gq + kQ - 1 >= gi0;  // group has valid upper entries
-                if (any) {
-                    uint32_t r[32];
-                    tmem_ld_32x32b_x32(tacc + q * kQ, r);
+            const int gi0 = it.ti * kTile + rbase, gj0 = it.tj * kTile;
+            const int half = lane >> 4, cc = lane & 15;
+            if (rbase < nr) {
+                for (int c0 = diag ? (rbase & ~(kQ - 1)) : 0; c0 < nc; c0 += kQ) {
+                    uint32_t r[16];
+                    tmem_ld_32x32b_x16(tacc + c0, r);
                     tmem_ld_wait();
+                    float4 *srow = reinterpret_cast<float4 *>(stg + lane * kStageLd);
 #pragma unroll
-                    for (int i = 0; i < 32; i++) stage_buf[row * kStageLd + i] = __uint_as_float(r[i]);
-                }
-                if (q == kTileN / kQ - 1) {
-                    tc_fence_before();
-                    mbar_arrive(&tempty[buf]);  // accumulator drained: the MMA may reuse it
-                }
-                if (any && dbg != 5) {
-                    named_bar_sync(2, kEpiThreads);
-                    if (part) {
-                        for (int r = warp; r < kTileM; r += 4)
-                            part[(size_t)r * kTileN + q * kQ + lane] = stage_buf[r * kStageLd + lane];
-                    } else {
-                        for (int r = warp; r < kTileM; r += 4) {
-                            const int gi = gi0 + r;
-                            if (gi >= pr.d) break;
-                            const int j = lane;
-                            if (gq + j >= gi && gq + j < pr.d) {
-                                float *orow = pr.out + ((int64_t)gi * dd - (int64_t)gi * (gi - 1) / 2 - gi);
-                                orow[gq + j] = pr.alpha * stage_buf[r * kStageLd + j];
+                    for (int m = 0; m < 4; m++)
+                        srow[m] = make_float4(__uint_as_float(r[4 * m]), __uint_as_float(r[4 * m + 1]),
+                                              __uint_as_float(r[4 * m + 2]), __uint_as_float(r[4 * m + 3]));
+                    __syncwarp();
+                    if (!no_store) {
+                        if (part) {
+                            float *dst = part + (size_t)rbase * kTile + c0 + cc;
+#pragma unroll 4
+                            for (int rr = half; rr < 32; rr += 2) dst[(size_t)rr * kTile] = stg[rr * kStageLd + cc];
+                        } else {
+                            const int gj = gj0 + c0 + cc;
+#pragma unroll 4
+                            for (int rr = half; rr < 32; rr += 2) {
+                                const int gi = gi0 + rr;
+                                if (gi < pr.d && gj < pr.d && gj >= gi)
+                                    pr.out[(int64_t)gi * dd - (int64_t)gi * (gi - 1) / 2 - gi + gj] =
+                                        pr.alpha * stg[rr * kStageLd + cc];
                             }
                         }
                     }
-                    named_bar_sync(2, kEpiThreads);
+                    __syncwarp();
                 }
             }
-            if (buf) tph1 ^= 1; else tph0 ^= 1;
-            buf ^= 1;
+            tc_fence_before();
+            mbar_arrive(&tempty[h]);  // this warp's accumulator quarter drained: the MMA may reuse it
+            FPROF(pf_b += clock64() - t0;)
+            tph ^= 1;
         }
     }
+#ifdef KFAC_FACTOR_PROF
+    if ((blockIdx.x == 0 || blockIdx.x == 100) && lane == 0 && (warp == 0 || warp == kMmaWarp || warp == kProdWarp0))
+        printf("[fprof] cta %d warp %d: total %lld  waitA %lld waitB %lld body %lld n %d\n", blockIdx.x, warp,
+               clock64() - pf_start, pf_a, pf_b, pf_c, pf_n);
+#endif
     tc_fence_before();
     __syncthreads();
     if (warp == kMmaWarp) {
@@ -446,9 +519,10 @@ __global__ void __launch_bounds__(kThreads, 1) factor_syrk_kernel(const __grid_c
 
 // ordered split-K fix-up: out = alpha * sum_{s=0..S-1} partial[s] (deterministic).
 // One block per (tile pair, 8-row group); warp = row, lane = 8 columns; all S x 8 loads independent.
+constexpr int kFixRowGroups = kTile / 8;
 __global__ void __launch_bounds__(256) factor_fixup_kernel(const __grid_constant__ FactorParams P) {
-    int b = blockIdx.x >> 4;
-    const int rg = blockIdx.x & 15;
+    int b = blockIdx.x / kFixRowGroups;
+    const int rg = blockIdx.x % kFixRowGroups;
     int p = 0;
     for (; p < P.nprobs; p++) {
         const FactorProb &pr = P.probs[p];
@@ -459,15 +533,15 @@ __global__ void __launch_bounds__(256) factor_fixup_kernel(const __grid_constant
     if (p >= P.nprobs) return;
     const FactorProb &pr = P.probs[p];
     int ti, tj;
-    decode_pair(b, pr.ntm, pr.ntn, ti, tj);
+    decode_pair(b, pr.nt, ti, tj);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int r = rg * 8 + warp;
-    const int gi = ti * kTileM + r, gj0 = tj * kTileN;
+    const int gi = ti * kTile + r, gj0 = tj * kTile;
     if (gi >= pr.d) return;
-    const int jlo = max(0, gi - gj0), jhi = min(kTileN, pr.d - gj0);
+    const int jlo = max(0, gi - gj0), jhi = min(kTile, pr.d - gj0);
     if (jlo >= jhi) return;
-    const size_t tile = (size_t)kTileM * kTileN, sstride = (size_t)pr.npairs * tile;
-    const float *src = pr.partial + (size_t)b * tile + (size_t)r * kTileN + lane;
+    const size_t tile = (size_t)kTile * kTile, sstride = (size_t)pr.npairs * tile;
+    const float *src = pr.partial + (size_t)b * tile + (size_t)r * kTile + lane;
     float acc[8];
 #pragma unroll
     for (int k = 0; k < 8; k++) acc[k] = 0.f;
@@ -574,8 +648,20 @@ static bool force_gather() {
     return e && e[0] == '1';
 }
 
-// Geometry of one factor problem (no pointers): the mode the kernel will use, the
-// chunking of K, the tile grid.  Shared by plan-time sizing and launch-time setup.
+static int pow2ceil(int x) {
+    int p = 1;
+    while (p < x) p <<= 1;
+    return p;
+}
+
+// right edge (exclusive) of the input columns filter column j may touch: output columns >= wo
+// (the box's phantom columns) land at or beyond it and are zero-filled by TMA
+static int tap_width(const FactorProb *pr, int j) {
+    return std::min<int>(pr->w, (pr->wo - 1) * pr->sw - pr->pw + j + 1);
+}
+
+// Geometry of one factor problem (no pointers): the mode the kernel will use, the chunking of
+// K, the tile grid, the descriptors it needs.  Shared by plan-time sizing and launch-time setup.
 static void prob_geometry(const FactorJob &j, bool src_aligned, FactorProb *pr) {
     const Geom &g = j.g;
     if (j.is_A) {
@@ -604,98 +690,128 @@ static void prob_geometry(const FactorJob &j, bool src_aligned, FactorProb *pr) 
         pr->d_out = g.dG;
     }
     pr->rows = j.n * (int64_t)pr->ho * pr->wo;
-    pr->ntm = (pr->d + kTileM - 1) / kTileM;
-    pr->ntn = (pr->d + kTileN - 1) / kTileN;
-    pr->npairs = 0;
-    for (int ti = 0; ti < pr->ntm; ti++) pr->npairs += pr->ntn - ti / 2;
+    pr->nt = (int16_t)((pr->d + kTile - 1) / kTile);
+    pr->npairs = pr->nt * (pr->nt + 1) / 2;
     const int C = pr->c;
     const bool plain = (pr->kh == 1 && pr->kw == 1 && pr->sh == 1 && pr->sw == 1 && pr->ph == 0 && pr->pw == 0);
     const bool aligned16 = (C % 8) == 0 && src_aligned;
     int mode = MODE_GATHER, cb = 64;
+    pr->wp = (int16_t)pow2ceil(pr->wo);
+    pr->bh = pr->bn = 1;
     if (!force_gather() && aligned16) {
         if (plain) {
             mode = MODE_TILED2D;
             cb = C >= 64 ? 64 : (C > 16 ? (C > 32 ? 64 : 32) : 16);
-        } else if (C % 16 == 0 && pr->wo <= kBK && (pr->wo - 1) * pr->sw + 1 <= 256 && pr->sw <= 8 && pr->sh <= 8) {
+            if (C > cb && C % cb) cb = (C % 32 == 0) ? 32 : 16;  // slots must tile the channels
+            if (C > cb && C % cb) mode = MODE_GATHER, cb = 64;
+        } else if (C % 16 == 0 && pr->wo <= kBK && pr->kw <= 8 && pr->sw <= 8 && pr->sh <= 8 &&
+                   (pr->wp - 1) * pr->sw + 1 <= 256) {
             mode = MODE_TILED4D;
             cb = (C % 64 == 0) ? 64 : ((C % 32 == 0) ? 32 : 16);
+            for (int jj = 0; jj < pr->kw; jj++)
+                if (tap_width(pr, jj) < 1) mode = MODE_GATHER, cb = 64;  // a column of pure padding
         }
     }
     pr->im2col_pre = 0;
     pr->cp = 0;
+    int Ceff = C;
     if (mode == MODE_GATHER && !force_gather() && j.is_A && !plain && src_aligned) {
         // channel stride not a multiple of 16 B (e.g. the RGB stem): TMA cannot address the
-        // pixels, so the patches are materialised once as [rows, cp] (cp = dF rounded to 8)
+        // pixels, so the patches are materialised once as [rows, cp] (cp = dF rounded to 64)
         // and staged by the 2-D TMA path
         pr->im2col_pre = 1;
-        pr->cp = (int16_t)((pr->d + 7) / 8 * 8);
+        pr->cp = (int16_t)((pr->d + 63) / 64 * 64);
         mode = MODE_TILED2D;
-        cb = pr->cp >= 64 ? 64 : (pr->cp > 16 ? (pr->cp > 32 ? 64 : 32) : 16);
+        cb = 64;
+        Ceff = pr->cp;
     }
-    pr->mode = mode;
-    pr->cb = cb;
-    pr->bh = pr->bn = 1;
-    pr->rpi = 1;
+    pr->mode = (int8_t)mode;
+    pr->cb = (int16_t)cb;
+    // channel slots per box: consecutive slots of one tap (the box never straddles a tap)
+    int S = 1;
+    if (mode != MODE_GATHER)
+        while (cb * S * 2 <= kTile && Ceff % (cb * S * 2) == 0) S *= 2;
+    pr->S = (int16_t)S;
+    pr->ksteps = kBK / 16;
+    pr->nmaps = 0;
+    pr->mapj = 0;
     if (mode == MODE_TILED4D) {
+        // 64-row chunks: wp (pow2 >= wo) columns x bh rows (pow2 dividing ho) x bn images
         int bh = 1;
-        for (int b = 1; b <= pr->ho; b++)
-            if (pr->ho % b == 0 && b * pr->wo <= kBK) bh = b;
-        pr->bh = bh;
-        pr->rpi = pr->ho / bh;
-        pr->bn = (bh == pr->ho) ? std::max(1, kBK / (pr->ho * pr->wo)) : 1;
-        pr->rpc = pr->bn * bh * pr->wo;
-        const int64_t N = j.n;
-        pr->kchunks = bh < pr->ho ? (int)(N * pr->rpi) : (int)((N + pr->bn - 1) / pr->bn);
+        while (pr->wp * bh * 2 <= kBK && pr->ho % (bh * 2) == 0) bh *= 2;
+        pr->bh = (int16_t)bh;
+        pr->bn = (int16_t)(kBK / (pr->wp * bh));
+        pr->rpi = (int16_t)(pr->ho / bh);
+        pr->kchunks = (int)((j.n + pr->bn - 1) / pr->bn) * pr->rpi;
+        // one descriptor per distinct right edge
+        int widths[8], nw = 0;
+        for (int jj = 0; jj < pr->kw; jj++) {
+            const int wj = tap_width(pr, jj);
+            int m = 0;
+            while (m < nw && widths[m] != wj) m++;
+            if (m == nw) widths[nw++] = wj;
+            pr->mapj |= (uint64_t)m << (8 * jj);
+        }
+        pr->nmaps = (int8_t)nw;
     } else {
-        pr->rpc = kBK;
+        pr->rpi = 1;
         pr->kchunks = (int)((pr->rows + kBK - 1) / kBK);
+        if (pr->kchunks == 1) pr->ksteps = (int16_t)((pr->rows + 15) / 16);  // e.g. FC at small batch
+        pr->nmaps = mode == MODE_TILED2D ? 1 : 0;
     }
-    pr->ksteps = (pr->rpc + 15) / 16;
 }
 
-// pointers + TMA descriptor of one factor problem
-static kfac_status setup_prob(const FactorJob &j, kfac_dtype dt, FactorProb *pr) {
+// pointers + TMA descriptors of one factor problem (written to maps[0 .. nmaps))
+static kfac_status setup_prob(const FactorJob &j, kfac_dtype dt, FactorProb *pr, CUtensorMap *maps) {
     pr->src = static_cast<const uint16_t *>(j.src);
     pr->out = j.out;
     pr->alpha = j.alpha;
     if (pr->mode == MODE_GATHER) return KFAC_OK;
     kfac_status s = load_driver_fns();
     if (s) return s;
-    const int C = pr->c, cb = pr->cb;
+    const int cb = pr->cb, S = pr->S;
     const CUtensorMapDataType dty = dt == KFAC_FP16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
     const int64_t N = pr->rows / ((int64_t)pr->ho * pr->wo);
-    const int64_t bytes = N * pr->h * pr->w * (int64_t)C * 2;
-    CUresult r;
+    const int64_t bytes = N * pr->h * pr->w * (int64_t)pr->c * 2;
+    CUresult r = CUDA_SUCCESS;
     if (pr->mode == MODE_TILED2D) {
-        const int64_t W = pr->im2col_pre ? pr->cp : C;
+        // {cb channels, rows, slot} over the [rows, C] matrix
+        const int64_t W = pr->im2col_pre ? pr->cp : pr->c;
         void *base = pr->im2col_pre ? (void *)pr->col : const_cast<void *>(j.src);
-        cuuint64_t dims[2] = {(cuuint64_t)W, (cuuint64_t)pr->rows};
-        cuuint64_t strides[1] = {(cuuint64_t)W * 2};
-        cuuint32_t box[2] = {(cuuint32_t)cb, (cuuint32_t)kBK};
-        cuuint32_t es[2] = {1, 1};
-        r = g_encTiled(&pr->tmap, dty, 2, base, dims, strides, box, es,
-                       CU_TENSOR_MAP_INTERLEAVE_NONE, swz_of(cb), CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        const bool one = W < cb;  // fewer channels than a slot: zero-filled to cb
+        cuuint64_t dims[3] = {(cuuint64_t)(one ? W : cb), (cuuint64_t)pr->rows, (cuuint64_t)(one ? 1 : W / cb)};
+        cuuint64_t strides[2] = {(cuuint64_t)W * 2, (cuuint64_t)(one ? W * 2 : cb * 2)};
+        cuuint32_t box[3] = {(cuuint32_t)cb, (cuuint32_t)kBK, (cuuint32_t)S};
+        cuuint32_t es[3] = {1, 1, 1};
+        r = g_encTiled(&maps[0], dty, 3, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz_of(cb),
+                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        small_tensor_fix(&maps[0], pr->im2col_pre ? pr->rows * W * 2 : bytes);
     } else {
-        // 4-D tiled box: cb channels x Wo output columns x bh output rows x bn images of one filter
-        // tap; the tap shifts the start coordinate, the conv stride is the traversal stride and the
-        // zero padding is the TMA out-of-bounds fill.
-        cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)pr->w, (cuuint64_t)pr->h, (cuuint64_t)N};
-        cuuint64_t strides[3] = {(cuuint64_t)C * 2, (cuuint64_t)C * 2 * pr->w, (cuuint64_t)C * 2 * pr->w * pr->h};
-        cuuint32_t box[4] = {(cuuint32_t)cb, (cuuint32_t)((pr->wo - 1) * pr->sw + 1),
-                             (cuuint32_t)((pr->bh - 1) * pr->sh + 1), (cuuint32_t)pr->bn};
-        cuuint32_t es[4] = {1, (cuuint32_t)pr->sw, (cuuint32_t)pr->sh, 1};
-        r = g_encTiled(&pr->tmap, dty, 4, const_cast<void *>(j.src), dims, strides, box, es,
-                       CU_TENSOR_MAP_INTERLEAVE_NONE, swz_of(cb), CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        // {cb channels, W, H, N, slot}: the filter tap shifts the start coordinate, the conv
+        // stride is the traversal stride, padding and phantom columns are the out-of-bounds fill
+        const int C = pr->c;
+        for (int m = 0; m < pr->nmaps && r == CUDA_SUCCESS; m++) {
+            int wj = -1;
+            for (int jj = 0; jj < pr->kw; jj++)
+                if ((int)((pr->mapj >> (8 * jj)) & 0xff) == m) wj = tap_width(pr, jj);
+            cuuint64_t dims[5] = {(cuuint64_t)cb, (cuuint64_t)wj, (cuuint64_t)pr->h, (cuuint64_t)N, (cuuint64_t)(C / cb)};
+            cuuint64_t strides[4] = {(cuuint64_t)C * 2, (cuuint64_t)C * 2 * pr->w, (cuuint64_t)C * 2 * pr->w * pr->h,
+                                     (cuuint64_t)cb * 2};
+            cuuint32_t box[5] = {(cuuint32_t)cb, (cuuint32_t)((pr->wp - 1) * pr->sw + 1),
+                                 (cuuint32_t)((pr->bh - 1) * pr->sh + 1), (cuuint32_t)pr->bn, (cuuint32_t)S};
+            cuuint32_t es[5] = {1, (cuuint32_t)pr->sw, (cuuint32_t)pr->sh, 1, 1};
+            r = g_encTiled(&maps[m], dty, 5, const_cast<void *>(j.src), dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, swz_of(cb), CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            small_tensor_fix(&maps[m], bytes);
+        }
     }
     if (r != CUDA_SUCCESS) {
         char buf[200];
-        snprintf(buf, sizeof buf, "cuTensorMapEncodeTiled failed (%d) for C=%d mode=%d wo=%d bh=%d bn=%d", (int)r, C,
-                 pr->mode, pr->wo, pr->bh, pr->bn);
+        snprintf(buf, sizeof buf, "cuTensorMapEncodeTiled failed (%d) for C=%d mode=%d wo=%d bh=%d bn=%d S=%d", (int)r,
+                 pr->c, pr->mode, pr->wo, pr->bh, pr->bn, S);
         return set_error(KFAC_ERR_UNSUPPORTED, buf);
     }
-    small_tensor_fix(&pr->tmap, bytes);
     return KFAC_OK;
 }
 
@@ -734,7 +850,7 @@ kfac_status factor_prepare(const std::vector<FactorJob> &jobs, kfac_dtype dt, vo
         S = (g.kchunks + cps - 1) / cps;
         splits[i] = S;
         item_cost[i] = (double)cps * g.ksteps;
-        if (S > 1) need += (int64_t)g.npairs * S * kTileM * kTileN * 4;
+        if (S > 1) need += (int64_t)g.npairs * S * kTile * kTile * 4;
     }
     int64_t col_need = 0;
     for (int i = 0; i < nj; i++)
@@ -744,30 +860,38 @@ kfac_status factor_prepare(const std::vector<FactorJob> &jobs, kfac_dtype dt, vo
         need = 0;
     }
     if (!dry_run && col_need > ws_cap) return set_error(KFAC_ERR_ARG, "factor workspace too small for im2col staging");
+    // the work-item counter lives after the partials and im2col staging (static striding without it)
+    int32_t *counter = nullptr;
+    if (ws && ws_cap >= need + col_need + 256)
+        counter = reinterpret_cast<int32_t *>(static_cast<uint8_t *>(ws) + need + col_need);
     // heaviest items first
     std::vector<int> order(nj);
     for (int i = 0; i < nj; i++) order[i] = i;
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return item_cost[a] > item_cost[b]; });
     int64_t ws_off = 0, col_off = 0;
-    for (int base = 0; base < nj; base += kMaxProbs) {
-        FactorParams P;
+    const int dbg = getenv("KFAC_DBG_MODE") ? atoi(getenv("KFAC_DBG_MODE")) : 0;
+    for (int base = 0; base < nj;) {
+        out->params.emplace_back();
+        FactorParams &P = out->params.back();
         memset(&P, 0, sizeof(P));
         P.ab_fmt = (int)dt;
-        P.dbg = getenv("KFAC_DBG_MODE") ? atoi(getenv("KFAC_DBG_MODE")) : 0;
-        int items = 0;
-        const int cnt = std::min(kMaxProbs, nj - base);
-        for (int k = 0; k < cnt; k++) {
-            const int i = order[base + k];
-            FactorProb &pr = P.probs[k];
+        P.dbg = dbg;
+        P.counter = counter;
+        int items = 0, cnt = 0, nmaps = 0;
+        while (base + cnt < nj && cnt < kMaxProbs && nmaps + geo[order[base + cnt]].nmaps <= kMaxMaps) {
+            const int i = order[base + cnt];
+            FactorProb &pr = P.probs[cnt];
             pr = geo[i];
+            pr.map0 = (int16_t)nmaps;
             if (pr.im2col_pre) {
                 pr.col = ws ? reinterpret_cast<uint16_t *>(static_cast<uint8_t *>(ws) + need + col_off) : nullptr;
                 col_off += (pr.rows * pr.cp * 2 + 255) / 256 * 256;
             }
             if (!dry_run) {
-                kfac_status s = setup_prob(jobs[i], dt, &pr);
+                kfac_status s = setup_prob(jobs[i], dt, &pr, &P.maps[nmaps]);
                 if (s) return s;
             }
+            nmaps += pr.nmaps;
             const int S = splits[i];
             pr.chunks_per_split = (pr.kchunks + S - 1) / S;
             pr.splits = S;
@@ -775,26 +899,28 @@ kfac_status factor_prepare(const std::vector<FactorJob> &jobs, kfac_dtype dt, vo
             items += pr.npairs * S;
             if (S > 1) {
                 pr.partial = ws ? reinterpret_cast<float *>(static_cast<uint8_t *>(ws) + ws_off) : nullptr;
-                ws_off += (int64_t)pr.npairs * S * kTileM * kTileN * 4;
+                ws_off += (int64_t)pr.npairs * S * kTile * kTile * 4;
             }
+            cnt++;
         }
         P.nprobs = cnt;
+        P.nmaps = nmaps;
         P.total_items = items;
         if (!dry_run && getenv("KFAC_DEBUG")) {
             for (int k = 0; k < cnt; k++) {
                 const FactorProb &pr = P.probs[k];
                 fprintf(stderr,
-                        "[kfac] factor prob %d: d=%d rows=%lld mode=%d cb=%d rpc=%d ksteps=%d bh=%d bn=%d pairs=%d "
-                        "kchunks=%d splits=%d\n",
-                        k, pr.d, (long long)pr.rows, pr.mode, pr.cb, pr.rpc, pr.ksteps, pr.bh, pr.bn, pr.npairs,
-                        pr.kchunks, pr.splits);
+                        "[kfac] factor prob %d: d=%d rows=%lld mode=%d cb=%d S=%d ksteps=%d wp=%d bh=%d bn=%d pairs=%d "
+                        "kchunks=%d splits=%d maps=%d\n",
+                        k, pr.d, (long long)pr.rows, pr.mode, pr.cb, pr.S, pr.ksteps, pr.wp, pr.bh, pr.bn, pr.npairs,
+                        pr.kchunks, pr.splits, pr.nmaps);
             }
-            fprintf(stderr, "[kfac] factor launch: %d problems, %d items, target %.0f k-steps/item\n", P.nprobs, items,
-                    target);
+            fprintf(stderr, "[kfac] factor launch: %d problems, %d descriptors, %d items, target %.0f k-steps/item\n",
+                    P.nprobs, P.nmaps, items, target);
         }
-        out->params.push_back(P);
+        base += cnt;
     }
-    out->ws_bytes = need + col_need;
+    out->ws_bytes = need + col_need + 256;
     return KFAC_OK;
 }
 
@@ -814,6 +940,7 @@ kfac_status factor_launch(const FactorLaunch &fl, const std::vector<FactorJob> &
             KFAC_CUDA_TRY(cudaGetLastError());
         }
         int grid = std::min(P.total_items, g_num_sms ? g_num_sms : 148);
+        if (P.counter) KFAC_CUDA_TRY(cudaMemsetAsync(P.counter, 0, sizeof(int32_t), st));
         factor_syrk_kernel<<<grid, kThreads, kSmemBytes, st>>>(P);
         KFAC_LAUNCHED();
         KFAC_CUDA_TRY(cudaGetLastError());
@@ -824,7 +951,7 @@ kfac_status factor_launch(const FactorLaunch &fl, const std::vector<FactorJob> &
             if (pr.d_out != pr.d) maxbias = std::max(maxbias, pr.d + 1);
         }
         if (fix && !getenv("KFAC_NO_FIXUP")) {
-            factor_fixup_kernel<<<fix * 16, 256, 0, st>>>(P);
+            factor_fixup_kernel<<<fix * kFixRowGroups, 256, 0, st>>>(P);
             KFAC_LAUNCHED();
             KFAC_CUDA_TRY(cudaGetLastError());
         }

@@ -35,34 +35,38 @@ struct Geom {  // derived geometry of one layer
 kfac_status make_geom(const kfac_layer_desc &d, Geom *g);
 
 // ---------------------------------------------------------------- factor kernel
-constexpr int kMaxProbs = 112;   // factor problems per grouped launch
-constexpr int kTileM = 128;      // feature rows per tile (A operand, MMA M)
-constexpr int kTileN = 256;      // feature cols per tile (B operand, MMA N)
+constexpr int kMaxProbs = 100;   // factor problems per grouped launch
+constexpr int kMaxMaps = 140;    // TMA descriptors per grouped launch
+constexpr int kTile = 256;       // square output tile (two M = 128 halves x N = 256)
 constexpr int kBK = 64;          // K rows (pixels) per pipeline stage
 
 enum FactorMode : int32_t { MODE_TILED2D = 0, MODE_TILED4D = 1, MODE_GATHER = 2 };
 
-struct alignas(64) FactorProb {  // 256 B: 112 of them fit the 32 KB kernel-parameter space
-    CUtensorMap tmap;       // 128 B, used by MODE_TILED2D / MODE_TILED4D
-    const uint16_t *src;    // NHWC half input (MODE_GATHER and bias column sums)
+struct alignas(64) FactorProb {  // 128 B
+    const uint16_t *src;    // NHWC half input (MODE_GATHER, bias column sums, im2col staging)
     float *out;             // packed upper output, dimension d_out
     float *partial;         // split-K partial tiles (splits > 1)
     int64_t rows;           // K = n * ho * wo
     uint16_t *col;          // materialised im2col rows [rows, cp] (only when im2col_pre)
+    uint64_t mapj;          // TILED4D: byte j = descriptor index (relative to map0) of filter column j
     float alpha;
     int32_t d, d_out, npairs, splits, kchunks, chunks_per_split, item_begin;
-    int16_t ntm, ntn, cb;   // row tiles (128), col tiles (256), channels per TMA box (16/32/64)
-    int16_t rpc, ksteps;    // rows per K chunk (<= kBK), 16-row MMA steps per chunk
-    int16_t bh, bn, rpi;    // TILED4D: output rows / images per chunk, row groups per image
-    int16_t c, h, w, ho, wo, cp;  // cp: padded im2col width (im2col_pre)
-    int8_t mode, kh, kw, sh, sw, ph, pw, im2col_pre;
+    int16_t nt, cb, S, map0;  // tiles per side, channels per slot, slots per TMA box, first descriptor
+    int16_t ksteps, bh, bn, rpi;  // 16-row MMA steps per chunk; TILED4D rows / images per chunk, row groups
+    int16_t c, h, w, ho, wo, cp, wp;  // cp: padded im2col width (im2col_pre); wp: box width (pow2 >= wo)
+    int8_t mode, kh, kw, sh, sw, ph, pw, im2col_pre, nmaps;
 };
-static_assert(sizeof(FactorProb) == 256, "FactorProb layout");
+static_assert(sizeof(FactorProb) == 128, "FactorProb layout");
 
-struct FactorParams {
-    int32_t nprobs, total_items, ab_fmt, dbg;
+struct FactorParams {  // kernel parameter block (< 32 KB)
+    int32_t nprobs, total_items, ab_fmt, dbg, nmaps;
+    int32_t pad0_;
+    int32_t *counter;     // work-item counter in the workspace (zeroed before the launch); null: static striding
+    int32_t pad_[8];
     FactorProb probs[kMaxProbs];
+    CUtensorMap maps[kMaxMaps];
 };
+static_assert(sizeof(FactorParams) <= 32760, "kernel parameter space");
 
 // one factor problem (a layer's A or G) as seen by the host planner
 struct FactorJob {
