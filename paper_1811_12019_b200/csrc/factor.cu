@@ -143,16 +143,16 @@ __device__ __forceinline__ uint32_t layout_of(int cb) {
 }
 
 // gather one element: feature f (< d) of output row q (< rows)  [bias kernel]
-__device__ __forceinline__ float gather_elem(const ProbRegs &pr, int fmt, int64_t q, int f) {
+__device__ __forceinline__ float gather_elem(const ProbRegs &pr, int fmt, int q, int f) {
     int hw = pr.ho * pr.wo;
-    int64_t n = q / hw;
-    int rem = (int)(q - n * hw);
+    int n = q / hw;
+    int rem = q - n * hw;
     int oh = rem / pr.wo, ow = rem - oh * pr.wo;
     int kk = f / pr.c, c = f - kk * pr.c;
     int i = kk / pr.kw, j = kk - i * pr.kw;
     int h = oh * pr.sh - pr.ph + i, w = ow * pr.sw - pr.pw + j;
     if (h < 0 || h >= pr.h || w < 0 || w >= pr.w) return 0.f;
-    return dec_half(__ldg(pr.src + (((n * pr.h + h) * pr.w + w) * pr.c + c)), fmt);
+    return dec_half(__ldg(pr.src + (((int64_t)(n * pr.h + h) * pr.w + w) * pr.c + c)), fmt);
 }
 
 // gather producer: fill 256 features (from f_base) x 64 rows in the SW128 MN-major slot layout
@@ -215,7 +215,7 @@ __device__ __forceinline__ void own_boxes(const ProbRegs &pr, int fa, int fb, bo
     int k = 0;
     for (int op = 0; op < (diag ? 1 : 2); op++) {
         const int f_base = op == 0 ? fb : fa;
-        const uint32_t base = op == 0 ? kOp : 0;
+        const uint32_t base = (op == 0 && !diag) ? kOp : 0;  // diagonal: B (== A) from the stage start
         const int nbox = (min(kTile, pr.d - f_base) + fpb - 1) / fpb;
         for (int b = 0; b < nbox; b++, k++) {
             if (k % kIssuers != w || ob.n >= kMaxOwned) continue;
@@ -238,6 +238,18 @@ __device__ __forceinline__ void own_boxes(const ProbRegs &pr, int fa, int fb, bo
     }
 }
 
+// K units (64-row chunks) per pipeline stage: an off-diagonal tile loads A and B (512 features
+// per unit, one unit fills a stage); a diagonal tile loads only B, so a stage holds 512 / (features
+// loaded) units -- more MMA work per stage round trip (each commit -> empty -> refill round trip
+// costs ~500 cycles of tensor-pipe time that only long enough stages hide).  Stage layout
+// [unit][slot][64 rows][cb].
+__device__ __forceinline__ int item_units(int mode, int fpb, int d, int tj, bool diag, int &unit_bytes) {
+    const int fl = (min(kTile, d - tj * kTile) + fpb - 1) / fpb * fpb;  // B features loaded per unit
+    unit_bytes = fl * kBK * 2;
+    if (!diag || mode == MODE_GATHER) return 1;
+    return min(8, 2 * kTile / fl);
+}
+
 // Work distribution: items are handed out in order (heaviest first) by a global atomic counter,
 // one at a time, to whichever CTA asks -- a dynamic longest-processing-time schedule.  Producer
 // warp 0 fetches item s on demand into a kQueue-deep shared-memory queue; every role reads the
@@ -258,6 +270,9 @@ __device__ __forceinline__ int next_item(uint32_t s, const FactorParams &P, int 
     return item;
 }
 
+#ifndef KFAC_EPI_V4
+#define KFAC_EPI_V4 1
+#endif
 #ifdef KFAC_FACTOR_PROF  // experiment build only: per-role cycle accounting printed by CTAs 0 and 100
 #define FPROF(...) __VA_ARGS__
 #else
@@ -265,7 +280,7 @@ __device__ __forceinline__ int next_item(uint32_t s, const FactorParams &P, int 
 #endif
 
 __global__ void __launch_bounds__(kThreads, 1) factor_syrk_kernel(const __grid_constant__ FactorParams P) {
-    FPROF(long long pf_start = clock64(); long long pf_a = 0, pf_b = 0, pf_c = 0; int pf_n = 0;)
+    FPROF(long long pf_start = clock64(); long long pf_a = 0, pf_b = 0, pf_c = 0, pf_i = 0, pf_q = 0, pf_e = 0; int pf_n = 0;)
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t *ops = smem;
@@ -333,14 +348,17 @@ __global__ void __launch_bounds__(kThreads, 1) factor_syrk_kernel(const __grid_c
             const int fa = it.ti * kTile, fb = it.tj * kTile;
             OwnedBoxes ob;
             if (pr.mode != MODE_GATHER && issuer) own_boxes(pr, fa, fb, diag, wid, ob);
+            int ub;
+            const int rf = item_units(pr.mode, pr.cb * pr.S, pr.d, it.tj, diag, ub);
             // TILED4D chunk origin (image n, first output row oh0), advanced incrementally
             int ig = it.k0 / pr.rpi, rg = it.k0 - ig * pr.rpi;
-            for (int kc = it.k0; kc < it.k1; kc++) {
+            for (int kc = it.k0; kc < it.k1;) {
+                const int units = min(rf, it.k1 - kc);
                 uint8_t *a = ops + (size_t)stage * kStageBytes;
                 uint8_t *b = a + kOp;
                 if (pr.mode == MODE_GATHER) {
                     mbar_wait(&empty[stage], phase ^ 1);
-                    gather_tile(pr, b, fb, kc, ptid);
+                    gather_tile(pr, diag ? a : b, fb, kc, ptid);  // diagonal: B (== A) at the stage start
                     if (!diag) gather_tile(pr, a, fa, kc, ptid);
                     fence_proxy_async_smem();
                     named_bar_sync(1, kProdThreads);
@@ -352,27 +370,37 @@ __global__ void __launch_bounds__(kThreads, 1) factor_syrk_kernel(const __grid_c
                     if (no_tma) {
                         mbar_arrive(&full[stage]);
                     } else {
-                        mbar_arrive_expect_tx(&full[stage], ob.bytes);
-                        const int n = ig * pr.bn, h0 = rg * pr.bh * pr.sh;
+                        mbar_arrive_expect_tx(&full[stage], ob.bytes * units);
+                        int ig2 = ig, rg2 = rg;
+                        for (int u = 0; u < units; u++) {
+                            const int n = ig2 * pr.bn, h0 = rg2 * pr.bh * pr.sh, k64 = (kc + u) * kBK;
+                            uint8_t *ubase = a + u * ub;
 #pragma unroll
-                        for (int q = 0; q < kMaxOwned; q++) {
-                            if (q < ob.n) {
-                                const uint32_t t = ob.tap[q];
-                                const CUtensorMap *m = &P.maps[t & 0xff];
-                                if (pr.mode == MODE_TILED2D)
-                                    tma_load_3d(a + ob.dst[q], m, &full[stage], 0, kc * kBK, (int)(t >> 24));
-                                else
-                                    tma_load_5d(a + ob.dst[q], m, &full[stage], 0, (int)((t >> 8) & 0xff) - 128,
-                                                h0 + (int)((t >> 16) & 0xff) - 128, n, (int)(t >> 24));
+                            for (int q = 0; q < kMaxOwned; q++) {
+                                if (q < ob.n) {
+                                    const uint32_t t = ob.tap[q];
+                                    const CUtensorMap *m = &P.maps[t & 0xff];
+                                    if (pr.mode == MODE_TILED2D)
+                                        tma_load_3d(ubase + ob.dst[q], m, &full[stage], 0, k64, (int)(t >> 24));
+                                    else
+                                        tma_load_5d(ubase + ob.dst[q], m, &full[stage], 0, (int)((t >> 8) & 0xff) - 128,
+                                                    h0 + (int)((t >> 16) & 0xff) - 128, n, (int)(t >> 24));
+                                }
+                            }
+                            if (++rg2 == pr.rpi) {
+                                rg2 = 0;
+                                ig2++;
                             }
                         }
                     }
                     FPROF(pf_c += clock64() - t0;)
                 }
-                if (++rg == pr.rpi) {
-                    rg = 0;
-                    ig++;
-                }
+                for (int u = 0; u < units; u++)
+                    if (++rg == pr.rpi) {
+                        rg = 0;
+                        ig++;
+                    }
+                kc += units;
                 // keep the non-issuing lanes in step with the issuers: an mbarrier parity wait
                 // cannot tell phases apart that are two or more apart, so a lane that ran ahead
                 // into a later gather item would see a stale "empty" phase as free
@@ -387,7 +415,9 @@ __global__ void __launch_bounds__(kThreads, 1) factor_syrk_kernel(const __grid_c
         // ============================ MMA issuer ============================
         uint32_t stage = 0, phase = 0, tph = 0;
         for (uint32_t s = 0;; s++) {
+            FPROF(long long tq = clock64();)
             const int item = next_item(s, P, qitem, qfull, qempty, false, lane);
+            FPROF(pf_q += clock64() - tq; tq = clock64();)
             if (item >= total) break;
             const ItemInfo it = decode_item(hdr, nprobs, item);
             const int cb = P.probs[it.p].cb, ksteps = P.probs[it.p].ksteps, d = P.probs[it.p].d;
@@ -409,34 +439,46 @@ __global__ void __launch_bounds__(kThreads, 1) factor_syrk_kernel(const __grid_c
                 mbar_wait(&tempty[1], tph ^ 1);
                 FPROF(pf_b += clock64() - t00;)
                 tc_fence_after();
-                for (int kc = it.k0; kc < it.k1; kc++) {
+                int ub;
+                const int rf = item_units(P.probs[it.p].mode, cb * P.probs[it.p].S, d, it.tj, diag, ub);
+                FPROF(long long tloop = clock64();)
+                for (int kc = it.k0; kc < it.k1;) {
+                    const int units = min(rf, it.k1 - kc);
                     FPROF(long long t1c = clock64();)
                     mbar_wait(&full[stage], phase);
-                    FPROF(pf_a += clock64() - t1c; pf_n++;)
+                    FPROF(pf_a += clock64() - t1c; pf_n++; t1c = clock64();
+                          pf_i += (long long)units * ksteps * (n0 / 2 + (h1 ? n1 / 2 : 0));)
                     tc_fence_after();
-                    const uint32_t b_base = smem_u32(ops + (size_t)stage * kStageBytes + kOp);
-                    const uint32_t a_base = diag ? b_base : smem_u32(ops + (size_t)stage * kStageBytes);
-                    const uint32_t b1_base = diag ? b_base + half_off : b_base;
+                    const uint32_t sbase = smem_u32(ops + (size_t)stage * kStageBytes);
                     if (no_mma) {
                         mbar_arrive(&empty[stage]);
                     } else {
-                        for (int k = 0; k < ksteps; k++) {
-                            const uint32_t acc = (kc > it.k0 || k > 0) ? 1u : 0u;
-                            mma_f16_ss(t0, umma_desc(a_base + k * kstep, lbo, sbo, lay),
-                                       umma_desc(b_base + k * kstep, lbo, sbo, lay), idesc0, acc);
-                            if (h1)
-                                mma_f16_ss(t1, umma_desc(a_base + half_off + k * kstep, lbo, sbo, lay),
-                                           umma_desc(b1_base + k * kstep, lbo, sbo, lay), idesc1, acc);
+                        for (int u = 0; u < units; u++) {
+                            const uint32_t b_base = diag ? sbase + u * ub : sbase + kOp;
+                            const uint32_t a_base = diag ? b_base : sbase;
+                            const uint32_t b1_base = diag ? b_base + half_off : b_base;
+                            for (int k = 0; k < ksteps; k++) {
+                                const uint32_t acc = (kc > it.k0 || u > 0 || k > 0) ? 1u : 0u;
+                                mma_f16_ss(t0, umma_desc(a_base + k * kstep, lbo, sbo, lay),
+                                           umma_desc(b_base + k * kstep, lbo, sbo, lay), idesc0, acc);
+                                if (h1)
+                                    mma_f16_ss(t1, umma_desc(a_base + half_off + k * kstep, lbo, sbo, lay),
+                                               umma_desc(b1_base + k * kstep, lbo, sbo, lay), idesc1, acc);
+                            }
                         }
                         mma_commit(&empty[stage]);
                     }
+                    FPROF(pf_c += clock64() - t1c;)
+                    kc += units;
                     if (++stage == kStages) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
+                FPROF(pf_e += clock64() - tloop; long long tz = clock64();)
                 if (no_mma) mbar_arrive(tfull);
                 else mma_commit(tfull);
+                FPROF(pf_q += clock64() - tz;)
             }
             __syncwarp();
             tph ^= 1;
@@ -467,47 +509,72 @@ __global__ void __launch_bounds__(kThreads, 1) factor_syrk_kernel(const __grid_c
                               : nullptr;
             const int64_t dd = pr.d_out;
             const int gi0 = it.ti * kTile + rbase, gj0 = it.tj * kTile;
-            const int half = lane >> 4, cc = lane & 15;
+            const int sub = lane >> 2, cq = (lane & 3) * 4, half = lane >> 4, cc = lane & 15;
+            bool released = false;
             if (rbase < nr) {
-                for (int c0 = diag ? (rbase & ~(kQ - 1)) : 0; c0 < nc; c0 += kQ) {
-                    uint32_t r[16];
-                    tmem_ld_32x32b_x16(tacc + c0, r);
+                // the TMEM load of group c0 + kQ is in flight while group c0 is stored
+                const int cbeg = diag ? (rbase & ~(kQ - 1)) : 0;
+                uint32_t r[16];
+                tmem_ld_32x32b_x16(tacc + cbeg, r);
+                const int d = pr.d;
+                const float alpha = pr.alpha;
+                for (int c0 = cbeg; c0 < nc; c0 += kQ) {
                     tmem_ld_wait();
                     float4 *srow = reinterpret_cast<float4 *>(stg + lane * kStageLd);
 #pragma unroll
                     for (int m = 0; m < 4; m++)
                         srow[m] = make_float4(__uint_as_float(r[4 * m]), __uint_as_float(r[4 * m + 1]),
                                               __uint_as_float(r[4 * m + 2]), __uint_as_float(r[4 * m + 3]));
+                    if (c0 + kQ < nc) {
+                        tmem_ld_32x32b_x16(tacc + c0 + kQ, r);
+                    } else {
+                        tc_fence_before();
+                        mbar_arrive(&tempty[h]);  // accumulator quarter drained: the MMA may reuse it
+                        released = true;
+                    }
                     __syncwarp();
                     if (!no_store) {
+                        // lane -> (row sub + 8 it, columns cq .. cq+3) of the staged 32 x 16 block
                         if (part) {
+#if KFAC_EPI_V4
+                            float *dst = part + (size_t)(rbase + sub) * kTile + c0 + cq;
+#pragma unroll
+                            for (int it = 0; it < 4; it++)
+                                *reinterpret_cast<float4 *>(dst + (size_t)it * 8 * kTile) =
+                                    *reinterpret_cast<const float4 *>(stg + (it * 8 + sub) * kStageLd + cq);
+#else
                             float *dst = part + (size_t)rbase * kTile + c0 + cc;
 #pragma unroll 4
                             for (int rr = half; rr < 32; rr += 2) dst[(size_t)rr * kTile] = stg[rr * kStageLd + cc];
+#endif
                         } else {
+                            // packed upper row-major: (gi, gj) at gi*dd - gi*(gi-1)/2 + (gj - gi); lanes
+                            // 0-15 / 16-31 write 64 contiguous bytes of rows rr / rr + 1
                             const int gj = gj0 + c0 + cc;
 #pragma unroll 4
                             for (int rr = half; rr < 32; rr += 2) {
                                 const int gi = gi0 + rr;
-                                if (gi < pr.d && gj < pr.d && gj >= gi)
-                                    pr.out[(int64_t)gi * dd - (int64_t)gi * (gi - 1) / 2 - gi + gj] =
-                                        pr.alpha * stg[rr * kStageLd + cc];
+                                if (gj >= gi && gj < d && gi < d)
+                                    pr.out[(int64_t)gi * dd - ((int64_t)gi * (gi - 1) >> 1) - gi + gj] =
+                                        alpha * stg[rr * kStageLd + cc];
                             }
                         }
                     }
                     __syncwarp();
                 }
             }
-            tc_fence_before();
-            mbar_arrive(&tempty[h]);  // this warp's accumulator quarter drained: the MMA may reuse it
+            if (!released) {
+                tc_fence_before();
+                mbar_arrive(&tempty[h]);
+            }
             FPROF(pf_b += clock64() - t0;)
             tph ^= 1;
         }
     }
 #ifdef KFAC_FACTOR_PROF
     if ((blockIdx.x == 0 || blockIdx.x == 100) && lane == 0 && (warp == 0 || warp == kMmaWarp || warp == kProdWarp0))
-        printf("[fprof] cta %d warp %d: total %lld  waitA %lld waitB %lld body %lld n %d\n", blockIdx.x, warp,
-               clock64() - pf_start, pf_a, pf_b, pf_c, pf_n);
+        printf("[fprof] cta %d warp %d: total %lld  waitA %lld waitB %lld body %lld ideal %lld q %lld pre %lld n %d\n",
+               blockIdx.x, warp, clock64() - pf_start, pf_a, pf_b, pf_c, pf_i, pf_q, pf_e, pf_n);
 #endif
     tc_fence_before();
     __syncthreads();
@@ -558,49 +625,76 @@ __global__ void __launch_bounds__(256) factor_fixup_kernel(const __grid_constant
     }
 }
 
-// materialise the im2col rows of problems with im2col_pre: col[q][f] = ã_f(q), zero for f >= d
+// materialise the im2col rows of problems with im2col_pre: col[q][f] = ã_f(q), zero for f >= d.
+// One warp per output pixel; lane k assembles features [8k, 8k+8) (feature f = (i*kw + j)*C + c,
+// walked incrementally) and writes them as one 16-byte vector, so a warp writes its pixel's
+// cp-element row contiguously.  32-bit index math only (rows < 2^31).
 __global__ void __launch_bounds__(256) im2col_kernel(const __grid_constant__ FactorParams P) {
-    const ProbRegs pr = load_prob(P.probs[blockIdx.y]);
-    if (!P.probs[blockIdx.y].im2col_pre) return;
-    uint16_t *col = P.probs[blockIdx.y].col;
-    const int cp = P.probs[blockIdx.y].cp, nq = cp / 8;
-    const int hw = pr.ho * pr.wo;
-    for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < pr.rows * nq; u += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t row = u / nq;
-        const int q = (int)(u - row * nq);
-        const int64_t n = row / hw;
-        const int rem = (int)(row - n * hw);
-        const int oh = rem / pr.wo, ow = rem - oh * pr.wo;
-        int f = q * 8;
-        int kk = f / pr.c, c = f - kk * pr.c;
-        int i = kk / pr.kw, j = kk - i * pr.kw;
-        const uint16_t *base = pr.src + n * (int64_t)pr.h * pr.w * pr.c;
-        uint32_t pk[4] = {0u, 0u, 0u, 0u};
+    int p = 0;  // blockIdx.y-th problem with materialised patches
+    for (int k = blockIdx.y;; p++) {
+        if (p >= P.nprobs) return;
+        if (P.probs[p].im2col_pre && k-- == 0) break;
+    }
+    const FactorProb &g = P.probs[p];
+    const int C = g.c, kw = g.kw, nq = g.cp / 8, hw = g.ho * g.wo, d = g.d;
+    const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
+    const int rows = (int)g.rows;
+    // lane q's 8 features are the same for every pixel: decode them once
+    // (tap row i, tap column j, offset (i*W + j)*C + c from the window corner; i = -1: zero)
+    int ti[8], tj[8], toff[8];
+    {
+        const int f = lane * 8;
+        int kk = f / C, c = f - kk * C;
+        int i = kk / kw, j = kk - i * kw;
 #pragma unroll
         for (int e = 0; e < 8; e++) {
-            uint16_t v = 0;
-            if (f + e < pr.d) {
-                const int h = oh * pr.sh - pr.ph + i, w = ow * pr.sw - pr.pw + j;
-                if (h >= 0 && h < pr.h && w >= 0 && w < pr.w) v = __ldg(base + ((int64_t)h * pr.w + w) * pr.c + c);
-            }
-            pk[e >> 1] |= (uint32_t)v << ((e & 1) * 16);
-            if (++c == pr.c) {
+            const bool ok = lane < nq && f + e < d;
+            ti[e] = ok ? i : -1;
+            tj[e] = j;
+            toff[e] = (i * g.w + j) * C + c;
+            if (++c == C) {
                 c = 0;
-                if (++j == pr.kw) {
+                if (++j == kw) {
                     j = 0;
                     ++i;
                 }
             }
         }
-        reinterpret_cast<uint4 *>(col)[u] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+    }
+    for (int row = blockIdx.x * wpb + (threadIdx.x >> 5); row < rows; row += gridDim.x * wpb) {
+        const int n = row / hw;
+        const int rem = row - n * hw;
+        const int oh = rem / g.wo, ow = rem - oh * g.wo;
+        const int h0 = oh * g.sh - g.ph, w0 = ow * g.sw - g.pw;
+        const uint16_t *corner = g.src + ((int64_t)n * g.h * g.w + (int64_t)h0 * g.w + w0) * C;
+        const bool inside = h0 >= 0 && h0 + g.kh <= g.h && w0 >= 0 && w0 + kw <= g.w;
+        uint32_t pk[4] = {0u, 0u, 0u, 0u};
+        if (inside) {  // warp-uniform: the whole window is inside the image
+#pragma unroll
+            for (int e = 0; e < 8; e++)
+                if (ti[e] >= 0) pk[e >> 1] |= (uint32_t)__ldg(corner + toff[e]) << ((e & 1) * 16);
+        } else {
+#pragma unroll
+            for (int e = 0; e < 8; e++) {
+                const int h = h0 + ti[e], w = w0 + tj[e];
+                if (ti[e] >= 0 && h >= 0 && h < g.h && w >= 0 && w < g.w)
+                    pk[e >> 1] |= (uint32_t)__ldg(corner + toff[e]) << ((e & 1) * 16);
+            }
+        }
+        if (lane < nq)
+            reinterpret_cast<uint4 *>(g.col + (int64_t)row * g.cp)[lane] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
     }
 }
 
 // bias row/column of A: A[f][dA-1] = alpha * sum_rows ã_f, A[dA-1][dA-1] = alpha * rows
 // (the homogeneous coordinate, reading R-5); one thread per feature, fixed row order.
 __global__ void __launch_bounds__(256) factor_bias_kernel(const __grid_constant__ FactorParams P) {
-    const ProbRegs pr = load_prob(P.probs[blockIdx.y]);
-    if (pr.d_out == pr.d) return;
+    int p = 0;  // blockIdx.y-th problem with a bias coordinate
+    for (int k = blockIdx.y;; p++) {
+        if (p >= P.nprobs) return;
+        if (P.probs[p].d_out != P.probs[p].d && k-- == 0) break;
+    }
+    const ProbRegs pr = load_prob(P.probs[p]);
     const int f = blockIdx.x * blockDim.x + threadIdx.x;
     const int dA = pr.d_out;
     if (f > pr.d) return;
@@ -608,7 +702,8 @@ __global__ void __launch_bounds__(256) factor_bias_kernel(const __grid_constant_
     if (f == pr.d) {
         s = (double)pr.rows;
     } else {
-        for (int64_t q = 0; q < pr.rows; q++) s += (double)gather_elem(pr, P.ab_fmt, q, f);
+        const int rows = (int)pr.rows;
+        for (int q = 0; q < rows; q++) s += (double)gather_elem(pr, P.ab_fmt, q, f);
     }
     const int64_t off = (int64_t)f * dA - (int64_t)f * (f - 1) / 2 + (dA - 1 - f);
     pr.out[off] = (float)(pr.alpha * s);
@@ -715,7 +810,7 @@ static void prob_geometry(const FactorJob &j, bool src_aligned, FactorProb *pr) 
     pr->im2col_pre = 0;
     pr->cp = 0;
     int Ceff = C;
-    if (mode == MODE_GATHER && !force_gather() && j.is_A && !plain && src_aligned) {
+    if (mode == MODE_GATHER && !force_gather() && j.is_A && !plain && src_aligned && (pr->d + 63) / 64 * 64 <= 256) {
         // channel stride not a multiple of 16 B (e.g. the RGB stem): TMA cannot address the
         // pixels, so the patches are materialised once as [rows, cp] (cp = dF rounded to 64)
         // and staged by the 2-D TMA path
@@ -932,10 +1027,10 @@ kfac_status factor_launch(const FactorLaunch &fl, const std::vector<FactorJob> &
     }
     for (const FactorParams &P : fl.params) {
         if (P.total_items == 0) continue;
-        bool pre = false;
-        for (int p = 0; p < P.nprobs; p++) pre |= P.probs[p].im2col_pre != 0;
-        if (pre) {
-            im2col_kernel<<<dim3(2 * (g_num_sms ? g_num_sms : 148), P.nprobs), 256, 0, st>>>(P);
+        int npre = 0;
+        for (int p = 0; p < P.nprobs; p++) npre += P.probs[p].im2col_pre != 0;
+        if (npre) {
+            im2col_kernel<<<dim3(8 * (g_num_sms ? g_num_sms : 148), npre), 256, 0, st>>>(P);
             KFAC_LAUNCHED();
             KFAC_CUDA_TRY(cudaGetLastError());
         }
@@ -944,11 +1039,11 @@ kfac_status factor_launch(const FactorLaunch &fl, const std::vector<FactorJob> &
         factor_syrk_kernel<<<grid, kThreads, kSmemBytes, st>>>(P);
         KFAC_LAUNCHED();
         KFAC_CUDA_TRY(cudaGetLastError());
-        int fix = 0, maxbias = 0;
+        int fix = 0, maxbias = 0, nbias = 0;
         for (int p = 0; p < P.nprobs; p++) {
             const FactorProb &pr = P.probs[p];
             if (pr.splits > 1) fix += pr.npairs;
-            if (pr.d_out != pr.d) maxbias = std::max(maxbias, pr.d + 1);
+            if (pr.d_out != pr.d) maxbias = std::max(maxbias, pr.d + 1), nbias++;
         }
         if (fix && !getenv("KFAC_NO_FIXUP")) {
             factor_fixup_kernel<<<fix * kFixRowGroups, 256, 0, st>>>(P);
@@ -956,7 +1051,7 @@ kfac_status factor_launch(const FactorLaunch &fl, const std::vector<FactorJob> &
             KFAC_CUDA_TRY(cudaGetLastError());
         }
         if (maxbias) {
-            dim3 g((maxbias + 255) / 256, P.nprobs);
+            dim3 g((maxbias + 255) / 256, nbias);
             factor_bias_kernel<<<g, 256, 0, st>>>(P);
             KFAC_LAUNCHED();
             KFAC_CUDA_TRY(cudaGetLastError());

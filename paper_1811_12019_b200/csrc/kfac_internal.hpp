@@ -35,7 +35,7 @@ struct Geom {  // derived geometry of one layer
 kfac_status make_geom(const kfac_layer_desc &d, Geom *g);
 
 // ---------------------------------------------------------------- factor kernel
-constexpr int kMaxProbs = 100;   // factor problems per grouped launch
+constexpr int kMaxProbs = 112;   // factor problems per grouped launch
 constexpr int kMaxMaps = 140;    // TMA descriptors per grouped launch
 constexpr int kTile = 256;       // square output tile (two M = 128 halves x N = 256)
 constexpr int kBK = 64;          // K rows (pixels) per pipeline stage
