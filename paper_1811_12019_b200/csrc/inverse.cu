@@ -526,15 +526,34 @@ __global__ void __launch_bounds__(256, 1) update_kernel(const __grid_constant__ 
     }
 }
 
-// ---- epilogue: inv = -M (symmetric, full fp32)
-__global__ void finalize_kernel(const __grid_constant__ InvParams P) {
+// ---- epilogue: inv = -M (symmetric, full fp32) from the upper storage, 32 x 32 tiles through
+// shared memory so that the mirrored (lower) half is read and written coalesced
+__global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ InvParams P) {
     const MatDesc &m = P.m[blockIdx.y];
-    const int64_t n = m.n, ld = m.ld;
-    for (int64_t i = blockIdx.x; i < n; i += gridDim.x)
-        for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
-            double v = (i <= j) ? m.work[i * ld + j] : m.work[j * ld + i];
-            m.inv[i * n + j] = (float)(-v);
+    const int n = m.n;
+    const int64_t ld = m.ld;
+    const int nt = (n + 31) / 32;
+    __shared__ double T[32][33];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    for (int t = blockIdx.x; t < nt * nt; t += gridDim.x) {
+        const int bi = t / nt, bj = t - bi * nt;
+        const int si = min(bi, bj) * 32, sj = max(bi, bj) * 32;  // source tile in the upper storage
+        __syncthreads();
+        for (int r = ty; r < 32; r += 8) {
+            const int i = si + r, j = sj + tx;
+            T[r][tx] = (i < n && j < n) ? m.work[(int64_t)i * ld + j] : 0.0;
         }
+        __syncthreads();
+        for (int r = ty; r < 32; r += 8) {
+            const int i = bi * 32 + r, j = bj * 32 + tx;
+            if (i >= n || j >= n) continue;
+            double v;
+            if (bi < bj) v = T[r][tx];
+            else if (bi > bj) v = T[tx][r];
+            else v = (r <= tx) ? T[r][tx] : T[tx][r];
+            m.inv[(int64_t)i * n + j] = (float)(-v);
+        }
+    }
 }
 
 static int g_inv_sms = 0;
@@ -633,7 +652,7 @@ kfac_status inverse_launch(const std::vector<InvMat> &mats, int npairs, float ga
         KFAC_LAUNCHED();
         KFAC_CUDA_TRY(cudaGetLastError());
     }
-    finalize_kernel<<<dim3(std::min(maxn, 2048), P.nm), 256, 0, st>>>(P);
+    finalize_kernel<<<dim3(std::min(((maxn + 31) / 32) * ((maxn + 31) / 32), 1184), P.nm), 256, 0, st>>>(P);
     KFAC_LAUNCHED();
     KFAC_CUDA_TRY(cudaGetLastError());
     return KFAC_OK;

@@ -227,16 +227,27 @@ struct SplitParams {
     int32_t n, pad;
     SplitJob j[kMaxG];
 };
-__global__ void split_kernel(const __grid_constant__ SplitParams P) {
+__global__ void __launch_bounds__(256) split_kernel(const __grid_constant__ SplitParams P) {
     const SplitJob &J = P.j[blockIdx.y];
     const int64_t tot = (int64_t)J.rows * J.Kp;
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t r = e / J.Kp;
-        const int k = (int)(e - r * J.Kp);
-        const float x = k < J.K ? J.src[r * J.ld_src + k] : 0.f;
-        const float hi = tf32_trunc(x);  // exact tf32 value, whatever rounding the MMA applies
-        J.dst[e] = hi;
-        J.dst[tot + e] = x - hi;
+    const int kq = J.Kp / 4;  // Kp is a multiple of 4: 16-byte hi / lo stores
+    // one row per (block, warp-group) step: coalesced loads of the (unaligned) source row
+    for (int r = blockIdx.x; r < J.rows; r += gridDim.x) {
+        const float *src = J.src + (int64_t)r * J.ld_src;
+        float4 *hi = reinterpret_cast<float4 *>(J.dst + (int64_t)r * J.Kp);
+        float4 *lo = reinterpret_cast<float4 *>(J.dst + tot + (int64_t)r * J.Kp);
+        for (int q = threadIdx.x; q < kq; q += blockDim.x) {
+            float x[4], h[4], l[4];
+#pragma unroll
+            for (int e = 0; e < 4; e++) {
+                const int k = 4 * q + e;
+                x[e] = k < J.K ? __ldg(src + k) : 0.f;
+                h[e] = tf32_trunc(x[e]);  // exact tf32 value, whatever rounding the MMA applies
+                l[e] = x[e] - h[e];
+            }
+            hi[q] = make_float4(h[0], h[1], h[2], h[3]);
+            lo[q] = make_float4(l[0], l[1], l[2], l[3]);
+        }
     }
 }
 
@@ -278,7 +289,9 @@ static kfac_status launch_splits(const std::vector<SplitJob> &js, cudaStream_t s
         memset(&P, 0, sizeof(P));
         P.n = (int)std::min<size_t>(kMaxG, js.size() - b);
         for (int i = 0; i < P.n; i++) P.j[i] = js[b + i];
-        split_kernel<<<dim3(64, P.n), 256, 0, st>>>(P);
+        int maxrows = 1;
+        for (int i = 0; i < P.n; i++) maxrows = std::max(maxrows, (int)P.j[i].rows);
+        split_kernel<<<dim3(std::min(maxrows, 1024), P.n), 256, 0, st>>>(P);
         KFAC_LAUNCHED();
         KFAC_CUDA_TRY(cudaGetLastError());
     }
