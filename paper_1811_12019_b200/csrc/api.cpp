@@ -199,7 +199,15 @@ kfac_status kfac_damped_inverse(kfac_plan_t p, int32_t rank, const float *recv, 
     const auto &ow = p->owned[rank];
     uint8_t *w = static_cast<uint8_t *>(ws);
     double *pair_scratch = reinterpret_cast<double *>(w);
-    int64_t off = align16(4 * (int64_t)ow.size()) * 8 + 1024;
+    int64_t sum_nt = 0, sum_tiles = 0, sum_tasks = 0;
+    for (int l : ow)
+        for (int n : {p->geoms[l].dA, p->geoms[l].dG}) {
+            const int64_t nt = (n + kPanel - 1) / kPanel;
+            sum_nt += nt;
+            sum_tiles += nt * (nt + 1) / 2;
+            sum_tasks += inverse_tasks(n);
+        }
+    int64_t off = align16(inverse_scratch_bytes((int)ow.size(), sum_nt, sum_tiles, sum_tasks));
     std::vector<InvMat> mats;
     for (size_t k = 0; k < ow.size(); k++) {
         const Geom &g = p->geoms[ow[k]];

@@ -31,25 +31,39 @@ namespace kfac {
 constexpr int kMaxMats = 128;
 constexpr int B = kPanel;     // 128
 constexpr int KC = 16;        // K rows per smem chunk of the tile product
-constexpr int kPivSmem = (B * (B + 1) + 2 * 32 * (B + 4) + 32 * 32) * 8 + 64;
+constexpr int kPivSmem = (B * (B + 1) + 2 * 32 * (B + 4) + 32 * 36 + 64) * 8 + 64;
 constexpr int kTileSmem = 2 * 2 * KC * (B + 4) * 8;  // double-buffered A/B chunks (padded rows): 66 KB
 constexpr int kUpdSmem = kPivSmem > kTileSmem + B * (B + 4) * 8 ? kPivSmem : kTileSmem + B * (B + 4) * 8;
-constexpr int kPanelSmem = B * (B + 1) * 8 > kTileSmem ? B * (B + 1) * 8 : kTileSmem;
+static_assert(kUpdSmem >= B * (B + 1) * 8, "panel staging fits the update kernel's shared memory");
 
 struct MatDesc {
     const float *packed;
     float *inv;
     double *work;
-    double *panel;  // [R: B x ld][Wp: B x ld][P_even: B x B][P_odd: B x B]
+    double *panel;  // [R_even | Wp_even | R_odd | Wp_odd: B x ld each][P_even | P_odd: B x B]
     int32_t *status;
-    int32_t n, ld, pair, is_A, tile_begin, col_begin, piv_idx, pad_;
+    int32_t n, ld, pair, is_A;
+    int32_t nt;          // column blocks
+    int32_t col_begin;   // prefix of nt over the (nt-descending) matrix list: column / step flags
+    int32_t tile_begin;  // prefix of nt (nt + 1) / 2: tile flags
+    int32_t pad_;
 };
+constexpr int kMaxSteps = 128;
 struct InvParams {
-    int32_t nm, total_tiles, k, total_cols, fuse, npiv;
+    int32_t nm, steps, total_tasks, pad0_;
     double gamma;
     double *pair_scratch;  // [npairs][4]: pi, dA, dG
-    int *counter;          // this step's tile counter (zeroed per inverse call)
     float *pi_out;
+    // dataflow state (zeroed per inverse call): one task counter, then per matrix / column / step
+    // stamps and counters -- see inverse_kernel
+    int *counter;
+    int *pivflag;      // [nm]        k + 1 once P_k is in its slot
+    int *colflag;      // [sum nt]    k + 1 once panel (R_J, Wp_J) of step k is written
+    int *panels_done;  // [sum nt]    per (matrix, step): completed panel tasks
+    int *tiles_done;   // [sum nt]    per (matrix, step): completed update tasks
+    int *tileflag;     // [sum tiles] k + 1 once tile (I, J) holds its step-k value
+    int4 *tasks;       // [total_tasks] task records (gen_step_tasks), built on the device per call
+    int32_t step_begin[kMaxSteps + 1];  // first record of each step's list
     MatDesc m[kMaxMats];
 };
 
@@ -132,33 +146,43 @@ __global__ void unpack_damp_kernel(const __grid_constant__ InvParams P) {
 //   S_IJ -= O_I^T W_J,  S_sJ = W_J,  S_Is = W_I^T,  S_ss = -Q   (O = old block row s, W = Q O).
 // Returns 0 or the failing pivot index + 1 (the sweep pivots are the LDL^T pivots).
 constexpr int S2 = 32;  // sub-pivot size
+constexpr int S2_ = S2;
+constexpr int QLD = S2 + 4;  // padded row stride of Q (conflict-free DMMA fragments)
 
-// scalar sweep of the 32 x 32 sub-pivot (smem, row-major, ping-pong buffers Q / Q2) by all 256
-// threads (4 elements each), one barrier per pivot; the result -inv(sub-pivot) ends in Q (an even
-// number of swaps).  Returns 0 or the failing pivot index + 1 (base-relative).
-__device__ __forceinline__ int block_sweep32(double *Q, double *Q2, int base) {
-    const int tid = threadIdx.x;
-    double *src = Q, *dst = Q2;
-    for (int t = 0; t < S2; t++) {
-        const double d = src[t * S2 + t];
+// sweep of the 32 x 32 sub-pivot S[s0.., s0..] by all 8 warps with the block in registers: thread
+// (w, lane) holds rows 4w..4w+3 of column `lane`.  The sweep keeps the block symmetric, so pivot
+// row t equals column t: per pivot its owner warp publishes row t (ping-pong buffer), one barrier,
+// then every thread updates its 4 elements.  Writes Q = inv(sub-pivot); returns 0 or the failing
+// pivot index + 1 (uniform across the block).
+__device__ __forceinline__ int block_sweep32(const double (*S)[B + 1], int s0, double *Q, double *rowbuf, int base) {
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double x[4];
+#pragma unroll
+    for (int r = 0; r < 4; r++) {
+        const int l = 4 * w + r;  // upper storage
+        x[r] = S[s0 + min(l, lane)][s0 + max(l, lane)];
+    }
+#pragma unroll
+    for (int t = 0; t < S2_; t++) {
+        double *rb = rowbuf + (t & 1) * 32;
+        if (w == (t >> 2)) rb[lane] = x[t & 3];
+        __syncthreads();
+        const double d = rb[t];
         if (!(d > 0.0)) return base + t + 1;  // uniform: every thread read the same d
         const double inv = __drcp_rn(d);
+        const double vj = rb[lane] * inv;  // (t, lane) / d
 #pragma unroll
-        for (int k = 0; k < 4; k++) {
-            const int e = tid + 256 * k, l = e >> 5, j = e & 31;
-            const double u = (l == t) ? -1.0 : src[l * S2 + t];
-            const double v = (j == t) ? -inv : src[t * S2 + j] * inv;
-            const double keep = (l == t || j == t) ? 0.0 : src[e];
-            dst[e] = fma(-u, v, keep);
+        for (int r = 0; r < 4; r++) {
+            const int l = 4 * w + r;
+            const double c = rb[l];  // (l, t) = (t, l)
+            if (l == t) x[r] = (lane == t) ? -inv : vj;
+            else x[r] = (lane == t) ? c * inv : fma(-c, vj, x[r]);
         }
-        __syncthreads();
-        double *tmp = src;
-        src = dst;
-        dst = tmp;
     }
+#pragma unroll
+    for (int r = 0; r < 4; r++) Q[(4 * w + r) * QLD + lane] = -x[r];
     return 0;
 }
-static_assert(S2 % 2 == 0, "block_sweep32 leaves its result in Q after an even number of swaps");
 
 #ifdef PIVOT_DBG
 __device__ int g_pivot_dbg;
@@ -172,8 +196,9 @@ __device__ int pivot_block(const double *__restrict__ W, int64_t ld, int k0, int
     double(*S)[B + 1] = reinterpret_cast<double(*)[B + 1]>(smem);
     double *O = smem + B * (B + 1);       // [S2][SLD] old block row
     double *Wr = O + S2 * SLD;            // [S2][SLD] Q * O
-    double *Q = Wr + S2 * SLD;            // [S2][S2] inverse of the sub-pivot
-    int *fsh = reinterpret_cast<int *>(Q + S2 * S2);
+    double *Q = Wr + S2 * SLD;            // [S2][QLD] inverse of the sub-pivot
+    double *colbuf = Q + S2 * QLD;        // [2][32] sweep broadcast buffers (ping-pong)
+    int *fsh = reinterpret_cast<int *>(colbuf + 64);
     const int tid = threadIdx.x;
     for (int e = tid; e < B * B; e += blockDim.x) {
         const int i = e >> 7, j = e & (B - 1);
@@ -187,102 +212,119 @@ __device__ int pivot_block(const double *__restrict__ W, int64_t ld, int k0, int
     for (int sb = 0; sb < B / S2; sb++) {
         const int s0 = sb * S2;
         if (s0 >= bk) break;
-        for (int e = tid; e < S2 * S2; e += blockDim.x) Q[e] = S[s0 + (e >> 5)][s0 + (e & 31)];
-        __syncthreads();
         {
-            const int f = block_sweep32(Q, Wr, k0 + s0);  // Q <- -inv(sub-pivot) (Wr: ping-pong scratch)
-            if (f && tid == 0) *fsh = f;
-            for (int e = tid; e < S2 * S2; e += blockDim.x) Q[e] = -Q[e];
+            const int f = block_sweep32(S, s0, Q, colbuf, k0 + s0);  // Q = inv(sub-pivot)
+            if (f) {
+                if (tid == 0) *fsh = f;
+                break;
+            }
         }
+        __syncthreads();
         PCLK(1 + 4 * sb)
-        for (int e = tid; e < S2 * B; e += blockDim.x) O[(e >> 7) * SLD + (e & (B - 1))] = S[s0 + (e >> 7)][e & (B - 1)];
+        for (int e = tid; e < S2 * B; e += blockDim.x) {  // old block row s (upper storage)
+            const int a = s0 + (e >> 7), c = e & (B - 1);
+            O[(e >> 7) * SLD + c] = S[min(a, c)][max(a, c)];
+        }
         __syncthreads();
         if (*fsh) break;
         PCLK(2 + 4 * sb)
 #ifdef PIVOT_DBG
         if (g_pivot_dbg == 1 && sb >= 1) break;
 #endif
-        // W = Q O  (32 x 128): thread -> column j = tid & 127, rows a = (tid >> 7) + 2k (16 chains)
+        // W = Q O  (32 x 128, K = 32) on the fp64 tensor cores: warp w owns columns 16w..16w+15,
+        // all four 8-row blocks (m8n8k4: A frag Q[row][k], B frag O[k][col])
         {
-            const int j = tid & (B - 1), a0 = tid >> 7;
-            double w[S2 / 2];
+            const int w = tid >> 5, lane = tid & 31, r8 = lane >> 2, k4 = lane & 3;
+            double c[4][2][2];
 #pragma unroll
-            for (int k = 0; k < S2 / 2; k++) w[k] = 0.0;
-            for (int b2 = 0; b2 < S2; b2++) {
-                const double o = O[b2 * SLD + j];
+            for (int i = 0; i < 4; i++)
 #pragma unroll
-                for (int k = 0; k < S2 / 2; k++) w[k] = fma(Q[(a0 + 2 * k) * S2 + b2], o, w[k]);
+                for (int j = 0; j < 2; j++) c[i][j][0] = c[i][j][1] = 0.0;
+#pragma unroll
+            for (int kk = 0; kk < S2 / 4; kk++) {
+                double a[4], b[2];
+#pragma unroll
+                for (int i = 0; i < 4; i++) a[i] = Q[(8 * i + r8) * QLD + 4 * kk + k4];
+#pragma unroll
+                for (int j = 0; j < 2; j++) b[j] = O[(4 * kk + k4) * SLD + 16 * w + 8 * j + r8];
+#pragma unroll
+                for (int i = 0; i < 4; i++)
+#pragma unroll
+                    for (int j = 0; j < 2; j++) dmma(c[i][j][0], c[i][j][1], a[i], b[j]);
             }
 #pragma unroll
-            for (int k = 0; k < S2 / 2; k++) Wr[(a0 + 2 * k) * SLD + j] = w[k];
+            for (int i = 0; i < 4; i++)
+#pragma unroll
+                for (int j = 0; j < 2; j++)
+                    *reinterpret_cast<double2 *>(Wr + (8 * i + r8) * SLD + 16 * w + 8 * j + 2 * k4) =
+                        make_double2(c[i][j][0], c[i][j][1]);
         }
         __syncthreads();
         PCLK(3 + 4 * sb)
 #ifdef PIVOT_DBG
         if (g_pivot_dbg == 2 && sb >= 1) break;
 #endif
-        // rank-32 sweep update of every element on the fp64 tensor cores (DMMA); each thread then
-        // writes only its own elements
-        double acc[8][8];
-#pragma unroll
-        for (int p = 0; p < 8; p++)
-#pragma unroll
-            for (int q = 0; q < 8; q++) acc[p][q] = 0.0;
+        // rank-32 sweep update S -= O^T W of the upper triangle on the fp64 tensor cores (DMMA):
+        // 8-row strips r and 15 - r (17 m8n8 blocks together) per warp, then the sub-block's rows
+        // and columns get their sweep values: S_sJ = W_J, S_Is = W_I^T, S_ss = -Q
         {
-            const int w = tid >> 5, lane = tid & 31;
-            const int arow = 64 * (w >> 2) + (lane >> 2), bcol = 32 * (w & 3) + (lane >> 2), kl = lane & 3;
+            const int w = tid >> 5, lane = tid & 31, r8 = lane >> 2, k4 = lane & 3;
+            const int nfirst = 16 - w;  // blocks of strip w (columns w..15); then strip 15-w
+            double acc[17][2];
+#pragma unroll
+            for (int x = 0; x < 17; x++) acc[x][0] = acc[x][1] = 0.0;
 #pragma unroll
             for (int kk = 0; kk < S2 / 4; kk++) {
-                const int t = kk * 4 + kl;
-                double a[8], b[4];
+                const int t = 4 * kk + k4;
+                const double aA = O[t * SLD + 8 * w + r8], aB = O[t * SLD + 8 * (15 - w) + r8];
 #pragma unroll
-                for (int p = 0; p < 8; p++) a[p] = O[t * SLD + arow + 8 * p];
-#pragma unroll
-                for (int q = 0; q < 4; q++) b[q] = Wr[t * SLD + bcol + 8 * q];
-#pragma unroll
-                for (int p = 0; p < 8; p++)
-#pragma unroll
-                    for (int q = 0; q < 4; q++) dmma(acc[p][2 * q], acc[p][2 * q + 1], a[p], b[q]);
+                for (int x = 0; x < 17; x++) {
+                    const bool first = x < nfirst;
+                    const int cb = first ? w + x : x - 1;
+                    dmma(acc[x][0], acc[x][1], first ? aA : aB, Wr[t * SLD + 8 * cb + r8]);
+                }
             }
-        }
 #pragma unroll
-        for (int p = 0; p < 8; p++) {
-            const int i = tile_row(p);
-            const bool is = (i >= s0 && i < s0 + S2);
-#pragma unroll
-            for (int q = 0; q < 8; q++) {
-                const int j = tile_col(q);
-                const bool js = (j >= s0 && j < s0 + S2);
-                // clamped indices: every load is in range whatever the compiler speculates
-                const int ii = min(max(i - s0, 0), S2 - 1), jj = min(max(j - s0, 0), S2 - 1);
-                const double vq = Q[ii * S2 + jj], vwi = Wr[ii * SLD + j], vwj = Wr[jj * SLD + i];
-                const double v = is ? (js ? -vq : vwi) : (js ? vwj : S[i][j] - acc[p][q]);
-                S[i][j] = v;
+            for (int x = 0; x < 17; x++) {
+                const bool first = x < nfirst;
+                const int i = 8 * (first ? w : 15 - w) + r8, j = 8 * (first ? w + x : x - 1) + 2 * k4;
+                S[i][j] -= acc[x][0];
+                S[i][j + 1] -= acc[x][1];
             }
         }
         __syncthreads();
+        for (int e = tid; e < S2 * B; e += blockDim.x) {
+            const int a = e >> 7, j = e & (B - 1);
+            if (j >= s0 && j < s0 + S2) S[s0 + a][j] = -Q[a * QLD + (j - s0)];
+            else if (j > s0) S[s0 + a][j] = Wr[a * SLD + j];  // right of the sub-block: its row band
+            else S[j][s0 + a] = Wr[a * SLD + j];              // left: its column band (upper storage)
+        }
+        __syncthreads();
+        PCLK(4 + 4 * sb)
     }
+    __syncthreads();
     PCLK(20)
     const int fail = *fsh;
     if (fail) return fail;
     for (int e = tid; e < B * B; e += blockDim.x) {  // P = -S (zero outside bk)
         const int i = e >> 7, j = e & (B - 1);
-        Pout[e] = (i < bk && j < bk) ? -S[i][j] : 0.0;
+        Pout[e] = (i < bk && j < bk) ? -S[min(i, j)][max(i, j)] : 0.0;
     }
     return 0;
 }
 
 __device__ __forceinline__ double *pivot_slot(const MatDesc &m, int k) {
-    return m.panel + 2 * (int64_t)B * m.ld + (int64_t)(k & 1) * B * B;
+    return m.panel + 4 * (int64_t)B * m.ld + (int64_t)(k & 1) * B * B;
 }
+__device__ __forceinline__ double *panel_R(const MatDesc &m, int k) { return m.panel + (int64_t)(k & 1) * 2 * B * m.ld; }
+__device__ __forceinline__ double *panel_Wp(const MatDesc &m, int k) { return panel_R(m, k) + (int64_t)B * m.ld; }
 
-// step 0 only: P_0 (later pivots are fused into the previous step's update kernel)
+// step 0 only: P_0 (later pivots are fused into the previous step's tile (K+1, K+1) update)
 __global__ void __launch_bounds__(256, 1) pivot_kernel(const __grid_constant__ InvParams P) {
     const MatDesc &m = P.m[blockIdx.x];
-    const int n = m.n, k0 = P.k * B;
-    if (k0 >= n || *m.status != 0) return;
+    if (*m.status != 0) return;
     extern __shared__ double dyn[];
-    const int f = pivot_block(m.work, m.ld, k0, min(B, n - k0), pivot_slot(m, P.k), dyn);
+    const int f = pivot_block(m.work, m.ld, 0, min(B, m.n), pivot_slot(m, 0), dyn);
     if (f && threadIdx.x == 0) *m.status = f;
 }
 
@@ -352,22 +394,15 @@ __device__ __forceinline__ void tile_product(const double *__restrict__ A, int64
     }
 }
 
-// ---- step 2: R_J = block row K (from upper storage), Wp_J = P R_J   (one CTA per 128-col block)
-__global__ void __launch_bounds__(256, 1) panel_kernel(const __grid_constant__ InvParams P) {
-    int cb = blockIdx.x, mi = 0;
-    while (mi + 1 < P.nm && P.m[mi + 1].col_begin <= cb) mi++;
-    const MatDesc &m = P.m[mi];
-    const int n = m.n, k0 = P.k * B;
+// ---- panel task (m, k, J): R_J = block row K (from upper storage), Wp_J = P_k R_J
+__device__ void panel_task(const MatDesc &m, int k, int J, double *dyn) {
+    const int n = m.n, k0 = k * B, K = k;
     const int64_t ld = m.ld;
-    if (k0 >= n || *m.status != 0) return;
-    const int J = cb - m.col_begin, K = P.k;
     const int j0 = J * B;
-    if (j0 >= n) return;
     const int bk = min(B, n - k0), bj = min(B, n - j0);
-    double *R = m.panel, *Wp = m.panel + (int64_t)B * ld;
+    double *R = panel_R(m, k), *Wp = panel_Wp(m, k);
     // R_J (rows t < bk, cols j < bj; zero up to the 16-aligned ld) staged through shared memory so
     // that both the read of W (upper storage, possibly transposed) and the write of R coalesce.
-    extern __shared__ double dyn[];
     double(*T)[B + 1] = reinterpret_cast<double(*)[B + 1]>(dyn);
     const int bjp = min(B, (int)ld - j0);
     const bool trans = J < K;  // block row K left of the diagonal lives in column K of the upper storage
@@ -394,58 +429,28 @@ __global__ void __launch_bounds__(256, 1) panel_kernel(const __grid_constant__ I
 #pragma unroll
         for (int q = 0; q < 8; q++) acc[p][q] = 0.0;
     // Wp[i][j] = sum_t P[t][i] R[t][j]   (P symmetric, zero outside bk)
-    tile_product(pivot_slot(m, P.k), B, bk, R + j0, ld, bj, bk, acc, dyn);
+    tile_product(pivot_slot(m, k), B, bk, R + j0, ld, bj, bk, acc, dyn);
 #pragma unroll
     for (int p = 0; p < 8; p++) {
         const int i = tile_row(p);
         if (i >= bk) continue;
 #pragma unroll
-        for (int q = 0; q < 8; q++) {
+        for (int q = 0; q < 8; q += 2) {
             const int j = tile_col(q);
-            if (j < bjp) Wp[(int64_t)i * ld + j0 + j] = acc[p][q];
+            if (j < bjp) *reinterpret_cast<double2 *>(Wp + (int64_t)i * ld + j0 + j) = make_double2(acc[p][q], acc[p][q + 1]);
         }
     }
 }
 
-// ---- step 3: rank-B update of every upper tile (I, J); the CTA of tile (K+1, K+1) then
-// inverts that block: the next step's pivot runs concurrently with this step's update.
-// Global tile order: first every matrix's (K+1, K+1) tile (so the fused pivots start at once),
-// then the remaining upper tiles matrix by matrix, row-major.  Persistent CTAs stride over it.
-__device__ __forceinline__ void update_tile(const InvParams &P, int g, double *dyn, const int *sbeg,
-                                            const int *spiv) {
-    int mi = 0, t = 0;
-    if (g < P.npiv) {
-        while (spiv[mi] != g) mi++;
-    } else {  // binary search of the (shared-memory copy of the) tile prefix
-        int lo = 0, hi = P.nm - 1;
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (sbeg[mid] <= g) lo = mid; else hi = mid - 1;
-        }
-        mi = lo;
-        t = g - sbeg[mi] + (spiv[mi] >= 0 ? 1 : 0);
-    }
-    const MatDesc &m = P.m[mi];
-    const int n = m.n, k0 = P.k * B;
+// ---- update task (m, k, I, J): rank-B sweep update of upper tile (I, J); the task of tile
+// (K+1, K+1) then inverts that block (the next step's pivot).  Returns 0 or a pivot failure.
+__device__ int update_task(const InvParams &P, const MatDesc &m, int k, int I, int J, double *dyn, const int *pflag) {
+    const int n = m.n, k0 = k * B, K = k;
     const int64_t ld = m.ld;
-    if (k0 >= n || *m.status != 0) return;
-    const int nt = (n + B - 1) / B, K = P.k;
-    const int ntiles = nt * (nt + 1) / 2;
-    if (t >= ntiles) return;
-    int I = 0, J = 0;
-    if (K + 1 < nt) {
-        const int dk = (K + 1) * nt - (K + 1) * K / 2;  // row-major index of (K+1, K+1)
-        t = (t == 0) ? dk : (t <= dk ? t - 1 : t);
-    }
-    while (t >= nt - I) {
-        t -= nt - I;
-        I++;
-    }
-    J = I + t;
     const int bk = min(B, n - k0);
     const int i0 = I * B, j0 = J * B;
     const int bi = min(B, n - i0), bj = min(B, n - j0);
-    const double *R = m.panel, *Wp = m.panel + (int64_t)B * ld;
+    const double *R = panel_R(m, k), *Wp = panel_Wp(m, k);
     double *W = m.work;
     if (I == K && J == K) {
         const double *Pm = pivot_slot(m, K);
@@ -453,21 +458,21 @@ __device__ __forceinline__ void update_tile(const InvParams &P, int g, double *d
             const int i = e / bk, j = e % bk;
             if (j >= i) W[(int64_t)(k0 + i) * ld + k0 + j] = -Pm[i * B + j];
         }
-        return;
+        return 0;
     }
     if (I == K) {  // M_KJ <- Wp_J
         for (int e = threadIdx.x; e < bk * bj; e += blockDim.x) {
             const int i = e / bj, j = e % bj;
             W[(int64_t)(k0 + i) * ld + j0 + j] = Wp[(int64_t)i * ld + j0 + j];
         }
-        return;
+        return 0;
     }
     if (J == K) {  // M_IK <- Wp_I^T
         for (int e = threadIdx.x; e < bi * bk; e += blockDim.x) {
             const int i = e / bk, j = e % bk;
             W[(int64_t)(i0 + i) * ld + k0 + j] = Wp[(int64_t)j * ld + i0 + i];
         }
-        return;
+        return 0;
     }
     double acc[8][8];
 #pragma unroll
@@ -487,42 +492,179 @@ __device__ __forceinline__ void update_tile(const InvParams &P, int g, double *d
     };
     // M_IJ -= R_I^T Wp_J : acc[i][j] = sum_t R[t][i0+i] Wp[t][j0+j]
     tile_product(R + i0, ld, bi, Wp + j0, ld, bj, bk, acc, dyn, cslice);
+    // column pairs (16-byte stores); rows are written whole up to the leading dimension: the lower
+    // half of a diagonal tile and the padding columns are never read (upper storage)
 #pragma unroll
     for (int p = 0; p < 8; p++) {
         const int i = tile_row(p);
         if (i >= bi) continue;
 #pragma unroll
-        for (int q = 0; q < 8; q++) {
+        for (int q = 0; q < 8; q += 2) {
             const int j = tile_col(q);
-            if (j >= bj || (I == J && j < i)) continue;
-            W[(int64_t)(i0 + i) * ld + j0 + j] = Cs[i * SLD + j] - acc[p][q];  // padded rows: conflict-free
+            if (j0 + j >= ld) continue;
+            const double2 c = *reinterpret_cast<const double2 *>(Cs + i * SLD + j);
+            *reinterpret_cast<double2 *>(W + (int64_t)(i0 + i) * ld + j0 + j) = make_double2(c.x - acc[p][q], c.y - acc[p][q + 1]);
         }
     }
-    if (P.fuse && I == K + 1 && J == K + 1) {  // fused next pivot: P_{K+1} = (updated M_{K+1,K+1})^-1
+    if (I == K + 1 && J == K + 1) {  // fused next pivot: P_{K+1} = (updated M_{K+1,K+1})^-1
         __threadfence_block();
         __syncthreads();
-        const int f = pivot_block(W, ld, i0, bi, pivot_slot(m, K + 1), dyn);
-        if (f && threadIdx.x == 0) *m.status = f;
+        // its slot held P_{k-1}: every step-(k-1) panel task must be done reading it
+        if (k >= 1 && threadIdx.x == 0) {
+            int v;
+            do {
+                asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(pflag) : "memory");
+                if (v < m.nt) __nanosleep(128);
+            } while (v < m.nt);
+        }
+        __syncthreads();
+        return pivot_block(W, ld, i0, bi, pivot_slot(m, K + 1), dyn);
     }
+    return 0;
 }
 
-// persistent CTAs take tiles from an atomic counter: the CTA that runs a fused pivot simply takes
-// fewer tiles, so the pivot hides behind the other CTAs' updates
-__global__ void __launch_bounds__(256, 1) update_kernel(const __grid_constant__ InvParams P) {
+#ifdef INV_TRACE  // experiment build only: per-task timeline
+struct TraceRec { int g, k, kind, I, J, sm; long long t0, t1, t2; };
+__device__ TraceRec g_trace[65536];
+__device__ __forceinline__ long long gtime() { long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t; }
+#define TRACE(...) __VA_ARGS__
+#else
+#define TRACE(...)
+#endif
+__device__ __forceinline__ void wait_ge(const int *f, int target) {
+    int v;
+    for (;;) {
+        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+        if (v >= target) return;
+        __nanosleep(200);
+    }
+}
+__device__ __forceinline__ int upper_index(int I, int J, int nt) { return I * nt - I * (I - 1) / 2 + (J - I); }
+
+// ---- the task list of step k (one record per task: {k, kind, matrix, I << 16 | J}, kind 0 panel J,
+// 1 update of tile (I, J)), ordered for the critical path K -> K+1 of every matrix:
+//   S1 the step's panels (column K+1 first at step 0; later it was issued early, see E)
+//   S2 (step 0 only) the next-pivot tiles (1, 1)
+//   S3 look-ahead tiles: the rest of block row / column K+1 and the diagonal tile (K+2, K+2)
+//   E  early tasks of step k+1: panel (k+1, K+2) and the next-pivot tile (K+2, K+2) at step k+1
+//      (their CTAs wait for P_{k+1}; the chain pivot -> panel -> tile -> pivot then runs without
+//      queueing behind the rest of the step)
+//   S5 the remaining tiles of step k
+// Matrices are sorted by nt descending (active ones are a prefix).  Returns the number of tasks.
+__host__ __device__ inline int gen_step_tasks(const int *nt, int nm, int k, int4 *out) {
+    int c = 0;
+    auto put = [&](int kk, int kind, int m, int I, int J) {
+        if (out) out[c] = make_int4(kk, kind, m, (I << 16) | J);
+        c++;
+    };
+    for (int m = 0; m < nm && nt[m] > k; m++) {  // S1
+        const bool moved = k >= 1 && nt[m] > k + 1;  // panel (k, K+1) was issued in E(k-1)
+        if (k == 0 && nt[m] > 1) put(k, 0, m, 0, 1);
+        for (int J = 0; J < nt[m]; J++) {
+            if (J == k + 1 && (moved || (k == 0 && nt[m] > 1))) continue;
+            put(k, 0, m, 0, J);
+        }
+    }
+    if (k == 0)  // S2
+        for (int m = 0; m < nm && nt[m] > 1; m++) put(0, 1, m, 1, 1);
+    for (int m = 0; m < nm && nt[m] > k + 1; m++) {  // S3
+        const int L = k + 1;
+        for (int I = 0; I < L; I++) put(k, 1, m, I, L);
+        for (int J = L + 1; J < nt[m]; J++) put(k, 1, m, L, J);
+        if (nt[m] > k + 2) put(k, 1, m, k + 2, k + 2);
+    }
+    for (int m = 0; m < nm && nt[m] > k + 2; m++) put(k + 1, 0, m, 0, k + 2);  // E: panels
+    for (int m = 0; m < nm && nt[m] > k + 2; m++) put(k + 1, 1, m, k + 2, k + 2);  // E: next pivots
+    for (int m = 0; m < nm && nt[m] > k; m++) {  // S5
+        const int L = k + 1;
+        const bool la = nt[m] > L;
+        for (int I = 0; I < nt[m]; I++)
+            for (int J = I; J < nt[m]; J++) {
+                if (la && (I == L || J == L)) continue;          // pivot tile + look-ahead (S2/E, S3)
+                if (nt[m] > k + 2 && I == k + 2 && J == k + 2) continue;  // S3
+                put(k, 1, m, I, J);
+            }
+    }
+    return c;
+}
+
+__global__ void inverse_tasks_kernel(const __grid_constant__ InvParams P) {
+    __shared__ int nt[kMaxMats];
+    for (int i = threadIdx.x; i < P.nm; i += blockDim.x) nt[i] = P.m[i].nt;
+    __syncthreads();
+    for (int k = threadIdx.x; k < P.steps; k += blockDim.x) gen_step_tasks(nt, P.nm, k, P.tasks + P.step_begin[k]);
+}
+
+// ---- the whole sweep as ONE persistent launch: CTAs take tasks from an atomic counter in the
+// order above, and each task waits on the stamps of the tasks it reads:
+//   panel (m,k,J):   tile (K,J) of step k-1, P_k, and (buffer reuse) all of step k-2's updates
+//   update (m,k,I,J): panels I and J of step k (P_k for the (K,K) tile) and its own step k-1 value;
+//                    the fused pivot also waits for step k-1's panels (pivot slot reuse)
+// Waits only point to earlier tasks, which are held by running CTAs: no deadlock.  Step k+1's
+// panels and updates start while step k's tail is still running (look-ahead).
+__global__ void __launch_bounds__(256, 1) inverse_kernel(const __grid_constant__ InvParams P) {
     extern __shared__ double dyn[];
     __shared__ int next;
-    __shared__ int sbeg[kMaxMats], spiv[kMaxMats];  // decode tables (dynamic param indexing is slow)
-    for (int i = threadIdx.x; i < P.nm; i += blockDim.x) {
-        sbeg[i] = P.m[i].tile_begin;
-        spiv[i] = P.m[i].piv_idx;
-    }
     for (;;) {
-        __syncthreads();  // the previous tile's epilogue / pivot is done with shared memory and `next`
+        __syncthreads();  // the previous task is done with shared memory and `next`
         if (threadIdx.x == 0) next = atomicAdd(P.counter, 1);
         __syncthreads();
         const int g = next;
-        if (g >= P.total_tiles) break;
-        update_tile(P, g, dyn, sbeg, spiv);
+        if (g >= P.total_tasks) break;
+        TRACE(long long tr0 = gtime(); long long tr1 = 0; int trI = -1, trJ = -1, trkind = 0;)
+        const int4 task = P.tasks[g];
+        const int k = task.x, mi = task.z, I = task.w >> 16, J = task.w & 0xffff;
+        const MatDesc &m = P.m[mi];
+        const int nt = m.nt;
+        if (task.y == 0) {
+            // ---------------- panel task
+            if (threadIdx.x == 0 && k >= 1) {
+                wait_ge(P.tileflag + m.tile_begin + (J >= k ? upper_index(k, J, nt) : upper_index(J, k, nt)), k);
+                wait_ge(P.pivflag + mi, k + 1);
+                if (k >= 2) wait_ge(P.tiles_done + m.col_begin + k - 2, nt * (nt + 1) / 2);
+            }
+            if (threadIdx.x == 0) next = *(volatile int *)m.status;  // one decision for the whole CTA
+            __syncthreads();
+            TRACE(tr1 = gtime(); trJ = J; trkind = 0;)
+            if (next == 0) panel_task(m, k, J, dyn);
+            __threadfence();
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(P.colflag + m.col_begin + J), "r"(k + 1) : "memory");
+                atomicAdd(P.panels_done + m.col_begin + k, 1);
+            }
+        } else {
+            // ---------------- update task
+            if (threadIdx.x == 0) {
+                if (I != k) wait_ge(P.colflag + m.col_begin + I, k + 1);
+                if (J != k && J != I) wait_ge(P.colflag + m.col_begin + J, k + 1);
+                if (I == k && J == k && k >= 1) wait_ge(P.pivflag + mi, k + 1);
+                if (k >= 1) wait_ge(P.tileflag + m.tile_begin + upper_index(I, J, nt), k);
+            }
+            if (threadIdx.x == 0) next = *(volatile int *)m.status;  // one decision for the whole CTA
+            __syncthreads();
+            TRACE(tr1 = gtime(); trI = I; trJ = J; trkind = (I == k + 1 && J == k + 1) ? 2 : 1;)
+            int f = 0;
+            if (next == 0)
+                f = update_task(P, m, k, I, J, dyn, P.panels_done + m.col_begin + (k >= 1 ? k - 1 : 0));
+            if (f && threadIdx.x == 0) *m.status = f;
+            __threadfence();
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(P.tileflag + m.tile_begin + upper_index(I, J, nt)), "r"(k + 1)
+                             : "memory");
+                if (I == k + 1 && J == k + 1)
+                    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(P.pivflag + mi), "r"(k + 2) : "memory");
+                atomicAdd(P.tiles_done + m.col_begin + k, 1);
+            }
+        }
+#ifdef INV_TRACE
+        if (threadIdx.x == 0 && g < 65536) {
+            int sm;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+            g_trace[g] = TraceRec{g, k, trkind, trI, trJ, sm, tr0, tr1, gtime()};
+        }
+#endif
     }
 }
 
@@ -559,9 +701,20 @@ __global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ I
 static int g_inv_sms = 0;
 
 int64_t inverse_ld(int n) { return (n + 15) / 16 * 16; }
+int64_t inverse_scratch_bytes(int npairs, int64_t sum_nt, int64_t sum_tiles, int64_t sum_tasks) {
+    // pair data | counter + pivflag (2 npairs) | colflag, panels_done, tiles_done (sum_nt each) |
+    // tileflag | task records (16 B each)
+    return ((4 * (int64_t)npairs + 15) / 16) * 16 * 8 +
+           ((16 + 2 * (int64_t)npairs + 3 * sum_nt + sum_tiles + 3) / 4) * 16 + sum_tasks * 16 + 256;
+}
+// tasks of one n x n matrix's sweep: nt panels + nt (nt + 1) / 2 tiles per step, nt steps
+int64_t inverse_tasks(int n) {
+    const int64_t nt = (n + B - 1) / B;
+    return nt * (nt + nt * (nt + 1) / 2);
+}
 int64_t inverse_ws_doubles(int n) {
     const int64_t ld = inverse_ld(n);
-    return (n * ld + 2 * (int64_t)B * ld + 2 * (int64_t)B * B + 31) / 32 * 32;
+    return (n * ld + 4 * (int64_t)B * ld + 2 * (int64_t)B * B + 31) / 32 * 32;
 }
 
 kfac_status inverse_launch(const std::vector<InvMat> &mats, int npairs, float gamma, double *pair_scratch,
@@ -576,8 +729,7 @@ kfac_status inverse_launch(const std::vector<InvMat> &mats, int npairs, float ga
     }
     if (!attr) {
         KFAC_CUDA_TRY(cudaFuncSetAttribute(pivot_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPivSmem));
-        KFAC_CUDA_TRY(cudaFuncSetAttribute(panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPanelSmem));
-        KFAC_CUDA_TRY(cudaFuncSetAttribute(update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kUpdSmem));
+        KFAC_CUDA_TRY(cudaFuncSetAttribute(inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kUpdSmem));
         attr = true;
     }
     InvParams P;
@@ -586,72 +738,67 @@ kfac_status inverse_launch(const std::vector<InvMat> &mats, int npairs, float ga
     P.gamma = (double)gamma;
     P.pair_scratch = pair_scratch;
     P.pi_out = pi_out;
-    int maxn = 0;
-    for (size_t i = 0; i < mats.size(); i++) {
-        MatDesc &d = P.m[i];
-        d.packed = mats[i].packed;
-        d.inv = mats[i].inv;
-        d.work = mats[i].work;
-        d.panel = mats[i].panel;
-        d.status = mats[i].status;
-        d.n = mats[i].n;
+    // matrices by column blocks, descending: the matrices active at step k are a prefix
+    std::vector<int> order(mats.size());
+    for (size_t i = 0; i < mats.size(); i++) order[i] = (int)i;
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return mats[a].n > mats[b].n; });
+    int maxn = 0, sum_nt = 0, sum_tiles = 0;
+    for (size_t r = 0; r < order.size(); r++) {
+        const InvMat &src = mats[order[r]];
+        MatDesc &d = P.m[r];
+        d.packed = src.packed;
+        d.inv = src.inv;
+        d.work = src.work;
+        d.panel = src.panel;
+        d.status = src.status;
+        d.n = src.n;
         d.ld = (int)inverse_ld(d.n);
-        d.pair = mats[i].pair;
-        d.is_A = mats[i].is_A;
+        d.pair = src.pair;
+        d.is_A = src.is_A;
+        d.nt = (d.n + B - 1) / B;
+        d.col_begin = sum_nt;
+        d.tile_begin = sum_tiles;
+        sum_nt += d.nt;
+        sum_tiles += d.nt * (d.nt + 1) / 2;
         maxn = std::max(maxn, d.n);
     }
+    const int steps = (maxn + B - 1) / B;
+    if (steps > kMaxSteps) return set_error(KFAC_ERR_UNSUPPORTED, "inverse: matrix too large (more than 128 column blocks)");
+    P.steps = steps;
+    std::vector<int> ntl(P.nm);
+    for (int i = 0; i < P.nm; i++) ntl[i] = P.m[i].nt;
+    int task = 0;
+    for (int k = 0; k < steps; k++) {
+        P.step_begin[k] = task;
+        task += gen_step_tasks(ntl.data(), P.nm, k, nullptr);
+    }
+    P.step_begin[steps] = task;
+    P.total_tasks = task;
+    // dataflow state after the pair data (inverse_scratch_bytes): zeroed once per call
+    int *state = reinterpret_cast<int *>(pair_scratch + ((4 * (int64_t)npairs + 15) / 16) * 16);
+    P.counter = state;
+    P.pivflag = state + 16;
+    P.colflag = P.pivflag + 2 * npairs;
+    P.panels_done = P.colflag + sum_nt;
+    P.tiles_done = P.panels_done + sum_nt;
+    P.tileflag = P.tiles_done + sum_nt;
+    P.tasks = reinterpret_cast<int4 *>(state + ((16 + 2 * (int64_t)npairs + 3 * sum_nt + sum_tiles + 3) / 4) * 4);
+    KFAC_CUDA_TRY(cudaMemsetAsync(state, 0, (16 + 2 * (int64_t)npairs + 3 * sum_nt + sum_tiles) * sizeof(int), st));
+    inverse_tasks_kernel<<<1, 128, 0, st>>>(P);
+    KFAC_LAUNCHED();
+    KFAC_CUDA_TRY(cudaGetLastError());
     damp_trace_kernel<<<P.nm, 256, 0, st>>>(P);
     KFAC_LAUNCHED();
     KFAC_CUDA_TRY(cudaGetLastError());
     unpack_damp_kernel<<<dim3(std::min(maxn, 1024), P.nm), 256, 0, st>>>(P);
     KFAC_LAUNCHED();
     KFAC_CUDA_TRY(cudaGetLastError());
-    const int steps = (maxn + B - 1) / B;
-    const int fuse = getenv("KFAC_INV_NOFUSE") ? 0 : 1;
-    // per-step tile counters live in the scratch after the pair data (plan reserves 1 KB)
-    int *counters = reinterpret_cast<int *>(pair_scratch + ((4 * (int64_t)npairs + 15) / 16) * 16);
-    if (steps > 256) return set_error(KFAC_ERR_UNSUPPORTED, "inverse: matrix too large for the step counters");
-    KFAC_CUDA_TRY(cudaMemsetAsync(counters, 0, steps * sizeof(int), st));
-    for (int k = 0; k < steps; k++) {
-        // active matrices only (n > k*B), with their upper-tile and column-block prefixes
-        InvParams Q;
-        memset(&Q, 0, offsetof(InvParams, m));
-        Q.gamma = P.gamma;
-        Q.k = k;
-        int nm = 0, tiles = 0, cols = 0, npiv = 0;
-        for (int i = 0; i < P.nm; i++) {
-            if (P.m[i].n <= k * B) continue;
-            Q.m[nm] = P.m[i];
-            const int nt = (P.m[i].n + B - 1) / B;
-            Q.m[nm].piv_idx = (fuse && k + 1 < nt) ? npiv++ : -1;
-            Q.m[nm].col_begin = cols;
-            cols += nt;
-            nm++;
-        }
-        tiles = npiv;
-        for (int i = 0; i < nm; i++) {
-            const int nt = (Q.m[i].n + B - 1) / B;
-            Q.m[i].tile_begin = tiles;
-            tiles += nt * (nt + 1) / 2 - (Q.m[i].piv_idx >= 0 ? 1 : 0);
-        }
-        Q.npiv = npiv;
-        Q.counter = counters + k;
-        Q.nm = nm;
-        Q.total_tiles = tiles;
-        Q.total_cols = cols;
-        Q.fuse = fuse;
-        if (k == 0 || !fuse) {
-            pivot_kernel<<<nm, 256, kPivSmem, st>>>(Q);
-            KFAC_LAUNCHED();
-            KFAC_CUDA_TRY(cudaGetLastError());
-        }
-        panel_kernel<<<cols, 256, kPanelSmem, st>>>(Q);
-        KFAC_LAUNCHED();
-        KFAC_CUDA_TRY(cudaGetLastError());
-        update_kernel<<<std::min(tiles, g_inv_sms), 256, kUpdSmem, st>>>(Q);
-        KFAC_LAUNCHED();
-        KFAC_CUDA_TRY(cudaGetLastError());
-    }
+    pivot_kernel<<<P.nm, 256, kPivSmem, st>>>(P);
+    KFAC_LAUNCHED();
+    KFAC_CUDA_TRY(cudaGetLastError());
+    inverse_kernel<<<std::min(P.total_tasks, g_inv_sms), 256, kUpdSmem, st>>>(P);
+    KFAC_LAUNCHED();
+    KFAC_CUDA_TRY(cudaGetLastError());
     finalize_kernel<<<dim3(std::min(((maxn + 31) / 32) * ((maxn + 31) / 32), 1184), P.nm), 256, 0, st>>>(P);
     KFAC_LAUNCHED();
     KFAC_CUDA_TRY(cudaGetLastError());

@@ -92,7 +92,7 @@ struct InvMat {        // one damped factor to invert
     const float *packed;  // packed upper fp32 (from rs_recv)
     float *inv;           // full fp32 output
     double *work;         // n*n fp64 working matrix
-    double *panel;        // 2 * kPanel * n fp64 (row panel R and W = P R)
+    double *panel;        // 4 * kPanel * ld + 2 * kPanel^2 fp64 (R, P R per step parity; two pivots)
     int32_t *status;      // device status word
     int32_t n;
     int32_t pair;         // index of the (A, G) pair this matrix belongs to
@@ -115,5 +115,9 @@ kfac_status replicate_launch(const std::vector<std::pair<const float *, float *>
 
 constexpr int kPanel = 128;  // sweep block size of the inverse
 int64_t inverse_ws_doubles(int n);  // fp64 working matrix + panels of one n x n inverse
+// pair data (pi, damping) + the dataflow state of the persistent sweep; over the owned matrices,
+// sum_nt = sum of nt = ceil(n / kPanel), sum_tiles = sum of nt (nt + 1) / 2
+int64_t inverse_scratch_bytes(int npairs, int64_t sum_nt, int64_t sum_tiles, int64_t sum_tasks);
+int64_t inverse_tasks(int n);  // tasks of one matrix's sweep (sum_tasks = sum over owned matrices)
 
 }  // namespace kfac

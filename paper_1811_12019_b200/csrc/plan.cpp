@@ -148,18 +148,24 @@ kfac_status plan_build(kfac_plan *p) {
     p->inv_floats.assign(P, 0);
     int64_t ws = 0;
     for (int r = 0; r < P; r++) {
-        int64_t off = 0, inv_ws = 0, prec_ws = 0;
+        int64_t off = 0, inv_ws = 0, prec_ws = 0, sum_nt = 0, sum_tiles = 0, sum_tasks = 0;
         for (int l : p->owned[r]) {
             const Geom &g = p->geoms[l];
             p->inv_off[r].push_back(off);
             off = align16(off + (int64_t)g.dA * g.dA);
             p->inv_off[r].push_back(off);
             off = align16(off + (int64_t)g.dG * g.dG);
-            for (int n : {g.dA, g.dG}) inv_ws += inverse_ws_doubles(n) * 8;
+            for (int n : {g.dA, g.dG}) {
+                const int64_t nt = (n + kPanel - 1) / kPanel;
+                inv_ws += inverse_ws_doubles(n) * 8;
+                sum_nt += nt;
+                sum_tiles += nt * (nt + 1) / 2;
+                sum_tasks += inverse_tasks(n);
+            }
             prec_ws += (align16(precond_ws_floats(g.dG, g.dA)) + align16((int64_t)g.dG * g.dA)) * 4;  // split operands + (redundant) output
         }
         p->inv_floats[r] = off;
-        inv_ws += align16(4 * (int64_t)p->owned[r].size()) * 8 + 1024;  // pair scratch
+        inv_ws += align16(inverse_scratch_bytes((int)p->owned[r].size(), sum_nt, sum_tiles, sum_tasks));  // pair scratch, counters, flags
         ws = std::max(ws, std::max(inv_ws, prec_ws));
     }
     // factor stage: split-K partials of the grouped launch (same planner as the kernel)

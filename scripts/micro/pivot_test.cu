@@ -47,5 +47,19 @@ int main(int argc, char **argv) {
             err = fmax(err, fabs(s - (i == j)));
         }
     printf("status %d  max|M P - I| = %.3e\n", st, err);
+    cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+    for (int r = 0; r < 20; r++) tkernel<<<1, 256, kPivSmem>>>(dW, n, n, dP, dst);
+    cudaEventRecord(e1); cudaEventSynchronize(e1);
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    printf("pivot_block n=%d: %.1f us per call\n", n, ms * 1e3 / 20);
+#ifdef PIVOT_DBG
+    long long c[64];
+    cudaMemcpyFromSymbol(c, g_pclk, sizeof(c));
+    for (int sb = 0; sb < 4; sb++)
+        printf("sb %d: sweep %lld  O-copy %lld  W=QO %lld  update %lld\n", sb, c[1 + 4 * sb] - (sb ? c[4 * sb] : c[0]),
+               c[2 + 4 * sb] - c[1 + 4 * sb], c[3 + 4 * sb] - c[2 + 4 * sb], c[4 + 4 * sb] - c[3 + 4 * sb]);
+    printf("total %lld cycles\n", c[20] - c[0]);
+#endif
     return 0;
 }

@@ -1,0 +1,25 @@
+"""Summarise an inverse task timeline (scripts/micro/inv_trace output): per step, when the panels,
+the fused pivot and the tiles ran; per CTA, work vs wait time."""
+import sys, collections
+rows = [list(map(int, l.split())) for l in open(sys.argv[1]) if l.strip()]
+t0 = min(r[6] for r in rows)
+steps = collections.defaultdict(list)
+for g, k, kind, I, J, sm, a, b, c in rows:
+    steps[k].append((kind, I, J, (a - t0) / 1e3, (b - t0) / 1e3, (c - t0) / 1e3))
+print("step  panels[start..end]   pivot-tile[start..end]   tiles[first start..last end]  (us)")
+for k in sorted(steps):
+    P = [x for x in steps[k] if x[0] == 0]
+    V = [x for x in steps[k] if x[0] == 2]
+    T = [x for x in steps[k] if x[0] == 1]
+    f = lambda L: f"{min(x[4] for x in L):8.1f}..{max(x[5] for x in L):8.1f}" if L else " " * 18
+    print(f"{k:4d}  {f(P)}  {f(V)}  {f(T)}")
+work = sum(r[8] - r[7] for r in rows) / 1e3
+wait = sum(r[7] - r[6] for r in rows) / 1e3
+end = (max(r[8] for r in rows) - t0) / 1e3
+ncta = len(set(r[5] for r in rows))
+print(f"total {end:.1f} us, CTAs {ncta}, work {work/ncta:.1f} us/CTA, wait {wait/ncta:.1f} us/CTA")
+kinds = collections.defaultdict(list)
+for r in rows:
+    kinds[r[2]].append((r[8] - r[7]) / 1e3)
+for kd, L in sorted(kinds.items()):
+    print(f"kind {kd}: n={len(L)} mean {sum(L)/len(L):.1f} us, max {max(L):.1f}")
