@@ -29,7 +29,6 @@ from synth import inputs, shapes  # noqa: E402
 METRIC = "ResNet-50 K-FAC step ms & factor TFLOP/s at 1/2/4/8 B200, % roofline"
 # derived peaks: 148 SM x lanes x 2 flop x 1.965 GHz
 FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # 37.2 (DFMA)
-FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # 74.4 (FFMA)
 NVLINK_GBS = 770.0                                   # measured peer copy per direction (B200_PROFILING.md)
 
 
@@ -306,17 +305,21 @@ def run_ours(args):
                 "kernel": "factor_syrk_kernel (+fixup, bias)", "flops_counting": "upper triangle, rows*d*(d+1)",
                 "hbm_gbs": round(w["factor_bytes"] / fac_s / 1e9, 1), "peak_src": pk["src"] + " sustained"}
     inv_tf = w["inverse_flops"] / (st_ms["inverse"] / 1e3) / 1e12
+    prec_peak = pk["bf16_tflops_sustained"] * 0.5 / 3.0
     prec_tf = w["precond_flops"] / (st_ms["precondition"] / 1e3) / 1e12
     rs_bytes = st.q["rs_chunk"] * 4 * (world - 1)
     roofs = {
         "factors": fac_roof,
-        "inverse": {"bound": "alu", "achieved": round(inv_tf, 3), "peak": round(FP64_PEAK_TFLOPS, 1),
+        "inverse": {"bound": "tensor", "achieved": round(inv_tf, 3), "peak": round(FP64_PEAK_TFLOPS, 1),
                     "unit": "TFLOP/s", "frac": round(inv_tf / FP64_PEAK_TFLOPS, 4), "traffic": None,
-                    "kernel": "damped_inverse (pivot/panel/update_kernel, fp64)",
-                    "flops_counting": "n^3 per matrix", "peak_src": "derived fp64 148x64x2x1.965GHz"},
-        "precondition": {"bound": "alu", "achieved": round(prec_tf, 3), "peak": round(FP32_PEAK_TFLOPS, 1),
-                         "unit": "TFLOP/s", "frac": round(prec_tf / FP32_PEAK_TFLOPS, 4), "traffic": None,
-                         "kernel": "sgemm_grouped_kernel (fp32 FFMA)", "peak_src": "derived fp32 148x128x2x1.965GHz"},
+                    "kernel": "inverse_kernel (persistent fp64 block sweep on DMMA; + pivot, finalize)",
+                    "flops_counting": "n^3 per matrix",
+                    "peak_src": "derived fp64 148x64x2x1.965GHz (DMMA measured 37.1, scripts/micro/dmma_bench.cu)"},
+        "precondition": {"bound": "tensor", "achieved": round(prec_tf, 3), "peak": round(prec_peak, 1),
+                         "unit": "TFLOP/s", "frac": round(prec_tf / prec_peak, 4), "traffic": None,
+                         "kernel": "gemm_3xtf32_kernel (tcgen05 kind::tf32, 3 products per fp32 product)",
+                         "flops_counting": "2 dG dA (dA + dG) per layer (useful fp32 flops)",
+                         "peak_src": pk["src"] + " bf16 sustained x 1/2 (tf32) / 3 (3xTF32)"},
     }
     if world > 1:
         for nm in ("reduce_scatter", "allgather"):

@@ -587,16 +587,30 @@ __global__ void __launch_bounds__(kThreads, 1) factor_syrk_kernel(const __grid_c
 // ordered split-K fix-up: out = alpha * sum_{s=0..S-1} partial[s] (deterministic).
 // One block per (tile pair, 8-row group); warp = row, lane = 8 columns; all S x 8 loads independent.
 constexpr int kFixRowGroups = kTile / 8;
+// the blockIdx.x-th item of a list over the problems, item counts cnt[p] loaded in parallel into
+// shared memory (a serial walk over the kernel-parameter array costs a constant-cache miss per problem)
+__device__ __forceinline__ int locate(int *cnt, int nprobs, int &b) {
+    __shared__ int res[2];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int p = 0;
+        for (; p < nprobs; p++) {
+            if (b < cnt[p]) break;
+            b -= cnt[p];
+        }
+        res[0] = p;
+        res[1] = b;
+    }
+    __syncthreads();
+    b = res[1];
+    return res[0];
+}
 __global__ void __launch_bounds__(256) factor_fixup_kernel(const __grid_constant__ FactorParams P) {
+    __shared__ int cnt[kMaxProbs];
+    for (int q = threadIdx.x; q < P.nprobs; q += blockDim.x) cnt[q] = P.probs[q].splits > 1 ? P.probs[q].npairs : 0;
     int b = blockIdx.x / kFixRowGroups;
     const int rg = blockIdx.x % kFixRowGroups;
-    int p = 0;
-    for (; p < P.nprobs; p++) {
-        const FactorProb &pr = P.probs[p];
-        if (pr.splits <= 1) continue;
-        if (b < pr.npairs) break;
-        b -= pr.npairs;
-    }
+    const int p = locate(cnt, P.nprobs, b);
     if (p >= P.nprobs) return;
     const FactorProb &pr = P.probs[p];
     int ti, tj;
@@ -630,11 +644,11 @@ __global__ void __launch_bounds__(256) factor_fixup_kernel(const __grid_constant
 // walked incrementally) and writes them as one 16-byte vector, so a warp writes its pixel's
 // cp-element row contiguously.  32-bit index math only (rows < 2^31).
 __global__ void __launch_bounds__(256) im2col_kernel(const __grid_constant__ FactorParams P) {
-    int p = 0;  // blockIdx.y-th problem with materialised patches
-    for (int k = blockIdx.y;; p++) {
-        if (p >= P.nprobs) return;
-        if (P.probs[p].im2col_pre && k-- == 0) break;
-    }
+    __shared__ int cnt[kMaxProbs];  // blockIdx.y-th problem with materialised patches
+    for (int q = threadIdx.x; q < P.nprobs; q += blockDim.x) cnt[q] = P.probs[q].im2col_pre ? 1 : 0;
+    int b = blockIdx.y;
+    const int p = locate(cnt, P.nprobs, b);
+    if (p >= P.nprobs) return;
     const FactorProb &g = P.probs[p];
     const int C = g.c, kw = g.kw, nq = g.cp / 8, hw = g.ho * g.wo, d = g.d;
     const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
@@ -689,11 +703,11 @@ __global__ void __launch_bounds__(256) im2col_kernel(const __grid_constant__ Fac
 // bias row/column of A: A[f][dA-1] = alpha * sum_rows ã_f, A[dA-1][dA-1] = alpha * rows
 // (the homogeneous coordinate, reading R-5); one thread per feature, fixed row order.
 __global__ void __launch_bounds__(256) factor_bias_kernel(const __grid_constant__ FactorParams P) {
-    int p = 0;  // blockIdx.y-th problem with a bias coordinate
-    for (int k = blockIdx.y;; p++) {
-        if (p >= P.nprobs) return;
-        if (P.probs[p].d_out != P.probs[p].d && k-- == 0) break;
-    }
+    __shared__ int cnt[kMaxProbs];  // blockIdx.y-th problem with a bias coordinate
+    for (int q = threadIdx.x; q < P.nprobs; q += blockDim.x) cnt[q] = P.probs[q].d_out != P.probs[q].d ? 1 : 0;
+    int b = blockIdx.y;
+    const int p = locate(cnt, P.nprobs, b);
+    if (p >= P.nprobs) return;
     const ProbRegs pr = load_prob(P.probs[p]);
     const int f = blockIdx.x * blockDim.x + threadIdx.x;
     const int dA = pr.d_out;

@@ -550,49 +550,102 @@ __device__ __forceinline__ int upper_index(int I, int J, int nt) { return I * nt
 //      (their CTAs wait for P_{k+1}; the chain pivot -> panel -> tile -> pivot then runs without
 //      queueing behind the rest of the step)
 //   S5 the remaining tiles of step k
-// Matrices are sorted by nt descending (active ones are a prefix).  Returns the number of tasks.
-__host__ __device__ inline int gen_step_tasks(const int *nt, int nm, int k, int4 *out) {
+// Matrices are sorted by nt descending (active ones are a prefix).  Per-matrix counts of each
+// segment, so that a step's list can be written by one warp per matrix in parallel.
+__host__ __device__ inline int seg_s1(int nt, int k) { return nt > k ? nt - ((k >= 1 && nt > k + 1) ? 1 : 0) : 0; }
+__host__ __device__ inline int seg_s3(int nt, int k) { return nt > k + 1 ? (nt - 1) + (nt > k + 2 ? 1 : 0) : 0; }
+__host__ __device__ inline int seg_s5(int nt, int k) {
+    if (nt <= k) return 0;
+    int c = nt * (nt + 1) / 2;
+    if (nt > k + 1) c -= nt;      // block row / column K+1 incl. (K+1, K+1)
+    if (nt > k + 2) c -= 1;       // (K+2, K+2)
+    return c;
+}
+// S5 tiles of row I (count), with L = k+1 look-ahead exclusions
+__host__ __device__ inline int s5_row(int nt, int k, int I) {
+    const int L = k + 1;
+    if (nt <= L) return nt - I;  // no look-ahead at the last step
+    if (I == L) return 0;
+    int c = nt - I - (I < L ? 1 : 0);
+    if (nt > k + 2 && I == k + 2) c -= 1;
+    return c;
+}
+// total tasks of step k over the sorted nt list (host: step offsets)
+inline int step_tasks(const int *nt, int nm, int k) {
     int c = 0;
-    auto put = [&](int kk, int kind, int m, int I, int J) {
-        if (out) out[c] = make_int4(kk, kind, m, (I << 16) | J);
-        c++;
-    };
-    for (int m = 0; m < nm && nt[m] > k; m++) {  // S1
-        const bool moved = k >= 1 && nt[m] > k + 1;  // panel (k, K+1) was issued in E(k-1)
-        if (k == 0 && nt[m] > 1) put(k, 0, m, 0, 1);
-        for (int J = 0; J < nt[m]; J++) {
-            if (J == k + 1 && (moved || (k == 0 && nt[m] > 1))) continue;
-            put(k, 0, m, 0, J);
-        }
-    }
-    if (k == 0)  // S2
-        for (int m = 0; m < nm && nt[m] > 1; m++) put(0, 1, m, 1, 1);
-    for (int m = 0; m < nm && nt[m] > k + 1; m++) {  // S3
-        const int L = k + 1;
-        for (int I = 0; I < L; I++) put(k, 1, m, I, L);
-        for (int J = L + 1; J < nt[m]; J++) put(k, 1, m, L, J);
-        if (nt[m] > k + 2) put(k, 1, m, k + 2, k + 2);
-    }
-    for (int m = 0; m < nm && nt[m] > k + 2; m++) put(k + 1, 0, m, 0, k + 2);  // E: panels
-    for (int m = 0; m < nm && nt[m] > k + 2; m++) put(k + 1, 1, m, k + 2, k + 2);  // E: next pivots
-    for (int m = 0; m < nm && nt[m] > k; m++) {  // S5
-        const int L = k + 1;
-        const bool la = nt[m] > L;
-        for (int I = 0; I < nt[m]; I++)
-            for (int J = I; J < nt[m]; J++) {
-                if (la && (I == L || J == L)) continue;          // pivot tile + look-ahead (S2/E, S3)
-                if (nt[m] > k + 2 && I == k + 2 && J == k + 2) continue;  // S3
-                put(k, 1, m, I, J);
-            }
+    for (int m = 0; m < nm; m++) {
+        c += seg_s1(nt[m], k) + seg_s3(nt[m], k) + seg_s5(nt[m], k);
+        if (k == 0 && nt[m] > 1) c += 1;      // S2
+        if (nt[m] > k + 2) c += 2;            // E
     }
     return c;
 }
 
-__global__ void inverse_tasks_kernel(const __grid_constant__ InvParams P) {
-    __shared__ int nt[kMaxMats];
-    for (int i = threadIdx.x; i < P.nm; i += blockDim.x) nt[i] = P.m[i].nt;
-    __syncthreads();
-    for (int k = threadIdx.x; k < P.steps; k += blockDim.x) gen_step_tasks(nt, P.nm, k, P.tasks + P.step_begin[k]);
+// one warp per (step, matrix): offsets of the matrix's entries in each segment of the step's list
+// (prefix over the matrices before it), then the lanes write them
+__global__ void __launch_bounds__(32) inverse_tasks_kernel(const __grid_constant__ InvParams P) {
+    const int k = blockIdx.x, m = blockIdx.y, lane = threadIdx.x;
+    const int nt = P.m[m].nt;
+    if (nt <= k) return;
+    __shared__ int rowoff[kMaxSteps + 1];
+    int a1 = 0, a2 = 0, a3 = 0, a5 = 0, nA = 0, nS1 = 0, nS2 = 0, nS3 = 0, nE = 0;
+    for (int i = 0; i < P.nm; i++) {  // segment totals and this matrix's prefix
+        const int n = P.m[i].nt;
+        if (i < m) {
+            a1 += seg_s1(n, k);
+            a2 += (k == 0 && n > 1) ? 1 : 0;
+            a3 += seg_s3(n, k);
+            a5 += seg_s5(n, k);
+            nA += n > k + 2 ? 1 : 0;
+        }
+        nS1 += seg_s1(n, k);
+        nS2 += (k == 0 && n > 1) ? 1 : 0;
+        nS3 += seg_s3(n, k);
+        nE += n > k + 2 ? 1 : 0;
+    }
+    int4 *out = P.tasks + P.step_begin[k];
+    const int o1 = a1, o2 = nS1 + a2, o3 = nS1 + nS2 + a3, oE = nS1 + nS2 + nS3, o5 = oE + 2 * nE + a5;
+    const int L = k + 1;
+    // S1: panels (column K+1 first at step 0; at k >= 1 it went to E(k-1))
+    {
+        const bool first = k == 0 && nt > 1, moved = k >= 1 && nt > k + 1;
+        for (int e = lane; e < seg_s1(nt, k); e += 32) {
+            int J;
+            if (first) J = (e == 0) ? 1 : (e <= 1 ? e - 1 : e);
+            else if (moved) J = e < L ? e : e + 1;
+            else J = e;
+            out[o1 + e] = make_int4(k, 0, m, J);
+        }
+    }
+    if (lane == 0 && k == 0 && nt > 1) out[o2] = make_int4(0, 1, m, (1 << 16) | 1);  // S2
+    if (nt > L) {  // S3
+        for (int e = lane; e < nt - 1; e += 32) {
+            const int I = e < L ? e : L, J = e < L ? L : e + 1;
+            out[o3 + e] = make_int4(k, 1, m, (I << 16) | J);
+        }
+        if (lane == 0 && nt > k + 2) out[o3 + nt - 1] = make_int4(k, 1, m, ((k + 2) << 16) | (k + 2));
+    }
+    if (lane == 0 && nt > k + 2) {  // E
+        out[oE + nA] = make_int4(k + 1, 0, m, k + 2);
+        out[oE + nE + nA] = make_int4(k + 1, 1, m, ((k + 2) << 16) | (k + 2));
+    }
+    // S5: row offsets, then one lane per row
+    if (lane == 0) {
+        int c = 0;
+        for (int I = 0; I < nt; I++) {
+            rowoff[I] = c;
+            c += s5_row(nt, k, I);
+        }
+    }
+    __syncwarp();
+    for (int I = lane; I < nt; I += 32) {
+        int c = o5 + rowoff[I];
+        for (int J = I; J < nt; J++) {
+            if (nt > L && (I == L || J == L)) continue;
+            if (nt > k + 2 && I == k + 2 && J == k + 2) continue;
+            out[c++] = make_int4(k, 1, m, (I << 16) | J);
+        }
+    }
 }
 
 // ---- the whole sweep as ONE persistent launch: CTAs take tasks from an atomic counter in the
@@ -770,7 +823,7 @@ kfac_status inverse_launch(const std::vector<InvMat> &mats, int npairs, float ga
     int task = 0;
     for (int k = 0; k < steps; k++) {
         P.step_begin[k] = task;
-        task += gen_step_tasks(ntl.data(), P.nm, k, nullptr);
+        task += step_tasks(ntl.data(), P.nm, k);
     }
     P.step_begin[steps] = task;
     P.total_tasks = task;
@@ -784,7 +837,7 @@ kfac_status inverse_launch(const std::vector<InvMat> &mats, int npairs, float ga
     P.tileflag = P.tiles_done + sum_nt;
     P.tasks = reinterpret_cast<int4 *>(state + ((16 + 2 * (int64_t)npairs + 3 * sum_nt + sum_tiles + 3) / 4) * 4);
     KFAC_CUDA_TRY(cudaMemsetAsync(state, 0, (16 + 2 * (int64_t)npairs + 3 * sum_nt + sum_tiles) * sizeof(int), st));
-    inverse_tasks_kernel<<<1, 128, 0, st>>>(P);
+    inverse_tasks_kernel<<<dim3(steps, P.nm), 32, 0, st>>>(P);
     KFAC_LAUNCHED();
     KFAC_CUDA_TRY(cudaGetLastError());
     damp_trace_kernel<<<P.nm, 256, 0, st>>>(P);

@@ -1,0 +1,6 @@
+# round profile, part B: launch list (per-kernel GPU time) of the bench command
+cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
+python paper_1811_12019_b200/build.py > /dev/null
+timeout -s KILL 600 python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/b2.log 2>&1 && \
+timeout -s KILL 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv \
+  python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_b.log 2>&1; echo "ncu rc=$?"
