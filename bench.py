@@ -262,35 +262,77 @@ def run_ours(args):
     ms = tot[0] / args.steps
     st_ms = {nm: tot[1 + i] / args.steps for i, nm in enumerate(names)}
 
-    # ---- end-to-end through the public API with host buffers (H2D inputs, D2H result)
+    # ---- end-to-end through the public API with host buffers (H2D inputs, D2H result).  Every
+    # step's inputs are copied from pinned host memory and its result read back inside the timed
+    # region; the copies run on their own streams (H2D and D2H directions concurrently) and are
+    # double-buffered, so step s+1's upload overlaps step s's compute (a training loop prefetching
+    # its next batch).  Dependencies: the dW upload waits for the previous step's ReduceScatter
+    # (dW lives in the send buffer), an input set is reused two steps later, the result read-back
+    # of step s must finish before step s+1's precondition rewrites the AllGather buffer.
     e2e = None
     if not args.no_e2e:
         out_h = torch.empty(st.ag_buf.numel(), dtype=torch.float32).pin_memory()
         dwv = [st.dw_view(l) for l in range(len(layers))]
-        for _ in range(2):
-            for x, xh in zip(xs, xs_h):
-                x.copy_(xh, non_blocking=True)
-            st.run(xs, gys, args.gamma, stream)
+        bufs = [(xs, gys), ([torch.empty_like(x) for x in xs], [torch.empty_like(g) for g in gys])]
+        up_s, down_s = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+
+        def e2e_run(ke):
+            E = lambda: torch.cuda.Event()  # noqa: E731
+            ev_up, ev_fac, ev_rs, ev_ag, ev_dn = ([E() for _ in range(ke)] for _ in range(5))
+
+            def upload(s):
+                X, Gy = bufs[s % 2]
+                if s >= 1:
+                    up_s.wait_event(ev_rs[s - 1])
+                if s >= 2:
+                    up_s.wait_event(ev_fac[s - 2])
+                with torch.cuda.stream(up_s):
+                    for x, xh in zip(X, xs_h):
+                        x.copy_(xh, non_blocking=True)
+                    for g, gh in zip(Gy, gys_h):
+                        g.copy_(gh, non_blocking=True)
+                    for d, dh in zip(dwv, dws_h):
+                        d.copy_(dh, non_blocking=True)
+                ev_up[s].record(up_s)
+
+            upload(0)
+            for s in range(ke):
+                X, Gy = bufs[s % 2]
+                stream.wait_event(ev_up[s])
+                st.factors(X, Gy, stream=stream)
+                ev_fac[s].record(stream)
+                st.reduce_scatter(stream)
+                ev_rs[s].record(stream)
+                if s + 1 < ke:
+                    upload(s + 1)
+                st.inverse(args.gamma, stream)
+                if s >= 1:
+                    stream.wait_event(ev_dn[s - 1])
+                st.precondition(stream)
+                st.allgather(stream)
+                ev_ag[s].record(stream)
+                down_s.wait_event(ev_ag[s])
+                with torch.cuda.stream(down_s):
+                    out_h.copy_(st.ag_buf, non_blocking=True)
+                ev_dn[s].record(down_s)
+            stream.wait_event(ev_dn[ke - 1])
+
+        e2e_run(2)
         barrier()
+        up_s.wait_stream(stream)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ke = max(2, min(args.steps, 6))
         e0.record(stream)
-        ke = max(1, min(args.steps, 5))
-        for _ in range(ke):
-            for x, xh in zip(xs, xs_h):
-                x.copy_(xh, non_blocking=True)
-            for g, gh in zip(gys, gys_h):
-                g.copy_(gh, non_blocking=True)
-            for d, dh in zip(dwv, dws_h):
-                d.copy_(dh, non_blocking=True)
-            st.run(xs, gys, args.gamma, stream)
-            out_h.copy_(st.ag_buf, non_blocking=True)
+        up_s.wait_event(e0)  # the first upload starts inside the timed region
+        e2e_run(ke)
         e1.record(stream)
         barrier()
         em = torch.tensor([e0.elapsed_time(e1) / ke], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(em, op=dist.ReduceOp.MAX)
         e2e = {"value": round(em.item(), 3), "unit": "ms", "h2d_bytes_per_step": in_bytes + dw_bytes,
-               "d2h_bytes_per_step": out_h.numel() * 4, "steps": ke}
+               "d2h_bytes_per_step": out_h.numel() * 4, "steps": ke,
+               "pipelining": "H2D of step s+1 overlaps step s (double-buffered inputs, separate copy streams)"}
 
     # ---- roofline of the dominant stage (+ the factor kernel, the north-star contraction)
     pk = peaks()
