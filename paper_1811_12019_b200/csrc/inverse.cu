@@ -192,7 +192,7 @@ __device__ long long g_pclk[64];
 #define PCLK(k)
 #endif
 __device__ int pivot_block(const double *__restrict__ W, int64_t ld, int k0, int bk, double *__restrict__ Pout,
-                           double *smem) {
+                           double *smem, bool preloaded = false) {
     double(*S)[B + 1] = reinterpret_cast<double(*)[B + 1]>(smem);
     double *O = smem + B * (B + 1);       // [S2][SLD] old block row
     double *Wr = O + S2 * SLD;            // [S2][SLD] Q * O
@@ -200,12 +200,14 @@ __device__ int pivot_block(const double *__restrict__ W, int64_t ld, int k0, int
     double *colbuf = Q + S2 * QLD;        // [2][32] sweep broadcast buffers (ping-pong)
     int *fsh = reinterpret_cast<int *>(colbuf + 64);
     const int tid = threadIdx.x;
-    for (int e = tid; e < B * B; e += blockDim.x) {
-        const int i = e >> 7, j = e & (B - 1);
-        double val = (i == j) ? 1.0 : 0.0;  // identity padding keeps the sweep well defined
-        if (i < bk && j < bk) val = W[(int64_t)(k0 + min(i, j)) * ld + (k0 + max(i, j))];
-        S[i][j] = val;
-    }
+    // only the upper triangle of S is ever read (min / max indexing below), so only it is loaded
+    // (coalesced rows); identity padding beyond bk keeps the sweep well defined
+    if (!preloaded)
+        for (int e = tid; e < B * B; e += blockDim.x) {
+            const int i = e >> 7, j = e & (B - 1);
+            if (j < i) continue;
+            S[i][j] = (i < bk && j < bk) ? W[(int64_t)(k0 + i) * ld + (k0 + j)] : (i == j ? 1.0 : 0.0);
+        }
     if (tid == 0) *fsh = 0;
     __syncthreads();
     PCLK(0)
@@ -492,6 +494,37 @@ __device__ int update_task(const InvParams &P, const MatDesc &m, int k, int I, i
     };
     // M_IJ -= R_I^T Wp_J : acc[i][j] = sum_t R[t][i0+i] Wp[t][j0+j]
     tile_product(R + i0, ld, bi, Wp + j0, ld, bj, bk, acc, dyn, cslice);
+    if (I == K + 1 && J == K + 1) {
+        // fused next pivot: P_{K+1} = (updated M_{K+1,K+1})^-1.  The updated tile goes straight into
+        // the pivot's shared-memory copy: its global value is dead (the next step's (K,K) tile
+        // overwrites it with -P and no panel reads the pivot column).
+#pragma unroll
+        for (int p = 0; p < 8; p++)
+#pragma unroll
+            for (int q = 0; q < 8; q++) acc[p][q] = Cs[tile_row(p) * SLD + tile_col(q)] - acc[p][q];
+        __syncthreads();  // Cs is read; the pivot's smem overlaps it
+        double(*S)[B + 1] = reinterpret_cast<double(*)[B + 1]>(dyn);
+#pragma unroll
+        for (int p = 0; p < 8; p++) {
+            const int i = tile_row(p);
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+                const int j = tile_col(q);
+                S[i][j] = (i < bi && j < bi) ? acc[p][q] : (i == j ? 1.0 : 0.0);
+            }
+        }
+        __syncthreads();
+        // its slot held P_{k-1}: every step-(k-1) panel task must be done reading it
+        if (k >= 1 && threadIdx.x == 0) {
+            int v;
+            do {
+                asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(pflag) : "memory");
+                if (v < m.nt) __nanosleep(128);
+            } while (v < m.nt);
+        }
+        __syncthreads();
+        return pivot_block(W, ld, i0, bi, pivot_slot(m, K + 1), dyn, true);
+    }
     // column pairs (16-byte stores); rows are written whole up to the leading dimension: the lower
     // half of a diagonal tile and the padding columns are never read (upper storage)
 #pragma unroll
@@ -505,20 +538,6 @@ __device__ int update_task(const InvParams &P, const MatDesc &m, int k, int I, i
             const double2 c = *reinterpret_cast<const double2 *>(Cs + i * SLD + j);
             *reinterpret_cast<double2 *>(W + (int64_t)(i0 + i) * ld + j0 + j) = make_double2(c.x - acc[p][q], c.y - acc[p][q + 1]);
         }
-    }
-    if (I == K + 1 && J == K + 1) {  // fused next pivot: P_{K+1} = (updated M_{K+1,K+1})^-1
-        __threadfence_block();
-        __syncthreads();
-        // its slot held P_{k-1}: every step-(k-1) panel task must be done reading it
-        if (k >= 1 && threadIdx.x == 0) {
-            int v;
-            do {
-                asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(pflag) : "memory");
-                if (v < m.nt) __nanosleep(128);
-            } while (v < m.nt);
-        }
-        __syncthreads();
-        return pivot_block(W, ld, i0, bi, pivot_slot(m, K + 1), dyn);
     }
     return 0;
 }
@@ -543,24 +562,19 @@ __device__ __forceinline__ int upper_index(int I, int J, int nt) { return I * nt
 
 // ---- the task list of step k (one record per task: {k, kind, matrix, I << 16 | J}, kind 0 panel J,
 // 1 update of tile (I, J)), ordered for the critical path K -> K+1 of every matrix:
-//   S1 the step's panels (column K+1 first at step 0; later it was issued early, see E)
-//   S2 (step 0 only) the next-pivot tiles (1, 1)
-//   S3 look-ahead tiles: the rest of block row / column K+1 and the diagonal tile (K+2, K+2)
-//   E  early tasks of step k+1: panel (k+1, K+2) and the next-pivot tile (K+2, K+2) at step k+1
-//      (their CTAs wait for P_{k+1}; the chain pivot -> panel -> tile -> pivot then runs without
-//      queueing behind the rest of the step)
-//   S5 the remaining tiles of step k
+//   [step 0 only: S1(0) its panels, column 1 first; S2 the next-pivot tiles (1, 1)]
+//   S3  look-ahead tiles: the rest of block row / column K+1 and the diagonal tile (K+2, K+2)
+//   E   early tasks of step k+1: panel (k+1, K+2) and the next-pivot tile (K+2, K+2) at step k+1
+//       (their CTAs wait for P_{k+1}; the chain pivot -> panel -> tile -> pivot then runs without
+//       queueing behind the rest of the step)
+//   S5a the first half (by tiles, whole rows) of the remaining tiles of step k
+//   S1  the other panels of step k+1: by the time they are taken P_{k+1} is (nearly) ready, so
+//       step k+1's tiles find their panels done when step k's tail ends
+//   S5b the rest of step k's tiles
 // Matrices are sorted by nt descending (active ones are a prefix).  Per-matrix counts of each
 // segment, so that a step's list can be written by one warp per matrix in parallel.
 __host__ __device__ inline int seg_s1(int nt, int k) { return nt > k ? nt - ((k >= 1 && nt > k + 1) ? 1 : 0) : 0; }
 __host__ __device__ inline int seg_s3(int nt, int k) { return nt > k + 1 ? (nt - 1) + (nt > k + 2 ? 1 : 0) : 0; }
-__host__ __device__ inline int seg_s5(int nt, int k) {
-    if (nt <= k) return 0;
-    int c = nt * (nt + 1) / 2;
-    if (nt > k + 1) c -= nt;      // block row / column K+1 incl. (K+1, K+1)
-    if (nt > k + 2) c -= 1;       // (K+2, K+2)
-    return c;
-}
 // S5 tiles of row I (count), with L = k+1 look-ahead exclusions
 __host__ __device__ inline int s5_row(int nt, int k, int I) {
     const int L = k + 1;
@@ -570,76 +584,91 @@ __host__ __device__ inline int s5_row(int nt, int k, int I) {
     if (nt > k + 2 && I == k + 2) c -= 1;
     return c;
 }
-// total tasks of step k over the sorted nt list (host: step offsets)
+// S5 of a matrix: total and the split row (rows < split form S5a, about half of the tiles)
+__host__ __device__ inline void seg_s5(int nt, int k, int &total, int &split, int &first) {
+    total = split = first = 0;
+    if (nt <= k) return;
+    for (int I = 0; I < nt; I++) total += s5_row(nt, k, I);
+    int c = 0;
+    while (split < nt && 2 * c < total) c += s5_row(nt, k, split++);
+    first = c;
+}
+// total tasks in step k's list (host: step offsets).  S1 of step k+1 sits in step k's list.
 inline int step_tasks(const int *nt, int nm, int k) {
     int c = 0;
     for (int m = 0; m < nm; m++) {
-        c += seg_s1(nt[m], k) + seg_s3(nt[m], k) + seg_s5(nt[m], k);
-        if (k == 0 && nt[m] > 1) c += 1;      // S2
-        if (nt[m] > k + 2) c += 2;            // E
+        int t5, sp, f5;
+        seg_s5(nt[m], k, t5, sp, f5);
+        c += seg_s3(nt[m], k) + t5 + seg_s1(nt[m], k + 1);
+        if (k == 0) c += seg_s1(nt[m], 0) + (nt[m] > 1 ? 1 : 0);  // S1(0), S2
+        if (nt[m] > k + 2) c += 2;                                // E
     }
     return c;
 }
 
 // one warp per (step, matrix): offsets of the matrix's entries in each segment of the step's list
 // (prefix over the matrices before it), then the lanes write them
+__device__ __forceinline__ void put_panels(int4 *out, int o, int kk, int m, int nt, int lane) {
+    // the panels of step kk of one matrix: column kk+1 first at step 0; at kk >= 1 it went to E(kk-1)
+    const bool first = kk == 0 && nt > 1, moved = kk >= 1 && nt > kk + 1;
+    for (int e = lane; e < seg_s1(nt, kk); e += 32) {
+        int J;
+        if (first) J = (e == 0) ? 1 : (e <= 1 ? e - 1 : e);
+        else if (moved) J = e < kk + 1 ? e : e + 1;
+        else J = e;
+        out[o + e] = make_int4(kk, 0, m, J);
+    }
+}
 __global__ void __launch_bounds__(32) inverse_tasks_kernel(const __grid_constant__ InvParams P) {
     const int k = blockIdx.x, m = blockIdx.y, lane = threadIdx.x;
     const int nt = P.m[m].nt;
     if (nt <= k) return;
     __shared__ int rowoff[kMaxSteps + 1];
-    int a1 = 0, a2 = 0, a3 = 0, a5 = 0, nA = 0, nS1 = 0, nS2 = 0, nS3 = 0, nE = 0;
-    for (int i = 0; i < P.nm; i++) {  // segment totals and this matrix's prefix
+    // segment totals over all matrices and this matrix's prefix in each
+    int a10 = 0, a2 = 0, a3 = 0, aE = 0, a5a = 0, a1 = 0, a5b = 0;
+    int n10 = 0, n2 = 0, n3 = 0, nE = 0, n5a = 0, n1 = 0;
+    for (int i = 0; i < P.nm; i++) {
         const int n = P.m[i].nt;
+        int t5, sp, f5;
+        seg_s5(n, k, t5, sp, f5);
+        const int s10 = k == 0 ? seg_s1(n, 0) : 0, s2 = (k == 0 && n > 1) ? 1 : 0, s3 = seg_s3(n, k);
+        const int e = n > k + 2 ? 1 : 0, s1 = seg_s1(n, k + 1);
         if (i < m) {
-            a1 += seg_s1(n, k);
-            a2 += (k == 0 && n > 1) ? 1 : 0;
-            a3 += seg_s3(n, k);
-            a5 += seg_s5(n, k);
-            nA += n > k + 2 ? 1 : 0;
+            a10 += s10; a2 += s2; a3 += s3; aE += e; a5a += f5; a1 += s1; a5b += t5 - f5;
         }
-        nS1 += seg_s1(n, k);
-        nS2 += (k == 0 && n > 1) ? 1 : 0;
-        nS3 += seg_s3(n, k);
-        nE += n > k + 2 ? 1 : 0;
+        n10 += s10; n2 += s2; n3 += s3; nE += e; n5a += f5; n1 += s1;
     }
     int4 *out = P.tasks + P.step_begin[k];
-    const int o1 = a1, o2 = nS1 + a2, o3 = nS1 + nS2 + a3, oE = nS1 + nS2 + nS3, o5 = oE + 2 * nE + a5;
+    const int o2 = n10, o3 = o2 + n2, oE = o3 + n3, o5a = oE + 2 * nE, o1 = o5a + n5a, o5b = o1 + n1;
     const int L = k + 1;
-    // S1: panels (column K+1 first at step 0; at k >= 1 it went to E(k-1))
-    {
-        const bool first = k == 0 && nt > 1, moved = k >= 1 && nt > k + 1;
-        for (int e = lane; e < seg_s1(nt, k); e += 32) {
-            int J;
-            if (first) J = (e == 0) ? 1 : (e <= 1 ? e - 1 : e);
-            else if (moved) J = e < L ? e : e + 1;
-            else J = e;
-            out[o1 + e] = make_int4(k, 0, m, J);
-        }
-    }
-    if (lane == 0 && k == 0 && nt > 1) out[o2] = make_int4(0, 1, m, (1 << 16) | 1);  // S2
+    if (k == 0) put_panels(out, a10, 0, m, nt, lane);                                  // S1(0)
+    if (lane == 0 && k == 0 && nt > 1) out[o2 + a2] = make_int4(0, 1, m, (1 << 16) | 1);  // S2
     if (nt > L) {  // S3
         for (int e = lane; e < nt - 1; e += 32) {
             const int I = e < L ? e : L, J = e < L ? L : e + 1;
-            out[o3 + e] = make_int4(k, 1, m, (I << 16) | J);
+            out[o3 + a3 + e] = make_int4(k, 1, m, (I << 16) | J);
         }
-        if (lane == 0 && nt > k + 2) out[o3 + nt - 1] = make_int4(k, 1, m, ((k + 2) << 16) | (k + 2));
+        if (lane == 0 && nt > k + 2) out[o3 + a3 + nt - 1] = make_int4(k, 1, m, ((k + 2) << 16) | (k + 2));
     }
     if (lane == 0 && nt > k + 2) {  // E
-        out[oE + nA] = make_int4(k + 1, 0, m, k + 2);
-        out[oE + nE + nA] = make_int4(k + 1, 1, m, ((k + 2) << 16) | (k + 2));
+        out[oE + aE] = make_int4(k + 1, 0, m, k + 2);
+        out[oE + nE + aE] = make_int4(k + 1, 1, m, ((k + 2) << 16) | (k + 2));
     }
-    // S5: row offsets, then one lane per row
+    put_panels(out, o1 + a1, k + 1, m, nt, lane);  // S1(k+1)
+    // S5a / S5b: row offsets, then one lane per row
+    int t5, sp, f5;
+    seg_s5(nt, k, t5, sp, f5);
     if (lane == 0) {
         int c = 0;
         for (int I = 0; I < nt; I++) {
+            if (I == sp) c = 0;
             rowoff[I] = c;
             c += s5_row(nt, k, I);
         }
     }
     __syncwarp();
     for (int I = lane; I < nt; I += 32) {
-        int c = o5 + rowoff[I];
+        int c = (I < sp ? o5a + a5a : o5b + a5b) + rowoff[I];
         for (int J = I; J < nt; J++) {
             if (nt > L && (I == L || J == L)) continue;
             if (nt > k + 2 && I == k + 2 && J == k + 2) continue;
@@ -679,7 +708,7 @@ __global__ void __launch_bounds__(256, 1) inverse_kernel(const __grid_constant__
             if (threadIdx.x == 0) next = *(volatile int *)m.status;  // one decision for the whole CTA
             __syncthreads();
             TRACE(tr1 = gtime(); trJ = J; trkind = 0;)
-            if (next == 0) panel_task(m, k, J, dyn);
+            if (next == 0 && J != k) panel_task(m, k, J, dyn);  // R_K / P R_K are never read
             __threadfence();
             __syncthreads();
             if (threadIdx.x == 0) {
