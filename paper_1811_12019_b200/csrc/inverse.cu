@@ -338,6 +338,25 @@ __device__ __forceinline__ void cp_async16(void *dst, const void *src, bool ok) 
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+// mbarrier + 1-D bulk copy (async proxy) for the C tile of an update
+__device__ __forceinline__ uint32_t s2u(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void cbar_expect(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s2u(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "W_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra W_%=;\n\t}" ::"r"(s2u(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_row(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(s2u(dst)),
+                 "l"(src), "r"(bytes), "r"(s2u(bar))
+                 : "memory");
+}
 
 // acc += sum_{t < kt} A[t][i] * Bm[t][j] for the 128 x 128 tile on the fp64 tensor cores
 // (mma.sync m8n8k4 f64, DMMA: 256 FMAs per warp instruction).  Warp w owns rows
@@ -446,7 +465,8 @@ __device__ void panel_task(const MatDesc &m, int k, int J, double *dyn) {
 
 // ---- update task (m, k, I, J): rank-B sweep update of upper tile (I, J); the task of tile
 // (K+1, K+1) then inverts that block (the next step's pivot).  Returns 0 or a pivot failure.
-__device__ int update_task(const InvParams &P, const MatDesc &m, int k, int I, int J, double *dyn, const int *pflag) {
+__device__ int update_task(const InvParams &P, const MatDesc &m, int k, int I, int J, double *dyn, const int *pflag,
+                           uint64_t *cbar, uint32_t &cph) {
     const int n = m.n, k0 = k * B, K = k;
     const int64_t ld = m.ld;
     const int bk = min(B, n - k0);
@@ -483,17 +503,21 @@ __device__ int update_task(const InvParams &P, const MatDesc &m, int k, int I, i
         for (int q = 0; q < 8; q++) acc[p][q] = 0.0;
     // the C tile M_IJ streams into shared memory in slices, one per K chunk of the product
     // (its HBM latency hides behind the tensor-core work instead of preceding it)
+    // the C tile M_IJ comes in by one asynchronous bulk copy per row (async proxy, completion on an
+    // mbarrier), issued before the product and awaited only at its end: it never stalls the
+    // product's chunk pipeline.  Rows are copied whole up to the leading dimension (the padding
+    // columns are never read).
     double *Cs = dyn + kTileSmem / 8;
-    auto cslice = [&](int c, int nch) {
-        const int r0 = c * B / nch, r1 = (c + 1) * B / nch;  // rows of this slice
-        for (int e = threadIdx.x; e < (r1 - r0) * (B / 2); e += 256) {
-            const int i = r0 + e / (B / 2), j = (e % (B / 2)) * 2;
-            const bool ok = i < bi && j < bj;
-            cp_async16(Cs + i * SLD + j, ok ? W + (int64_t)(i0 + i) * ld + j0 + j : W, ok);
-        }
-    };
+    {
+        const uint32_t rowb = (uint32_t)min((int64_t)B, ld - j0) * 8;
+        if (threadIdx.x == 0) cbar_expect(cbar, rowb * bi);
+        __syncthreads();  // expect_tx before any complete_tx
+        if (threadIdx.x < bi) bulk_row(Cs + threadIdx.x * SLD, W + (int64_t)(i0 + threadIdx.x) * ld + j0, rowb, cbar);
+    }
     // M_IJ -= R_I^T Wp_J : acc[i][j] = sum_t R[t][i0+i] Wp[t][j0+j]
-    tile_product(R + i0, ld, bi, Wp + j0, ld, bj, bk, acc, dyn, cslice);
+    tile_product(R + i0, ld, bi, Wp + j0, ld, bj, bk, acc, dyn);
+    cbar_wait(cbar, cph);
+    cph ^= 1;
     if (I == K + 1 && J == K + 1) {
         // fused next pivot: P_{K+1} = (updated M_{K+1,K+1})^-1.  The updated tile goes straight into
         // the pivot's shared-memory copy: its global value is dead (the next step's (K,K) tile
@@ -544,7 +568,7 @@ __device__ int update_task(const InvParams &P, const MatDesc &m, int k, int I, i
 
 #ifdef INV_TRACE  // experiment build only: per-task timeline
 struct TraceRec { int g, k, kind, I, J, sm; long long t0, t1, t2; };
-__device__ TraceRec g_trace[65536];
+__device__ TraceRec g_trace[1 << 17];
 __device__ __forceinline__ long long gtime() { long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t; }
 #define TRACE(...) __VA_ARGS__
 #else
@@ -687,6 +711,12 @@ __global__ void __launch_bounds__(32) inverse_tasks_kernel(const __grid_constant
 __global__ void __launch_bounds__(256, 1) inverse_kernel(const __grid_constant__ InvParams P) {
     extern __shared__ double dyn[];
     __shared__ int next;
+    __shared__ uint64_t cbar;  // C tile bulk loads of update tasks
+    uint32_t cph = 0;
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s2u(&cbar)) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     for (;;) {
         __syncthreads();  // the previous task is done with shared memory and `next`
         if (threadIdx.x == 0) next = atomicAdd(P.counter, 1);
@@ -728,7 +758,7 @@ __global__ void __launch_bounds__(256, 1) inverse_kernel(const __grid_constant__
             TRACE(tr1 = gtime(); trI = I; trJ = J; trkind = (I == k + 1 && J == k + 1) ? 2 : 1;)
             int f = 0;
             if (next == 0)
-                f = update_task(P, m, k, I, J, dyn, P.panels_done + m.col_begin + (k >= 1 ? k - 1 : 0));
+                f = update_task(P, m, k, I, J, dyn, P.panels_done + m.col_begin + (k >= 1 ? k - 1 : 0), &cbar, cph);
             if (f && threadIdx.x == 0) *m.status = f;
             __threadfence();
             __syncthreads();
@@ -741,7 +771,7 @@ __global__ void __launch_bounds__(256, 1) inverse_kernel(const __grid_constant__
             }
         }
 #ifdef INV_TRACE
-        if (threadIdx.x == 0 && g < 65536) {
+        if (threadIdx.x == 0 && g < (1 << 17)) {
             int sm;
             asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
             g_trace[g] = TraceRec{g, k, trkind, trI, trJ, sm, tr0, tr1, gtime()};
@@ -780,6 +810,12 @@ __global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ I
     }
 }
 
+#ifdef INV_TRACE
+extern "C" __attribute__((visibility("default"))) int kfac_debug_inverse_trace(void *host, int max) {
+    const int n = max < (1 << 17) ? max : (1 << 17);
+    return (int)cudaMemcpyFromSymbol(host, g_trace, sizeof(TraceRec) * n);
+}
+#endif
 static int g_inv_sms = 0;
 
 int64_t inverse_ld(int n) { return (n + 15) / 16 * 16; }

@@ -1,0 +1,27 @@
+"""Timeline of the persistent inverse inside one full RN50 step (library built with
+KFAC_NVCC_EXTRA=-DINV_TRACE): trace_step.py <out.txt>"""
+import ctypes, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+import paper_1811_12019_b200 as K
+from synth import shapes, inputs
+layers, n = shapes.config("resnet50")
+st = K.KfacStep(layers, n, device=torch.device("cuda"), policy=1)
+xs = [inputs.layer_x(l, i, n).cuda() for i, l in enumerate(layers)]
+gys = [inputs.layer_gy(l, i, n).cuda() for i, l in enumerate(layers)]
+st.set_dw([inputs.layer_dw(l, i).cuda() for i, l in enumerate(layers)])
+for _ in range(3):
+    st.run(xs, gys, 2.5e-2)
+torch.cuda.synchronize()
+lib = K.kfac._lib
+buf = np.zeros((1 << 17) * 9 * 2, dtype=np.int32)  # TraceRec: 6 ints + 3 int64 = 48 B
+lib.kfac_debug_inverse_trace(buf.ctypes.data_as(ctypes.c_void_p), 1 << 17)
+rec = buf.view(np.uint8).reshape(-1, 48)
+ints = rec[:, :24].copy().view(np.int32).reshape(-1, 6)
+ts = rec[:, 24:].copy().view(np.int64).reshape(-1, 3)
+with open(sys.argv[1], "w") as f:
+    for i in range(len(ints)):
+        if ts[i, 2]:
+            f.write(" ".join(map(str, list(ints[i]) + list(ts[i]))) + "\n")
+print("records", int((ts[:, 2] != 0).sum()))
