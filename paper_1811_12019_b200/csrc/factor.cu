@@ -701,26 +701,32 @@ __global__ void __launch_bounds__(256) im2col_kernel(const __grid_constant__ Fac
 }
 
 // bias row/column of A: A[f][dA-1] = alpha * sum_rows ã_f, A[dA-1][dA-1] = alpha * rows
-// (the homogeneous coordinate, reading R-5); one thread per feature, fixed row order.
+// (the homogeneous coordinate, reading R-5).  Block = 32 features x 8 row-strided warps, fp64
+// partial sums combined in a fixed order (deterministic).
 __global__ void __launch_bounds__(256) factor_bias_kernel(const __grid_constant__ FactorParams P) {
     __shared__ int cnt[kMaxProbs];  // blockIdx.y-th problem with a bias coordinate
+    __shared__ double part[8][33];
     for (int q = threadIdx.x; q < P.nprobs; q += blockDim.x) cnt[q] = P.probs[q].d_out != P.probs[q].d ? 1 : 0;
     int b = blockIdx.y;
     const int p = locate(cnt, P.nprobs, b);
     if (p >= P.nprobs) return;
     const ProbRegs pr = load_prob(P.probs[p]);
-    const int f = blockIdx.x * blockDim.x + threadIdx.x;
-    const int dA = pr.d_out;
-    if (f > pr.d) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int f = blockIdx.x * 32 + lane;
+    if (blockIdx.x * 32 > pr.d) return;
+    const int dA = pr.d_out, rows = (int)pr.rows;
     double s = 0.0;
-    if (f == pr.d) {
-        s = (double)pr.rows;
-    } else {
-        const int rows = (int)pr.rows;
-        for (int q = 0; q < rows; q++) s += (double)gather_elem(pr, P.ab_fmt, q, f);
+    if (f < pr.d)
+        for (int q = warp; q < rows; q += 8) s += (double)gather_elem(pr, P.ab_fmt, q, f);
+    part[warp][lane] = s;
+    __syncthreads();
+    if (warp == 0 && f <= pr.d) {
+        double t = 0.0;
+        for (int w = 0; w < 8; w++) t += part[w][lane];
+        if (f == pr.d) t = (double)pr.rows;
+        const int64_t off = (int64_t)f * dA - (int64_t)f * (f - 1) / 2 + (dA - 1 - f);
+        pr.out[off] = (float)(pr.alpha * t);
     }
-    const int64_t off = (int64_t)f * dA - (int64_t)f * (f - 1) / 2 + (dA - 1 - f);
-    pr.out[off] = (float)(pr.alpha * s);
 }
 
 // ---------------------------------------------------------------- host side
@@ -1065,7 +1071,7 @@ kfac_status factor_launch(const FactorLaunch &fl, const std::vector<FactorJob> &
             KFAC_CUDA_TRY(cudaGetLastError());
         }
         if (maxbias) {
-            dim3 g((maxbias + 255) / 256, nbias);
+            dim3 g((maxbias + 31) / 32, nbias);
             factor_bias_kernel<<<g, 256, 0, st>>>(P);
             KFAC_LAUNCHED();
             KFAC_CUDA_TRY(cudaGetLastError());
