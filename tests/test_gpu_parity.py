@@ -63,6 +63,13 @@ GEOMS = {  # name: (layer, n) -- each exercises one staging path / edge case
     "fc_bias_c1000": (shapes.linear("fc", 1000, 1000), 8),
     "fc_c10_gather": (shapes.linear("fc", 200, 10), 5),
     "ragged_rows_d_not_128": (shapes.conv("c", 48, 40, 3, 1, 1, 5), 3),
+    # 5-D slot-merged boxes: 7x7 outputs -> 8-wide boxes, 8 images per chunk (phantom images)
+    "im2col_c256_3x3_7x7_phantom": (shapes.conv("c", 256, 64, 3, 1, 1, 7), 3),
+    "im2col_c64_3x3_14x14": (shapes.conv("c", 64, 32, 3, 1, 1, 14), 2),
+    # 16-channel slots: 16 boxes per 256-feature operand (the owned-box list at its limit)
+    "tiled_c304_cb16_many_boxes": (shapes.linear("fc", 304, 24, bias=0), 100),
+    # two 256-tiles per side: diagonal (multi-unit stages) and off-diagonal items
+    "tiled_c512_two_tiles": (shapes.conv("c", 512, 40, 1, 1, 0, 6), 3),
 }
 
 
@@ -216,6 +223,44 @@ def test_inverse_ill_conditioned(K, orc, n):
     print(f"n={n} cond={np.linalg.cond(Ad):.1e} err={e:.2e}")
     assert s == 0 and st.dev_status.cpu().tolist() == [0, 0]
     assert e <= TOL_INV
+
+
+@pytest.mark.timeout(300)
+def test_inverse_batched_dataflow(K, orc):
+    """Several owned matrices of mixed sizes (ragged tails, 1x1, multi-step) in ONE persistent
+    dataflow launch, one of them not PD mid-sweep (pivot 400 of 1000: its tasks stop, the others
+    must complete and stay exact -- no deadlock on the skipped tasks' stamps)."""
+    layers = [shapes.linear("a", 700, 17, bias=0), shapes.linear("b", 129, 300, bias=0),
+              shapes.linear("c", 1000, 1, bias=0), shapes.linear("d", 128, 65, bias=0)]
+    st = K.KfacStep(layers, 1)
+    rng = np.random.default_rng(7)
+    mats = []
+    for k, l in enumerate(layers):
+        d_a, d_g = shapes.dims(l)
+        pair = []
+        for d in (d_a, d_g):
+            X = np.maximum(rng.standard_normal((max(d // 2, 1), d)), 0)
+            M = (X.T @ X / X.shape[0] + 0.05 * np.eye(d)).astype(np.float32).astype(np.float64)
+            pair.append(M)
+        if k == 2:
+            pair[0][400, 400] = -10.0  # not PD: the LDL^T pivot 400 is negative
+        _, pa, pg = st.recv_views(k)
+        pa.copy_(torch.as_tensor(orc.pack(pair[0]), dtype=torch.float32))
+        pg.copy_(torch.as_tensor(orc.pack(pair[1]), dtype=torch.float32))
+        mats.append(pair)
+    st.inverse(2.5e-3)
+    torch.cuda.synchronize()
+    status = st.dev_status.cpu().tolist()
+    for k in range(len(layers)):
+        Ad, Gd, _ = orc.damp(mats[k][0], mats[k][1], 2.5e-3)
+        Ai, Gi = st.inv_views(k)
+        for which, (Md, Mi) in enumerate(((Ad, Ai), (Gd, Gi))):
+            ref, s_ref = orc.inverse(Md)
+            assert status[2 * k + which] == s_ref, (k, which, status)
+            if s_ref == 0:
+                e = relerr(Mi.cpu().double().numpy(), ref)
+                assert e <= TOL_INV, (k, which, e)
+    assert status[4] == 401
 
 
 # --------------------------------------------------------------- full-size, sampled
