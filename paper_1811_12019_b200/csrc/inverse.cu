@@ -40,7 +40,7 @@ struct MatDesc {
     const float *packed;
     float *inv;
     double *work;
-    double *panel;  // [R_even | Wp_even | R_odd | Wp_odd: B x ld each][P_even | P_odd: B x B]
+    double *panel;  // [R | Wp per step mod 3: B x ld each][P_even | P_odd: B x B]
     int32_t *status;
     int32_t n, ld, pair, is_A;
     int32_t nt;          // column blocks
@@ -63,7 +63,7 @@ struct InvParams {
     int *tiles_done;   // [sum nt]    per (matrix, step): completed update tasks
     int *tileflag;     // [sum tiles] k + 1 once tile (I, J) holds its step-k value
     int4 *tasks;       // [total_tasks] task records (gen_step_tasks), built on the device per call
-    int32_t step_begin[kMaxSteps + 1];  // first record of each step's list
+    int32_t step_begin[kMaxSteps + 1];  // first record of each pair's list (steps 2p, 2p+1)
     MatDesc m[kMaxMats];
 };
 
@@ -191,7 +191,9 @@ __device__ long long g_pclk[64];
 #else
 #define PCLK(k)
 #endif
-__device__ int pivot_block(const double *__restrict__ W, int64_t ld, int k0, int bk, double *__restrict__ Pout,
+// P = (S)^-1 into Pout (B x B, zero outside bk); -P also goes straight into the upper tile (K, K) of W,
+// the value the sweep gives that tile at step K (no later task has to read the pivot slot for it)
+__device__ int pivot_block(double *__restrict__ W, int64_t ld, int k0, int bk, double *__restrict__ Pout,
                            double *smem, bool preloaded = false) {
     double(*S)[B + 1] = reinterpret_cast<double(*)[B + 1]>(smem);
     double *O = smem + B * (B + 1);       // [S2][SLD] old block row
@@ -308,17 +310,21 @@ __device__ int pivot_block(const double *__restrict__ W, int64_t ld, int k0, int
     PCLK(20)
     const int fail = *fsh;
     if (fail) return fail;
-    for (int e = tid; e < B * B; e += blockDim.x) {  // P = -S (zero outside bk)
+    for (int e = tid; e < B * B; e += blockDim.x) {  // P = -S (zero outside bk); W_KK = -P (upper)
         const int i = e >> 7, j = e & (B - 1);
-        Pout[e] = (i < bk && j < bk) ? -S[min(i, j)][max(i, j)] : 0.0;
+        const bool in = i < bk && j < bk;
+        Pout[e] = in ? -S[min(i, j)][max(i, j)] : 0.0;
+        if (in && j >= i) W[(int64_t)(k0 + i) * ld + k0 + j] = S[i][j];
     }
     return 0;
 }
 
 __device__ __forceinline__ double *pivot_slot(const MatDesc &m, int k) {
-    return m.panel + 4 * (int64_t)B * m.ld + (int64_t)(k & 1) * B * B;
+    return m.panel + 6 * (int64_t)B * m.ld + (int64_t)(k & 1) * B * B;
 }
-__device__ __forceinline__ double *panel_R(const MatDesc &m, int k) { return m.panel + (int64_t)(k & 1) * 2 * B * m.ld; }
+// three R / P R panel buffers (step mod 3): a merged task reads steps k and k+1 while step k+2's
+// panels are written
+__device__ __forceinline__ double *panel_R(const MatDesc &m, int k) { return m.panel + (int64_t)(k % 3) * 2 * B * m.ld; }
 __device__ __forceinline__ double *panel_Wp(const MatDesc &m, int k) { return panel_R(m, k) + (int64_t)B * m.ld; }
 
 // step 0 only: P_0 (later pivots are fused into the previous step's tile (K+1, K+1) update)
@@ -465,8 +471,10 @@ __device__ void panel_task(const MatDesc &m, int k, int J, double *dyn) {
 
 // ---- update task (m, k, I, J): rank-B sweep update of upper tile (I, J); the task of tile
 // (K+1, K+1) then inverts that block (the next step's pivot).  Returns 0 or a pivot failure.
-__device__ int update_task(const InvParams &P, const MatDesc &m, int k, int I, int J, double *dyn, const int *pflag,
-                           uint64_t *cbar, uint32_t &cph) {
+// nsteps = 1: the update of tile (I, J) at step k (incl. the copy tiles of row / column k);
+// nsteps = 2: the merged update for steps k and k+1 (I, J not in {k, k+1}).
+__device__ int update_task(const InvParams &P, const MatDesc &m, int k, int nsteps, int I, int J, double *dyn,
+                           const int *pflag, uint64_t *cbar, uint32_t &cph) {
     const int n = m.n, k0 = k * B, K = k;
     const int64_t ld = m.ld;
     const int bk = min(B, n - k0);
@@ -474,14 +482,7 @@ __device__ int update_task(const InvParams &P, const MatDesc &m, int k, int I, i
     const int bi = min(B, n - i0), bj = min(B, n - j0);
     const double *R = panel_R(m, k), *Wp = panel_Wp(m, k);
     double *W = m.work;
-    if (I == K && J == K) {
-        const double *Pm = pivot_slot(m, K);
-        for (int e = threadIdx.x; e < bk * bk; e += blockDim.x) {
-            const int i = e / bk, j = e % bk;
-            if (j >= i) W[(int64_t)(k0 + i) * ld + k0 + j] = -Pm[i * B + j];
-        }
-        return 0;
-    }
+    if (I == K && J == K) return 0;  // M_KK <- -P_K: written by the pivot itself (pivot_block)
     if (I == K) {  // M_KJ <- Wp_J
         for (int e = threadIdx.x; e < bk * bj; e += blockDim.x) {
             const int i = e / bj, j = e % bj;
@@ -514,11 +515,16 @@ __device__ int update_task(const InvParams &P, const MatDesc &m, int k, int I, i
         __syncthreads();  // expect_tx before any complete_tx
         if (threadIdx.x < bi) bulk_row(Cs + threadIdx.x * SLD, W + (int64_t)(i0 + threadIdx.x) * ld + j0, rowb, cbar);
     }
-    // M_IJ -= R_I^T Wp_J : acc[i][j] = sum_t R[t][i0+i] Wp[t][j0+j]
+    // M_IJ -= R_I^T Wp_J : acc[i][j] = sum_t R[t][i0+i] Wp[t][j0+j]   (for each step of the task)
     tile_product(R + i0, ld, bi, Wp + j0, ld, bj, bk, acc, dyn);
+    if (nsteps == 2) {
+        __syncthreads();  // the first product's last chunk is consumed before the loader reuses it
+        tile_product(panel_R(m, k + 1) + i0, ld, bi, panel_Wp(m, k + 1) + j0, ld, bj, min(B, n - k0 - B), acc, dyn);
+    }
     cbar_wait(cbar, cph);
     cph ^= 1;
-    if (I == K + 1 && J == K + 1) {
+    const int last = k + nsteps - 1;  // the step whose value the tile now holds
+    if (I == last + 1 && J == last + 1) {
         // fused next pivot: P_{K+1} = (updated M_{K+1,K+1})^-1.  The updated tile goes straight into
         // the pivot's shared-memory copy: its global value is dead (the next step's (K,K) tile
         // overwrites it with -P and no panel reads the pivot column).
@@ -538,8 +544,8 @@ __device__ int update_task(const InvParams &P, const MatDesc &m, int k, int I, i
             }
         }
         __syncthreads();
-        // its slot held P_{k-1}: every step-(k-1) panel task must be done reading it
-        if (k >= 1 && threadIdx.x == 0) {
+        // its slot held P_{last-1}: every step-(last-1) panel task must be done reading it
+        if (last >= 1 && threadIdx.x == 0) {
             int v;
             do {
                 asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(pflag) : "memory");
@@ -547,7 +553,7 @@ __device__ int update_task(const InvParams &P, const MatDesc &m, int k, int I, i
             } while (v < m.nt);
         }
         __syncthreads();
-        return pivot_block(W, ld, i0, bi, pivot_slot(m, K + 1), dyn, true);
+        return pivot_block(W, ld, i0, bi, pivot_slot(m, last + 1), dyn, true);
     }
     // column pairs (16-byte stores); rows are written whole up to the leading dimension: the lower
     // half of a diagonal tile and the padding columns are never read (upper storage)
@@ -584,121 +590,31 @@ __device__ __forceinline__ void wait_ge(const int *f, int target) {
 }
 __device__ __forceinline__ int upper_index(int I, int J, int nt) { return I * nt - I * (I - 1) / 2 + (J - I); }
 
-// ---- the task list of step k (one record per task: {k, kind, matrix, I << 16 | J}, kind 0 panel J,
-// 1 update of tile (I, J)), ordered for the critical path K -> K+1 of every matrix:
-//   [step 0 only: S1(0) its panels, column 1 first; S2 the next-pivot tiles (1, 1)]
-//   S3  look-ahead tiles: the rest of block row / column K+1 and the diagonal tile (K+2, K+2)
-//   E   early tasks of step k+1: panel (k+1, K+2) and the next-pivot tile (K+2, K+2) at step k+1
-//       (their CTAs wait for P_{k+1}; the chain pivot -> panel -> tile -> pivot then runs without
-//       queueing behind the rest of the step)
-//   S5a the first half (by tiles, whole rows) of the remaining tiles of step k
-//   S1  the other panels of step k+1: by the time they are taken P_{k+1} is (nearly) ready, so
-//       step k+1's tiles find their panels done when step k's tail ends
-//   S5b the rest of step k's tiles
-// Matrices are sorted by nt descending (active ones are a prefix).  Per-matrix counts of each
-// segment, so that a step's list can be written by one warp per matrix in parallel.
-__host__ __device__ inline int seg_s1(int nt, int k) { return nt > k ? nt - ((k >= 1 && nt > k + 1) ? 1 : 0) : 0; }
-__host__ __device__ inline int seg_s3(int nt, int k) { return nt > k + 1 ? (nt - 1) + (nt > k + 2 ? 1 : 0) : 0; }
-// S5 tiles of row I (count), with L = k+1 look-ahead exclusions
-__host__ __device__ inline int s5_row(int nt, int k, int I) {
-    const int L = k + 1;
-    if (nt <= L) return nt - I;  // no look-ahead at the last step
-    if (I == L) return 0;
-    int c = nt - I - (I < L ? 1 : 0);
-    if (nt > k + 2 && I == k + 2) c -= 1;
-    return c;
-}
-// S5 of a matrix: total and the split row (rows < split form S5a, about half of the tiles)
-__host__ __device__ inline void seg_s5(int nt, int k, int &total, int &split, int &first) {
-    total = split = first = 0;
-    if (nt <= k) return;
-    for (int I = 0; I < nt; I++) total += s5_row(nt, k, I);
-    int c = 0;
-    while (split < nt && 2 * c < total) c += s5_row(nt, k, split++);
-    first = c;
-}
-// total tasks in step k's list (host: step offsets).  S1 of step k+1 sits in step k's list.
-inline int step_tasks(const int *nt, int nm, int k) {
-    int c = 0;
-    for (int m = 0; m < nm; m++) {
-        int t5, sp, f5;
-        seg_s5(nt[m], k, t5, sp, f5);
-        c += seg_s3(nt[m], k) + t5 + seg_s1(nt[m], k + 1);
-        if (k == 0) c += seg_s1(nt[m], 0) + (nt[m] > 1 ? 1 : 0);  // S1(0), S2
-        if (nt[m] > k + 2) c += 2;                                // E
-    }
-    return c;
-}
+#include "inverse_tasks.hpp"
+using namespace kfac_inv;
 
-// one warp per (step, matrix): offsets of the matrix's entries in each segment of the step's list
-// (prefix over the matrices before it), then the lanes write them
-__device__ __forceinline__ void put_panels(int4 *out, int o, int kk, int m, int nt, int lane) {
-    // the panels of step kk of one matrix: column kk+1 first at step 0; at kk >= 1 it went to E(kk-1)
-    const bool first = kk == 0 && nt > 1, moved = kk >= 1 && nt > kk + 1;
-    for (int e = lane; e < seg_s1(nt, kk); e += 32) {
-        int J;
-        if (first) J = (e == 0) ? 1 : (e <= 1 ? e - 1 : e);
-        else if (moved) J = e < kk + 1 ? e : e + 1;
-        else J = e;
-        out[o + e] = make_int4(kk, 0, m, J);
-    }
-}
-__global__ void __launch_bounds__(32) inverse_tasks_kernel(const __grid_constant__ InvParams P) {
-    const int k = blockIdx.x, m = blockIdx.y, lane = threadIdx.x;
-    const int nt = P.m[m].nt;
+// one thread per (pair, matrix): the matrix's cursor in each segment of the pair's list is the
+// segment's start plus the counts of the matrices before it
+__global__ void inverse_tasks_kernel(const __grid_constant__ InvParams P) {
+    const int pr = blockIdx.x, m = blockIdx.y * blockDim.x + threadIdx.x;
+    if (m >= P.nm) return;
+    const int k = 2 * pr, nt = P.m[m].nt;
     if (nt <= k) return;
-    __shared__ int rowoff[kMaxSteps + 1];
-    // segment totals over all matrices and this matrix's prefix in each
-    int a10 = 0, a2 = 0, a3 = 0, aE = 0, a5a = 0, a1 = 0, a5b = 0;
-    int n10 = 0, n2 = 0, n3 = 0, nE = 0, n5a = 0, n1 = 0;
+    int tot[kSegs], pre[kSegs], c[kSegs];
+    for (int q = 0; q < kSegs; q++) tot[q] = pre[q] = 0;
     for (int i = 0; i < P.nm; i++) {
-        const int n = P.m[i].nt;
-        int t5, sp, f5;
-        seg_s5(n, k, t5, sp, f5);
-        const int s10 = k == 0 ? seg_s1(n, 0) : 0, s2 = (k == 0 && n > 1) ? 1 : 0, s3 = seg_s3(n, k);
-        const int e = n > k + 2 ? 1 : 0, s1 = seg_s1(n, k + 1);
-        if (i < m) {
-            a10 += s10; a2 += s2; a3 += s3; aE += e; a5a += f5; a1 += s1; a5b += t5 - f5;
-        }
-        n10 += s10; n2 += s2; n3 += s3; nE += e; n5a += f5; n1 += s1;
-    }
-    int4 *out = P.tasks + P.step_begin[k];
-    const int o2 = n10, o3 = o2 + n2, oE = o3 + n3, o5a = oE + 2 * nE, o1 = o5a + n5a, o5b = o1 + n1;
-    const int L = k + 1;
-    if (k == 0) put_panels(out, a10, 0, m, nt, lane);                                  // S1(0)
-    if (lane == 0 && k == 0 && nt > 1) out[o2 + a2] = make_int4(0, 1, m, (1 << 16) | 1);  // S2
-    if (nt > L) {  // S3
-        for (int e = lane; e < nt - 1; e += 32) {
-            const int I = e < L ? e : L, J = e < L ? L : e + 1;
-            out[o3 + a3 + e] = make_int4(k, 1, m, (I << 16) | J);
-        }
-        if (lane == 0 && nt > k + 2) out[o3 + a3 + nt - 1] = make_int4(k, 1, m, ((k + 2) << 16) | (k + 2));
-    }
-    if (lane == 0 && nt > k + 2) {  // E
-        out[oE + aE] = make_int4(k + 1, 0, m, k + 2);
-        out[oE + nE + aE] = make_int4(k + 1, 1, m, ((k + 2) << 16) | (k + 2));
-    }
-    put_panels(out, o1 + a1, k + 1, m, nt, lane);  // S1(k+1)
-    // S5a / S5b: row offsets, then one lane per row
-    int t5, sp, f5;
-    seg_s5(nt, k, t5, sp, f5);
-    if (lane == 0) {
-        int c = 0;
-        for (int I = 0; I < nt; I++) {
-            if (I == sp) c = 0;
-            rowoff[I] = c;
-            c += s5_row(nt, k, I);
+        pair_counts(P.m[i].nt, k, c);
+        for (int q = 0; q < kSegs; q++) {
+            tot[q] += c[q];
+            if (i < m) pre[q] += c[q];
         }
     }
-    __syncwarp();
-    for (int I = lane; I < nt; I += 32) {
-        int c = (I < sp ? o5a + a5a : o5b + a5b) + rowoff[I];
-        for (int J = I; J < nt; J++) {
-            if (nt > L && (I == L || J == L)) continue;
-            if (nt > k + 2 && I == k + 2 && J == k + 2) continue;
-            out[c++] = make_int4(k, 1, m, (I << 16) | J);
-        }
+    int cur[kSegs], base = 0;
+    for (int q = 0; q < kSegs; q++) {
+        cur[q] = base + pre[q];
+        base += tot[q];
     }
+    pair_emit(nt, k, m, cur, P.tasks + P.step_begin[pr]);
 }
 
 // ---- the whole sweep as ONE persistent launch: CTAs take tasks from an atomic counter in the
@@ -733,7 +649,7 @@ __global__ void __launch_bounds__(256, 1) inverse_kernel(const __grid_constant__
             if (threadIdx.x == 0 && k >= 1) {
                 wait_ge(P.tileflag + m.tile_begin + (J >= k ? upper_index(k, J, nt) : upper_index(J, k, nt)), k);
                 wait_ge(P.pivflag + mi, k + 1);
-                if (k >= 2) wait_ge(P.tiles_done + m.col_begin + k - 2, nt * (nt + 1) / 2);
+                if (k >= 3) wait_ge(P.tiles_done + m.col_begin + k - 3, nt * (nt + 1) / 2);  // buffer k mod 3
             }
             if (threadIdx.x == 0) next = *(volatile int *)m.status;  // one decision for the whole CTA
             __syncthreads();
@@ -746,28 +662,34 @@ __global__ void __launch_bounds__(256, 1) inverse_kernel(const __grid_constant__
                 atomicAdd(P.panels_done + m.col_begin + k, 1);
             }
         } else {
-            // ---------------- update task
+            // ---------------- update task (kind 1) / merged update of steps k, k+1 (kind 2)
+            const int ns = task.y == 2 ? 2 : 1, last = k + ns - 1;
             if (threadIdx.x == 0) {
-                if (I != k) wait_ge(P.colflag + m.col_begin + I, k + 1);
-                if (J != k && J != I) wait_ge(P.colflag + m.col_begin + J, k + 1);
+                // panels of step `last` (for a merged task they complete after step k's, which
+                // they depend on), P_k for the (K, K) copy, the tile's step k-1 value
+                if (I != k) wait_ge(P.colflag + m.col_begin + I, last + 1);
+                if (J != k && J != I) wait_ge(P.colflag + m.col_begin + J, last + 1);
                 if (I == k && J == k && k >= 1) wait_ge(P.pivflag + mi, k + 1);
                 if (k >= 1) wait_ge(P.tileflag + m.tile_begin + upper_index(I, J, nt), k);
             }
             if (threadIdx.x == 0) next = *(volatile int *)m.status;  // one decision for the whole CTA
             __syncthreads();
-            TRACE(tr1 = gtime(); trI = I; trJ = J; trkind = (I == k + 1 && J == k + 1) ? 2 : 1;)
+            TRACE(tr1 = gtime(); trI = I; trJ = J; trkind = (I == last + 1 && J == last + 1) ? 2 : (ns == 2 ? 3 : 1);)
             int f = 0;
             if (next == 0)
-                f = update_task(P, m, k, I, J, dyn, P.panels_done + m.col_begin + (k >= 1 ? k - 1 : 0), &cbar, cph);
+                f = update_task(P, m, k, ns, I, J, dyn, P.panels_done + m.col_begin + (last >= 1 ? last - 1 : 0), &cbar,
+                                cph);
             if (f && threadIdx.x == 0) *m.status = f;
             __threadfence();
             __syncthreads();
             if (threadIdx.x == 0) {
-                asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(P.tileflag + m.tile_begin + upper_index(I, J, nt)), "r"(k + 1)
+                asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(P.tileflag + m.tile_begin + upper_index(I, J, nt)),
+                             "r"(last + 1)
                              : "memory");
-                if (I == k + 1 && J == k + 1)
-                    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(P.pivflag + mi), "r"(k + 2) : "memory");
+                if (I == last + 1 && J == last + 1)
+                    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(P.pivflag + mi), "r"(last + 2) : "memory");
                 atomicAdd(P.tiles_done + m.col_begin + k, 1);
+                if (ns == 2) atomicAdd(P.tiles_done + m.col_begin + k + 1, 1);
             }
         }
 #ifdef INV_TRACE
@@ -832,7 +754,7 @@ int64_t inverse_tasks(int n) {
 }
 int64_t inverse_ws_doubles(int n) {
     const int64_t ld = inverse_ld(n);
-    return (n * ld + 4 * (int64_t)B * ld + 2 * (int64_t)B * B + 31) / 32 * 32;
+    return (n * ld + 6 * (int64_t)B * ld + 2 * (int64_t)B * B + 31) / 32 * 32;
 }
 
 kfac_status inverse_launch(const std::vector<InvMat> &mats, int npairs, float gamma, double *pair_scratch,
@@ -886,11 +808,12 @@ kfac_status inverse_launch(const std::vector<InvMat> &mats, int npairs, float ga
     std::vector<int> ntl(P.nm);
     for (int i = 0; i < P.nm; i++) ntl[i] = P.m[i].nt;
     int task = 0;
-    for (int k = 0; k < steps; k++) {
-        P.step_begin[k] = task;
-        task += step_tasks(ntl.data(), P.nm, k);
+    const int npairs_steps = (steps + 1) / 2;
+    for (int pr = 0; pr < npairs_steps; pr++) {
+        P.step_begin[pr] = task;
+        task += pair_tasks(ntl.data(), P.nm, 2 * pr);
     }
-    P.step_begin[steps] = task;
+    P.step_begin[npairs_steps] = task;
     P.total_tasks = task;
     // dataflow state after the pair data (inverse_scratch_bytes): zeroed once per call
     int *state = reinterpret_cast<int *>(pair_scratch + ((4 * (int64_t)npairs + 15) / 16) * 16);
@@ -902,7 +825,7 @@ kfac_status inverse_launch(const std::vector<InvMat> &mats, int npairs, float ga
     P.tileflag = P.tiles_done + sum_nt;
     P.tasks = reinterpret_cast<int4 *>(state + ((16 + 2 * (int64_t)npairs + 3 * sum_nt + sum_tiles + 3) / 4) * 4);
     KFAC_CUDA_TRY(cudaMemsetAsync(state, 0, (16 + 2 * (int64_t)npairs + 3 * sum_nt + sum_tiles) * sizeof(int), st));
-    inverse_tasks_kernel<<<dim3(steps, P.nm), 32, 0, st>>>(P);
+    inverse_tasks_kernel<<<dim3(npairs_steps, (P.nm + 31) / 32), 32, 0, st>>>(P);
     KFAC_LAUNCHED();
     KFAC_CUDA_TRY(cudaGetLastError());
     damp_trace_kernel<<<P.nm, 256, 0, st>>>(P);

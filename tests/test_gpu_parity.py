@@ -202,7 +202,7 @@ def test_inverse_reports_not_pd(K, orc):
     assert want == 2
 
 
-@pytest.mark.parametrize("n", [64, 65, 130, 300])
+@pytest.mark.parametrize("n", [64, 65, 130, 300, 513, 1153])
 def test_inverse_ill_conditioned(K, orc, n):
     """Rank-deficient ReLU-like factors at small damping (kappa ~ 1e4): fp64 sweep meets 1e-5."""
     rng = np.random.default_rng(n)
@@ -261,6 +261,42 @@ def test_inverse_batched_dataflow(K, orc):
                 e = relerr(Mi.cpu().double().numpy(), ref)
                 assert e <= TOL_INV, (k, which, e)
     assert status[4] == 401
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("n", [2049, 4608])
+def test_fullsize_inverse_residual(K, n):
+    """BASELINE config 5's largest factors (FC 2049, conv 4608; 17 / 36 sweep steps, merged
+    two-step updates, odd and even step counts).  A rigorous bound on the relative error of the
+    returned fp32 inverse X from its fp64 residual R = M X - I:
+    ||X - M^-1||_F = ||M^-1 R||_F <= ||R||_F / lambda_min(M), and ||M^-1||_F >= ||X||_F - that."""
+    g = 64
+    layers = [shapes.linear("fc", n, g, bias=0)]
+    st = K.KfacStep(layers, 1)
+    gen = torch.Generator(device="cuda").manual_seed(n)
+    X = torch.relu(torch.randn(n // 2, n, generator=gen, device="cuda", dtype=torch.float64))
+    A = (X.T @ X / X.shape[0]).float()
+    iu = torch.triu_indices(n, n, device="cuda")
+    _, pa, pg = st.recv_views(0)
+    pa.copy_(A[iu[0], iu[1]])
+    pg.copy_(torch.eye(g, device="cuda")[torch.triu_indices(g, g, device="cuda").unbind()])
+    gamma = 2.5e-3
+    st.inverse(gamma)
+    torch.cuda.synchronize()
+    assert st.dev_status.cpu().tolist() == [0, 0]
+    # the damping the library applied (R-1): pi from the traces, A_d = A + pi sqrt(gamma) I
+    A64 = A.double()
+    pi = float(np.sqrt((torch.trace(A64).item() / n) / 1.0))
+    Ad = A64 + pi * np.sqrt(gamma) * torch.eye(n, device="cuda", dtype=torch.float64)
+    Ai, _ = st.inv_views(0)
+    Xi = Ai.double()
+    res = torch.linalg.norm(Ad @ Xi - torch.eye(n, device="cuda", dtype=torch.float64)).item()
+    lam_min = torch.linalg.eigvalsh(Ad)[0].item()
+    err_abs = res / lam_min
+    err_rel = err_abs / (torch.linalg.norm(Xi).item() - err_abs)
+    print(f"n={n} residual {res:.2e} lambda_min {lam_min:.2e} relative error <= {err_rel:.2e}")
+    assert 0 < err_rel <= TOL_INV
+    assert torch.allclose(Xi, Xi.T)
 
 
 # --------------------------------------------------------------- full-size, sampled
