@@ -421,7 +421,15 @@ __device__ __forceinline__ void tile_product(const double *__restrict__ A, int64
     }
 }
 
-// ---- panel task (m, k, J): R_J = block row K (from upper storage), Wp_J = P_k R_J
+__device__ __forceinline__ void cp_async8(void *dst, const void *src, bool ok) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src),
+                 "r"(ok ? 8 : 0)
+                 : "memory");
+}
+
+// ---- panel task (m, k, J): R_J = block row K (from upper storage), Wp_J = P_k R_J.  The task also
+// gives tile (K, J) its step-k value Wp_J (M_KJ <- Wp_J, or M_JK <- Wp_J^T left of the diagonal):
+// nothing else reads that tile at step k, so the row / column K "copy" updates have no work left.
 __device__ void panel_task(const MatDesc &m, int k, int J, double *dyn) {
     const int n = m.n, k0 = k * B, K = k;
     const int64_t ld = m.ld;
@@ -430,16 +438,21 @@ __device__ void panel_task(const MatDesc &m, int k, int J, double *dyn) {
     double *R = panel_R(m, k), *Wp = panel_Wp(m, k);
     // R_J (rows t < bk, cols j < bj; zero up to the 16-aligned ld) staged through shared memory so
     // that both the read of W (upper storage, possibly transposed) and the write of R coalesce.
+    // The tile comes in by 8-byte cp.async (all 64 loads of a thread in flight at once).
     double(*T)[B + 1] = reinterpret_cast<double(*)[B + 1]>(dyn);
     const int bjp = min(B, (int)ld - j0);
     const bool trans = J < K;  // block row K left of the diagonal lives in column K of the upper storage
     const int r0 = trans ? j0 : k0, c0 = trans ? k0 : j0, nr = trans ? bj : bk, nc = trans ? bk : bj;
-    for (int e = threadIdx.x; e < B * B; e += blockDim.x) {
-        const int r = e >> 7, c = e & (B - 1);
-        T[r][c] = (r < nr && c < nc && (J != K || c >= r)) ? m.work[(int64_t)(r0 + r) * ld + c0 + c] : 0.0;
+#pragma unroll 16
+    for (int it = 0; it < B * B / 256; it++) {
+        const int e = it * 256 + threadIdx.x, r = e >> 7, c = e & (B - 1);
+        const bool ok = r < nr && c < nc && (J != K || c >= r);
+        cp_async8(&T[r][c], ok ? m.work + (int64_t)(r0 + r) * ld + c0 + c : m.work, ok);
     }
+    cp_async_commit();
+    cp_async_wait_0();
     __syncthreads();
-    for (int e = threadIdx.x; e < bk * B; e += blockDim.x) {
+    for (int e = threadIdx.x; e < bk * B; e += 256) {
         const int t = e >> 7, j = e & (B - 1);
         if (j >= bjp) continue;
         double v;
@@ -457,16 +470,25 @@ __device__ void panel_task(const MatDesc &m, int k, int J, double *dyn) {
         for (int q = 0; q < 8; q++) acc[p][q] = 0.0;
     // Wp[i][j] = sum_t P[t][i] R[t][j]   (P symmetric, zero outside bk)
     tile_product(pivot_slot(m, k), B, bk, R + j0, ld, bj, bk, acc, dyn);
+    __syncthreads();  // the product's staging buffers are free: the result goes through T
 #pragma unroll
-    for (int p = 0; p < 8; p++) {
-        const int i = tile_row(p);
-        if (i >= bk) continue;
+    for (int p = 0; p < 8; p++)
 #pragma unroll
-        for (int q = 0; q < 8; q += 2) {
-            const int j = tile_col(q);
-            if (j < bjp) *reinterpret_cast<double2 *>(Wp + (int64_t)i * ld + j0 + j) = make_double2(acc[p][q], acc[p][q + 1]);
-        }
+        for (int q = 0; q < 8; q++) T[tile_row(p)][tile_col(q)] = acc[p][q];
+    __syncthreads();
+    // Wp_J into the panel buffer (rows whole up to ld) and the step-k value of tile (K, J)
+    for (int e = threadIdx.x; e < bk * B; e += 256) {
+        const int t = e >> 7, j = e & (B - 1);
+        if (j >= bjp) continue;
+        const double v = T[t][j];
+        Wp[(int64_t)t * ld + j0 + j] = v;
+        if (!trans) m.work[(int64_t)(k0 + t) * ld + j0 + j] = v;
     }
+    if (trans)  // M_JK <- Wp_J^T: row j of tile (J, K), consecutive threads along t
+        for (int e = threadIdx.x; e < bj * B; e += 256) {
+            const int j = e >> 7, t = e & (B - 1);
+            if (t < bk) m.work[(int64_t)(j0 + j) * ld + k0 + t] = T[t][j];
+        }
 }
 
 // ---- update task (m, k, I, J): rank-B sweep update of upper tile (I, J); the task of tile
@@ -483,20 +505,7 @@ __device__ int update_task(const InvParams &P, const MatDesc &m, int k, int nste
     const double *R = panel_R(m, k), *Wp = panel_Wp(m, k);
     double *W = m.work;
     if (I == K && J == K) return 0;  // M_KK <- -P_K: written by the pivot itself (pivot_block)
-    if (I == K) {  // M_KJ <- Wp_J
-        for (int e = threadIdx.x; e < bk * bj; e += blockDim.x) {
-            const int i = e / bj, j = e % bj;
-            W[(int64_t)(k0 + i) * ld + j0 + j] = Wp[(int64_t)i * ld + j0 + j];
-        }
-        return 0;
-    }
-    if (J == K) {  // M_IK <- Wp_I^T
-        for (int e = threadIdx.x; e < bi * bk; e += blockDim.x) {
-            const int i = e / bk, j = e % bk;
-            W[(int64_t)(i0 + i) * ld + k0 + j] = Wp[(int64_t)j * ld + i0 + i];
-        }
-        return 0;
-    }
+    if (I == K || J == K) return 0;  // M_KJ <- Wp_J / M_IK <- Wp_I^T: written by the panel tasks
     double acc[8][8];
 #pragma unroll
     for (int p = 0; p < 8; p++)
@@ -674,7 +683,7 @@ __global__ void __launch_bounds__(256, 1) inverse_kernel(const __grid_constant__
             }
             if (threadIdx.x == 0) next = *(volatile int *)m.status;  // one decision for the whole CTA
             __syncthreads();
-            TRACE(tr1 = gtime(); trI = I; trJ = J; trkind = (I == last + 1 && J == last + 1) ? 2 : (ns == 2 ? 3 : 1);)
+            TRACE(tr1 = gtime(); trI = I; trJ = J; trkind = (I == last + 1 && J == last + 1) ? 2 : (ns == 2 ? 3 : ((I == k || J == k) ? 4 : 1));)
             int f = 0;
             if (next == 0)
                 f = update_task(P, m, k, ns, I, J, dyn, P.panels_done + m.col_begin + (last >= 1 ? last - 1 : 0), &cbar,
