@@ -30,9 +30,16 @@ namespace kfac {
 
 constexpr int kMaxMats = 128;
 constexpr int B = kPanel;     // 128
-constexpr int KC = 16;        // K rows per smem chunk of the tile product
+#ifndef KFAC_INV_KC  // experiment overrides (KFAC_NVCC_EXTRA)
+#define KFAC_INV_KC 8
+#endif
+#ifndef KFAC_INV_STAGES
+#define KFAC_INV_STAGES 4
+#endif
+constexpr int KC = KFAC_INV_KC;  // K rows per shared-memory ring stage of the tile product
+constexpr int kStages = KFAC_INV_STAGES;  // ring depth
 constexpr int kPivSmem = (B * (B + 1) + 2 * 32 * (B + 4) + 32 * 36 + 64) * 8 + 64;
-constexpr int kTileSmem = 2 * 2 * KC * (B + 4) * 8;  // double-buffered A/B chunks (padded rows): 66 KB
+constexpr int kTileSmem = kStages * 2 * KC * (B + 4) * 8;  // A/B chunk ring (padded rows): 66 KB
 constexpr int kUpdSmem = kPivSmem > kTileSmem + B * (B + 4) * 8 ? kPivSmem : kTileSmem + B * (B + 4) * 8;
 static_assert(kUpdSmem >= B * (B + 1) * 8, "panel staging fits the update kernel's shared memory");
 
@@ -368,42 +375,59 @@ __device__ __forceinline__ void bulk_row(void *dst, const void *src, uint32_t by
 // (mma.sync m8n8k4 f64, DMMA: 256 FMAs per warp instruction).  Warp w owns rows
 // 64*(w>>2) + [0, 64) and columns 32*(w&3) + [0, 32) as 8 x 4 m8n8 blocks; acc[p][q] is the
 // element (tile_row(p), tile_col(q)) below.  A and Bm are row-major with 16-aligned leading
-// dimensions; columns >= acols / bcols and rows >= kt read as zero.  Chunks of KC rows are
-// double-buffered with cp.async; shared rows are padded to 132 doubles (conflict-free fragments).
-struct NoExtra {
-    __device__ __forceinline__ void operator()(int, int) const {}
+// dimensions; columns >= aw / bw and rows >= kt read as zero (cp.async zero fill).  Operand rows
+// stream through a kStages-deep shared-memory ring of KC-row chunks: every thread copies its
+// share of a chunk with 16-byte cp.async and signals the stage's `full` mbarrier on completion
+// (cp.async.mbarrier.arrive.noinc); each warp releases a stage on its `empty` mbarrier once its
+// fragments are loaded.  No CTA-wide barrier inside the product: warps drift up to a chunk
+// apart, so their shared-load phases do not line up.  Two K segments (a merged two-step update)
+// run as one chunk stream.  Shared rows are padded to 132 doubles (conflict-free fragments).
+struct Seg {
+    const double *A;
+    int64_t lda;
+    int aw;
+    const double *Bm;
+    int64_t ldb;
+    int bw;
+    int kt;
 };
-template <typename Extra = NoExtra>
-__device__ __forceinline__ void tile_product(const double *__restrict__ A, int64_t lda, int acols,
-                                             const double *__restrict__ Bm, int64_t ldb, int bcols, int kt,
-                                             double (&acc)[8][8], double *smem, Extra extra = Extra()) {
-    double *As = smem, *Bs = smem + 2 * KC * SLD;
+struct Ring {
+    uint64_t *full, *empty;  // [kStages] each
+    uint32_t g;              // chunks this CTA has streamed so far (uniform over the CTA)
+};
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s2u(bar)) : "memory");
+}
+__device__ __forceinline__ void tile_product(const Seg &s0, const Seg &s1, double (&acc)[8][8], double *smem, Ring &ring) {
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int arow = 64 * (w >> 2) + (lane >> 2), bcol = 32 * (w & 3) + (lane >> 2), kl = lane & 3;
-    const int nchunks = (kt + KC - 1) / KC;
-    auto load = [&](int c, int buf) {
-        const int t0 = c * KC;
-        for (int e = threadIdx.x; e < KC * B / 2; e += 256) {  // pairs of doubles
-            const int t = e >> 6, i = (e & 63) * 2;
-            const bool okr = t0 + t < kt;
-            const bool oka = okr && i < acols, okb = okr && i < bcols;
-            cp_async16(As + buf * KC * SLD + t * SLD + i, oka ? A + (int64_t)(t0 + t) * lda + i : A, oka);
-            cp_async16(Bs + buf * KC * SLD + t * SLD + i, okb ? Bm + (int64_t)(t0 + t) * ldb + i : Bm, okb);
+    const int n0 = (s0.kt + KC - 1) / KC, nch = n0 + (s1.kt + KC - 1) / KC;
+    __syncthreads();  // the caller's shared-memory use (staging, pivots, epilogues) is over
+    auto produce = [&](int c) {  // every thread: its 16-byte pieces of chunk c
+        const uint32_t G = ring.g + c, st = G % kStages;
+        const bool first = c < n0;
+        const double *A = first ? s0.A : s1.A, *Bm = first ? s0.Bm : s1.Bm;
+        const int64_t lda = first ? s0.lda : s1.lda, ldb = first ? s0.ldb : s1.ldb;
+        const int aw = first ? s0.aw : s1.aw, bw = first ? s0.bw : s1.bw;
+        const int t0 = (first ? c : c - n0) * KC, kt = first ? s0.kt : s1.kt;
+        if (G >= kStages) cbar_wait(ring.empty + st, ((G / kStages) + 1) & 1);  // chunk G - kStages consumed
+        double *dst = smem + st * 2 * KC * SLD;
+#pragma unroll
+        for (int it = 0; it < 2 * KC * B / 2 / 256; it++) {
+            const int e = it * 256 + threadIdx.x, r = e >> 6, i = (e & 63) * 2;  // r < KC: A rows, else B
+            const bool isA = r < KC;
+            const int t = t0 + (isA ? r : r - KC);
+            const bool ok = t < kt && i < (isA ? aw : bw);
+            const double *src = isA ? A + (int64_t)t * lda + i : Bm + (int64_t)t * ldb + i;
+            cp_async16(dst + r * SLD + i, ok ? src : A, ok);
         }
-        extra(c, nchunks);  // e.g. a slice of the C tile, in the same cp.async group
-        cp_async_commit();
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(s2u(ring.full + st)) : "memory");
     };
-    load(0, 0);
-    for (int c = 0; c < nchunks; c++) {
-        const int buf = c & 1;
-        if (c + 1 < nchunks) {
-            load(c + 1, buf ^ 1);
-            cp_async_wait_1();
-        } else {
-            cp_async_wait_0();
-        }
-        __syncthreads();
-        const double *as = As + buf * KC * SLD, *bs = Bs + buf * KC * SLD;
+    for (int c = 0; c < min(kStages - 1, nch); c++) produce(c);
+    for (int c = 0; c < nch; c++) {
+        const uint32_t G = ring.g + c, st = G % kStages;
+        cbar_wait(ring.full + st, (G / kStages) & 1);
+        const double *as = smem + st * 2 * KC * SLD, *bs = as + KC * SLD;
 #pragma unroll
         for (int kk = 0; kk < KC / 4; kk++) {
             const int t = kk * 4 + kl;
@@ -417,8 +441,12 @@ __device__ __forceinline__ void tile_product(const double *__restrict__ A, int64
 #pragma unroll
                 for (int q = 0; q < 4; q++) dmma(acc[p][2 * q], acc[p][2 * q + 1], a[p], b[q]);
         }
-        __syncthreads();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(ring.empty + st);
+        if (c + kStages - 1 < nch) produce(c + kStages - 1);
     }
+    ring.g += nch;
+    __syncthreads();  // every warp is done with the ring before the caller reuses the shared memory
 }
 
 __device__ __forceinline__ void cp_async8(void *dst, const void *src, bool ok) {
@@ -430,7 +458,7 @@ __device__ __forceinline__ void cp_async8(void *dst, const void *src, bool ok) {
 // ---- panel task (m, k, J): R_J = block row K (from upper storage), Wp_J = P_k R_J.  The task also
 // gives tile (K, J) its step-k value Wp_J (M_KJ <- Wp_J, or M_JK <- Wp_J^T left of the diagonal):
 // nothing else reads that tile at step k, so the row / column K "copy" updates have no work left.
-__device__ void panel_task(const MatDesc &m, int k, int J, double *dyn) {
+__device__ void panel_task(const MatDesc &m, int k, int J, double *dyn, Ring &ring) {
     const int n = m.n, k0 = k * B, K = k;
     const int64_t ld = m.ld;
     const int j0 = J * B;
@@ -469,7 +497,8 @@ __device__ void panel_task(const MatDesc &m, int k, int J, double *dyn) {
 #pragma unroll
         for (int q = 0; q < 8; q++) acc[p][q] = 0.0;
     // Wp[i][j] = sum_t P[t][i] R[t][j]   (P symmetric, zero outside bk)
-    tile_product(pivot_slot(m, k), B, bk, R + j0, ld, bj, bk, acc, dyn);
+    const Seg seg{pivot_slot(m, k), B, B, R + j0, ld, bjp, bk}, none{nullptr, 0, 0, nullptr, 0, 0, 0};
+    tile_product(seg, none, acc, dyn, ring);
     __syncthreads();  // the product's staging buffers are free: the result goes through T
 #pragma unroll
     for (int p = 0; p < 8; p++)
@@ -496,7 +525,7 @@ __device__ void panel_task(const MatDesc &m, int k, int J, double *dyn) {
 // nsteps = 1: the update of tile (I, J) at step k (incl. the copy tiles of row / column k);
 // nsteps = 2: the merged update for steps k and k+1 (I, J not in {k, k+1}).
 __device__ int update_task(const InvParams &P, const MatDesc &m, int k, int nsteps, int I, int J, double *dyn,
-                           const int *pflag, uint64_t *cbar, uint32_t &cph) {
+                           const int *pflag, uint64_t *cbar, uint32_t &cph, Ring &ring) {
     const int n = m.n, k0 = k * B, K = k;
     const int64_t ld = m.ld;
     const int bk = min(B, n - k0);
@@ -525,11 +554,10 @@ __device__ int update_task(const InvParams &P, const MatDesc &m, int k, int nste
         if (threadIdx.x < bi) bulk_row(Cs + threadIdx.x * SLD, W + (int64_t)(i0 + threadIdx.x) * ld + j0, rowb, cbar);
     }
     // M_IJ -= R_I^T Wp_J : acc[i][j] = sum_t R[t][i0+i] Wp[t][j0+j]   (for each step of the task)
-    tile_product(R + i0, ld, bi, Wp + j0, ld, bj, bk, acc, dyn);
-    if (nsteps == 2) {
-        __syncthreads();  // the first product's last chunk is consumed before the loader reuses it
-        tile_product(panel_R(m, k + 1) + i0, ld, bi, panel_Wp(m, k + 1) + j0, ld, bj, min(B, n - k0 - B), acc, dyn);
-    }
+    const int aw = min((int64_t)B, ld - i0), bw = min((int64_t)B, ld - j0);
+    const Seg s0{R + i0, ld, aw, Wp + j0, ld, bw, bk};
+    const Seg s1{panel_R(m, k + 1) + i0, ld, aw, panel_Wp(m, k + 1) + j0, ld, bw, nsteps == 2 ? min(B, n - k0 - B) : 0};
+    tile_product(s0, s1, acc, dyn, ring);
     cbar_wait(cbar, cph);
     cph ^= 1;
     const int last = k + nsteps - 1;  // the step whose value the tile now holds
@@ -637,9 +665,15 @@ __global__ void __launch_bounds__(256, 1) inverse_kernel(const __grid_constant__
     extern __shared__ double dyn[];
     __shared__ int next;
     __shared__ uint64_t cbar;  // C tile bulk loads of update tasks
+    __shared__ uint64_t ring_full[kStages], ring_empty[kStages];
     uint32_t cph = 0;
+    Ring ring{ring_full, ring_empty, 0};
     if (threadIdx.x == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s2u(&cbar)) : "memory");
+        for (int st = 0; st < kStages; st++) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 256;" ::"r"(s2u(ring_full + st)) : "memory");
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 8;" ::"r"(s2u(ring_empty + st)) : "memory");
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     for (;;) {
@@ -663,7 +697,7 @@ __global__ void __launch_bounds__(256, 1) inverse_kernel(const __grid_constant__
             if (threadIdx.x == 0) next = *(volatile int *)m.status;  // one decision for the whole CTA
             __syncthreads();
             TRACE(tr1 = gtime(); trJ = J; trkind = 0;)
-            if (next == 0 && J != k) panel_task(m, k, J, dyn);  // R_K / P R_K are never read
+            if (next == 0 && J != k) panel_task(m, k, J, dyn, ring);  // R_K / P R_K are never read
             __threadfence();
             __syncthreads();
             if (threadIdx.x == 0) {
@@ -687,7 +721,7 @@ __global__ void __launch_bounds__(256, 1) inverse_kernel(const __grid_constant__
             int f = 0;
             if (next == 0)
                 f = update_task(P, m, k, ns, I, J, dyn, P.panels_done + m.col_begin + (last >= 1 ? last - 1 : 0), &cbar,
-                                cph);
+                                cph, ring);
             if (f && threadIdx.x == 0) *m.status = f;
             __threadfence();
             __syncthreads();
