@@ -520,12 +520,21 @@ __device__ void panel_task(const MatDesc &m, int k, int J, double *dyn, Ring &ri
         }
 }
 
+#ifdef INV_TRACE  // experiment build only: per-task timeline
+struct TraceRec { int g, k, kind, I, J, sm; long long t0, t1, t2, t3, t4; };
+__device__ TraceRec g_trace[1 << 17];
+__device__ long long g_trace_sub[1024][2];  // per CTA: end of the product, end of the C-tile wait
+__device__ __forceinline__ long long gtime() { long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t; }
+#define TRACE(...) __VA_ARGS__
+#else
+#define TRACE(...)
+#endif
 // ---- update task (m, k, I, J): rank-B sweep update of upper tile (I, J); the task of tile
 // (K+1, K+1) then inverts that block (the next step's pivot).  Returns 0 or a pivot failure.
 // nsteps = 1: the update of tile (I, J) at step k (incl. the copy tiles of row / column k);
 // nsteps = 2: the merged update for steps k and k+1 (I, J not in {k, k+1}).
 __device__ int update_task(const InvParams &P, const MatDesc &m, int k, int nsteps, int I, int J, double *dyn,
-                           const int *pflag, uint64_t *cbar, uint32_t &cph, Ring &ring) {
+                           const int *pflag, uint64_t *cbar, uint32_t &cph, Ring &ring, bool &deferred) {
     const int n = m.n, k0 = k * B, K = k;
     const int64_t ld = m.ld;
     const int bk = min(B, n - k0);
@@ -558,8 +567,10 @@ __device__ int update_task(const InvParams &P, const MatDesc &m, int k, int nste
     const Seg s0{R + i0, ld, aw, Wp + j0, ld, bw, bk};
     const Seg s1{panel_R(m, k + 1) + i0, ld, aw, panel_Wp(m, k + 1) + j0, ld, bw, nsteps == 2 ? min(B, n - k0 - B) : 0};
     tile_product(s0, s1, acc, dyn, ring);
+    TRACE(if (threadIdx.x == 0) g_trace_sub[blockIdx.x][0] = gtime();)
     cbar_wait(cbar, cph);
     cph ^= 1;
+    TRACE(if (threadIdx.x == 0) g_trace_sub[blockIdx.x][1] = gtime();)
     const int last = k + nsteps - 1;  // the step whose value the tile now holds
     if (I == last + 1 && J == last + 1) {
         // fused next pivot: P_{K+1} = (updated M_{K+1,K+1})^-1.  The updated tile goes straight into
@@ -593,7 +604,9 @@ __device__ int update_task(const InvParams &P, const MatDesc &m, int k, int nste
         return pivot_block(W, ld, i0, bi, pivot_slot(m, last + 1), dyn, true);
     }
     // column pairs (16-byte stores); rows are written whole up to the leading dimension: the lower
-    // half of a diagonal tile and the padding columns are never read (upper storage)
+    // half of a diagonal tile and the padding columns are never read (upper storage).  The task
+    // does not wait for the stores: the kernel loop releases the tile's stamp at the start of the
+    // CTA's next task (the drain overlaps the next task fetch).
 #pragma unroll
     for (int p = 0; p < 8; p++) {
         const int i = tile_row(p);
@@ -606,17 +619,10 @@ __device__ int update_task(const InvParams &P, const MatDesc &m, int k, int nste
             *reinterpret_cast<double2 *>(W + (int64_t)(i0 + i) * ld + j0 + j) = make_double2(c.x - acc[p][q], c.y - acc[p][q + 1]);
         }
     }
+    deferred = true;
     return 0;
 }
 
-#ifdef INV_TRACE  // experiment build only: per-task timeline
-struct TraceRec { int g, k, kind, I, J, sm; long long t0, t1, t2; };
-__device__ TraceRec g_trace[1 << 17];
-__device__ __forceinline__ long long gtime() { long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t; }
-#define TRACE(...) __VA_ARGS__
-#else
-#define TRACE(...)
-#endif
 __device__ __forceinline__ void wait_ge(const int *f, int target) {
     int v;
     for (;;) {
@@ -676,9 +682,24 @@ __global__ void __launch_bounds__(256, 1) inverse_kernel(const __grid_constant__
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    // deferred release of the previous update task (its tile stores may still be draining)
+    bool pend = false, pend_two = false;
+    int *pend_tile = nullptr, *pend_done = nullptr;
+    int pend_val = 0;
     for (;;) {
         __syncthreads();  // the previous task is done with shared memory and `next`
-        if (threadIdx.x == 0) next = atomicAdd(P.counter, 1);
+        if (threadIdx.x == 0) {
+            const int gn = atomicAdd(P.counter, 1);
+            if (pend) {  // the previous update's stores precede this release (bar.sync + cumulative fence);
+                         // done before any wait of the next task: the deadlock-freedom argument needs it
+                __threadfence();
+                asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(pend_tile), "r"(pend_val) : "memory");
+                atomicAdd(pend_done, 1);
+                if (pend_two) atomicAdd(pend_done + 1, 1);
+            }
+            next = gn;
+        }
+        pend = false;
         __syncthreads();
         const int g = next;
         if (g >= P.total_tasks) break;
@@ -689,12 +710,15 @@ __global__ void __launch_bounds__(256, 1) inverse_kernel(const __grid_constant__
         const int nt = m.nt;
         if (task.y == 0) {
             // ---------------- panel task
-            if (threadIdx.x == 0 && k >= 1) {
-                wait_ge(P.tileflag + m.tile_begin + (J >= k ? upper_index(k, J, nt) : upper_index(J, k, nt)), k);
-                wait_ge(P.pivflag + mi, k + 1);
-                if (k >= 3) wait_ge(P.tiles_done + m.col_begin + k - 3, nt * (nt + 1) / 2);  // buffer k mod 3
+            if (threadIdx.x < 32) {  // lanes poll one stamp each: one L2 round trip, not three
+                const int lane = threadIdx.x;
+                if (lane == 0 && k >= 1)
+                    wait_ge(P.tileflag + m.tile_begin + (J >= k ? upper_index(k, J, nt) : upper_index(J, k, nt)), k);
+                if (lane == 1 && k >= 1) wait_ge(P.pivflag + mi, k + 1);
+                if (lane == 2 && k >= 3) wait_ge(P.tiles_done + m.col_begin + k - 3, nt * (nt + 1) / 2);  // buffer k mod 3
+                __syncwarp();  // orders the lanes' acquires before lane 0's status read
+                if (lane == 0) next = *(volatile int *)m.status;  // one decision for the whole CTA
             }
-            if (threadIdx.x == 0) next = *(volatile int *)m.status;  // one decision for the whole CTA
             __syncthreads();
             TRACE(tr1 = gtime(); trJ = J; trkind = 0;)
             if (next == 0 && J != k) panel_task(m, k, J, dyn, ring);  // R_K / P R_K are never read
@@ -707,25 +731,35 @@ __global__ void __launch_bounds__(256, 1) inverse_kernel(const __grid_constant__
         } else {
             // ---------------- update task (kind 1) / merged update of steps k, k+1 (kind 2)
             const int ns = task.y == 2 ? 2 : 1, last = k + ns - 1;
-            if (threadIdx.x == 0) {
+            if (threadIdx.x < 32) {
                 // panels of step `last` (for a merged task they complete after step k's, which
                 // they depend on), P_k for the (K, K) copy, the tile's step k-1 value
-                if (I != k) wait_ge(P.colflag + m.col_begin + I, last + 1);
-                if (J != k && J != I) wait_ge(P.colflag + m.col_begin + J, last + 1);
-                if (I == k && J == k && k >= 1) wait_ge(P.pivflag + mi, k + 1);
-                if (k >= 1) wait_ge(P.tileflag + m.tile_begin + upper_index(I, J, nt), k);
+                const int lane = threadIdx.x;
+                if (lane == 0 && I != k) wait_ge(P.colflag + m.col_begin + I, last + 1);
+                if (lane == 1 && J != k && J != I) wait_ge(P.colflag + m.col_begin + J, last + 1);
+                if (lane == 2 && I == k && J == k && k >= 1) wait_ge(P.pivflag + mi, k + 1);
+                if (lane == 3 && k >= 1) wait_ge(P.tileflag + m.tile_begin + upper_index(I, J, nt), k);
+                __syncwarp();
+                if (lane == 0) next = *(volatile int *)m.status;  // one decision for the whole CTA
             }
-            if (threadIdx.x == 0) next = *(volatile int *)m.status;  // one decision for the whole CTA
             __syncthreads();
             TRACE(tr1 = gtime(); trI = I; trJ = J; trkind = (I == last + 1 && J == last + 1) ? 2 : (ns == 2 ? 3 : ((I == k || J == k) ? 4 : 1));)
             int f = 0;
+            bool deferred = false;
             if (next == 0)
                 f = update_task(P, m, k, ns, I, J, dyn, P.panels_done + m.col_begin + (last >= 1 ? last - 1 : 0), &cbar,
-                                cph, ring);
+                                cph, ring, deferred);
+            if (deferred) {  // tile stores still draining: release at the next task's start
+                pend = true;
+                pend_tile = P.tileflag + m.tile_begin + upper_index(I, J, nt);
+                pend_val = last + 1;
+                pend_done = P.tiles_done + m.col_begin + k;
+                pend_two = ns == 2;
+                            }
             if (f && threadIdx.x == 0) *m.status = f;
-            __threadfence();
+            if (!deferred) __threadfence();
             __syncthreads();
-            if (threadIdx.x == 0) {
+            if (threadIdx.x == 0 && !deferred) {
                 asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(P.tileflag + m.tile_begin + upper_index(I, J, nt)),
                              "r"(last + 1)
                              : "memory");
@@ -739,7 +773,7 @@ __global__ void __launch_bounds__(256, 1) inverse_kernel(const __grid_constant__
         if (threadIdx.x == 0 && g < (1 << 17)) {
             int sm;
             asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
-            g_trace[g] = TraceRec{g, k, trkind, trI, trJ, sm, tr0, tr1, gtime()};
+            g_trace[g] = TraceRec{g, k, trkind, trI, trJ, sm, tr0, tr1, gtime(), g_trace_sub[blockIdx.x][0], g_trace_sub[blockIdx.x][1]};
         }
 #endif
     }

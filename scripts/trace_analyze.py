@@ -4,7 +4,7 @@ import sys, collections
 rows = [list(map(int, l.split())) for l in open(sys.argv[1]) if l.strip()]
 t0 = min(r[6] for r in rows)
 steps = collections.defaultdict(list)
-for g, k, kind, I, J, sm, a, b, c in rows:
+for g, k, kind, I, J, sm, a, b, c, *_ in rows:
     steps[k].append((kind, I, J, (a - t0) / 1e3, (b - t0) / 1e3, (c - t0) / 1e3))
 print("step  panels[start..end]   pivot-tile[start..end]   tiles[first start..last end]  (us)")
 for k in sorted(steps):
@@ -23,3 +23,13 @@ for r in rows:
     kinds[r[2]].append((r[8] - r[7]) / 1e3)
 for kd, L in sorted(kinds.items()):
     print(f"kind {kd}: n={len(L)} mean {sum(L)/len(L):.1f} us, max {max(L):.1f}")
+# update tasks with sub-phase stamps (INV_TRACE builds of the current kernel): start -> product
+# end -> C-tile wait end -> task end
+for kd in (1, 3):
+    sub = [r for r in rows if r[2] == kd and len(r) >= 11 and r[9] >= r[7] and r[10] >= r[9] and r[8] >= r[10]]
+    if sub:
+        n = len(sub)
+        pr = sum(r[9] - r[7] for r in sub) / n / 1e3
+        cw = sum(r[10] - r[9] for r in sub) / n / 1e3
+        ep = sum(r[8] - r[10] for r in sub) / n / 1e3
+        print(f"kind {kd} phases: product {pr:.1f} us, C wait {cw:.1f} us, epilogue+flags {ep:.1f} us (n={n})")

@@ -15,11 +15,11 @@ for _ in range(3):
     st.run(xs, gys, 2.5e-2)
 torch.cuda.synchronize()
 lib = K.kfac._lib
-buf = np.zeros((1 << 17) * 9 * 2, dtype=np.int32)  # TraceRec: 6 ints + 3 int64 = 48 B
+buf = np.zeros((1 << 17) * 16, dtype=np.int32)  # TraceRec: 6 ints + 5 int64 = 64 B
 lib.kfac_debug_inverse_trace(buf.ctypes.data_as(ctypes.c_void_p), 1 << 17)
-rec = buf.view(np.uint8).reshape(-1, 48)
+rec = buf.view(np.uint8).reshape(-1, 64)
 ints = rec[:, :24].copy().view(np.int32).reshape(-1, 6)
-ts = rec[:, 24:].copy().view(np.int64).reshape(-1, 3)
+ts = rec[:, 24:].copy().view(np.int64).reshape(-1, 5)
 with open(sys.argv[1], "w") as f:
     for i in range(len(ints)):
         if ts[i, 2]:
