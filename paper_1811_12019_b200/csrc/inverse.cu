@@ -779,32 +779,32 @@ __global__ void __launch_bounds__(256, 1) inverse_kernel(const __grid_constant__
     }
 }
 
-// ---- epilogue: inv = -M (symmetric, full fp32) from the upper storage, 32 x 32 tiles through
-// shared memory so that the mirrored (lower) half is read and written coalesced
+// ---- epilogue: inv = -M (symmetric, full fp32) from the upper storage.  Each upper 32 x 32 tile is
+// read once (coalesced, through shared memory) and written to both of its output blocks.
 __global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ InvParams P) {
     const MatDesc &m = P.m[blockIdx.y];
     const int n = m.n;
     const int64_t ld = m.ld;
-    const int nt = (n + 31) / 32;
+    const int nt = (n + 31) / 32, npairs = nt * (nt + 1) / 2;
     __shared__ double T[32][33];
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-    for (int t = blockIdx.x; t < nt * nt; t += gridDim.x) {
-        const int bi = t / nt, bj = t - bi * nt;
-        const int si = min(bi, bj) * 32, sj = max(bi, bj) * 32;  // source tile in the upper storage
+    for (int t = blockIdx.x; t < npairs; t += gridDim.x) {
+        int bi = 0, rem = t;
+        while (rem >= nt - bi) rem -= nt - bi++;
+        const int bj = bi + rem;
         __syncthreads();
         for (int r = ty; r < 32; r += 8) {
-            const int i = si + r, j = sj + tx;
+            const int i = bi * 32 + r, j = bj * 32 + tx;
             T[r][tx] = (i < n && j < n) ? m.work[(int64_t)i * ld + j] : 0.0;
         }
         __syncthreads();
         for (int r = ty; r < 32; r += 8) {
             const int i = bi * 32 + r, j = bj * 32 + tx;
-            if (i >= n || j >= n) continue;
-            double v;
-            if (bi < bj) v = T[r][tx];
-            else if (bi > bj) v = T[tx][r];
-            else v = (r <= tx) ? T[r][tx] : T[tx][r];
-            m.inv[(int64_t)i * n + j] = (float)(-v);
+            if (i < n && j < n) m.inv[(int64_t)i * n + j] = (float)(-((bi < bj || r <= tx) ? T[r][tx] : T[tx][r]));
+            if (bi < bj) {
+                const int i2 = bj * 32 + r, j2 = bi * 32 + tx;
+                if (i2 < n && j2 < n) m.inv[(int64_t)i2 * n + j2] = (float)(-T[tx][r]);
+            }
         }
     }
 }
@@ -917,7 +917,8 @@ kfac_status inverse_launch(const std::vector<InvMat> &mats, int npairs, float ga
     inverse_kernel<<<std::min(P.total_tasks, g_inv_sms), 256, kUpdSmem, st>>>(P);
     KFAC_LAUNCHED();
     KFAC_CUDA_TRY(cudaGetLastError());
-    finalize_kernel<<<dim3(std::min(((maxn + 31) / 32) * ((maxn + 31) / 32), 1184), P.nm), 256, 0, st>>>(P);
+    const int max32 = (maxn + 31) / 32;
+    finalize_kernel<<<dim3(std::min(max32 * (max32 + 1) / 2, 592), P.nm), 256, 0, st>>>(P);
     KFAC_LAUNCHED();
     KFAC_CUDA_TRY(cudaGetLastError());
     return KFAC_OK;

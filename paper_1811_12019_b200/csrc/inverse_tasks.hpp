@@ -12,9 +12,11 @@ namespace kfac_inv {
 // individual tasks.  Records {k, kind, matrix, I << 16 | J}: kind 0 panel (k, J), 1 update of tile
 // (I, J) at step k, 2 merged update of tile (I, J) for steps k and k+1.  The order of pair k
 // (segment-major over the matrices, sorted by nt descending) follows the critical path
-// P_k -> panel(k+1, K+2) -> merged tile (K+2, K+2) -> P_{k+2} -> ...:
+// P_k -> panel(k+1, K+2) -> tile (K+2, K+2) at step k+1 -> P_{k+2} -> ...:
 //   a  [k = 0] step 0's panels (column 1 first) and the pivot tile (1, 1)
-//   b  look-ahead row / column k+1 at step k            c  panel (k+1, k+2), merged tile (k+2, k+2)
+//   b  look-ahead row / column k+1 at step k, and tile (k+2, k+2) at step k
+//   c  panel (k+1, k+2), then tile (k+2, k+2) at step k+1 (the fused pivot P_{k+2}: a single-step
+//      task, so the critical chain P_k -> ... -> P_{k+2} carries one product per pivot, not two)
 //   d  row / column k at step k (copies of P R)         e  the other panels of step k+1
 //   f  rows / columns k, k+1 at step k+1                g  merged tiles in rows / columns k+2, k+3
 //   h  panel (k+2, k+3) and update (k+2, k+3, k+3) (the next pair's pivot tile)
@@ -35,7 +37,7 @@ __host__ __device__ inline void pair_counts(int nt, int k, int *c) {
     const int Bp = nt - 2, x = (nt > k + 2 ? 1 : 0) + (nt > k + 3 ? 1 : 0);
     const int la = Bp * (Bp + 1) / 2 - (Bp - x) * (Bp - x + 1) / 2 - (d22 ? 1 : 0);
     const int rest = (nt - 2) * (nt - 1) / 2 - la - (d22 ? 1 : 0);
-    c[1] = nt - 1;
+    c[1] = nt - 1 + (d22 ? 1 : 0);
     c[2] = d22 ? 2 : 0;
     c[3] = nt - 1;
     c[4] = nt - (d22 ? 1 : 0);
@@ -65,9 +67,10 @@ __host__ __device__ inline void pair_emit(int nt, int k, int m, int *cur, int4 *
     }
     for (int I = 0; I < L; I++) put(1, k, 1, I, L);
     for (int J = L + 1; J < nt; J++) put(1, k, 1, L, J);
+    if (d22) put(1, k, 1, k + 2, k + 2);
     if (d22) {
         put(2, k + 1, 0, 0, k + 2);
-        put(2, k, 2, k + 2, k + 2);
+        put(2, k + 1, 1, k + 2, k + 2);
     }
     for (int I = 0; I < k; I++) put(3, k, 1, I, k);
     for (int J = k; J < nt; J++)

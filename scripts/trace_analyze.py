@@ -33,3 +33,13 @@ for kd in (1, 3):
         cw = sum(r[10] - r[9] for r in sub) / n / 1e3
         ep = sum(r[8] - r[10] for r in sub) / n / 1e3
         print(f"kind {kd} phases: product {pr:.1f} us, C wait {cw:.1f} us, epilogue+flags {ep:.1f} us (n={n})")
+# utilisation over time: fraction of CTAs busy (work phase) per 5% of the kernel
+T = max(r[8] for r in rows) - t0
+bins = [0.0] * 20
+for r in rows:
+    a, b = r[7] - t0, r[8] - t0
+    for q in range(20):
+        lo, hi = q * T / 20, (q + 1) * T / 20
+        bins[q] += max(0, min(b, hi) - max(a, lo))
+ncta = len(set(r[5] for r in rows))
+print("busy by 5% slice:", " ".join(f"{b / (T / 20 * ncta) * 100:.0f}" for b in bins))
