@@ -112,20 +112,20 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_sample(layers, n, small_dim, threads=0):
-    """Bounded oracle sample, scaled to one full step (ms).  Factors: 1 image of n (rows scale
-    linearly); inverse + precondition: layers with max(dA, dG) <= small_dim, scaled by flops."""
+def cpu_sample(layers, n, small_dim, threads=0, images=2):
+    """Bounded oracle sample, scaled to one full step (ms).  Factors: `images` images of n (rows
+    scale linearly); inverse + precondition: layers with max(dA, dG) <= small_dim, scaled by flops."""
     import numpy as np
 
     import oracle
     oracle.build()
     t_fac = 0.0
     for i, l in enumerate(layers):
-        x = inputs.half_bits(inputs.layer_x(l, i, 1))
-        gy = inputs.half_bits(inputs.layer_gy(l, i, 1))
+        x = inputs.half_bits(inputs.layer_x(l, i, images))
+        gy = inputs.half_bits(inputs.layer_gy(l, i, images))
         t0 = time.perf_counter()
-        oracle.factor_A(l, x, 1, threads=threads)
-        oracle.factor_G(gy, shapes.rows(l, 1), l["c_out"], threads=threads)
+        oracle.factor_A(l, x, images, threads=threads)
+        oracle.factor_G(gy, shapes.rows(l, images), l["c_out"], threads=threads)
         t_fac += time.perf_counter() - t0
     t_inv = 0.0
     f_s = f_all = 0
@@ -148,8 +148,8 @@ def cpu_sample(layers, n, small_dim, threads=0):
         Gi, _ = oracle.inverse(Gd, threads)
         oracle.precondition(Gi, Ai, dW, threads)
         t_inv += time.perf_counter() - t0
-    scaled = (t_fac * n + t_inv * (f_all / max(f_s, 1))) * 1e3
-    desc = (f"oracle factors on 1 of {n} images (x{n}) + damp/inverse/precondition of layers with dim <= {small_dim} "
+    scaled = (t_fac * n / images + t_inv * (f_all / max(f_s, 1))) * 1e3
+    desc = (f"oracle factors on {images} of {n} images (x{n / images:g}) + damp/inverse/precondition of layers with dim <= {small_dim} "
             f"({100.0 * f_s / f_all:.1f}% of stage-4/5 flops, scaled by flops); measured {t_fac + t_inv:.1f} s")
     return scaled, desc, oracle.max_threads(), t_fac + t_inv
 
@@ -159,7 +159,7 @@ def run_reference(args):
     if rank != 0:
         return 0
     layers, n = shapes.config(args.config)
-    small = 576 if args.config in ("resnet50", "resnet18_cifar") else 10 ** 9
+    small = 1024 if args.config in ("resnet50", "resnet18_cifar") else 10 ** 9
     if args.config == "stress":
         small = 1000
     for _ in range(args.warmup):
@@ -380,7 +380,7 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        small = 576 if args.config in ("resnet50", "resnet18_cifar") else (1000 if args.config == "stress" else 10 ** 9)
+        small = 1024 if args.config in ("resnet50", "resnet18_cifar") else (1000 if args.config == "stress" else 10 ** 9)
         v, desc, cores, _ = cpu_sample(layers, n, small)
         cpu = {"value": round(v, 1), "unit": "ms", "cores": cores, "kind": "oracle", "sample": desc}
 

@@ -29,6 +29,7 @@
 namespace kfac {
 
 constexpr int kMaxMats = 128;
+constexpr int kPanelBufs = 4;  // panel buffers per matrix (step mod 4)
 constexpr int B = kPanel;     // 128
 #ifndef KFAC_INV_KC  // experiment overrides (KFAC_NVCC_EXTRA)
 #define KFAC_INV_KC 8
@@ -47,7 +48,7 @@ struct MatDesc {
     const float *packed;
     float *inv;
     double *work;
-    double *panel;  // [R | Wp per step mod 3: B x ld each][P_even | P_odd: B x B]
+    double *panel;  // [R | Wp per step mod kPanelBufs: B x ld each][P_even | P_odd: B x B]
     int32_t *status;
     int32_t n, ld, pair, is_A;
     int32_t nt;          // column blocks
@@ -70,7 +71,7 @@ struct InvParams {
     int *tiles_done;   // [sum nt]    per (matrix, step): completed update tasks
     int *tileflag;     // [sum tiles] k + 1 once tile (I, J) holds its step-k value
     int4 *tasks;       // [total_tasks] task records (gen_step_tasks), built on the device per call
-    int32_t step_begin[kMaxSteps + 1];  // first record of each pair's list (steps 2p, 2p+1)
+    int32_t step_begin[kMaxSteps + 1];  // first record of each pair's list (inverse_tasks.hpp)
     MatDesc m[kMaxMats];
 };
 
@@ -156,6 +157,18 @@ constexpr int S2 = 32;  // sub-pivot size
 constexpr int S2_ = S2;
 constexpr int QLD = S2 + 4;  // padded row stride of Q (conflict-free DMMA fragments)
 
+// 1/d for a positive normal d: the hardware approximation refined by two Newton steps (error
+// squared each time: full double precision up to the last bit or two; the sweep tolerates that,
+// and it is off the IEEE-rounded __drcp_rn's longer software sequence on the sweep's serial chain)
+__device__ __forceinline__ double rcp_fast(double d) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+    double e = fma(-d, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-d, r, 1.0);
+    return fma(r, e, r);
+}
+
 // sweep of the 32 x 32 sub-pivot S[s0.., s0..] by all 8 warps with the block in registers: thread
 // (w, lane) holds rows 4w..4w+3 of column `lane`.  The sweep keeps the block symmetric, so pivot
 // row t equals column t: per pivot its owner warp publishes row t (ping-pong buffer), one barrier,
@@ -176,7 +189,7 @@ __device__ __forceinline__ int block_sweep32(const double (*S)[B + 1], int s0, d
         __syncthreads();
         const double d = rb[t];
         if (!(d > 0.0)) return base + t + 1;  // uniform: every thread read the same d
-        const double inv = __drcp_rn(d);
+        const double inv = rcp_fast(d);
         const double vj = rb[lane] * inv;  // (t, lane) / d
 #pragma unroll
         for (int r = 0; r < 4; r++) {
@@ -327,11 +340,12 @@ __device__ int pivot_block(double *__restrict__ W, int64_t ld, int k0, int bk, d
 }
 
 __device__ __forceinline__ double *pivot_slot(const MatDesc &m, int k) {
-    return m.panel + 6 * (int64_t)B * m.ld + (int64_t)(k & 1) * B * B;
+    return m.panel + 2 * kPanelBufs * (int64_t)B * m.ld + (int64_t)(k & 1) * B * B;
 }
-// three R / P R panel buffers (step mod 3): a merged task reads steps k and k+1 while step k+2's
-// panels are written
-__device__ __forceinline__ double *panel_R(const MatDesc &m, int k) { return m.panel + (int64_t)(k % 3) * 2 * B * m.ld; }
+// kPanelBufs R / P R panel buffers (step mod 4): a merged task reads steps k and k+1 while later
+// steps' panels are written; with four, a panel's buffer wait (all updates of step k-4) points to
+// the pair two pairs back, so chain tasks do not wait for the current bulk tiles
+__device__ __forceinline__ double *panel_R(const MatDesc &m, int k) { return m.panel + (int64_t)(k % kPanelBufs) * 2 * B * m.ld; }
 __device__ __forceinline__ double *panel_Wp(const MatDesc &m, int k) { return panel_R(m, k) + (int64_t)B * m.ld; }
 
 // step 0 only: P_0 (later pivots are fused into the previous step's tile (K+1, K+1) update)
@@ -708,25 +722,46 @@ __global__ void __launch_bounds__(256, 1) inverse_kernel(const __grid_constant__
         const int k = task.x, mi = task.z, I = task.w >> 16, J = task.w & 0xffff;
         const MatDesc &m = P.m[mi];
         const int nt = m.nt;
-        if (task.y == 0) {
-            // ---------------- panel task
+        if (task.y == 0 || task.y == 3) {
+            // ---------------- panel task (kind 0) / chain task (kind 3: panel (k, J = k+1), then the
+            // update of tile (J, J) at step k and its inverse P_{k+1}, in one task)
             if (threadIdx.x < 32) {  // lanes poll one stamp each: one L2 round trip, not three
                 const int lane = threadIdx.x;
                 if (lane == 0 && k >= 1)
                     wait_ge(P.tileflag + m.tile_begin + (J >= k ? upper_index(k, J, nt) : upper_index(J, k, nt)), k);
                 if (lane == 1 && k >= 1) wait_ge(P.pivflag + mi, k + 1);
-                if (lane == 2 && k >= 3) wait_ge(P.tiles_done + m.col_begin + k - 3, nt * (nt + 1) / 2);  // buffer k mod 3
+                if (lane == 2 && k >= kPanelBufs)  // its buffer's previous user: all updates of step k - kPanelBufs
+                    wait_ge(P.tiles_done + m.col_begin + k - kPanelBufs, nt * (nt + 1) / 2);
+                if (lane == 3 && task.y == 3 && k >= 1) wait_ge(P.tileflag + m.tile_begin + upper_index(J, J, nt), k);
                 __syncwarp();  // orders the lanes' acquires before lane 0's status read
                 if (lane == 0) next = *(volatile int *)m.status;  // one decision for the whole CTA
             }
             __syncthreads();
-            TRACE(tr1 = gtime(); trJ = J; trkind = 0;)
-            if (next == 0 && J != k) panel_task(m, k, J, dyn, ring);  // R_K / P R_K are never read
+            TRACE(tr1 = gtime(); trJ = J; trkind = task.y == 3 ? 5 : 0;)
+            const bool live = next == 0;
+            if (live && J != k) panel_task(m, k, J, dyn, ring);  // R_K / P R_K are never read
             __threadfence();
             __syncthreads();
             if (threadIdx.x == 0) {
                 asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(P.colflag + m.col_begin + J), "r"(k + 1) : "memory");
                 atomicAdd(P.panels_done + m.col_begin + k, 1);
+            }
+            if (task.y == 3) {
+                int f = 0;
+                bool deferred = false;  // stays false: the pivot path writes W itself
+                if (live)
+                    f = update_task(P, m, k, 1, J, J, dyn, P.panels_done + m.col_begin + (k >= 1 ? k - 1 : 0), &cbar, cph,
+                                    ring, deferred);
+                if (f && threadIdx.x == 0) *m.status = f;
+                __threadfence();
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(P.tileflag + m.tile_begin + upper_index(J, J, nt)),
+                                 "r"(k + 1)
+                                 : "memory");
+                    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(P.pivflag + mi), "r"(k + 2) : "memory");
+                    atomicAdd(P.tiles_done + m.col_begin + k, 1);
+                }
             }
         } else {
             // ---------------- update task (kind 1) / merged update of steps k, k+1 (kind 2)
@@ -831,7 +866,7 @@ int64_t inverse_tasks(int n) {
 }
 int64_t inverse_ws_doubles(int n) {
     const int64_t ld = inverse_ld(n);
-    return (n * ld + 6 * (int64_t)B * ld + 2 * (int64_t)B * B + 31) / 32 * 32;
+    return (n * ld + 2 * kPanelBufs * (int64_t)B * ld + 2 * (int64_t)B * B + 31) / 32 * 32;
 }
 
 kfac_status inverse_launch(const std::vector<InvMat> &mats, int npairs, float gamma, double *pair_scratch,

@@ -92,7 +92,7 @@ struct InvMat {        // one damped factor to invert
     const float *packed;  // packed upper fp32 (from rs_recv)
     float *inv;           // full fp32 output
     double *work;         // n*n fp64 working matrix
-    double *panel;        // 6 * kPanel * ld + 2 * kPanel^2 fp64 (R, P R per step mod 3; two pivots)
+    double *panel;        // 8 * kPanel * ld + 2 * kPanel^2 fp64 (R, P R per step mod 4; two pivots)
     int32_t *status;      // device status word
     int32_t n;
     int32_t pair;         // index of the (A, G) pair this matrix belongs to

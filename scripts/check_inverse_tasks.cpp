@@ -88,12 +88,14 @@ static bool check_mix(std::vector<int> nt) {
     for (int g = 0; g < (int)list.size(); g++) {
         const int4 t = list[g];
         const int k = t.x, m = t.z, I = t.w >> 16, J = t.w & 0xffff;
-        if (t.y == 0) {
+        if (t.y == 0 || t.y == 3) {  // a chain task (3) is panel (k, J) + update (k, J, J) + P_{k+1}
             CHECK(!panel.count({m, k, J}), "panel (%d,%d,%d) twice", m, k, J);
             panel[{m, k, J}] = g;
             last_panel[{m, k}] = std::max(last_panel.count({m, k}) ? last_panel[{m, k}] : -1, g);
             npanel[{m, k}]++;
-        } else {
+            if (t.y == 3) CHECK(I == J && J == k + 1, "chain task at (%d,%d) step %d", I, J, k);
+        }
+        if (t.y != 0) {
             const int ns = t.y == 2 ? 2 : 1, last = k + ns - 1;
             CHECK(I <= J && J < nt[m], "bad tile (%d,%d) nt %d", I, J, nt[m]);
             if (ns == 2) CHECK(I != k && I != k + 1 && J != k && J != k + 1 && k + 1 < nt[m], "merged task on a pivot row/col");
@@ -135,21 +137,24 @@ static bool check_mix(std::vector<int> nt) {
     for (int g = 0; g < (int)list.size(); g++) {
         const int4 t = list[g];
         const int k = t.x, m = t.z, I = t.w >> 16, J = t.w & 0xffff;
-        if (t.y == 0) {
+        if (t.y == 0 || t.y == 3) {
             if (k >= 1) {
                 before(val(m, k, J, k - 1), g, "tile (K, J) of step k-1", t);
                 before(pivot[{m, k}], g, "P_k", t);
-                if (k >= 3) before(last_tile[{m, k - 3}], g, "step k-3's tiles (panel buffer k mod 3)", t);
+                if (k >= 4) before(last_tile[{m, k - 4}], g, "step k-4's tiles (panel buffer k mod 4)", t);
             }
-        } else {
+        }
+        if (t.y != 0) {
             const int ns = t.y == 2 ? 2 : 1, last = k + ns - 1;
-            if (I != k) before(panel[{m, last, I}], g, "panel I of step last", t);
-            if (J != k && J != I) before(panel[{m, last, J}], g, "panel J of step last", t);
+            // a chain task's own panel is done inside the task, before its update
+            auto pan = [&](int s, int c) { return (t.y == 3 && s == k && c == J) ? -1 : panel[{m, s, c}]; };
+            if (I != k) before(pan(last, I), g, "panel I of step last", t);
+            if (J != k && J != I) before(pan(last, J), g, "panel J of step last", t);
             if (ns == 2) {  // step k's panels I, J: transitively via step k+1's (checked directly here)
-                before(panel[{m, k, I}], g, "panel I of step k", t);
-                before(panel[{m, k, J}], g, "panel J of step k", t);
+                before(pan(k, I), g, "panel I of step k", t);
+                before(pan(k, J), g, "panel J of step k", t);
             } else if (!(I == k || J == k)) {
-                before(panel[{m, k, I}], g, "panel I", t);
+                before(pan(k, I), g, "panel I", t);
             }
             if (I == k && J == k && k >= 1) before(pivot[{m, k}], g, "P_k", t);
             if (k >= 1) before(val(m, I, J, k - 1), g, "the tile's step k-1 value", t);

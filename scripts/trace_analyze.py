@@ -9,7 +9,7 @@ for g, k, kind, I, J, sm, a, b, c, *_ in rows:
 print("step  panels[start..end]   pivot-tile[start..end]   tiles[first start..last end]  (us)")
 for k in sorted(steps):
     P = [x for x in steps[k] if x[0] == 0]
-    V = [x for x in steps[k] if x[0] == 2]
+    V = [x for x in steps[k] if x[0] in (2, 5)]
     T = [x for x in steps[k] if x[0] == 1]
     f = lambda L: f"{min(x[4] for x in L):8.1f}..{max(x[5] for x in L):8.1f}" if L else " " * 18
     print(f"{k:4d}  {f(P)}  {f(V)}  {f(T)}")
