@@ -42,7 +42,7 @@ constexpr int kStages = KFAC_INV_STAGES;  // ring depth
 constexpr int kPivSmem = (B * (B + 1) + 2 * 32 * (B + 4) + 32 * 36 + 64) * 8 + 64;
 constexpr int kTileSmem = kStages * 2 * KC * (B + 4) * 8;  // A/B chunk ring (padded rows): 66 KB
 constexpr int kUpdSmem = kPivSmem > kTileSmem + B * (B + 4) * 8 ? kPivSmem : kTileSmem + B * (B + 4) * 8;
-static_assert(kUpdSmem >= B * (B + 1) * 8, "panel staging fits the update kernel's shared memory");
+static_assert(kUpdSmem >= B * (B + 1) * 8 + kTileSmem, "panel staging + ring fit the update kernel's shared memory");
 
 struct MatDesc {
     const float *packed;
@@ -412,7 +412,11 @@ struct Ring {
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s2u(bar)) : "memory");
 }
-__device__ __forceinline__ void tile_product(const Seg &s0, const Seg &s1, double (&acc)[8][8], double *smem, Ring &ring) {
+// BSRC: 0 both operands through the ring; 1 / 2 the B operand is already resident in shared memory
+// (Tb, row stride B+1: element (t, j) at Tb[t][j], or at Tb[j][t] for 2) and only A streams.
+template <int BSRC = 0>
+__device__ __forceinline__ void tile_product(const Seg &s0, const Seg &s1, double (&acc)[8][8], double *smem, Ring &ring,
+                                             const double *Tb = nullptr) {
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int arow = 64 * (w >> 2) + (lane >> 2), bcol = 32 * (w & 3) + (lane >> 2), kl = lane & 3;
     const int n0 = (s0.kt + KC - 1) / KC, nch = n0 + (s1.kt + KC - 1) / KC;
@@ -427,7 +431,7 @@ __device__ __forceinline__ void tile_product(const Seg &s0, const Seg &s1, doubl
         if (G >= kStages) cbar_wait(ring.empty + st, ((G / kStages) + 1) & 1);  // chunk G - kStages consumed
         double *dst = smem + st * 2 * KC * SLD;
 #pragma unroll
-        for (int it = 0; it < 2 * KC * B / 2 / 256; it++) {
+        for (int it = 0; it < (BSRC ? 1 : 2) * KC * B / 2 / 256; it++) {
             const int e = it * 256 + threadIdx.x, r = e >> 6, i = (e & 63) * 2;  // r < KC: A rows, else B
             const bool isA = r < KC;
             const int t = t0 + (isA ? r : r - KC);
@@ -448,8 +452,11 @@ __device__ __forceinline__ void tile_product(const Seg &s0, const Seg &s1, doubl
             double a[8], b[4];
 #pragma unroll
             for (int p = 0; p < 8; p++) a[p] = as[t * SLD + arow + 8 * p];
+            const int tg = (c < n0 ? c : c - n0) * KC + t;  // K row within the segment (resident B)
 #pragma unroll
-            for (int q = 0; q < 4; q++) b[q] = bs[t * SLD + bcol + 8 * q];
+            for (int q = 0; q < 4; q++)
+                b[q] = BSRC == 0 ? bs[t * SLD + bcol + 8 * q]
+                                 : (BSRC == 1 ? Tb[tg * (B + 1) + bcol + 8 * q] : Tb[(bcol + 8 * q) * (B + 1) + tg]);
 #pragma unroll
             for (int p = 0; p < 8; p++)
 #pragma unroll
@@ -503,16 +510,17 @@ __device__ void panel_task(const MatDesc &m, int k, int J, double *dyn, Ring &ri
         else v = T[t][j];
         R[(int64_t)t * ld + j0 + j] = v;
     }
-    __threadfence_block();
-    __syncthreads();
     double acc[8][8];
 #pragma unroll
     for (int p = 0; p < 8; p++)
 #pragma unroll
         for (int q = 0; q < 8; q++) acc[p][q] = 0.0;
-    // Wp[i][j] = sum_t P[t][i] R[t][j]   (P symmetric, zero outside bk)
-    const Seg seg{pivot_slot(m, k), B, B, R + j0, ld, bjp, bk}, none{nullptr, 0, 0, nullptr, 0, 0, 0};
-    tile_product(seg, none, acc, dyn, ring);
+    // Wp[i][j] = sum_t P[t][i] R[t][j]   (P symmetric, zero outside bk).  R is read straight from the
+    // staged tile T (resident; zero outside the block), only P streams through the ring placed
+    // after T -- the product does not wait for R's global write.
+    const Seg seg{pivot_slot(m, k), B, B, nullptr, 0, 0, bk}, none{nullptr, 0, 0, nullptr, 0, 0, 0};
+    if (trans) tile_product<2>(seg, none, acc, dyn + B * (B + 1), ring, &T[0][0]);
+    else tile_product<1>(seg, none, acc, dyn + B * (B + 1), ring, &T[0][0]);
     __syncthreads();  // the product's staging buffers are free: the result goes through T
 #pragma unroll
     for (int p = 0; p < 8; p++)
