@@ -18,6 +18,9 @@ parts of the method in plain Python:
 * ``all_gather``       AllGatherV of the primary owners' 𝒢.
 * ``damping_schedule`` warmup damping recurrence (reading R-2).
 * ``kfac_step``        Algorithm 1's body minus fwd/bwd/update.
+* ``refresh_interval`` / ``refresh`` / ``fim_diff`` / ``diff_percentiles`` /
+  ``stale_results`` and ``plan(stale=True)``: stale Fisher information
+  (NEXT-1; reading R-17).
 
 Parity status: every function here is pinned by tests/test_oracle_*.py (see
 DESIGN.md §Oracle pins); none is "parity unpinned".
@@ -277,7 +280,7 @@ def layer_cost(layer):
     return a ** 3 + g ** 3 + 2 * g * g * a + 2 * g * a * a
 
 
-def plan(layers, world, policy=POLICY_RR):
+def plan(layers, world, policy=POLICY_RR, stale=False):
     """Owner map and owner-major segment layout.
 
     owner[l]: primary owner.  RR: l mod P.  LPT: layers by (-cost, l), each to
@@ -286,6 +289,11 @@ def plan(layers, world, policy=POLICY_RR):
     each with segments [∇W (dG·dA), A packed, G packed], every segment start
     aligned to 16 elements; rs_chunk = max chunk.  AG: each rank's chunk holds
     its primary layers' 𝒢 (dG·dA) ascending, aligned; ag_chunk = max.
+
+    stale=True: the wire layout of a step that reuses stale factors (P:701-704,
+    "reduce the frequency of updating (A, G, F)"; reading R-17): the same
+    owners, but each owned layer carries only its ∇W segment; the A and G
+    offsets are None (seg_off -1).  The AG layout is unchanged.
     """
     L, P = len(layers), int(world)
     if L < 1 or P < 1:
@@ -311,6 +319,9 @@ def plan(layers, world, policy=POLICY_RR):
             a, g = dims(layers[l])
             o_w = off
             off = _align(off + g * a)
+            if stale:
+                m[l] = (o_w, None, None)
+                continue
             o_a = off
             off = _align(off + packed_len(a))
             o_g = off
@@ -322,7 +333,7 @@ def plan(layers, world, policy=POLICY_RR):
     seg_off = np.zeros((L, 3), dtype=np.int64)
     for l in range(L):
         r = owner[l]
-        seg_off[l] = [r * rs_chunk + v for v in local[r][l]]
+        seg_off[l] = [-1 if v is None else r * rs_chunk + v for v in local[r][l]]
     ag_local, ag_chunks = [], []
     for r in range(P):
         off, m = 0, {}
@@ -337,7 +348,7 @@ def plan(layers, world, policy=POLICY_RR):
     ag_off = np.array([owner[l] * ag_chunk + ag_local[owner[l]][l] for l in range(L)], dtype=np.int64)
     return dict(owner=np.array(owner, dtype=np.int32), owned=owned, local=local,
                 seg_off=seg_off, rs_chunk=int(rs_chunk), ag_off=ag_off, ag_chunk=int(ag_chunk),
-                world=P, L=L)
+                world=P, L=L, stale=bool(stale))
 
 
 # --------------------------------------------------------------------------
@@ -363,15 +374,18 @@ def all_gather(slots, pl):
 # Algorithm 1 body: factors -> RS -> damp+invert -> precondition -> AG
 # --------------------------------------------------------------------------
 def build_send(layers, pl, rank, factors, dws):
-    """Rank `rank`'s RS send buffer: (∇W, A packed, G packed) of every layer at every owner copy."""
+    """Rank `rank`'s RS send buffer: (∇W, A packed, G packed) of every layer at every owner copy
+    (∇W only for a stale plan; `factors` may then be None)."""
     P, c = pl["world"], pl["rs_chunk"]
     send = np.zeros(P * c, dtype=np.float64)
     for r in range(P):
         for l, (o_w, o_a, o_g) in pl["local"][r].items():
-            A, G = factors[l]
             a, g = dims(layers[l])
             base = r * c
             send[base + o_w: base + o_w + g * a] = np.asarray(dws[l], dtype=np.float64).reshape(-1)
+            if o_a is None:  # stale layout: ∇W only
+                continue
+            A, G = factors[l]
             send[base + o_a: base + o_a + packed_len(a)] = pack(A)
             send[base + o_g: base + o_g + packed_len(g)] = pack(G)
     return send
@@ -423,3 +437,75 @@ def kfac_step(layers, rank_inputs, world, gamma, policy=POLICY_RR, fmt="bf16", t
         slots.append(slot)
     gathered = all_gather(slots, pl)
     return dict(plan=pl, sends=sends, recvs=recvs, results=results, gathered=gathered)
+
+
+# --------------------------------------------------------------------------
+# NEXT-1: stale Fisher information
+# --------------------------------------------------------------------------
+def refresh_interval(epoch, schedule="rampup"):
+    """interval⁽ᵉ⁾ of the epoch-e refresh schedule.
+
+    "rampup": min(20, 5·⌊e/5⌋ + 1)            (the 10-minute run)
+    "step13": 1 if e < 13 else 20             (the BN-diagonal study)
+    """
+    e = int(epoch)
+    if e < 0:
+        raise ValueError("epoch >= 0")
+    if schedule == "rampup":
+        return min(20, 5 * (e // 5) + 1)
+    if schedule == "step13":
+        return 1 if e < 13 else 20
+    raise ValueError("unknown schedule")
+
+
+def refresh(t, epoch, schedule="rampup", fresh_floor=500, interval=None):
+    """Refresh decision of iteration t in epoch e: every iteration
+    before `fresh_floor` ("after 500 iterations"), then when
+    t mod interval⁽ᵉ⁾ = 0.  `interval` overrides the schedule (must be >= 1)."""
+    iv = refresh_interval(epoch, schedule) if interval is None else int(interval)
+    if iv < 1:
+        raise ValueError("interval >= 1")
+    return int(t) < int(fresh_floor) or int(t) % iv == 0
+
+
+def fim_diff(X_cur, X_prev):
+    """Diff⁽ᵗ⁾ = ‖X⁽ᵗ⁾ − X⁽ᵗ⁻¹⁾‖_F / ‖X⁽ᵗ⁻¹⁾‖_F of two full
+    matrices, in fp64; None when ‖X⁽ᵗ⁻¹⁾‖_F = 0 (S:558, "recorded as missing")."""
+    X_cur = np.asarray(X_cur, dtype=np.float64)
+    X_prev = np.asarray(X_prev, dtype=np.float64)
+    if X_cur.shape != X_prev.shape:
+        raise ValueError("fim_diff: shapes differ")
+    den = math.sqrt(float(np.sum(X_prev * X_prev)))
+    if den == 0.0:
+        return None
+    D = X_cur - X_prev
+    return math.sqrt(float(np.sum(D * D))) / den
+
+
+def diff_percentiles(diffs, qs=(5, 25, 50, 75, 95)):
+    """{5,25,50,75,95}th percentiles of the per-layer Diff values (Fig. 5
+    caption), linear interpolation between order statistics; missing
+    (None) values are dropped."""
+    v = sorted(float(d) for d in diffs if d is not None)
+    if not v:
+        return {q: None for q in qs}
+    out = {}
+    for q in qs:
+        pos = (len(v) - 1) * q / 100.0
+        lo = int(math.floor(pos))
+        hi = min(lo + 1, len(v) - 1)
+        out[q] = v[lo] + (v[hi] - v[lo]) * (pos - lo)
+    return out
+
+
+def stale_results(layers, pl_stale, rank, recv, cached):
+    """Stage 5 of a stale step on one rank: 𝒢 = G_d⁻¹ ∇W A_d⁻¹ with the cached
+    inverses of the last refresh (`cached[l] = (Ainv, Ginv)`), ∇W from the
+    stale-layout recv chunk (R-17)."""
+    out = {}
+    for l, (o_w, _, _) in pl_stale["local"][rank].items():
+        a, g = dims(layers[l])
+        dW = recv[o_w:o_w + g * a].reshape(g, a)
+        Ainv, Ginv = cached[l]
+        out[l] = dict(dW=dW, precond=precondition(Ginv, Ainv, dW))
+    return out
