@@ -141,6 +141,42 @@ KFAC_API kfac_status kfac_plan_rank_layers(kfac_plan_t plan, int32_t rank, int32
 
 KFAC_API void kfac_plan_destroy(kfac_plan_t plan);
 
+/* ------------------------------------------------------------------ stale Fisher (NEXT-1)
+ * The paper refreshes (A, G) only every interval^(e) iterations after the
+ * first 500 and reuses the previous preconditioner in
+ * between (reading R-17: the owner keeps its cached A_d^-1, G_d^-1 in inv_ws).
+ *
+ * kfac_plan_create_stale: a plan for the steps that reuse stale factors.  It
+ * has the same owners, owned lists, AllGather layout, inverse layout
+ * (inv_off, inv_floats) and ws_bytes as `full`, but every owned layer's
+ * ReduceScatter segment list is [dW] only: seg_off / local_off of A and G are
+ * -1 and rs_chunk shrinks to the gradient payload (a stale step moves
+ * strictly fewer bytes in stage 3).  On a stale plan
+ *   kfac_factor_all            launches no factor kernel; it only refreshes the
+ *                              dW of redundant owner copies (xs, gys may be NULL);
+ *   kfac_reduce_scatter_factors, kfac_precondition, kfac_allgather_precond
+ *                              work unchanged (precondition reads the cached
+ *                              inverses the last full step left in inv_ws);
+ *   kfac_damped_inverse, kfac_factor_diff  return KFAC_ERR_STATE.
+ * `full` must outlive nothing: the stale plan is independent (destroy both).
+ * Errors: KFAC_ERR_ARG (NULL), KFAC_ERR_STATE (`full` is itself stale).       */
+KFAC_API kfac_status kfac_plan_create_stale(kfac_plan_t full, kfac_plan_t *out /* host */);
+/* 1 for a plan made by kfac_plan_create_stale, else 0. */
+KFAC_API int32_t kfac_plan_is_stale(kfac_plan_t plan);
+
+/* Refresh schedules of the stale-Fisher runs (host-only, no device work). */
+typedef enum {
+    KFAC_REFRESH_RAMPUP = 0, /* interval^(e) = min(20, 5 floor(e/5) + 1) */
+    KFAC_REFRESH_STEP13 = 1  /* interval^(e) = 1 if e < 13 else 20 */
+} kfac_refresh_schedule;
+/* interval^(e) of `schedule` for epoch e >= 0; -1 for a bad argument. */
+KFAC_API int32_t kfac_refresh_interval(int32_t schedule, int32_t epoch);
+/* Refresh decision of iteration t in epoch e: 1 if t < fresh_floor
+ * (the paper's 500) or t mod interval == 0, else 0, where interval
+ * is `interval` if > 0, else kfac_refresh_interval(schedule, epoch); -1 for a
+ * bad argument (t < 0, unknown schedule).                                    */
+KFAC_API int32_t kfac_refresh(int64_t t, int32_t epoch, int32_t schedule, int64_t fresh_floor, int32_t interval);
+
 /* ------------------------------------------------------------------ comm
  * NCCL communicator over NVLink/NVSwitch (one process per GPU).  Rank 0 calls
  * kfac_comm_unique_id and broadcasts the 128 host bytes (e.g. with
@@ -205,6 +241,20 @@ KFAC_API kfac_status kfac_reduce_scatter_factors(kfac_comm_t comm, kfac_plan_t p
  * owned layer.  Errors: KFAC_ERR_ARG (gamma <= 0, NULL), KFAC_ERR_STATE.    */
 KFAC_API kfac_status kfac_damped_inverse(kfac_plan_t plan, int32_t rank, const float *rs_recv, float gamma, float *inv_ws,
                                 int32_t *dev_status, float *pi_out, void *ws, void *stream);
+
+/* Change rate of the Kronecker factors between two refreshes:
+ * for the k-th layer owned by `rank` (kfac_plan_rank_layers order),
+ *   diff[2k + 0] = ||A_cur - A_prev||_F / ||A_prev||_F,  diff[2k + 1] likewise for G,
+ * Frobenius norms of the full symmetric matrices, computed in fp64 from the
+ * packed segments of two recv chunks of the FULL plan (recv_cur = this
+ * refresh's ReduceScatter output, recv_prev = the previous refresh's, kept by
+ * the caller).  NaN where ||X_prev||_F = 0 ("recorded as missing").
+ * diff: device fp64 [2 * n_owned].  ws: >= ws_bytes of the plan (block
+ * partials).  Two launches, HBM-bound (reads both chunks' factor segments
+ * once).  Errors: KFAC_ERR_ARG (NULL, a misaligned chunk), KFAC_ERR_STATE
+ * (stale plan, rank out of range).                                          */
+KFAC_API kfac_status kfac_factor_diff(kfac_plan_t plan, int32_t rank, const float *recv_cur, const float *recv_prev,
+                             double *diff, void *ws, void *stream);
 
 /* ------------------------------------------------------------------ stage 5
  * For every layer owned by `rank`: P = G_d^-1 * dW * A_d^-1, dW

@@ -47,6 +47,22 @@ static kfac_status one_factor(const kfac_layer_desc *layer, const void *src, kfa
     return factor_launch(fl, jobs, S(stream));
 }
 
+// Stale plan: no factor kernel; the dW segment of each redundant owner copy is
+// refreshed from the primary copy, as kfac_factor_all does on a full step.
+static kfac_status replicate_dw(kfac_plan *p, float *rs_send, void *stream) {
+    std::vector<std::pair<const float *, float *>> sd;
+    std::vector<int64_t> cnt;
+    for (int r = 0; r < p->world; r++)
+        for (size_t k = 0; k < p->owned[r].size(); k++) {
+            const int l = p->owned[r][k];
+            if (p->owner[l] == r) continue;
+            sd.push_back({rs_send + p->seg_off[3 * l], rs_send + (int64_t)r * p->rs_chunk + p->local[r][k][0]});
+            cnt.push_back((int64_t)p->geoms[l].dG * p->geoms[l].dA);
+        }
+    if (!sd.empty()) return replicate_launch(sd, cnt, S(stream));
+    return KFAC_OK;
+}
+
 extern "C" {
 
 kfac_status kfac_factor_A(const kfac_layer_desc *layer, const void *x, kfac_dtype dt, int32_t n, float alpha,
@@ -76,6 +92,7 @@ kfac_status kfac_factor_ws_bytes(const kfac_layer_desc *layer, int32_t n, int32_
 
 kfac_status kfac_factor_all(kfac_plan_t p, const void *const *xs, const void *const *gys, kfac_dtype dt,
                             const float *alphaA, const float *alphaG, float *rs_send, void *ws, void *stream) {
+    if (p && p->stale && rs_send) return replicate_dw(p, rs_send, stream);
     if (!p || !xs || !gys || !rs_send) return set_error(KFAC_ERR_ARG, "kfac_factor_all: NULL argument");
     if (dt != KFAC_BF16 && dt != KFAC_FP16) return set_error(KFAC_ERR_ARG, "kfac_factor_all: dtype");
     if (p->factor_ws > 0 && !ws) return set_error(KFAC_ERR_ARG, "kfac_factor_all: workspace required");
@@ -143,6 +160,29 @@ kfac_status kfac_factor_all(kfac_plan_t p, const void *const *xs, const void *co
     return KFAC_OK;
 }
 
+// ------------------------------------------------------------------ stale Fisher (NEXT-1)
+kfac_status kfac_factor_diff(kfac_plan_t p, int32_t rank, const float *recv_cur, const float *recv_prev, double *diff,
+                             void *ws, void *stream) {
+    if (!p || !recv_cur || !recv_prev || !diff || !ws) return set_error(KFAC_ERR_ARG, "kfac_factor_diff: NULL argument");
+    if (p->stale) return set_error(KFAC_ERR_STATE, "kfac_factor_diff: a stale plan carries no factors");
+    if (rank < 0 || rank >= p->world) return set_error(KFAC_ERR_STATE, "kfac_factor_diff: rank out of range");
+    const auto &ow = p->owned[rank];
+    std::vector<DiffMat> mats;
+    for (size_t k = 0; k < ow.size(); k++) {
+        const Geom &g = p->geoms[ow[k]];
+        for (int which = 0; which < 2; which++) {
+            DiffMat m{};
+            m.n = which == 0 ? g.dA : g.dG;
+            m.cur = recv_cur + p->local[rank][k][1 + which];
+            m.prev = recv_prev + p->local[rank][k][1 + which];
+            m.out = diff + 2 * k + which;
+            mats.push_back(m);
+        }
+    }
+    if (mats.empty()) return KFAC_OK;
+    return diff_launch(mats, static_cast<double *>(ws), p->ws_bytes, S(stream));
+}
+
 // ------------------------------------------------------------------ comm
 kfac_status kfac_comm_unique_id(uint8_t id[128]) {
     if (!id) return set_error(KFAC_ERR_ARG, "kfac_comm_unique_id: NULL");
@@ -194,6 +234,7 @@ kfac_status kfac_reduce_scatter_factors(kfac_comm_t c, kfac_plan_t p, const floa
 kfac_status kfac_damped_inverse(kfac_plan_t p, int32_t rank, const float *recv, float gamma, float *inv_ws,
                                 int32_t *dev_status, float *pi_out, void *ws, void *stream) {
     if (!p || !recv || !inv_ws || !dev_status || !ws) return set_error(KFAC_ERR_ARG, "kfac_damped_inverse: NULL argument");
+    if (p->stale) return set_error(KFAC_ERR_STATE, "kfac_damped_inverse: a stale plan carries no factors (reuse the cached inverses)");
     if (!(gamma > 0.f)) return set_error(KFAC_ERR_ARG, "kfac_damped_inverse: gamma must be > 0");
     if (rank < 0 || rank >= p->world) return set_error(KFAC_ERR_STATE, "kfac_damped_inverse: rank out of range");
     const auto &ow = p->owned[rank];

@@ -109,6 +109,12 @@ struct PrecJob {
 kfac_status inverse_launch(const std::vector<InvMat> &mats, int npairs, float gamma, double *pair_scratch,
                            float *pi_out, cudaStream_t st);
 kfac_status precond_launch(const std::vector<PrecJob> &jobs, cudaStream_t st);
+struct DiffMat {          // one packed factor of the stale-Fisher change rate (diff.cu)
+    const float *cur, *prev;  // packed upper, 16-byte aligned
+    double *out;
+    int32_t n;
+};
+kfac_status diff_launch(const std::vector<DiffMat> &mats, double *ws, int64_t ws_bytes, cudaStream_t st);
 int64_t precond_ws_floats(int dG, int dA);  // split operands of one layer's two products
 kfac_status replicate_launch(const std::vector<std::pair<const float *, float *>> &src_dst,
                              const std::vector<int64_t> &counts, cudaStream_t st);

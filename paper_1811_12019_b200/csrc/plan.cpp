@@ -112,6 +112,11 @@ kfac_status plan_build(kfac_plan *p) {
             std::array<int64_t, 3> o;
             o[0] = off;
             off = align16(off + (int64_t)g.dG * g.dA);
+            if (p->stale) {  // stale step: the owner reuses its cached inverses, only dW travels
+                o[1] = o[2] = -1;
+                p->local[r].push_back(o);
+                continue;
+            }
             o[1] = off;
             off = align16(off + packed_len(g.dA));
             o[2] = off;
@@ -126,7 +131,8 @@ kfac_status plan_build(kfac_plan *p) {
         const int r = p->owner[l];
         const auto &ow = p->owned[r];
         const size_t k = std::find(ow.begin(), ow.end(), l) - ow.begin();
-        for (int s = 0; s < 3; s++) p->seg_off[3 * l + s] = (int64_t)r * p->rs_chunk + p->local[r][k][s];
+        for (int s = 0; s < 3; s++)
+            p->seg_off[3 * l + s] = p->local[r][k][s] < 0 ? -1 : (int64_t)r * p->rs_chunk + p->local[r][k][s];
     }
     // AG layout (primary copies only)
     std::vector<int64_t> agl(L, 0);
@@ -218,6 +224,40 @@ kfac_status kfac_plan_create(const kfac_layer_desc *layers, int32_t L, int32_t w
     }
     *out = p;
     return KFAC_OK;
+}
+
+kfac_status kfac_plan_create_stale(kfac_plan_t full, kfac_plan_t *out) {
+    if (!full || !out) return set_error(KFAC_ERR_ARG, "kfac_plan_create_stale: NULL argument");
+    if (full->stale) return set_error(KFAC_ERR_STATE, "kfac_plan_create_stale: plan is already a stale plan");
+    kfac_plan *p = new kfac_plan();
+    p->layers = full->layers;
+    p->L = full->L;
+    p->world = full->world;
+    p->n_local = full->n_local;
+    p->policy = full->policy;
+    p->stale = true;
+    kfac_status s = plan_build(p);
+    if (s) {
+        delete p;
+        return s;
+    }
+    *out = p;
+    return KFAC_OK;
+}
+
+int32_t kfac_plan_is_stale(kfac_plan_t p) { return p && p->stale ? 1 : 0; }
+
+int32_t kfac_refresh_interval(int32_t schedule, int32_t epoch) {
+    if (epoch < 0) return -1;
+    if (schedule == KFAC_REFRESH_RAMPUP) return std::min(20, 5 * (epoch / 5) + 1);
+    if (schedule == KFAC_REFRESH_STEP13) return epoch < 13 ? 1 : 20;
+    return -1;
+}
+
+int32_t kfac_refresh(int64_t t, int32_t epoch, int32_t schedule, int64_t fresh_floor, int32_t interval) {
+    const int32_t iv = interval > 0 ? interval : kfac_refresh_interval(schedule, epoch);
+    if (iv < 1 || t < 0) return -1;
+    return (t < fresh_floor || t % iv == 0) ? 1 : 0;
 }
 
 kfac_status kfac_plan_query(kfac_plan_t p, int32_t *owner, int64_t *seg_off, int64_t *rs_chunk, int64_t *ag_off,

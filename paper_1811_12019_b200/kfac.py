@@ -80,11 +80,18 @@ _reduce_scatter = _sig("kfac_reduce_scatter_factors", [_P, _P, _P, _P, _P])
 _damped_inverse = _sig("kfac_damped_inverse", [_P, _i32, _P, _f32, _P, _P, _P, _P, _P])
 _precondition = _sig("kfac_precondition", [_P, _i32, _P, _P, _P, _P, _P])
 _allgather = _sig("kfac_allgather_precond", [_P, _P, _P, _P])
+_plan_create_stale = _sig("kfac_plan_create_stale", [_P, ctypes.POINTER(_P)])
+_plan_is_stale = _sig("kfac_plan_is_stale", [_P])
+_refresh_interval = _sig("kfac_refresh_interval", [_i32, _i32])
+_refresh = _sig("kfac_refresh", [_i64, _i32, _i32, _i64, _i32])
+_factor_diff = _sig("kfac_factor_diff", [_P, _i32, _P, _P, _P, _P, _P])
+RAMPUP, STEP13 = 0, 1
 
 EXPORTS = ["kfac_last_error", "kfac_version", "kfac_launch_count", "kfac_plan_create", "kfac_plan_query", "kfac_plan_rank_layers",
            "kfac_plan_destroy", "kfac_comm_unique_id", "kfac_comm_create", "kfac_comm_destroy", "kfac_factor_A",
            "kfac_factor_G", "kfac_factor_ws_bytes", "kfac_factor_all", "kfac_reduce_scatter_factors",
-           "kfac_damped_inverse", "kfac_precondition", "kfac_allgather_precond"]
+           "kfac_damped_inverse", "kfac_precondition", "kfac_allgather_precond", "kfac_plan_create_stale",
+           "kfac_plan_is_stale", "kfac_refresh_interval", "kfac_refresh", "kfac_factor_diff"]
 
 
 def _check(st, where):
@@ -123,13 +130,17 @@ def _stream(stream):
 class Plan:
     """kfac_plan_create / _query / _rank_layers / _destroy."""
 
-    def __init__(self, layers, world, n_local, policy=RR):
+    def __init__(self, layers, world, n_local, policy=RR, stale_of=None):
         self.layers = list(layers)
-        arr = (LayerDesc * len(layers))(*[layer_desc(l) for l in layers])
         h = _P()
-        _check(_plan_create(arr, len(layers), int(world), int(n_local), int(policy), ctypes.byref(h)),
-               "kfac_plan_create")
+        if stale_of is not None:  # kfac_plan_create_stale: the dW-only layout of `stale_of`
+            _check(_plan_create_stale(stale_of.h, ctypes.byref(h)), "kfac_plan_create_stale")
+        else:
+            arr = (LayerDesc * len(layers))(*[layer_desc(l) for l in layers])
+            _check(_plan_create(arr, len(layers), int(world), int(n_local), int(policy), ctypes.byref(h)),
+                   "kfac_plan_create")
         self.h = h
+        self.stale = bool(_plan_is_stale(h))
         self.world, self.n_local, self.L = int(world), int(n_local), len(layers)
         self._q = None
 
@@ -164,6 +175,22 @@ class Plan:
         k = n.value
         return dict(layers=list(layers[:k]), local_off=[list(loc[3 * i:3 * i + 3]) for i in range(k)],
                     inv_off=[list(inv[2 * i:2 * i + 2]) for i in range(k)], inv_floats=nf.value)
+
+
+    def stale_plan(self):
+        """kfac_plan_create_stale: the plan of the steps that reuse stale factors."""
+        return Plan(self.layers, self.world, self.n_local, stale_of=self)
+
+
+def refresh_interval(schedule, epoch):
+    return int(_refresh_interval(int(schedule), int(epoch)))
+
+
+def refresh(t, epoch, schedule=RAMPUP, fresh_floor=500, interval=0):
+    r = int(_refresh(int(t), int(epoch), int(schedule), int(fresh_floor), int(interval)))
+    if r < 0:
+        raise ValueError("kfac_refresh: bad argument (t < 0 or unknown schedule)")
+    return bool(r)
 
 
 # ------------------------------------------------------------------ comm
@@ -208,6 +235,10 @@ def factor_G(layer, gy, n, alpha, out, ws=None, stream=None):
 
 def factor_all(plan, xs, gys, rs_send, ws, alphaA=None, alphaG=None, stream=None):
     L = plan.L
+    if plan.stale:  # no factors on a stale step: only the redundant owners' dW copies
+        _check(_factor_all(plan.h, None, None, 0, None, None, _ptr(rs_send), _ptr(ws), _stream(stream)),
+               "kfac_factor_all")
+        return
     xa = (_P * L)(*[x.data_ptr() for x in xs])
     ga = (_P * L)(*[g.data_ptr() for g in gys])
     aA = (ctypes.c_float * L)(*alphaA) if alphaA is not None else None
@@ -234,3 +265,9 @@ def precondition(plan, rank, rs_recv, inv_ws, ag_buf, ws, stream=None):
 def allgather_precond(comm, plan, ag_buf, stream=None):
     _check(_allgather(comm.h if comm is not None else None, plan.h, _ptr(ag_buf), _stream(stream)),
            "kfac_allgather_precond")
+
+
+def factor_diff(plan, rank, recv_cur, recv_prev, diff, ws, stream=None):
+    """kfac_factor_diff: Diff of every owned A, G between two refreshes, fp64 [2 * n_owned]."""
+    _check(_factor_diff(plan.h, int(rank), _ptr(recv_cur), _ptr(recv_prev), _ptr(diff), _ptr(ws), _stream(stream)),
+           "kfac_factor_diff")

@@ -13,7 +13,15 @@ from . import kfac
 
 
 class KfacStep:
-    def __init__(self, layers, n_local, rank=0, world=1, policy=kfac.RR, comm=None, device=None):
+    """Caller-owned buffers of one rank + the six stages.
+
+    stale=True also prepares the steps that reuse stale factors (NEXT-1,
+    P:701-711; R-17): a stale plan (dW-only ReduceScatter layout) with its own
+    send/recv buffers, and a second recv chunk so that kfac_factor_diff can
+    compare the factors of two consecutive refreshes.
+    """
+
+    def __init__(self, layers, n_local, rank=0, world=1, policy=kfac.RR, comm=None, device=None, stale=False):
         self.layers = list(layers)
         self.rank, self.world, self.n_local = int(rank), int(world), int(n_local)
         self.comm = comm
@@ -31,6 +39,15 @@ class KfacStep:
         n_owned = len(self.rl["layers"])
         self.dev_status = torch.zeros(max(2 * n_owned, 1), dtype=torch.int32, device=dev)
         self.pi = torch.zeros(max(n_owned, 1), dtype=torch.float32, device=dev)
+        self.splan = None
+        if stale:
+            self.splan = self.plan.stale_plan()
+            self.sq = self.splan.query()
+            self.s_send = torch.zeros(world * self.sq["rs_chunk"], dtype=torch.float32, device=dev)
+            self.s_recv = torch.zeros(self.sq["rs_chunk"], dtype=torch.float32, device=dev)
+            self.rs_recv_prev = torch.zeros_like(self.rs_recv)  # the previous refresh's factors
+            self.diff = torch.full((max(2 * n_owned, 1),), float("nan"), dtype=torch.float64, device=dev)
+            self.refreshes = 0
 
     # ---- views (zero-copy: the caller's dW lives in the send buffer)
     def dims(self, l):
@@ -45,6 +62,15 @@ class KfacStep:
     def set_dw(self, dws):
         for l, d in enumerate(dws):
             self.dw_view(l).copy_(d, non_blocking=True)
+
+    def stale_dw_view(self, l):
+        da, dg = self.dims(l)
+        o = self.sq["seg_off"][l][0]
+        return self.s_send[o:o + dg * da].view(dg, da)
+
+    def set_stale_dw(self, dws):
+        for l, d in enumerate(dws):
+            self.stale_dw_view(l).copy_(d, non_blocking=True)
 
     def send_factor_view(self, l, which):
         da, dg = self.dims(l)
@@ -87,6 +113,30 @@ class KfacStep:
 
     def allgather(self, stream=None):
         kfac.allgather_precond(self.comm, self.plan, self.ag_buf, stream)
+
+    def run_stale(self, stream=None, events=None):
+        """A step with stale factors (R-17): dW (set_stale_dw) -> ReduceScatter of the dW-only layout ->
+        precondition with the inverses cached by the last full step -> AllGather.  No factor, no inverse."""
+        stages = (lambda: kfac.factor_all(self.splan, None, None, self.s_send, self.ws, stream=stream),
+                  lambda: kfac.reduce_scatter_factors(self.comm, self.splan, self.s_send, self.s_recv, stream),
+                  lambda: None,
+                  lambda: kfac.precondition(self.splan, self.rank, self.s_recv, self.inv_ws, self.ag_buf, self.ws,
+                                            stream),
+                  lambda: self.allgather(stream))
+        for i, f in enumerate(stages):
+            f()
+            if events is not None:
+                events[i].record(stream)
+
+    def run_refresh(self, xs, gys, gamma, stream=None, events=None):
+        """A full step that also measures Diff against the previous refresh: the recv chunks
+        ping-pong, and self.diff[2k + {0, 1}] receives the A / G change rate of the k-th owned layer
+        (NaN before the second refresh)."""
+        self.rs_recv, self.rs_recv_prev = self.rs_recv_prev, self.rs_recv
+        self.run(xs, gys, gamma, stream, events)
+        self.refreshes += 1
+        if self.refreshes >= 2:
+            kfac.factor_diff(self.plan, self.rank, self.rs_recv, self.rs_recv_prev, self.diff, self.ws, stream)
 
     def run(self, xs, gys, gamma, stream=None, events=None):
         """Stages 1-6.  `events`: optional list of 6 torch.cuda.Event recorded after each stage."""

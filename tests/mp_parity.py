@@ -7,7 +7,9 @@ ReduceScatter / AllGather over NVLink); rank 0 then checks, against the fp64
 oracle simulating the same P ranks (oracle.kfac_step):
   * the reduced factors each owner received (stage 3),
   * every layer's preconditioned gradient in the gathered buffer (stage 6),
-  * that the AllGather buffers of all ranks are bitwise identical (replica consistency).
+  * that the AllGather buffers of all ranks are bitwise identical (replica consistency);
+then a stale-factor step (NEXT-1, R-17: new dW, dW-only ReduceScatter, the
+cached inverses) against oracle.stale_results, replicas again identical.
 Exit code 0 on success.
 """
 import os
@@ -58,7 +60,7 @@ def main():
     comm = K.Comm(bytes(uid.cpu().numpy().tobytes()), rank, world, local)
     layers, n = NETS[cfg]()
     gamma = 2.5e-2
-    st = K.KfacStep(layers, n, rank=rank, world=world, policy=policy, comm=comm, device=dev)
+    st = K.KfacStep(layers, n, rank=rank, world=world, policy=policy, comm=comm, device=dev, stale=True)
     xs = [inputs.layer_x(l, i, n, rank) for i, l in enumerate(layers)]
     gys = [inputs.layer_gy(l, i, n, rank) for i, l in enumerate(layers)]
     dws = [inputs.layer_dw(l, i, rank) for i, l in enumerate(layers)]
@@ -103,6 +105,32 @@ def main():
         print(f"mp_parity {cfg} P={world} policy={policy}: stage3 err {stage3:.2e}, end-to-end max err {err:.2e}, "
               f"replicas identical {ok}", flush=True)
         ok &= err <= 2e-3
+    # ---- a stale step: new dW, cached inverses
+    dws2 = [inputs.layer_dw(l, i, rank, seed=4242) for i, l in enumerate(layers)]
+    st.set_stale_dw([d.to(dev) for d in dws2])
+    st.run_stale()
+    torch.cuda.synchronize()
+    bufs = [torch.empty_like(st.ag_buf) for _ in range(world)]
+    dist.all_gather(bufs, st.ag_buf)
+    all_dw2 = [None] * world
+    dist.all_gather_object(all_dw2, [d.numpy() for d in dws2])
+    if rank == 0:
+        import oracle
+        for b in bufs[1:]:
+            ok &= torch.equal(b, bufs[0])
+        sp = oracle.plan(layers, world, policy, stale=True)
+        srecvs = oracle.reduce_scatter([oracle.build_send(layers, sp, r, None, all_dw2[r]) for r in range(world)], sp)
+        g = bufs[0].cpu().double().numpy()
+        serr = 0.0
+        for l in range(len(layers)):
+            da, dg = shapes.dims(layers[l])
+            owner = pl["owner"][l]
+            cached = {m: (v["Ainv"], v["Ginv"]) for m, v in ref["results"][owner].items()}
+            want = oracle.stale_results(layers, sp, owner, srecvs[owner], cached)[l]["precond"]
+            serr = max(serr, relerr(g[pl["ag_off"][l]:pl["ag_off"][l] + dg * da], want.reshape(-1)))
+        print(f"mp_parity {cfg} P={world} stale step: end-to-end max err {serr:.2e}, replicas identical {ok}",
+              flush=True)
+        ok &= serr <= 2e-3
     flag = torch.tensor([1 if ok else 0], device=dev)
     dist.broadcast(flag, 0)
     dist.barrier(device_ids=[local])

@@ -86,3 +86,42 @@ def test_factor_ws_bytes_split_k(K):
     L = shapes.resnet50()
     assert K.factor_ws_bytes(L[1], 32, 0) > 0  # l1b0c1: dA=64, 100k rows
     assert K.factor_ws_bytes(L[-1], 32, 0) == 256  # fc: 32 rows -> no partials, only the work-item counter
+
+
+@pytest.mark.parametrize("cfg", ["single_conv", "resnet50", "stress"])
+@pytest.mark.parametrize("P", [1, 2, 5, 8])
+@pytest.mark.parametrize("policy", [0, 1])
+def test_stale_plan_bit_exact_vs_oracle(K, orc, cfg, P, policy):
+    """kfac_plan_create_stale: dW-only layout, bit-exact against oracle.plan(stale=True) (R-17)."""
+    L, n = shapes.config(cfg)
+    full = K.Plan(L, P, n, policy)
+    st = full.stale_plan()
+    assert st.stale and not full.stale
+    q, qf = st.query(), full.query()
+    ref = orc.plan(L, P, policy, stale=True)
+    assert q["owner"] == ref["owner"].tolist() == qf["owner"]
+    assert q["rs_chunk"] == ref["rs_chunk"] < qf["rs_chunk"]
+    assert np.array_equal(np.array(q["seg_off"]), ref["seg_off"])
+    assert q["ag_off"] == qf["ag_off"] and q["ag_chunk"] == qf["ag_chunk"] and q["ws_bytes"] == qf["ws_bytes"]
+    for r in range(P):
+        rl, rf = st.rank_layers(r), full.rank_layers(r)
+        assert rl["layers"] == rf["layers"] == ref["owned"][r]
+        assert rl["inv_off"] == rf["inv_off"] and rl["inv_floats"] == rf["inv_floats"]
+        assert [tuple(-1 if v is None else v for v in ref["local"][r][l]) for l in ref["owned"][r]] == \
+            [tuple(o) for o in rl["local_off"]]
+    with pytest.raises(K.KfacError, match="ERR_STATE"):
+        K.Plan(L, P, n, stale_of=st)
+
+
+def test_refresh_controller_vs_oracle(K, orc):
+    """kfac_refresh_interval / kfac_refresh against the oracle's schedules (pinned to P:705-711)."""
+    for sched, name in ((K.RAMPUP, "rampup"), (K.STEP13, "step13")):
+        for e in range(0, 60):
+            assert K.refresh_interval(sched, e) == orc.refresh_interval(e, name)
+            for t in (0, 3, 499, 500, 501, 520, 1000, 1001, 1234):
+                for floor in (0, 50, 500):
+                    assert K.refresh(t, e, sched, floor) == orc.refresh(t, e, name, floor)
+    assert K.refresh(30, 40, K.RAMPUP, 0, interval=3) == orc.refresh(30, 40, fresh_floor=0, interval=3)
+    assert K.refresh_interval(9, 0) == -1 and K.refresh_interval(0, -1) == -1
+    with pytest.raises(ValueError):
+        K.refresh(-1, 0)
