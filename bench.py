@@ -207,7 +207,8 @@ def run_ours(args):
 
     layers, n = shapes.config(args.config)
     policy = K.LPT if args.policy == "lpt" else K.RR
-    st = K.KfacStep(layers, n, rank=rank, world=world, policy=policy, comm=comm, device=dev)
+    st = K.KfacStep(layers, n, rank=rank, world=world, policy=policy, comm=comm, device=dev,
+                    stale=not args.no_stale)
     # synthetic inputs of this rank (global-sample seeded), pinned host copies for the e2e leg
     t0 = time.time()
     xs_h = [inputs.layer_x(l, i, n, rank, args.seed).pin_memory() for i, l in enumerate(layers)]
@@ -261,6 +262,50 @@ def run_ours(args):
     tot = mine.cpu().tolist()
     ms = tot[0] / args.steps
     st_ms = {nm: tot[1 + i] / args.steps for i, nm in enumerate(names)}
+
+    # ---- stale-Fisher steps (NEXT-1; R-20): dW-only ReduceScatter, cached inverses, no factor
+    # or inverse work; and the Diff kernel a refresh step adds.  Same timing rules.
+    stale = None
+    if not args.no_stale:
+        st.set_stale_dw([d.to(dev) for d in dws_h])
+        st.rs_recv_prev.copy_(st.rs_recv).mul_(0.5)
+        for _ in range(args.warmup):
+            st.run_stale(stream)
+            K.factor_diff(st.plan, rank, st.rs_recv, st.rs_recv_prev, st.diff, st.ws, stream)
+        sev = [[torch.cuda.Event(enable_timing=True) for _ in range(nst + 1)] for _ in range(args.steps)]
+        dev_ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
+        barrier()
+        for s in range(args.steps):
+            if flush.numel():
+                flush.fill_(s & 0xFF)
+            sev[s][0].record(stream)
+            st.run_stale(stream, events=sev[s][1:])
+        for s in range(args.steps):
+            dev_ev[s][0].record(stream)
+            K.factor_diff(st.plan, rank, st.rs_recv, st.rs_recv_prev, st.diff, st.ws, stream)
+            dev_ev[s][1].record(stream)
+        barrier()
+        sm = torch.tensor([sum(e[0].elapsed_time(e[nst]) for e in sev)] +
+                          [sum(e[i].elapsed_time(e[i + 1]) for e in sev) for i in range(nst)] +
+                          [sum(e[0].elapsed_time(e[1]) for e in dev_ev)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(sm, op=dist.ReduceOp.MAX)
+        sm = (sm / args.steps).cpu().tolist()
+        diff_bytes = 0
+        for li in st.rl["layers"]:
+            da, dg = shapes.dims(layers[li])
+            diff_bytes += 8 * (da * (da + 1) // 2 + dg * (dg + 1) // 2)  # both chunks' packed factors, 4 B each
+        dgbs = diff_bytes / (sm[-1] / 1e3) / 1e9
+        hbm = peaks()["hbm_gbs"]
+        iv = K.refresh_interval(K.RAMPUP, 44)  # the schedule's steady-state interval (20)
+        stale = {"step_ms": round(sm[0], 3), "stage_ms": {k: round(sm[1 + i], 3) for i, k in enumerate(names)},
+                 "rs_bytes_per_rank": st.sq["rs_chunk"] * 4, "full_rs_bytes_per_rank": st.q["rs_chunk"] * 4,
+                 "refresh_interval": iv, "amortized_ms": round((ms + (iv - 1) * sm[0]) / iv, 3),
+                 "diff_ms": round(sm[-1], 4),
+                 "diff_roofline": {"bound": "hbm", "achieved": round(dgbs, 1), "peak": hbm, "unit": "GB/s",
+                                   "frac": round(dgbs / hbm, 4), "traffic": None,
+                                   "kernel": "diff_partial_kernel + diff_final_kernel",
+                                   "bytes_counting": "8 B per owned packed factor element (cur + prev fp32)"}}
 
     # ---- end-to-end through the public API with host buffers (H2D inputs, D2H result).  Every
     # step's inputs are copied from pinned host memory and its result read back inside the timed
@@ -400,6 +445,7 @@ def run_ours(args):
             "roofline_factors": fac_roof,
             "roofline_stages": roofs,
             "e2e": e2e,
+            "stale": stale,
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "timed_wall_s": round(wall_s, 3),
@@ -427,6 +473,7 @@ def main():
     ap.add_argument("--seed", type=int, default=1811)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-stale", action="store_true", help="skip the stale-Fisher step timing (NEXT-1)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

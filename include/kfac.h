@@ -144,7 +144,7 @@ KFAC_API void kfac_plan_destroy(kfac_plan_t plan);
 /* ------------------------------------------------------------------ stale Fisher (NEXT-1)
  * The paper refreshes (A, G) only every interval^(e) iterations after the
  * first 500 and reuses the previous preconditioner in
- * between (reading R-17: the owner keeps its cached A_d^-1, G_d^-1 in inv_ws).
+ * between (reading R-20: the owner keeps its cached A_d^-1, G_d^-1 in inv_ws).
  *
  * kfac_plan_create_stale: a plan for the steps that reuse stale factors.  It
  * has the same owners, owned lists, AllGather layout, inverse layout

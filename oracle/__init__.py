@@ -20,7 +20,9 @@ parts of the method in plain Python:
 * ``kfac_step``        Algorithm 1's body minus fwd/bwd/update.
 * ``refresh_interval`` / ``refresh`` / ``fim_diff`` / ``diff_percentiles`` /
   ``stale_results`` and ``plan(stale=True)``: stale Fisher information
-  (NEXT-1; reading R-17).
+  (NEXT-1; reading R-20).
+* ``learning_rate`` / ``momentum`` / ``apply_update`` / ``rescale_weights`` /
+  ``update_layer``: the update after the AllGather (NEXT-3; R-21).
 
 Parity status: every function here is pinned by tests/test_oracle_*.py (see
 DESIGN.md §Oracle pins); none is "parity unpinned".
@@ -291,7 +293,7 @@ def plan(layers, world, policy=POLICY_RR, stale=False):
     its primary layers' 𝒢 (dG·dA) ascending, aligned; ag_chunk = max.
 
     stale=True: the wire layout of a step that reuses stale factors (P:701-704,
-    "reduce the frequency of updating (A, G, F)"; reading R-17): the same
+    "reduce the frequency of updating (A, G, F)"; reading R-20): the same
     owners, but each owned layer carries only its ∇W segment; the A and G
     offsets are None (seg_off -1).  The AG layout is unchanged.
     """
@@ -501,7 +503,7 @@ def diff_percentiles(diffs, qs=(5, 25, 50, 75, 95)):
 def stale_results(layers, pl_stale, rank, recv, cached):
     """Stage 5 of a stale step on one rank: 𝒢 = G_d⁻¹ ∇W A_d⁻¹ with the cached
     inverses of the last refresh (`cached[l] = (Ainv, Ginv)`), ∇W from the
-    stale-layout recv chunk (R-17)."""
+    stale-layout recv chunk (R-20)."""
     out = {}
     for l, (o_w, _, _) in pl_stale["local"][rank].items():
         a, g = dims(layers[l])
@@ -509,3 +511,54 @@ def stale_results(layers, pl_stale, rank, recv, cached):
         Ainv, Ginv = cached[l]
         out[l] = dict(dW=dW, precond=precondition(Ginv, Ainv, dW))
     return out
+
+
+# --------------------------------------------------------------------------
+# NEXT-3: the update after the AllGather
+# --------------------------------------------------------------------------
+def learning_rate(eta0, e_start, e_end, p_decay, epoch):
+    """η⁽ᵉ⁾ = η⁽⁰⁾·(1 − (e − e_start)/(e_end − e_start))^p_decay, clamped to η⁽⁰⁾
+    before e_start and to 0 after e_end."""
+    e = float(epoch)
+    if e <= e_start:
+        return float(eta0)
+    if e >= e_end:
+        return 0.0
+    return float(eta0) * (1.0 - (e - e_start) / (e_end - e_start)) ** p_decay
+
+
+def momentum(m0, eta0, eta_e):
+    """m⁽ᵉ⁾ = (m⁽⁰⁾/η⁽⁰⁾)·η⁽ᵉ⁾ (P:517-521)."""
+    return float(m0) / float(eta0) * float(eta_e)
+
+
+def apply_update(w, w_prev, precond, eta, m):
+    """Eq. paramupdate (P:522-530): w⁽ᵗ⁺¹⁾ = w⁽ᵗ⁾ − η·𝒢⁽ᵗ⁾ + m·(w⁽ᵗ⁾ − w⁽ᵗ⁻¹⁾), fp64.
+    Returns (w⁽ᵗ⁺¹⁾, w⁽ᵗ⁾) -- the new weights and the new 'previous' weights."""
+    w = np.asarray(w, dtype=np.float64)
+    w_prev = np.asarray(w_prev, dtype=np.float64)
+    precond = np.asarray(precond, dtype=np.float64)
+    if w.shape != w_prev.shape or w.shape != precond.shape:
+        raise ValueError("apply_update: shapes differ")
+    return w - eta * precond + m * (w - w_prev), w.copy()
+
+
+def rescale_weights(w, d_out, eps=1e-9):
+    """Normalizing Weights: w ← √(2·d_out)·w/(‖w‖ + ε), ‖·‖ the Frobenius norm of the
+    layer's weight tensor."""
+    if int(d_out) < 1:
+        raise ValueError("d_out >= 1")
+    w = np.asarray(w, dtype=np.float64)
+    return math.sqrt(2.0 * int(d_out)) * w / (math.sqrt(float(np.sum(w * w))) + eps)
+
+
+def update_layer(w, w_prev, precond, eta, m, has_bias, rescale=True, eps=1e-9):
+    """The whole post-AllGather update of one layer (reading R-21): Eq. paramupdate on the
+    [d_out, dA] matrix [W | b] (𝒢 carries the bias column last, R-5), then Normalizing Weights on
+    W only (the bias column is not rescaled), d_out = the layer's output channels."""
+    w_new, w_keep = apply_update(w, w_prev, precond, eta, m)
+    if rescale:
+        nb = w_new.shape[1] - (1 if has_bias else 0)
+        w_new = w_new.copy()
+        w_new[:, :nb] = rescale_weights(w_new[:, :nb], w_new.shape[0], eps)
+    return w_new, w_keep

@@ -16,7 +16,7 @@ class KfacStep:
     """Caller-owned buffers of one rank + the six stages.
 
     stale=True also prepares the steps that reuse stale factors (NEXT-1,
-    P:701-711; R-17): a stale plan (dW-only ReduceScatter layout) with its own
+    P:701-711; R-20): a stale plan (dW-only ReduceScatter layout) with its own
     send/recv buffers, and a second recv chunk so that kfac_factor_diff can
     compare the factors of two consecutive refreshes.
     """
@@ -115,7 +115,7 @@ class KfacStep:
         kfac.allgather_precond(self.comm, self.plan, self.ag_buf, stream)
 
     def run_stale(self, stream=None, events=None):
-        """A step with stale factors (R-17): dW (set_stale_dw) -> ReduceScatter of the dW-only layout ->
+        """A step with stale factors (R-20): dW (set_stale_dw) -> ReduceScatter of the dW-only layout ->
         precondition with the inverses cached by the last full step -> AllGather.  No factor, no inverse."""
         stages = (lambda: kfac.factor_all(self.splan, None, None, self.s_send, self.ws, stream=stream),
                   lambda: kfac.reduce_scatter_factors(self.comm, self.splan, self.s_send, self.s_recv, stream),

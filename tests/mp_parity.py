@@ -8,7 +8,7 @@ oracle simulating the same P ranks (oracle.kfac_step):
   * the reduced factors each owner received (stage 3),
   * every layer's preconditioned gradient in the gathered buffer (stage 6),
   * that the AllGather buffers of all ranks are bitwise identical (replica consistency);
-then a stale-factor step (NEXT-1, R-17: new dW, dW-only ReduceScatter, the
+then a stale-factor step (NEXT-1, R-20: new dW, dW-only ReduceScatter, the
 cached inverses) against oracle.stale_results, replicas again identical.
 Exit code 0 on success.
 """

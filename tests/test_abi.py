@@ -92,7 +92,7 @@ def test_factor_ws_bytes_split_k(K):
 @pytest.mark.parametrize("P", [1, 2, 5, 8])
 @pytest.mark.parametrize("policy", [0, 1])
 def test_stale_plan_bit_exact_vs_oracle(K, orc, cfg, P, policy):
-    """kfac_plan_create_stale: dW-only layout, bit-exact against oracle.plan(stale=True) (R-17)."""
+    """kfac_plan_create_stale: dW-only layout, bit-exact against oracle.plan(stale=True) (R-20)."""
     L, n = shapes.config(cfg)
     full = K.Plan(L, P, n, policy)
     st = full.stale_plan()

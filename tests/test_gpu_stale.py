@@ -5,7 +5,7 @@
   oracle factors (the factor tolerance 2e-3), the degenerate cases (equal
   factors -> 0 exactly, a zero previous factor -> NaN) and the full
   ResNet-50 layout.
-* a stale step (dW-only ReduceScatter, cached inverses, R-17) against
+* a stale step (dW-only ReduceScatter, cached inverses, R-20) against
   oracle.stale_results, world 1 (world 2/4 in tests/mp_parity.py).
 """
 import numpy as np
