@@ -307,6 +307,35 @@ def run_ours(args):
                                    "kernel": "diff_partial_kernel + diff_final_kernel",
                                    "bytes_counting": "8 B per owned packed factor element (cur + prev fp32)"}}
 
+    # ---- the update after the AllGather (NEXT-3): Eq. paramupdate + Normalizing Weights on
+    # every layer's weights (replicated on every rank), timed over K launches like the rest.
+    upd = None
+    if not args.no_stale:
+        gw = torch.Generator(device=dev).manual_seed(args.seed)
+        w_l = [torch.randn(shapes.dims(l)[1] * shapes.dims(l)[0], generator=gw, device=dev) * 0.05 for l in layers]
+        wp_l = [w + 0.01 for w in w_l]
+        for _ in range(args.warmup):
+            st.update(w_l, wp_l, 8.18e-3, 0.997, stream=stream)
+        uev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
+        barrier()
+        for s in range(args.steps):
+            uev[s][0].record(stream)
+            st.update(w_l, wp_l, 8.18e-3, 0.997, stream=stream)
+            uev[s][1].record(stream)
+        barrier()
+        um = torch.tensor([sum(e[0].elapsed_time(e[1]) for e in uev) / args.steps], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(um, op=dist.ReduceOp.MAX)
+        nw = sum(w.numel() for w in w_l)
+        ugbs = 20 * nw / (um.item() / 1e3) / 1e9
+        hbm = peaks()["hbm_gbs"]
+        upd = {"ms": round(um.item(), 4), "weights": nw, "rescale": True,
+               "roofline": {"bound": "hbm", "achieved": round(ugbs, 1), "peak": hbm, "unit": "GB/s",
+                            "frac": round(ugbs / hbm, 4), "traffic": None,
+                            "kernel": "update_step_kernel + update_scale_kernel",
+                            "bytes_counting": "20 B per weight (w, w_prev, P read; w, w_prev written)"}}
+        del w_l, wp_l
+
     # ---- end-to-end through the public API with host buffers (H2D inputs, D2H result).  Every
     # step's inputs are copied from pinned host memory and its result read back inside the timed
     # region; the copies run on their own streams (H2D and D2H directions concurrently) and are
@@ -446,6 +475,7 @@ def run_ours(args):
             "roofline_stages": roofs,
             "e2e": e2e,
             "stale": stale,
+            "update": upd,
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "timed_wall_s": round(wall_s, 3),
@@ -473,7 +503,7 @@ def main():
     ap.add_argument("--seed", type=int, default=1811)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-stale", action="store_true", help="skip the stale-Fisher step timing (NEXT-1)")
+    ap.add_argument("--no-stale", action="store_true", help="skip the stale-Fisher step (NEXT-1) and update (NEXT-3) timings")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

@@ -269,6 +269,24 @@ KFAC_API kfac_status kfac_precondition(kfac_plan_t plan, int32_t rank, const flo
  * world == 1 (no-op).                                                        */
 KFAC_API kfac_status kfac_allgather_precond(kfac_comm_t comm, kfac_plan_t plan, float *ag_buf, void *stream);
 
+/* ------------------------------------------------------------------ NEXT-3: the update
+ * After the AllGather every rank applies, for every layer l (Eq. paramupdate):
+ *   w_l <- w_l - lr * P_l + momentum * (w_l - w_prev_l),   w_prev_l <- (old) w_l
+ * with P_l the preconditioned gradient at ag_off[l] in ag_buf, and then, if
+ * rescale != 0, Normalizing Weights on the weight columns:
+ *   W_l <- sqrt(2 dG) * W_l / (||W_l||_F + eps)     (the paper's eps = 1e-9)
+ * where W_l is w_l without its bias column (the last column when has_bias;
+ * reading R-21: the bias is updated but not rescaled).  w[l], w_prev[l]:
+ * host arrays of L device pointers to [dG, dA] row-major fp32 (the layout of
+ * dW, bias column last), updated in place; 16-byte alignment enables vector
+ * access.  lr / momentum are this epoch's eta^(e), m^(e).
+ * Arithmetic is fp32 per element, the norm is accumulated in fp64.
+ * ws: >= ws_bytes of the plan.  One or two launches, HBM-bound (20 B per
+ * weight).  Errors: KFAC_ERR_ARG (NULL, non-finite lr / momentum, eps < 0).   */
+KFAC_API kfac_status kfac_update(kfac_plan_t plan, const float *ag_buf, float *const *w /* host [L] */,
+                        float *const *w_prev /* host [L] */, float lr, float momentum, int32_t rescale, float eps,
+                        void *ws, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -4,6 +4,7 @@
 // in NCCL; nothing here computes on the host.
 #include <dlfcn.h>
 
+#include <cmath>
 #include <cstring>
 #include <string>
 
@@ -301,6 +302,28 @@ kfac_status kfac_precondition(kfac_plan_t p, int32_t rank, const float *recv, co
     }
     if (off * 4 > p->ws_bytes) return set_error(KFAC_ERR_STATE, "kfac_precondition: workspace layout exceeds ws_bytes");
     return precond_launch(jobs, S(stream));
+}
+
+// ------------------------------------------------------------------ NEXT-3: the update after stage 6
+kfac_status kfac_update(kfac_plan_t p, const float *ag_buf, float *const *w, float *const *w_prev, float lr,
+                        float momentum, int32_t rescale, float eps, void *ws, void *stream) {
+    if (!p || !ag_buf || !w || !w_prev || !ws) return set_error(KFAC_ERR_ARG, "kfac_update: NULL argument");
+    if (!(eps >= 0.f) || !std::isfinite(lr) || !std::isfinite(momentum))
+        return set_error(KFAC_ERR_ARG, "kfac_update: lr, momentum finite and eps >= 0");
+    std::vector<UpdJob> jobs;
+    for (int l = 0; l < p->L; l++) {
+        if (!w[l] || !w_prev[l]) return set_error(KFAC_ERR_ARG, "kfac_update: NULL layer pointer");
+        const Geom &g = p->geoms[l];
+        UpdJob u{};
+        u.w = w[l];
+        u.w_prev = w_prev[l];
+        u.g = ag_buf + p->ag_off[l];
+        u.dG = g.dG;
+        u.dA = g.dA;
+        u.bias = g.bias;
+        jobs.push_back(u);
+    }
+    return update_launch(jobs, lr, momentum, rescale ? 1 : 0, eps, static_cast<double *>(ws), p->ws_bytes, S(stream));
 }
 
 // ------------------------------------------------------------------ stage 6

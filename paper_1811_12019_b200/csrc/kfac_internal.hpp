@@ -114,6 +114,13 @@ struct DiffMat {          // one packed factor of the stale-Fisher change rate (
     double *out;
     int32_t n;
 };
+struct UpdJob {            // one layer of the post-AllGather update (update.cu)
+    float *w, *w_prev;        // [dG, dA] row-major fp32, caller-owned
+    const float *g;           // preconditioned gradient in the AllGather buffer
+    int32_t dG, dA, bias;
+};
+kfac_status update_launch(const std::vector<UpdJob> &jobs, float lr, float mom, int rescale, float eps, double *ws,
+                          int64_t ws_bytes, cudaStream_t st);
 kfac_status diff_launch(const std::vector<DiffMat> &mats, double *ws, int64_t ws_bytes, cudaStream_t st);
 int64_t precond_ws_floats(int dG, int dA);  // split operands of one layer's two products
 kfac_status replicate_launch(const std::vector<std::pair<const float *, float *>> &src_dst,

@@ -86,12 +86,13 @@ _refresh_interval = _sig("kfac_refresh_interval", [_i32, _i32])
 _refresh = _sig("kfac_refresh", [_i64, _i32, _i32, _i64, _i32])
 _factor_diff = _sig("kfac_factor_diff", [_P, _i32, _P, _P, _P, _P, _P])
 RAMPUP, STEP13 = 0, 1
+_update = _sig("kfac_update", [_P, _P, ctypes.POINTER(_P), ctypes.POINTER(_P), _f32, _f32, _i32, _f32, _P, _P])
 
 EXPORTS = ["kfac_last_error", "kfac_version", "kfac_launch_count", "kfac_plan_create", "kfac_plan_query", "kfac_plan_rank_layers",
            "kfac_plan_destroy", "kfac_comm_unique_id", "kfac_comm_create", "kfac_comm_destroy", "kfac_factor_A",
            "kfac_factor_G", "kfac_factor_ws_bytes", "kfac_factor_all", "kfac_reduce_scatter_factors",
            "kfac_damped_inverse", "kfac_precondition", "kfac_allgather_precond", "kfac_plan_create_stale",
-           "kfac_plan_is_stale", "kfac_refresh_interval", "kfac_refresh", "kfac_factor_diff"]
+           "kfac_plan_is_stale", "kfac_refresh_interval", "kfac_refresh", "kfac_factor_diff", "kfac_update"]
 
 
 def _check(st, where):
@@ -271,3 +272,12 @@ def factor_diff(plan, rank, recv_cur, recv_prev, diff, ws, stream=None):
     """kfac_factor_diff: Diff of every owned A, G between two refreshes, fp64 [2 * n_owned]."""
     _check(_factor_diff(plan.h, int(rank), _ptr(recv_cur), _ptr(recv_prev), _ptr(diff), _ptr(ws), _stream(stream)),
            "kfac_factor_diff")
+
+
+def update(plan, ag_buf, ws_, w_prev, lr, momentum, ws, rescale=True, eps=1e-9, stream=None):
+    """kfac_update: Eq. paramupdate + Normalizing Weights for every layer, in place."""
+    L = plan.L
+    wa = (_P * L)(*[_ptr(t).value for t in ws_])
+    pa = (_P * L)(*[_ptr(t).value for t in w_prev])
+    _check(_update(plan.h, _ptr(ag_buf), wa, pa, float(lr), float(momentum), 1 if rescale else 0, float(eps), _ptr(ws),
+                   _stream(stream)), "kfac_update")

@@ -138,6 +138,10 @@ class KfacStep:
         if self.refreshes >= 2:
             kfac.factor_diff(self.plan, self.rank, self.rs_recv, self.rs_recv_prev, self.diff, self.ws, stream)
 
+    def update(self, w, w_prev, lr, momentum, rescale=True, eps=1e-9, stream=None):
+        """NEXT-3: Eq. paramupdate + Normalizing Weights on every layer's [dG, dA] weights."""
+        kfac.update(self.plan, self.ag_buf, w, w_prev, lr, momentum, self.ws, rescale, eps, stream)
+
     def run(self, xs, gys, gamma, stream=None, events=None):
         """Stages 1-6.  `events`: optional list of 6 torch.cuda.Event recorded after each stage."""
         stages = (lambda: self.factors(xs, gys, stream=stream), lambda: self.reduce_scatter(stream),
