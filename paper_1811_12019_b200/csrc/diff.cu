@@ -20,7 +20,7 @@ namespace kfac {
 namespace {
 
 constexpr int kDiffThreads = 256;
-constexpr int64_t kDiffChunk = 16384;  // packed elements per range block (64 KB of each input)
+constexpr int64_t kDiffChunk = 32768;  // packed elements per range block (128 KB of each input)
 constexpr int kDiffMaxMats = 256;
 
 struct DiffParams {
@@ -55,8 +55,12 @@ __device__ __forceinline__ double2 block_sum2(double a, double b, double2 *sh) {
 __global__ void __launch_bounds__(kDiffThreads) diff_partial_kernel(const __grid_constant__ DiffParams P) {
     __shared__ double2 sh[kDiffThreads / 32];
     const int b = blockIdx.x;
-    int m = 0;
-    while (m + 1 < P.nmats && P.first[m + 1] <= b) m++;
+    int m = 0, hi_m = P.nmats - 1;  // binary search: the last matrix whose first block <= b
+    while (m < hi_m) {
+        const int mid = (m + hi_m + 1) >> 1;
+        if (P.first[mid] <= b) m = mid;
+        else hi_m = mid - 1;
+    }
     const float *cur = P.cur[m], *prev = P.prev[m];
     double num = 0.0, den = 0.0;
     const int nrange = P.first[m + 1] - P.first[m] - 1;
@@ -68,8 +72,9 @@ __global__ void __launch_bounds__(kDiffThreads) diff_partial_kernel(const __grid
         const int64_t nv = (hi - lo) / 4;
         const float4 *c4 = reinterpret_cast<const float4 *>(cur + lo);
         const float4 *p4 = reinterpret_cast<const float4 *>(prev + lo);
+#pragma unroll 4
         for (int64_t i = threadIdx.x; i < nv; i += kDiffThreads) {
-            const float4 c = __ldg(c4 + i), p = __ldg(p4 + i);
+            const float4 c = __ldcs(c4 + i), p = __ldcs(p4 + i);  // streamed once: evict-first
             const double d0 = (double)c.x - p.x, d1 = (double)c.y - p.y, d2 = (double)c.z - p.z,
                          d3 = (double)c.w - p.w;
             num += d0 * d0 + d1 * d1 + d2 * d2 + d3 * d3;

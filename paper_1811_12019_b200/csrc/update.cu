@@ -80,13 +80,15 @@ __global__ void __launch_bounds__(kUpdThreads) update_step_kernel(const __grid_c
         float4 *w4 = reinterpret_cast<float4 *>(w + lo), *p4 = reinterpret_cast<float4 *>(wp + lo);
         const float4 *g4 = reinterpret_cast<const float4 *>(g + lo);
         for (int64_t i = threadIdx.x; i < nv; i += kUpdThreads) {
-            const float4 a = w4[i], b = p4[i], c = __ldg(g4 + i);
+            // w_prev and P are touched once: streamed (evict-first), so the fresh w that
+            // update_scale_kernel re-reads has the best chance to stay in L2
+            const float4 a = w4[i], b = __ldcs(p4 + i), c = __ldcs(g4 + i);
             float4 r;
             r.x = upd1(a.x, b.x, c.x, P.lr, P.mom);
             r.y = upd1(a.y, b.y, c.y, P.lr, P.mom);
             r.z = upd1(a.z, b.z, c.z, P.lr, P.mom);
             r.w = upd1(a.w, b.w, c.w, P.lr, P.mom);
-            p4[i] = a;
+            __stcs(p4 + i, a);
             w4[i] = r;
             if (P.rescale) {
                 const float v[4] = {r.x, r.y, r.z, r.w};
