@@ -2,7 +2,7 @@
 
   python scripts/summarize_profiles.py <tag>
 
-Inputs (gpurun_out/, written by scripts/gpu_prof_a.sh / gpu_prof_b.sh):
+Inputs (gpurun_out/, written by scripts/gpurun/gpu_evidence.sh (or gpu_prof_a.sh / gpu_prof_b.sh)):
   launches.csv          ncu --metrics gpu__time_duration.sum launch list of the bench command
   prof_hot_rn50.ncu-rep ncu --set full capture of factor_syrk_kernel, inverse_kernel, gemm_3xtf32_kernel
 Outputs:
