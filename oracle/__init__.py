@@ -23,6 +23,9 @@ parts of the method in plain Python:
   (NEXT-1; reading R-20).
 * ``learning_rate`` / ``momentum`` / ``apply_update`` / ``rescale_weights`` /
   ``update_layer``: the update after the AllGather (NEXT-3; R-21).
+* ``bn_sample_grads`` / ``bn_fisher`` / ``bn_precondition``: the Batch
+  Normalization Fisher, full and diagonal (NEXT-2; P:493-494, P:665-668,
+  P:740-763; R-22).
 
 Parity status: every function here is pinned by tests/test_oracle_*.py (see
 DESIGN.md §Oracle pins); none is "parity unpinned".
@@ -562,3 +565,65 @@ def update_layer(w, w_prev, precond, eta, m, has_bias, rescale=True, eps=1e-9):
         w_new = w_new.copy()
         w_new[:, :nb] = rescale_weights(w_new[:, :nb], w_new.shape[0], eps)
     return w_new, w_keep
+
+
+# --------------------------------------------------------------------------
+# NEXT-2: Fisher of the Batch Normalization layers (
+# S:231-246; reading R-22).  Not factored into A and G: F is the empirical
+# Fisher of the 2C parameters [scale γ_1..γ_C, shift β_1..β_C] of one BN layer.
+# --------------------------------------------------------------------------
+def _decode(bits, fmt):
+    """Exact fp64 values of 16-bit bf16 / fp16 patterns."""
+    b = np.ascontiguousarray(np.asarray(bits).reshape(-1)).view(np.uint16)
+    if fmt == "bf16":
+        return (b.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    if fmt == "fp16":
+        return b.view(np.float16).astype(np.float64)
+    raise ValueError("fmt: bf16 | fp16")
+
+
+def bn_sample_grads(xhat_bits, gy_bits, n, hw, c, fmt="bf16"):
+    """Per-sample BN parameter gradients S[s] = [Σ_p gy[s,p,:]·x̂[s,p,:], Σ_p gy[s,p,:]] (2C values,
+    scale first then shift; y = γ·x̂ + β so ∂y/∂γ_c = x̂_c, ∂y/∂β_c = 1), p over the hw pixels of
+    sample s, from the NHWC half-precision bit patterns the GPU consumes, in fp64."""
+    x = _decode(xhat_bits, fmt).reshape(n, hw, c)
+    g = _decode(gy_bits, fmt).reshape(n, hw, c)
+    S = np.zeros((n, 2 * c), dtype=np.float64)
+    for s in range(n):
+        for p in range(hw):
+            S[s, :c] += g[s, p] * x[s, p]
+            S[s, c:] += g[s, p]
+    return S
+
+
+def bn_fisher(S, mode="full"):
+    """F = (1/N) Σ_s S[s] S[s]ᵀ ("full", 2C x 2C) or its diagonal (1/N) Σ_s S[s]² ("diag",
+    P:740-747 'approximate it with a diagonal matrix'); S:235-236."""
+    S = np.asarray(S, dtype=np.float64)
+    if mode == "full":
+        F = np.zeros((S.shape[1], S.shape[1]), dtype=np.float64)
+        for s in range(S.shape[0]):
+            F += np.outer(S[s], S[s])
+        return F / S.shape[0]
+    if mode == "diag":
+        return np.sum(S * S, axis=0) / S.shape[0]
+    raise ValueError("mode: full | diag")
+
+
+def bn_precondition(F, grad, gamma_bn):
+    """(F + γ_BN·I)⁻¹·grad for a full F (via the oracle's Cholesky inverse), grad_i/(F_i + γ_BN) for a
+    diagonal F; γ_BN = ρ_BN·γ."""
+    if not gamma_bn > 0:
+        raise ValueError("gamma_bn > 0")
+    F = np.asarray(F, dtype=np.float64)
+    grad = np.asarray(grad, dtype=np.float64)
+    if F.ndim == 1:
+        if F.shape != grad.shape:
+            raise ValueError("bn_precondition: dimension mismatch")
+        return grad / (F + gamma_bn)
+    if F.shape != (grad.shape[0], grad.shape[0]):
+        raise ValueError("bn_precondition: dimension mismatch")
+    X, st = inverse(F + gamma_bn * np.eye(F.shape[0]))
+    if st:
+        raise ValueError("bn_precondition: F + gamma_bn I not positive definite")
+    return X @ grad
