@@ -336,6 +336,53 @@ def run_ours(args):
                             "bytes_counting": "20 B per weight (w, w_prev, P read; w, w_prev written)"}}
         del w_l, wp_l
 
+    # ---- the Batch Normalization Fisher (NEXT-2, R-22): per-sample scale / shift gradients of the 53
+    # RN50 BN layers (one after every conv) from xhat, gy of the conv-output shape, then the diagonal and
+    # the full (Woodbury) preconditioners with gamma_BN = rho_BN * gamma (Table 3: rho_BN = 16).
+    bn = None
+    if not args.no_stale and args.config == "resnet50":
+        convs = [l for l in layers if l["kind"] == 0]
+        bc = [l["c_out"] for l in convs]
+        bhw = [shapes.out_hw(l)[0] * shapes.out_hw(l)[1] for l in convs]
+        gb = torch.Generator(device=dev).manual_seed(args.seed + 7)
+        bx = [torch.randn(n, hw, c, generator=gb, device=dev).to(torch.bfloat16) for c, hw in zip(bc, bhw)]
+        bg = [(torch.randn(n, hw, c, generator=gb, device=dev) * 0.01).to(torch.bfloat16) for c, hw in zip(bc, bhw)]
+        bS = [torch.empty(n, 2 * c, device=dev) for c in bc]
+        bgr = [torch.randn(2 * c, generator=gb, device=dev) for c in bc]
+        bo = [torch.empty(2 * c, device=dev) for c in bc]
+        lam = 16.0 * args.gamma
+
+        def bn_run(full):
+            K.bn_grads(bc, bhw, bx, bg, n, bS, stream)
+            K.bn_precondition(bc, n, bS, bgr, lam, full, bo, stream)
+
+        res = {}
+        for full in (0, 1):
+            for _ in range(args.warmup):
+                bn_run(full)
+            bev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+            barrier()
+            for s in range(args.steps):
+                bev[s][0].record(stream)
+                K.bn_grads(bc, bhw, bx, bg, n, bS, stream)
+                bev[s][1].record(stream)
+                K.bn_precondition(bc, n, bS, bgr, lam, full, bo, stream)
+                bev[s][2].record(stream)
+            barrier()
+            res[full] = (sum(e[0].elapsed_time(e[1]) for e in bev) / args.steps,
+                         sum(e[1].elapsed_time(e[2]) for e in bev) / args.steps)
+        bbytes = sum(4 * n * hw * c for c, hw in zip(bc, bhw))  # xhat + gy, 2 B each, read once
+        ggbs = bbytes / (res[1][0] / 1e3) / 1e9
+        hbm = peaks()["hbm_gbs"]
+        bn = {"layers": len(bc), "grads_ms": round(res[1][0], 4), "precond_diag_ms": round(res[0][1], 4),
+              "precond_full_ms": round(res[1][1], 4),
+              "full_fim_bytes_paper": sum(4 * (2 * c) * (2 * c + 1) // 2 for c in bc),
+              "full_fim_bytes_woodbury_S": sum(4 * n * 2 * c for c in bc),
+              "grads_roofline": {"bound": "hbm", "achieved": round(ggbs, 1), "peak": hbm, "unit": "GB/s",
+                                 "frac": round(ggbs / hbm, 4), "traffic": None, "kernel": "bn_grads_kernel",
+                                 "bytes_counting": "4 B per (sample, pixel, channel): xhat + gy bf16"}}
+        del bx, bg
+
     # ---- end-to-end through the public API with host buffers (H2D inputs, D2H result).  Every
     # step's inputs are copied from pinned host memory and its result read back inside the timed
     # region; the copies run on their own streams (H2D and D2H directions concurrently) and are
@@ -476,6 +523,7 @@ def run_ours(args):
             "e2e": e2e,
             "stale": stale,
             "update": upd,
+            "bn_fisher": bn,
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "timed_wall_s": round(wall_s, 3),
@@ -503,7 +551,7 @@ def main():
     ap.add_argument("--seed", type=int, default=1811)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-stale", action="store_true", help="skip the stale-Fisher step (NEXT-1) and update (NEXT-3) timings")
+    ap.add_argument("--no-stale", action="store_true", help="skip the stale-Fisher step (NEXT-1), update (NEXT-3) and BN Fisher (NEXT-2) timings")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

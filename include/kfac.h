@@ -287,6 +287,34 @@ KFAC_API kfac_status kfac_update(kfac_plan_t plan, const float *ag_buf, float *c
                         float *const *w_prev /* host [L] */, float lr, float momentum, int32_t rescale, float eps,
                         void *ws, void *stream);
 
+/* ------------------------------------------------------------------ NEXT-2: Batch Normalization Fisher
+ * A BN layer y = gamma * xhat + beta has 2C parameters, ordered [gamma_1..gamma_C, beta_1..beta_C]
+ * (reading R-22).  Its Fisher is not factored into A and G:
+ *   F = (1/n) sum_s S_s S_s^T,  S_s = [sum_p gy_{s,p} * xhat_{s,p} ; sum_p gy_{s,p}]   (2C)
+ * over the n samples s and hw pixels p; the paper damps it with gamma_BN = rho_BN * gamma
+ * and also uses its diagonal ("approximate it with a diagonal matrix").
+ *
+ * kfac_bn_grads: S[l] ([n][2C] fp32, device) for nl BN layers in one launch, from xhat[l] and
+ * gy[l] (NHWC half [n, hw[l], c[l]], the normalised BN input and the gradient w.r.t. the BN
+ * output; the caller folds any per-sample loss scale into gy, R-4).  fp32 accumulation.
+ * c, hw, xhat, gy, S: host arrays [nl].  Errors: KFAC_ERR_ARG (NULL, n < 1, dtype),
+ * KFAC_ERR_SHAPE (c < 2, hw < 1), KFAC_ERR_UNSUPPORTED (odd c, xhat / gy not 4-byte aligned). */
+KFAC_API kfac_status kfac_bn_grads(int32_t nl, const int32_t *c /* host [nl] */, const int32_t *hw /* host [nl] */,
+                          const void *const *xhat /* host [nl] */, const void *const *gy /* host [nl] */,
+                          kfac_dtype dtype, int32_t n, float *const *S /* host [nl] */, void *stream);
+
+/* kfac_bn_precondition: out[l] = (F_l + gamma_bn I)^-1 grad[l] (full != 0) or
+ * grad[l]_i / (F_l,ii + gamma_bn) (full == 0, the diagonal FIM), F_l from S[l] as above.
+ * The full mode never forms F: F has rank <= n, and by the Woodbury identity
+ *   (F + gamma_bn I)^-1 v = (v - S^T (gamma_bn n I + S S^T)^-1 S v) / gamma_bn,
+ * an n x n fp64 Cholesky solve per layer (one CTA per layer); n <= 128 (e.g. the samples of
+ * up to 4 ranks of 32 after an all-gather of S).  grad / out: [2C] fp32 device (out may not
+ * alias grad).  Errors: KFAC_ERR_ARG (NULL, gamma_bn <= 0, n < 1), KFAC_ERR_SHAPE (c < 1),
+ * KFAC_ERR_UNSUPPORTED (full mode with n > 128).                                          */
+KFAC_API kfac_status kfac_bn_precondition(int32_t nl, const int32_t *c /* host [nl] */, int32_t n,
+                                 const float *const *S /* host [nl] */, const float *const *grad /* host [nl] */,
+                                 float gamma_bn, int32_t full, float *const *out /* host [nl] */, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -590,9 +590,8 @@ def bn_sample_grads(xhat_bits, gy_bits, n, hw, c, fmt="bf16"):
     g = _decode(gy_bits, fmt).reshape(n, hw, c)
     S = np.zeros((n, 2 * c), dtype=np.float64)
     for s in range(n):
-        for p in range(hw):
-            S[s, :c] += g[s, p] * x[s, p]
-            S[s, c:] += g[s, p]
+        S[s, :c] = np.sum(g[s] * x[s], axis=0)
+        S[s, c:] = np.sum(g[s], axis=0)
     return S
 
 

@@ -326,6 +326,51 @@ kfac_status kfac_update(kfac_plan_t p, const float *ag_buf, float *const *w, flo
     return update_launch(jobs, lr, momentum, rescale ? 1 : 0, eps, static_cast<double *>(ws), p->ws_bytes, S(stream));
 }
 
+// ------------------------------------------------------------------ NEXT-2: Batch Normalization Fisher
+kfac_status kfac_bn_grads(int32_t nl, const int32_t *c, const int32_t *hw, const void *const *xhat,
+                          const void *const *gy, kfac_dtype dt, int32_t n, float *const *Sv, void *stream) {
+    if (nl < 1 || !c || !hw || !xhat || !gy || !Sv) return set_error(KFAC_ERR_ARG, "kfac_bn_grads: NULL argument / nl < 1");
+    if (n < 1) return set_error(KFAC_ERR_ARG, "kfac_bn_grads: n >= 1 (empty capture)");
+    if (dt != KFAC_BF16 && dt != KFAC_FP16) return set_error(KFAC_ERR_ARG, "kfac_bn_grads: dtype");
+    std::vector<BnJob> jobs;
+    for (int l = 0; l < nl; l++) {
+        if (!xhat[l] || !gy[l] || !Sv[l]) return set_error(KFAC_ERR_ARG, "kfac_bn_grads: NULL layer pointer");
+        if (c[l] < 2 || hw[l] < 1) return set_error(KFAC_ERR_SHAPE, "kfac_bn_grads: c >= 2, hw >= 1");
+        if ((c[l] & 1) || ((reinterpret_cast<uintptr_t>(xhat[l]) | reinterpret_cast<uintptr_t>(gy[l])) & 3))
+            return set_error(KFAC_ERR_UNSUPPORTED, "kfac_bn_grads: c must be even and xhat / gy 4-byte aligned");
+        BnJob b{};
+        b.xhat = xhat[l];
+        b.gy = gy[l];
+        b.S = Sv[l];
+        b.c = c[l];
+        b.hw = hw[l];
+        jobs.push_back(b);
+    }
+    return bn_grads_launch(jobs, n, dt == KFAC_FP16 ? 1 : 0, S(stream));
+}
+
+kfac_status kfac_bn_precondition(int32_t nl, const int32_t *c, int32_t n, const float *const *Sv,
+                                 const float *const *grad, float gamma_bn, int32_t full, float *const *out,
+                                 void *stream) {
+    if (nl < 1 || !c || !Sv || !grad || !out) return set_error(KFAC_ERR_ARG, "kfac_bn_precondition: NULL argument / nl < 1");
+    if (!(gamma_bn > 0.f)) return set_error(KFAC_ERR_ARG, "kfac_bn_precondition: gamma_bn must be > 0");
+    if (n < 1) return set_error(KFAC_ERR_ARG, "kfac_bn_precondition: n >= 1");
+    if (full && n > kBnMaxSamples)
+        return set_error(KFAC_ERR_UNSUPPORTED, "kfac_bn_precondition: full mode supports n <= 128 samples");
+    std::vector<BnJob> jobs;
+    for (int l = 0; l < nl; l++) {
+        if (!Sv[l] || !grad[l] || !out[l]) return set_error(KFAC_ERR_ARG, "kfac_bn_precondition: NULL layer pointer");
+        if (c[l] < 1) return set_error(KFAC_ERR_SHAPE, "kfac_bn_precondition: c >= 1");
+        BnJob b{};
+        b.S = const_cast<float *>(Sv[l]);
+        b.grad = grad[l];
+        b.out = out[l];
+        b.c = c[l];
+        jobs.push_back(b);
+    }
+    return bn_precond_launch(jobs, n, full ? 1 : 0, (double)gamma_bn, S(stream));
+}
+
 // ------------------------------------------------------------------ stage 6
 kfac_status kfac_allgather_precond(kfac_comm_t c, kfac_plan_t p, float *ag_buf, void *stream) {
     if (!p || !ag_buf) return set_error(KFAC_ERR_ARG, "kfac_allgather_precond: NULL argument");

@@ -121,6 +121,16 @@ struct UpdJob {            // one layer of the post-AllGather update (update.cu)
 };
 kfac_status update_launch(const std::vector<UpdJob> &jobs, float lr, float mom, int rescale, float eps, double *ws,
                           int64_t ws_bytes, cudaStream_t st);
+struct BnJob {             // one Batch Normalization layer (bn.cu)
+    const void *xhat, *gy;    // NHWC half [n, hw, c]
+    float *S;                 // per-sample gradients [n][2c]
+    const float *grad;        // [2c] (scale, shift)
+    float *out;               // [2c]
+    int32_t c, hw;
+};
+constexpr int kBnMaxSamples = 128;  // full-mode Woodbury solve in shared memory
+kfac_status bn_grads_launch(const std::vector<BnJob> &jobs, int n, int fp16, cudaStream_t st);
+kfac_status bn_precond_launch(const std::vector<BnJob> &jobs, int n, int full, double lambda, cudaStream_t st);
 kfac_status diff_launch(const std::vector<DiffMat> &mats, double *ws, int64_t ws_bytes, cudaStream_t st);
 int64_t precond_ws_floats(int dG, int dA);  // split operands of one layer's two products
 kfac_status replicate_launch(const std::vector<std::pair<const float *, float *>> &src_dst,

@@ -86,13 +86,18 @@ _refresh_interval = _sig("kfac_refresh_interval", [_i32, _i32])
 _refresh = _sig("kfac_refresh", [_i64, _i32, _i32, _i64, _i32])
 _factor_diff = _sig("kfac_factor_diff", [_P, _i32, _P, _P, _P, _P, _P])
 RAMPUP, STEP13 = 0, 1
+_bn_grads = _sig("kfac_bn_grads", [_i32, _pi32, _pi32, ctypes.POINTER(_P), ctypes.POINTER(_P), ctypes.c_int, _i32,
+                                    ctypes.POINTER(_P)])
+_bn_precondition = _sig("kfac_bn_precondition", [_i32, _pi32, _i32, ctypes.POINTER(_P), ctypes.POINTER(_P), _f32, _i32,
+                                                  ctypes.POINTER(_P), _P])
 _update = _sig("kfac_update", [_P, _P, ctypes.POINTER(_P), ctypes.POINTER(_P), _f32, _f32, _i32, _f32, _P, _P])
 
 EXPORTS = ["kfac_last_error", "kfac_version", "kfac_launch_count", "kfac_plan_create", "kfac_plan_query", "kfac_plan_rank_layers",
            "kfac_plan_destroy", "kfac_comm_unique_id", "kfac_comm_create", "kfac_comm_destroy", "kfac_factor_A",
            "kfac_factor_G", "kfac_factor_ws_bytes", "kfac_factor_all", "kfac_reduce_scatter_factors",
            "kfac_damped_inverse", "kfac_precondition", "kfac_allgather_precond", "kfac_plan_create_stale",
-           "kfac_plan_is_stale", "kfac_refresh_interval", "kfac_refresh", "kfac_factor_diff", "kfac_update"]
+           "kfac_plan_is_stale", "kfac_refresh_interval", "kfac_refresh", "kfac_factor_diff", "kfac_update", "kfac_bn_grads",
+           "kfac_bn_precondition"]
 
 
 def _check(st, where):
@@ -281,3 +286,21 @@ def update(plan, ag_buf, ws_, w_prev, lr, momentum, ws, rescale=True, eps=1e-9, 
     pa = (_P * L)(*[_ptr(t).value for t in w_prev])
     _check(_update(plan.h, _ptr(ag_buf), wa, pa, float(lr), float(momentum), 1 if rescale else 0, float(eps), _ptr(ws),
                    _stream(stream)), "kfac_update")
+
+
+def _parr(ts):
+    return (_P * len(ts))(*[_ptr(t).value for t in ts])
+
+
+def bn_grads(c, hw, xhat, gy, n, S, stream=None):
+    """kfac_bn_grads: per-sample BN scale / shift gradients S[l] [n, 2C] (NEXT-2, R-22)."""
+    nl = len(c)
+    _check(_bn_grads(nl, (ctypes.c_int32 * nl)(*c), (ctypes.c_int32 * nl)(*hw), _parr(xhat), _parr(gy),
+                     _DT[xhat[0].dtype], int(n), _parr(S), _stream(stream)), "kfac_bn_grads")
+
+
+def bn_precondition(c, n, S, grad, gamma_bn, full, out, stream=None):
+    """kfac_bn_precondition: (F + gamma_bn I)^-1 grad (full, Woodbury) or the diagonal version."""
+    nl = len(c)
+    _check(_bn_precondition(nl, (ctypes.c_int32 * nl)(*c), int(n), _parr(S), _parr(grad), float(gamma_bn),
+                            1 if full else 0, _parr(out), _stream(stream)), "kfac_bn_precondition")
