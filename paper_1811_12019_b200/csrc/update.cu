@@ -129,6 +129,20 @@ __global__ void __launch_bounds__(kUpdThreads) update_scale_kernel(const __grid_
     float *w = P.w[l];
     const int cols = P.cols[l];
     const bool bias = P.bias[l] != 0;
+    if (!bias && (reinterpret_cast<uintptr_t>(w) & 15) == 0) {  // no bias column: float4 sweep
+        float4 *w4 = reinterpret_cast<float4 *>(w + lo);
+        const int64_t nv = (hi - lo) / 4;
+        for (int64_t i = threadIdx.x; i < nv; i += kUpdThreads) {
+            float4 a = w4[i];
+            a.x *= sc;
+            a.y *= sc;
+            a.z *= sc;
+            a.w *= sc;
+            w4[i] = a;
+        }
+        for (int64_t e = lo + nv * 4 + threadIdx.x; e < hi; e += kUpdThreads) w[e] *= sc;
+        return;
+    }
     for (int64_t e = lo + threadIdx.x; e < hi; e += kUpdThreads)
         if (!bias || (int)e % cols != cols - 1) w[e] *= sc;
 }
