@@ -54,48 +54,52 @@ __device__ __forceinline__ double2 block_sum2(double a, double b, double2 *sh) {
 
 __global__ void __launch_bounds__(kDiffThreads) diff_partial_kernel(const __grid_constant__ DiffParams P) {
     __shared__ double2 sh[kDiffThreads / 32];
-    const int b = blockIdx.x;
-    int m = 0, hi_m = P.nmats - 1;  // binary search: the last matrix whose first block <= b
-    while (m < hi_m) {
-        const int mid = (m + hi_m + 1) >> 1;
-        if (P.first[mid] <= b) m = mid;
-        else hi_m = mid - 1;
-    }
-    const float *cur = P.cur[m], *prev = P.prev[m];
-    double num = 0.0, den = 0.0;
-    const int nrange = P.first[m + 1] - P.first[m] - 1;
-    const int rb = b - P.first[m];
-    if (rb < nrange) {  // packed range [lo, hi)
-        const int64_t lo = (int64_t)rb * kDiffChunk;
-        const int64_t hi = min(lo + kDiffChunk, P.len[m]);
-        // segments start 16-element aligned in the recv chunk, and so does lo
-        const int64_t nv = (hi - lo) / 4;
-        const float4 *c4 = reinterpret_cast<const float4 *>(cur + lo);
-        const float4 *p4 = reinterpret_cast<const float4 *>(prev + lo);
+    // grid-stride over the work items (one resident wave, no wave-quantisation tail); each item
+    // still writes its own partial, so the combine order does not depend on the grid
+    for (int b = blockIdx.x; b < P.first[P.nmats]; b += gridDim.x) {
+        int m = 0, hi_m = P.nmats - 1;  // binary search: the last matrix whose first block <= b
+        while (m < hi_m) {
+            const int mid = (m + hi_m + 1) >> 1;
+            if (P.first[mid] <= b) m = mid;
+            else hi_m = mid - 1;
+        }
+        const float *cur = P.cur[m], *prev = P.prev[m];
+        double num = 0.0, den = 0.0;
+        const int nrange = P.first[m + 1] - P.first[m] - 1;
+        const int rb = b - P.first[m];
+        if (rb < nrange) {  // packed range [lo, hi)
+            const int64_t lo = (int64_t)rb * kDiffChunk;
+            const int64_t hi = min(lo + kDiffChunk, P.len[m]);
+            // segments start 16-element aligned in the recv chunk, and so does lo
+            const int64_t nv = (hi - lo) / 4;
+            const float4 *c4 = reinterpret_cast<const float4 *>(cur + lo);
+            const float4 *p4 = reinterpret_cast<const float4 *>(prev + lo);
 #pragma unroll 4
-        for (int64_t i = threadIdx.x; i < nv; i += kDiffThreads) {
-            const float4 c = __ldcs(c4 + i), p = __ldcs(p4 + i);  // streamed once: evict-first
-            const double d0 = (double)c.x - p.x, d1 = (double)c.y - p.y, d2 = (double)c.z - p.z,
-                         d3 = (double)c.w - p.w;
-            num += d0 * d0 + d1 * d1 + d2 * d2 + d3 * d3;
-            den += (double)p.x * p.x + (double)p.y * p.y + (double)p.z * p.z + (double)p.w * p.w;
+            for (int64_t i = threadIdx.x; i < nv; i += kDiffThreads) {
+                const float4 c = __ldcs(c4 + i), p = __ldcs(p4 + i);  // streamed once: evict-first
+                const double d0 = (double)c.x - p.x, d1 = (double)c.y - p.y, d2 = (double)c.z - p.z,
+                             d3 = (double)c.w - p.w;
+                num += d0 * d0 + d1 * d1 + d2 * d2 + d3 * d3;
+                den += (double)p.x * p.x + (double)p.y * p.y + (double)p.z * p.z + (double)p.w * p.w;
+            }
+            for (int64_t i = lo + nv * 4 + threadIdx.x; i < hi; i += kDiffThreads) {
+                const double d = (double)cur[i] - prev[i];
+                num += d * d;
+                den += (double)prev[i] * prev[i];
+            }
+        } else {  // the diagonal: X_ii at i*n - i(i-1)/2
+            const int64_t n = P.n[m];
+            for (int64_t i = threadIdx.x; i < n; i += kDiffThreads) {
+                const int64_t k = i * n - i * (i - 1) / 2;
+                const double d = (double)cur[k] - prev[k];
+                num += d * d;
+                den += (double)prev[k] * prev[k];
+            }
         }
-        for (int64_t i = lo + nv * 4 + threadIdx.x; i < hi; i += kDiffThreads) {
-            const double d = (double)cur[i] - prev[i];
-            num += d * d;
-            den += (double)prev[i] * prev[i];
-        }
-    } else {  // the diagonal: X_ii at i*n - i(i-1)/2
-        const int64_t n = P.n[m];
-        for (int64_t i = threadIdx.x; i < n; i += kDiffThreads) {
-            const int64_t k = i * n - i * (i - 1) / 2;
-            const double d = (double)cur[k] - prev[k];
-            num += d * d;
-            den += (double)prev[k] * prev[k];
-        }
+        const double2 r = block_sum2(num, den, sh);
+        if (threadIdx.x == 0) P.part[b] = r;
+        __syncthreads();  // sh is reused by the next item
     }
-    const double2 r = block_sum2(num, den, sh);
-    if (threadIdx.x == 0) P.part[b] = r;
 }
 
 // one warp per matrix: ||.||_F^2 = 2 * (range sum) - (diagonal sum), fixed-order combine
@@ -144,7 +148,15 @@ kfac_status diff_launch(const std::vector<DiffMat> &mats, double *ws, int64_t ws
         if ((int64_t)nb * (int64_t)sizeof(double2) > ws_bytes)
             return set_error(KFAC_ERR_STATE, "kfac_factor_diff: workspace too small for the block partials");
         P.part = reinterpret_cast<double2 *>(ws);
-        diff_partial_kernel<<<nb, kDiffThreads, 0, st>>>(P);
+        static int grid = 0;
+        if (!grid) {
+            int dev = 0, sms = 0, per = 0;
+            KFAC_CUDA_TRY(cudaGetDevice(&dev));
+            KFAC_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+            KFAC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, diff_partial_kernel, kDiffThreads, 0));
+            grid = sms * std::max(per, 1);
+        }
+        diff_partial_kernel<<<std::min(nb, grid), kDiffThreads, 0, st>>>(P);
         KFAC_LAUNCHED();
         KFAC_CUDA_TRY(cudaGetLastError());
         diff_final_kernel<<<(P.nmats + 7) / 8, 256, 0, st>>>(P);
