@@ -15,6 +15,7 @@ from synth import inputs, shapes
 pytestmark = pytest.mark.gpu
 TOL = 2e-3
 RHO_BN, GAMMA = 16.0, 2.5e-2  # Table 3: gamma_BN = rho_BN * gamma = 0.4
+DENSE_MAX = 1024  # largest 2C checked against the dense oracle inverse
 
 
 @pytest.fixture(scope="module")
@@ -56,16 +57,26 @@ def _run(K, orc, cs, hws, n, dt=torch.bfloat16, seed=0, check_e2e=True):
     for l, (c, hw) in enumerate(zip(cs, hws)):
         Sg = S[l].cpu().double().numpy()
         gr = grads[l].double().numpy()
-        for full, key in ((0, "diag"), (1, "full")):
-            F_same = orc.bn_fisher(Sg, "full" if full else "diag")
-            stage = relerr(outs[full][l].cpu().numpy(), orc.bn_precondition(F_same, gr, lam))
-            worst["stage"] = max(worst["stage"], stage)
-        if check_e2e:
-            So = orc.bn_sample_grads(inputs.half_bits(xs[l]), inputs.half_bits(gys[l]), n, hw, c, fmt)
+        So = orc.bn_sample_grads(inputs.half_bits(xs[l]), inputs.half_bits(gys[l]), n, hw, c, fmt) if check_e2e else None
+        if So is not None:
             worst["S"] = max(worst["S"], relerr(Sg, So))
-            for full, key in ((0, "diag"), (1, "full")):
+        for full, key in ((0, "diag"), (1, "full")):
+            got = outs[full][l].cpu().double().numpy()
+            if full and 2 * c > DENSE_MAX:
+                # past DENSE_MAX the dense oracle inverse is minutes of CPU: check the defining equation
+                # (F + lambda I) x = grad instead, F x = S^T (S x) / n in fp64 (holds at any size)
+                for Sx, k2, tol in ((Sg, "stage", 1e-6), (So, key, TOL)):
+                    if Sx is None:
+                        continue
+                    Fx = Sx.T @ (Sx @ got) / n
+                    r = np.linalg.norm(Fx + lam * got - gr) / (np.linalg.norm(Fx) + lam * np.linalg.norm(got) + np.linalg.norm(gr))
+                    worst[k2] = max(worst[k2], r)
+                continue
+            F_same = orc.bn_fisher(Sg, "full" if full else "diag")
+            worst["stage"] = max(worst["stage"], relerr(got, orc.bn_precondition(F_same, gr, lam)))
+            if So is not None:
                 want = orc.bn_precondition(orc.bn_fisher(So, "full" if full else "diag"), gr, lam)
-                worst[key] = max(worst[key], relerr(outs[full][l].cpu().numpy(), want))
+                worst[key] = max(worst[key], relerr(got, want))
     print({k: f"{v:.2e}" for k, v in worst.items()})
     assert worst["stage"] <= 1e-6
     assert worst["S"] <= TOL and worst["diag"] <= TOL and worst["full"] <= TOL
