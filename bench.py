@@ -351,10 +351,11 @@ def run_ours(args):
         bgr = [torch.randn(2 * c, generator=gb, device=dev) for c in bc]
         bo = [torch.empty(2 * c, device=dev) for c in bc]
         lam = 16.0 * args.gamma
+        bws = torch.empty(K.bn_ws_bytes(bc, n), dtype=torch.uint8, device=dev)
 
         def bn_run(full):
             K.bn_grads(bc, bhw, bx, bg, n, bS, stream)
-            K.bn_precondition(bc, n, bS, bgr, lam, full, bo, stream)
+            K.bn_precondition(bc, n, bS, bgr, lam, full, bo, bws, stream)
 
         res = {}
         for full in (0, 1):
@@ -366,7 +367,7 @@ def run_ours(args):
                 bev[s][0].record(stream)
                 K.bn_grads(bc, bhw, bx, bg, n, bS, stream)
                 bev[s][1].record(stream)
-                K.bn_precondition(bc, n, bS, bgr, lam, full, bo, stream)
+                K.bn_precondition(bc, n, bS, bgr, lam, full, bo, bws, stream)
                 bev[s][2].record(stream)
             barrier()
             res[full] = (sum(e[0].elapsed_time(e[1]) for e in bev) / args.steps,

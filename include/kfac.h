@@ -307,13 +307,19 @@ KFAC_API kfac_status kfac_bn_grads(int32_t nl, const int32_t *c /* host [nl] */,
  * grad[l]_i / (F_l,ii + gamma_bn) (full == 0, the diagonal FIM), F_l from S[l] as above.
  * The full mode never forms F: F has rank <= n, and by the Woodbury identity
  *   (F + gamma_bn I)^-1 v = (v - S^T (gamma_bn n I + S S^T)^-1 S v) / gamma_bn,
- * an n x n fp64 Cholesky solve per layer (one CTA per layer); n <= 128 (e.g. the samples of
- * up to 4 ranks of 32 after an all-gather of S).  grad / out: [2C] fp32 device (out may not
- * alias grad).  Errors: KFAC_ERR_ARG (NULL, gamma_bn <= 0, n < 1), KFAC_ERR_SHAPE (c < 1),
- * KFAC_ERR_UNSUPPORTED (full mode with n > 128).                                          */
+ * i.e. a column-parallel fp64 Gram S S^T (all layers in one launch) and an n x n fp64
+ * Cholesky solve per layer; n <= 128 (e.g. the samples of up to 4 ranks of 32 after an
+ * all-gather of S).  grad / out: [2C] fp32 device (out may not alias grad).  ws: device
+ * scratch of kfac_bn_ws_bytes (full mode; may be NULL for the diagonal mode).
+ * Errors: KFAC_ERR_ARG (NULL, gamma_bn <= 0, n < 1, full mode without enough ws),
+ * KFAC_ERR_SHAPE (c < 1), KFAC_ERR_UNSUPPORTED (full mode with n > 128).                */
 KFAC_API kfac_status kfac_bn_precondition(int32_t nl, const int32_t *c /* host [nl] */, int32_t n,
                                  const float *const *S /* host [nl] */, const float *const *grad /* host [nl] */,
-                                 float gamma_bn, int32_t full, float *const *out /* host [nl] */, void *stream);
+                                 float gamma_bn, int32_t full, float *const *out /* host [nl] */, void *ws,
+                                 int64_t ws_bytes, void *stream);
+/* Workspace bytes kfac_bn_precondition's full mode needs for these layers and n. */
+KFAC_API kfac_status kfac_bn_ws_bytes(int32_t nl, const int32_t *c /* host [nl] */, int32_t n,
+                             int64_t *bytes /* host */);
 
 #ifdef __cplusplus
 }

@@ -349,9 +349,15 @@ kfac_status kfac_bn_grads(int32_t nl, const int32_t *c, const int32_t *hw, const
     return bn_grads_launch(jobs, n, dt == KFAC_FP16 ? 1 : 0, S(stream));
 }
 
+kfac_status kfac_bn_ws_bytes(int32_t nl, const int32_t *c, int32_t n, int64_t *bytes) {
+    if (nl < 1 || !c || !bytes || n < 1) return set_error(KFAC_ERR_ARG, "kfac_bn_ws_bytes");
+    *bytes = bn_ws_bytes(std::vector<int>(c, c + nl), n);
+    return KFAC_OK;
+}
+
 kfac_status kfac_bn_precondition(int32_t nl, const int32_t *c, int32_t n, const float *const *Sv,
                                  const float *const *grad, float gamma_bn, int32_t full, float *const *out,
-                                 void *stream) {
+                                 void *ws, int64_t ws_bytes, void *stream) {
     if (nl < 1 || !c || !Sv || !grad || !out) return set_error(KFAC_ERR_ARG, "kfac_bn_precondition: NULL argument / nl < 1");
     if (!(gamma_bn > 0.f)) return set_error(KFAC_ERR_ARG, "kfac_bn_precondition: gamma_bn must be > 0");
     if (n < 1) return set_error(KFAC_ERR_ARG, "kfac_bn_precondition: n >= 1");
@@ -368,7 +374,7 @@ kfac_status kfac_bn_precondition(int32_t nl, const int32_t *c, int32_t n, const 
         b.c = c[l];
         jobs.push_back(b);
     }
-    return bn_precond_launch(jobs, n, full ? 1 : 0, (double)gamma_bn, S(stream));
+    return bn_precond_launch(jobs, n, full ? 1 : 0, (double)gamma_bn, static_cast<double *>(ws), ws_bytes, S(stream));
 }
 
 // ------------------------------------------------------------------ stage 6

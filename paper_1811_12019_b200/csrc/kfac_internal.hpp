@@ -130,7 +130,9 @@ struct BnJob {             // one Batch Normalization layer (bn.cu)
 };
 constexpr int kBnMaxSamples = 128;  // full-mode Woodbury solve in shared memory
 kfac_status bn_grads_launch(const std::vector<BnJob> &jobs, int n, int fp16, cudaStream_t st);
-kfac_status bn_precond_launch(const std::vector<BnJob> &jobs, int n, int full, double lambda, cudaStream_t st);
+kfac_status bn_precond_launch(const std::vector<BnJob> &jobs, int n, int full, double lambda, double *ws,
+                              int64_t ws_bytes, cudaStream_t st);
+int64_t bn_ws_bytes(const std::vector<int> &cs, int n);  // full-mode Gram partials
 kfac_status diff_launch(const std::vector<DiffMat> &mats, double *ws, int64_t ws_bytes, cudaStream_t st);
 int64_t precond_ws_floats(int dG, int dA);  // split operands of one layer's two products
 kfac_status replicate_launch(const std::vector<std::pair<const float *, float *>> &src_dst,

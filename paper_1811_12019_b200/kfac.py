@@ -89,7 +89,8 @@ RAMPUP, STEP13 = 0, 1
 _bn_grads = _sig("kfac_bn_grads", [_i32, _pi32, _pi32, ctypes.POINTER(_P), ctypes.POINTER(_P), ctypes.c_int, _i32,
                                     ctypes.POINTER(_P)])
 _bn_precondition = _sig("kfac_bn_precondition", [_i32, _pi32, _i32, ctypes.POINTER(_P), ctypes.POINTER(_P), _f32, _i32,
-                                                  ctypes.POINTER(_P), _P])
+                                                  ctypes.POINTER(_P), _P, _i64, _P])
+_bn_ws_bytes = _sig("kfac_bn_ws_bytes", [_i32, _pi32, _i32, _pi64])
 _update = _sig("kfac_update", [_P, _P, ctypes.POINTER(_P), ctypes.POINTER(_P), _f32, _f32, _i32, _f32, _P, _P])
 
 EXPORTS = ["kfac_last_error", "kfac_version", "kfac_launch_count", "kfac_plan_create", "kfac_plan_query", "kfac_plan_rank_layers",
@@ -97,7 +98,7 @@ EXPORTS = ["kfac_last_error", "kfac_version", "kfac_launch_count", "kfac_plan_cr
            "kfac_factor_G", "kfac_factor_ws_bytes", "kfac_factor_all", "kfac_reduce_scatter_factors",
            "kfac_damped_inverse", "kfac_precondition", "kfac_allgather_precond", "kfac_plan_create_stale",
            "kfac_plan_is_stale", "kfac_refresh_interval", "kfac_refresh", "kfac_factor_diff", "kfac_update", "kfac_bn_grads",
-           "kfac_bn_precondition"]
+           "kfac_bn_precondition", "kfac_bn_ws_bytes"]
 
 
 def _check(st, where):
@@ -299,8 +300,16 @@ def bn_grads(c, hw, xhat, gy, n, S, stream=None):
                      _DT[xhat[0].dtype], int(n), _parr(S), _stream(stream)), "kfac_bn_grads")
 
 
-def bn_precondition(c, n, S, grad, gamma_bn, full, out, stream=None):
-    """kfac_bn_precondition: (F + gamma_bn I)^-1 grad (full, Woodbury) or the diagonal version."""
+def bn_ws_bytes(c, n):
     nl = len(c)
+    b = ctypes.c_int64()
+    _check(_bn_ws_bytes(nl, (ctypes.c_int32 * nl)(*c), int(n), ctypes.byref(b)), "kfac_bn_ws_bytes")
+    return b.value
+
+
+def bn_precondition(c, n, S, grad, gamma_bn, full, out, ws=None, stream=None):
+    """kfac_bn_precondition: (F + gamma_bn I)^-1 grad (full, Woodbury; ws of bn_ws_bytes) or the diagonal."""
+    nl = len(c)
+    wsb = ws.numel() * ws.element_size() if ws is not None else 0
     _check(_bn_precondition(nl, (ctypes.c_int32 * nl)(*c), int(n), _parr(S), _parr(grad), float(gamma_bn),
-                            1 if full else 0, _parr(out), _stream(stream)), "kfac_bn_precondition")
+                            1 if full else 0, _parr(out), _ptr(ws), wsb, _stream(stream)), "kfac_bn_precondition")

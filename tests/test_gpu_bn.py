@@ -48,9 +48,10 @@ def _run(K, orc, cs, hws, n, dt=torch.bfloat16, seed=0, check_e2e=True):
     K.bn_grads(cs, hws, [x.cuda() for x in xs], [g.cuda() for g in gys], n, S)
     lam = RHO_BN * GAMMA
     outs = {}
+    ws = torch.empty(K.bn_ws_bytes(cs, n), dtype=torch.uint8, device="cuda")
     for full in (0, 1):
         o = [torch.empty(2 * c, device="cuda") for c in cs]
-        K.bn_precondition(cs, n, S, [g.cuda() for g in grads], lam, full, o)
+        K.bn_precondition(cs, n, S, [g.cuda() for g in grads], lam, full, o, ws if full else None)
         outs[full] = o
     torch.cuda.synchronize()
     worst = {"S": 0.0, "diag": 0.0, "full": 0.0, "stage": 0.0}
@@ -102,6 +103,8 @@ def test_bn_sample_limit(K, orc):
     g = [torch.zeros(128, device="cuda")]
     with pytest.raises(K.KfacError, match="ERR_UNSUPPORTED"):
         K.bn_precondition([64], 129, S, g, 0.4, 1, [torch.empty(128, device="cuda")])
+    with pytest.raises(K.KfacError, match="ERR_ARG"):  # full mode without its workspace
+        K.bn_precondition([64], 4, S, g, 0.4, 1, [torch.empty(128, device="cuda")])
     K.bn_precondition([64], 129, S, g, 0.4, 0, [torch.empty(128, device="cuda")])  # diag: any n
     with pytest.raises(K.KfacError, match="ERR_ARG"):
         K.bn_precondition([64], 4, S, g, 0.0, 0, [torch.empty(128, device="cuda")])
