@@ -143,9 +143,8 @@ __device__ __forceinline__ void grads_octets(const BnGradParams &P, int l, int b
             red[warp][lane][8 + e] = sb[e];
         }
     __syncthreads();
-    // thread t < 2 * 8 * lpp: octet lane t / 16, element (t % 16): scale e < 8, shift e >= 8
-    const int t = threadIdx.x;
-    if (t < 16 * lpp) {
+    // item t < 16 * lpp: octet lane t / 16, element t % 16 (scale e < 8, shift e >= 8)
+    for (int t = threadIdx.x; t < 16 * lpp; t += kBnThreads) {
         const int ol = t / 16, e = t % 16;
         float v = 0.f;
 #pragma unroll
@@ -246,6 +245,7 @@ __global__ void __launch_bounds__(kBnThreads) bn_solve_kernel(const __grid_const
     const int it0 = P.item0[l], nit = P.item0[l + 1] - it0;
     for (int q = tid; q < npair + n; q += kBnThreads) {
         double acc = 0.0;
+#pragma unroll 8
         for (int it = 0; it < nit; it++) acc += P.ws[(int64_t)(it0 + it) * (npair + n) + q];
         if (q < npair) {
             int a, bb;
@@ -271,22 +271,27 @@ __global__ void __launch_bounds__(kBnThreads) bn_solve_kernel(const __grid_const
         }
         __syncthreads();
     }
-    if (tid == 0) {  // L z = u, L^T y = z (y in u)
+    if (tid < 32) {  // L z = u, then L^T y = z (y in u): warp 0, column-oriented, lanes over rows
         for (int i = 0; i < n; i++) {
-            double t = u[i];
-            for (int j = 0; j < i; j++) t -= K[i * n + j] * u[j];
-            u[i] = t / K[i * n + i];
+            const double zi = u[i] / K[i * n + i];
+            __syncwarp();
+            if (tid == 0) u[i] = zi;
+            for (int j = i + 1 + tid; j < n; j += 32) u[j] -= K[j * n + i] * zi;
+            __syncwarp();
         }
         for (int i = n - 1; i >= 0; i--) {
-            double t = u[i];
-            for (int j = i + 1; j < n; j++) t -= K[j * n + i] * u[j];
-            u[i] = t / K[i * n + i];
+            const double yi = u[i] / K[i * n + i];
+            __syncwarp();
+            if (tid == 0) u[i] = yi;
+            for (int j = tid; j < i; j += 32) u[j] -= K[i * n + j] * yi;
+            __syncwarp();
         }
     }
     __syncthreads();
     for (int i = tid; i < C2; i += kBnThreads) {
         double t = v[i];
-        for (int a = 0; a < n; a++) t -= (double)S[(int64_t)a * C2 + i] * u[a];
+#pragma unroll 8
+        for (int a = 0; a < n; a++) t -= (double)__ldg(S + (int64_t)a * C2 + i) * u[a];
         out[i] = (float)(t / lam);
     }
 }
