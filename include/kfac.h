@@ -317,6 +317,16 @@ KFAC_API kfac_status kfac_bn_precondition(int32_t nl, const int32_t *c /* host [
                                  const float *const *S /* host [nl] */, const float *const *grad /* host [nl] */,
                                  float gamma_bn, int32_t full, float *const *out /* host [nl] */, void *ws,
                                  int64_t ws_bytes, void *stream);
+/* Multi-GPU BN Fisher: every rank receives all ranks' per-sample gradients,
+ * S_all[l] = [S_local[l] of rank 0; ...; of rank world-1] ([world * n_local][2C], the
+ * samples of the global batch, so F over S_all is the mean of the ranks' F, P:319-321,
+ * R-11), and grad[l] becomes the mean over ranks in place; then every rank runs
+ * kfac_bn_precondition with n = world * n_local (BN work is tiny, so it is replicated
+ * instead of owned, R-22).  One NCCL group of AllGathers / AllReduces over NVLink.
+ * Errors: KFAC_ERR_ARG, KFAC_ERR_NCCL.                                              */
+KFAC_API kfac_status kfac_bn_exchange(kfac_comm_t comm, int32_t nl, const int32_t *c /* host [nl] */, int32_t n_local,
+                             const float *const *S_local /* host [nl] */, float *const *S_all /* host [nl] */,
+                             float *const *grad /* host [nl] */, void *stream);
 /* Workspace bytes kfac_bn_precondition's full mode needs for these layers and n. */
 KFAC_API kfac_status kfac_bn_ws_bytes(int32_t nl, const int32_t *c /* host [nl] */, int32_t n,
                              int64_t *bytes /* host */);

@@ -349,6 +349,22 @@ kfac_status kfac_bn_grads(int32_t nl, const int32_t *c, const int32_t *hw, const
     return bn_grads_launch(jobs, n, dt == KFAC_FP16 ? 1 : 0, S(stream));
 }
 
+kfac_status kfac_bn_exchange(kfac_comm_t cm, int32_t nl, const int32_t *c, int32_t n_local, const float *const *S_local,
+                             float *const *S_all, float *const *grad, void *stream) {
+    if (!cm || nl < 1 || !c || !S_local || !S_all || !grad || n_local < 1)
+        return set_error(KFAC_ERR_ARG, "kfac_bn_exchange: NULL argument / nl, n_local < 1");
+    for (int l = 0; l < nl; l++)
+        if (!S_local[l] || !S_all[l] || !grad[l] || c[l] < 1) return set_error(KFAC_ERR_ARG, "kfac_bn_exchange: layer argument");
+    KFAC_NCCL_TRY(ncclGroupStart());
+    for (int l = 0; l < nl; l++) {
+        const size_t cnt = (size_t)n_local * 2 * c[l];
+        KFAC_NCCL_TRY(ncclAllGather(S_local[l], S_all[l], cnt, ncclFloat32, cm->comm, S(stream)));
+        KFAC_NCCL_TRY(ncclAllReduce(grad[l], grad[l], (size_t)2 * c[l], ncclFloat32, ncclAvg, cm->comm, S(stream)));
+    }
+    KFAC_NCCL_TRY(ncclGroupEnd());
+    return KFAC_OK;
+}
+
 kfac_status kfac_bn_ws_bytes(int32_t nl, const int32_t *c, int32_t n, int64_t *bytes) {
     if (nl < 1 || !c || !bytes || n < 1) return set_error(KFAC_ERR_ARG, "kfac_bn_ws_bytes");
     *bytes = bn_ws_bytes(std::vector<int>(c, c + nl), n);

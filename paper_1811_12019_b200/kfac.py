@@ -90,6 +90,8 @@ _bn_grads = _sig("kfac_bn_grads", [_i32, _pi32, _pi32, ctypes.POINTER(_P), ctype
                                     ctypes.POINTER(_P)])
 _bn_precondition = _sig("kfac_bn_precondition", [_i32, _pi32, _i32, ctypes.POINTER(_P), ctypes.POINTER(_P), _f32, _i32,
                                                   ctypes.POINTER(_P), _P, _i64, _P])
+_bn_exchange = _sig("kfac_bn_exchange", [_P, _i32, _pi32, _i32, ctypes.POINTER(_P), ctypes.POINTER(_P),
+                                          ctypes.POINTER(_P), _P])
 _bn_ws_bytes = _sig("kfac_bn_ws_bytes", [_i32, _pi32, _i32, _pi64])
 _update = _sig("kfac_update", [_P, _P, ctypes.POINTER(_P), ctypes.POINTER(_P), _f32, _f32, _i32, _f32, _P, _P])
 
@@ -98,7 +100,7 @@ EXPORTS = ["kfac_last_error", "kfac_version", "kfac_launch_count", "kfac_plan_cr
            "kfac_factor_G", "kfac_factor_ws_bytes", "kfac_factor_all", "kfac_reduce_scatter_factors",
            "kfac_damped_inverse", "kfac_precondition", "kfac_allgather_precond", "kfac_plan_create_stale",
            "kfac_plan_is_stale", "kfac_refresh_interval", "kfac_refresh", "kfac_factor_diff", "kfac_update", "kfac_bn_grads",
-           "kfac_bn_precondition", "kfac_bn_ws_bytes"]
+           "kfac_bn_precondition", "kfac_bn_ws_bytes", "kfac_bn_exchange"]
 
 
 def _check(st, where):
@@ -313,3 +315,10 @@ def bn_precondition(c, n, S, grad, gamma_bn, full, out, ws=None, stream=None):
     wsb = ws.numel() * ws.element_size() if ws is not None else 0
     _check(_bn_precondition(nl, (ctypes.c_int32 * nl)(*c), int(n), _parr(S), _parr(grad), float(gamma_bn),
                             1 if full else 0, _parr(out), _ptr(ws), wsb, _stream(stream)), "kfac_bn_precondition")
+
+
+def bn_exchange(comm, c, n_local, S_local, S_all, grad, stream=None):
+    """kfac_bn_exchange: AllGather of the per-sample BN gradients, mean AllReduce of the BN grads."""
+    nl = len(c)
+    _check(_bn_exchange(comm.h, nl, (ctypes.c_int32 * nl)(*c), int(n_local), _parr(S_local), _parr(S_all), _parr(grad),
+                        _stream(stream)), "kfac_bn_exchange")

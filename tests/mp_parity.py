@@ -9,7 +9,8 @@ oracle simulating the same P ranks (oracle.kfac_step):
   * every layer's preconditioned gradient in the gathered buffer (stage 6),
   * that the AllGather buffers of all ranks are bitwise identical (replica consistency);
 then a stale-factor step (NEXT-1, R-20: new dW, dW-only ReduceScatter, the
-cached inverses) against oracle.stale_results, replicas again identical.
+cached inverses) against oracle.stale_results, replicas again identical; and the BN
+Fisher across ranks (kfac_bn_exchange + replicated kfac_bn_precondition, R-22).
 Exit code 0 on success.
 """
 import os
@@ -131,6 +132,42 @@ def main():
         print(f"mp_parity {cfg} P={world} stale step: end-to-end max err {serr:.2e}, replicas identical {ok}",
               flush=True)
         ok &= serr <= 2e-3
+    # ---- BN Fisher across ranks (NEXT-2, R-22): AllGather of S, mean of the BN grads, replicated solve
+    bc, bhw = [64, 256, 6], [25, 9, 16]
+    gb = torch.Generator().manual_seed(500 + rank)
+    bx = [torch.randn(n, hw, c, generator=gb).to(torch.bfloat16) for c, hw in zip(bc, bhw)]
+    bg = [(torch.randn(n, hw, c, generator=gb) * 0.05).to(torch.bfloat16) for c, hw in zip(bc, bhw)]
+    bgr = [torch.randn(2 * c, generator=gb) for c in bc]
+    S_loc = [torch.empty(n, 2 * c, device=dev) for c in bc]
+    S_all = [torch.empty(world * n, 2 * c, device=dev) for c in bc]
+    gdev = [g.to(dev) for g in bgr]
+    K.bn_grads(bc, bhw, [x.to(dev) for x in bx], [g.to(dev) for g in bg], n, S_loc)
+    K.bn_exchange(comm, bc, n, S_loc, S_all, gdev)
+    bws = torch.empty(K.bn_ws_bytes(bc, world * n), dtype=torch.uint8, device=dev)
+    bout = {f: [torch.empty(2 * c, device=dev) for c in bc] for f in (0, 1)}
+    for f in (0, 1):
+        K.bn_precondition(bc, world * n, S_all, gdev, 0.4, f, bout[f], bws if f else None)
+    torch.cuda.synchronize()
+    ball = [None] * world
+    dist.all_gather_object(ball, ([inputs.half_bits(x) for x in bx], [inputs.half_bits(g) for g in bg],
+                                  [g.numpy() for g in bgr]))
+    mine = [torch.cat([bout[0][i], bout[1][i]]) for i in range(len(bc))]
+    allb = [[torch.empty_like(m) for _ in range(world)] for m in mine]
+    for i, m in enumerate(mine):
+        dist.all_gather(allb[i], m)
+    if rank == 0:
+        import oracle
+        berr = 0.0
+        for i, (c, hw) in enumerate(zip(bc, bhw)):
+            ok &= all(torch.equal(b, allb[i][0]) for b in allb[i][1:])  # replicated: identical on every rank
+            Sg = np.concatenate([oracle.bn_sample_grads(ball[r][0][i], ball[r][1][i], n, hw, c) for r in range(world)])
+            gm = sum(ball[r][2][i].astype(np.float64) for r in range(world)) / world
+            got = allb[i][0].cpu().double().numpy()
+            for f, mode in ((0, "diag"), (1, "full")):
+                want = oracle.bn_precondition(oracle.bn_fisher(Sg, mode), gm, 0.4)
+                berr = max(berr, relerr(got[f * 2 * c:(f + 1) * 2 * c], want))
+        print(f"mp_parity {cfg} P={world} BN Fisher: max err {berr:.2e}, replicas identical {ok}", flush=True)
+        ok &= berr <= 2e-3
     flag = torch.tensor([1 if ok else 0], device=dev)
     dist.broadcast(flag, 0)
     dist.barrier(device_ids=[local])

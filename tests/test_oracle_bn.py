@@ -58,3 +58,14 @@ def test_bn_sample_grads_vs_autograd(orc, fmt):
         (y * gy[s].double()).sum().backward()
         want = torch.cat([gam.grad, bet.grad]).numpy()
         assert np.allclose(S[s], want, rtol=1e-12, atol=1e-12)
+
+
+def test_bn_fisher_rank_mean(orc):
+    """The ranks' mean of F (the paper's ReduceScatter mean) is F of the concatenated
+    per-sample gradients (what kfac_bn_exchange + a replicated solve computes, R-22)."""
+    rng = np.random.default_rng(2)
+    parts = [rng.standard_normal((4, 10)) for _ in range(3)]
+    mean_F = sum(orc.bn_fisher(p, "full") for p in parts) / 3
+    assert np.allclose(orc.bn_fisher(np.concatenate(parts), "full"), mean_F, rtol=1e-13, atol=1e-13)
+    mean_d = sum(orc.bn_fisher(p, "diag") for p in parts) / 3
+    assert np.allclose(orc.bn_fisher(np.concatenate(parts), "diag"), mean_d, rtol=1e-13, atol=1e-13)
