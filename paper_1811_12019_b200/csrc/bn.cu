@@ -19,7 +19,8 @@
 //   bn_gram_kernel     full mode: partial K = S S^T and u = S v over 64-column work items (all layers
 //                      in one launch, S staged as fp64 in shared memory).
 //   bn_solve_kernel    full mode, one CTA per layer: fixed-order sum of the partials, K + lambda N I,
-//                      fp64 Cholesky solve, out = (v - S^T y) / lambda.
+//                      fp64 Cholesky solve for y;
+//   bn_out_kernel      out = (v - S^T y) / lambda, column-parallel.
 #include <cmath>
 
 #include <cuda_fp16.h>
@@ -53,6 +54,7 @@ struct BnPrecParams {
     int32_t nl, n;
     double lambda;
     double *ws;  // Gram partials: per item n(n+1)/2 + n doubles
+    double *y;   // [nl][n] solved y of each layer (after the partials in the workspace)
 };
 
 __device__ __forceinline__ float2 h2f(uint32_t v, int fp16) {
@@ -237,8 +239,6 @@ __global__ void __launch_bounds__(kBnThreads) bn_gram_kernel(const __grid_consta
 __global__ void __launch_bounds__(kBnThreads) bn_solve_kernel(const __grid_constant__ BnPrecParams P) {
     extern __shared__ double bsm[];
     const int l = blockIdx.x, C2 = 2 * P.c[l], n = P.n, tid = threadIdx.x, npair = n * (n + 1) / 2;
-    const float *S = P.S[l], *v = P.grad[l];
-    float *out = P.out[l];
     const double lam = P.lambda;
     double *K = bsm;       // [n][n]
     double *u = K + n * n;  // [n]
@@ -288,12 +288,22 @@ __global__ void __launch_bounds__(kBnThreads) bn_solve_kernel(const __grid_const
         }
     }
     __syncthreads();
-    for (int i = tid; i < C2; i += kBnThreads) {
-        double t = v[i];
+    if (tid < n) P.y[l * n + tid] = u[tid];  // bn_out_kernel finishes the layer column-parallel
+}
+
+// full Fisher, phase 3: out = (v - S^T y) / lambda, grid (256-column blocks, layer)
+__global__ void __launch_bounds__(kBnThreads) bn_out_kernel(const __grid_constant__ BnPrecParams P) {
+    __shared__ double ys[kBnMaxSamples];
+    const int l = blockIdx.y, C2 = 2 * P.c[l], n = P.n;
+    for (int a = threadIdx.x; a < n; a += kBnThreads) ys[a] = P.y[l * n + a];
+    __syncthreads();
+    const int i = blockIdx.x * kBnThreads + threadIdx.x;
+    if (i >= C2) return;
+    const float *S = P.S[l];
+    double t = P.grad[l][i];
 #pragma unroll 8
-        for (int a = 0; a < n; a++) t -= (double)__ldg(S + (int64_t)a * C2 + i) * u[a];
-        out[i] = (float)(t / lam);
-    }
+    for (int a = 0; a < n; a++) t -= (double)__ldg(S + (int64_t)a * C2 + i) * ys[a];
+    P.out[l][i] = (float)(t / P.lambda);
 }
 
 }  // namespace
@@ -303,7 +313,7 @@ static int64_t gram_items(int c) { return (2 * (int64_t)c + kGramCols - 1) / kGr
 int64_t bn_ws_bytes(const std::vector<int> &cs, int n) {
     int64_t items = 0;
     for (int c : cs) items += gram_items(c);
-    return items * ((int64_t)n * (n + 1) / 2 + n) * 8;
+    return items * ((int64_t)n * (n + 1) / 2 + n) * 8 + (int64_t)cs.size() * n * 8;
 }
 
 kfac_status bn_grads_launch(const std::vector<BnJob> &jobs, int n, int fp16, cudaStream_t st) {
@@ -370,10 +380,14 @@ kfac_status bn_precond_launch(const std::vector<BnJob> &jobs, int n, int full, d
         }
         if (!ws || bn_ws_bytes(cs, n) > ws_bytes)
             return set_error(KFAC_ERR_ARG, "kfac_bn_precondition: full mode needs kfac_bn_ws_bytes of workspace");
+        P.y = ws + (bn_ws_bytes(cs, n) / 8 - (int64_t)P.nl * n);
         bn_gram_kernel<<<items, kBnThreads, gsmem, st>>>(P);
         KFAC_LAUNCHED();
         KFAC_CUDA_TRY(cudaGetLastError());
         bn_solve_kernel<<<P.nl, kBnThreads, ssmem, st>>>(P);
+        KFAC_LAUNCHED();
+        KFAC_CUDA_TRY(cudaGetLastError());
+        bn_out_kernel<<<dim3((2 * cmax + kBnThreads - 1) / kBnThreads, P.nl), kBnThreads, 0, st>>>(P);
         KFAC_LAUNCHED();
         KFAC_CUDA_TRY(cudaGetLastError());
     }
