@@ -238,7 +238,7 @@ __global__ void __launch_bounds__(kBnThreads) bn_gram_kernel(const __grid_consta
 // Cholesky K = L L^T and the two triangular solves in shared memory; out = (v - S^T y) / lambda
 __global__ void __launch_bounds__(kBnThreads) bn_solve_kernel(const __grid_constant__ BnPrecParams P) {
     extern __shared__ double bsm[];
-    const int l = blockIdx.x, C2 = 2 * P.c[l], n = P.n, tid = threadIdx.x, npair = n * (n + 1) / 2;
+    const int l = blockIdx.x, n = P.n, tid = threadIdx.x, npair = n * (n + 1) / 2;
     const double lam = P.lambda;
     double *K = bsm;       // [n][n]
     double *u = K + n * n;  // [n]
