@@ -292,6 +292,9 @@ kfac_status kfac_precondition(kfac_plan_t p, int32_t rank, const float *recv, co
         j.Ginv = inv_ws + p->inv_off[rank][2 * k + 1];
         j.tmp = w + off;
         off += align16(precond_ws_floats(g.dG, g.dA));
+        j.sA = const_cast<float *>(inv_ws) + p->split_off[rank][2 * k];
+        j.sG = const_cast<float *>(inv_ws) + p->split_off[rank][2 * k + 1];
+        j.resplit = p->stale ? 0 : 1;
         if (p->owner[l] == rank) {
             j.out = ag_buf + p->ag_off[l];
         } else {

@@ -17,6 +17,7 @@ struct kfac_plan {
     std::vector<int64_t> seg_off, ag_off;
     int64_t rs_chunk = 0, ag_chunk = 0, ws_bytes = 0, factor_ws = 0;
     std::vector<std::vector<int64_t>> inv_off;  // per rank: 2 per owned layer
+    std::vector<std::vector<int64_t>> split_off;  // per rank: 2 per owned layer (3xTF32 split cache, after the inverses)
     std::vector<int64_t> inv_floats;
     // cached grouped factor launch (re-encoded when the pointers change)
     std::vector<const void *> c_xs, c_gys;

@@ -151,6 +151,7 @@ kfac_status plan_build(kfac_plan *p) {
     for (int l = 0; l < L; l++) p->ag_off[l] = (int64_t)p->owner[l] * p->ag_chunk + agl[l];
     // per-rank inverse layout and stage workspaces
     p->inv_off.assign(P, {});
+    p->split_off.assign(P, {});
     p->inv_floats.assign(P, 0);
     int64_t ws = 0;
     for (int r = 0; r < P; r++) {
@@ -169,6 +170,14 @@ kfac_status plan_build(kfac_plan *p) {
                 sum_tasks += inverse_tasks(n);
             }
             prec_ws += (align16(precond_ws_floats(g.dG, g.dA)) + align16((int64_t)g.dG * g.dA)) * 4;  // split operands + (redundant) output
+        }
+        // the inverses' 3xTF32 hi / lo split, written by a full step's precondition and reused by stale steps
+        for (int l : p->owned[r]) {
+            const Geom &g = p->geoms[l];
+            p->split_off[r].push_back(off);
+            off = align16(off + precond_split_floats(g.dA));
+            p->split_off[r].push_back(off);
+            off = align16(off + precond_split_floats(g.dG));
         }
         p->inv_floats[r] = off;
         inv_ws += align16(inverse_scratch_bytes((int)p->owned[r].size(), sum_nt, sum_tiles, sum_tasks));  // pair scratch, counters, flags

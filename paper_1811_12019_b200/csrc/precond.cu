@@ -278,6 +278,8 @@ static kfac_status split_map(CUtensorMap *m, float *base, int rows, int Kp) {
 
 static int64_t kpad(int k) { return (k + 3) / 4 * 4; }
 
+int64_t precond_split_floats(int n) { return 2 * (int64_t)n * kpad(n); }
+
 int64_t precond_ws_floats(int dG, int dA) {
     // A_d^-1 split, G_d^-1 split, dW split, T^T split (all [2][rows][Kp]) + output staging
     return 2 * ((int64_t)dA * kpad(dA) + (int64_t)dG * kpad(dG) + (int64_t)dG * kpad(dA) + (int64_t)dA * kpad(dG)) + 64;
@@ -338,15 +340,15 @@ kfac_status precond_launch(const std::vector<PrecJob> &jobs, cudaStream_t st) {
     for (const PrecJob &j : jobs) {
         float *w = j.tmp;
         const int dA = j.dA, dG = j.dG;
-        float *sA = w;
+        float *sA = j.sA ? j.sA : w;  // the inverses' split lives in inv_ws when the plan provides it
         w += 2 * (int64_t)dA * kpad(dA);
-        float *sG = w;
+        float *sG = j.sG ? j.sG : w;
         w += 2 * (int64_t)dG * kpad(dG);
         float *sW = w;
         w += 2 * (int64_t)dG * kpad(dA);
         float *sT = w;
-        sj.push_back({j.Ainv, sA, dA, dA, dA, (int32_t)kpad(dA)});
-        sj.push_back({j.Ginv, sG, dG, dG, dG, (int32_t)kpad(dG)});
+        if (j.resplit || !j.sA) sj.push_back({j.Ainv, sA, dA, dA, dA, (int32_t)kpad(dA)});
+        if (j.resplit || !j.sG) sj.push_back({j.Ginv, sG, dG, dG, dG, (int32_t)kpad(dG)});
         sj.push_back({j.dW, sW, dG, dA, dA, (int32_t)kpad(dA)});
         GemmProb a{};
         kfac_status s = split_map(&a.tA, sA, dA, (int)kpad(dA));
