@@ -318,7 +318,7 @@ int64_t bn_ws_bytes(const std::vector<int> &cs, int n) {
 
 kfac_status bn_grads_launch(const std::vector<BnJob> &jobs, int n, int fp16, cudaStream_t st) {
     for (size_t j0 = 0; j0 < jobs.size(); j0 += kBnMax) {
-        static BnGradParams P;
+        thread_local BnGradParams P;  // host staging (per thread: calls may come from several threads)
         P.nl = (int)std::min<size_t>(kBnMax, jobs.size() - j0);
         P.n = n;
         P.fp16 = fp16;
@@ -353,7 +353,7 @@ kfac_status bn_precond_launch(const std::vector<BnJob> &jobs, int n, int full, d
         KFAC_CUDA_TRY(cudaFuncSetAttribute(bn_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssmem));
     }
     for (size_t j0 = 0; j0 < jobs.size(); j0 += kBnMax) {
-        static BnPrecParams P;
+        thread_local BnPrecParams P;
         P.nl = (int)std::min<size_t>(kBnMax, jobs.size() - j0);
         P.n = n;
         P.lambda = lambda;

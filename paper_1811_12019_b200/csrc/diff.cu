@@ -129,7 +129,7 @@ __global__ void diff_final_kernel(const __grid_constant__ DiffParams P) {
 
 kfac_status diff_launch(const std::vector<DiffMat> &mats, double *ws, int64_t ws_bytes, cudaStream_t st) {
     for (size_t b0 = 0; b0 < mats.size(); b0 += kDiffMaxMats) {
-        static DiffParams P;  // host staging of the (large) parameter block
+        thread_local DiffParams P;  // host staging of the (large) parameter block, per calling thread
         P.nmats = (int)std::min<size_t>(kDiffMaxMats, mats.size() - b0);
         int32_t nb = 0;
         for (int k = 0; k < P.nmats; k++) {

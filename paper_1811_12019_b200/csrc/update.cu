@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(kUpdThreads) update_scale_kernel(const __grid_
 kfac_status update_launch(const std::vector<UpdJob> &jobs, float lr, float mom, int rescale, float eps, double *ws,
                           int64_t ws_bytes, cudaStream_t st) {
     for (size_t j0 = 0; j0 < jobs.size(); j0 += kUpdMaxLayers) {
-        static UpdParams P;  // host staging of the parameter block
+        thread_local UpdParams P;  // host staging of the parameter block, per calling thread
         P.nlayers = (int)std::min<size_t>(kUpdMaxLayers, jobs.size() - j0);
         int32_t nb = 0;
         for (int k = 0; k < P.nlayers; k++) {
