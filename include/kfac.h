@@ -259,8 +259,12 @@ KFAC_API kfac_status kfac_factor_diff(kfac_plan_t plan, int32_t rank, const floa
 /* ------------------------------------------------------------------ stage 5
  * For every layer owned by `rank`: P = G_d^-1 * dW * A_d^-1, dW
  * read from rs_recv.  The primary owner writes P into ag_buf at ag_off[l]
- * (its own AllGather slot); a redundant owner writes into `ws`.             */
-KFAC_API kfac_status kfac_precondition(kfac_plan_t plan, int32_t rank, const float *rs_recv, const float *inv_ws,
+ * (its own AllGather slot); a redundant owner writes into `ws`.  inv_ws is
+ * read AND written: on a full plan the call stores the 3xTF32 hi / lo split of
+ * each inverse after the inverses (the tail of inv_floats), and on a stale
+ * plan it reuses that split instead of re-splitting (R-20), so a stale step
+ * must follow a full-plan precondition on the same inv_ws.                  */
+KFAC_API kfac_status kfac_precondition(kfac_plan_t plan, int32_t rank, const float *rs_recv, float *inv_ws,
                               float *ag_buf /* [world*ag_chunk] */, void *ws, void *stream);
 
 /* ------------------------------------------------------------------ stage 6

@@ -273,7 +273,7 @@ kfac_status kfac_damped_inverse(kfac_plan_t p, int32_t rank, const float *recv, 
 }
 
 // ------------------------------------------------------------------ stage 5
-kfac_status kfac_precondition(kfac_plan_t p, int32_t rank, const float *recv, const float *inv_ws, float *ag_buf,
+kfac_status kfac_precondition(kfac_plan_t p, int32_t rank, const float *recv, float *inv_ws, float *ag_buf,
                               void *ws, void *stream) {
     if (!p || !recv || !inv_ws || !ag_buf || !ws) return set_error(KFAC_ERR_ARG, "kfac_precondition: NULL argument");
     if (rank < 0 || rank >= p->world) return set_error(KFAC_ERR_STATE, "kfac_precondition: rank out of range");
@@ -292,8 +292,8 @@ kfac_status kfac_precondition(kfac_plan_t p, int32_t rank, const float *recv, co
         j.Ginv = inv_ws + p->inv_off[rank][2 * k + 1];
         j.tmp = w + off;
         off += align16(precond_ws_floats(g.dG, g.dA));
-        j.sA = const_cast<float *>(inv_ws) + p->split_off[rank][2 * k];
-        j.sG = const_cast<float *>(inv_ws) + p->split_off[rank][2 * k + 1];
+        j.sA = inv_ws + p->split_off[rank][2 * k];
+        j.sG = inv_ws + p->split_off[rank][2 * k + 1];
         j.resplit = p->stale ? 0 : 1;
         if (p->owner[l] == rank) {
             j.out = ag_buf + p->ag_off[l];
