@@ -135,7 +135,8 @@ KFAC_API kfac_status kfac_plan_query(kfac_plan_t plan, int32_t *owner, int64_t *
  * (each may be NULL): n_owned; layers[n_owned]; local_off[3*n_owned] =
  * offsets of (dW, A, G) inside the rank's recv chunk; inv_off[2*n_owned] =
  * offsets (floats) of A_d^-1 and G_d^-1 inside inv_ws; inv_floats = size of
- * inv_ws in floats for this rank.                                           */
+ * inv_ws in floats for this rank (the inverses, then the precondition's
+ * cached 3xTF32 split of them).  A stale plan reports the same layout.      */
 KFAC_API kfac_status kfac_plan_rank_layers(kfac_plan_t plan, int32_t rank, int32_t *n_owned, int32_t *layers,
                                   int64_t *local_off, int64_t *inv_off, int64_t *inv_floats);
 
