@@ -165,6 +165,20 @@ KFAC_API kfac_status kfac_plan_create_stale(kfac_plan_t full, kfac_plan_t *out /
 /* 1 for a plan made by kfac_plan_create_stale, else 0. */
 KFAC_API int32_t kfac_plan_is_stale(kfac_plan_t plan);
 
+/* kfac_plan_create_grefresh: the plan of a step that refreshes G but keeps A stale (P:688-692,
+ * "we can also consider refreshing A_{l-1} less frequently than G_l"; S:549 per-kind
+ * intervals).  Same owners / inverse layout as `full`; each owned layer's segments are
+ * [dW, G packed] (A's seg_off / local_off are -1).  On this plan
+ *   kfac_factor_all       computes only the G factors (xs may be NULL);
+ *   kfac_damped_inverse   inverts only G_d = G + sqrt(gamma)/pi I, with pi READ from pi_out
+ *                         (the value the last full refresh wrote there, R-20); A_d^-1 in
+ *                         inv_ws and dev_status[2k] are left as they are;
+ *   kfac_precondition     re-splits G_d^-1 and reuses A_d^-1's cached split;
+ *   kfac_factor_diff      returns KFAC_ERR_STATE.                                          */
+KFAC_API kfac_status kfac_plan_create_grefresh(kfac_plan_t full, kfac_plan_t *out /* host */);
+/* 0 full plan, 1 G-refresh plan, 2 stale plan, -1 NULL. */
+KFAC_API int32_t kfac_plan_refresh_kind(kfac_plan_t plan);
+
 /* Refresh schedules of the stale-Fisher runs (host-only, no device work). */
 typedef enum {
     KFAC_REFRESH_RAMPUP = 0, /* interval^(e) = min(20, 5 floor(e/5) + 1) */

@@ -18,8 +18,9 @@ parts of the method in plain Python:
 * ``all_gather``       AllGatherV of the primary owners' 𝒢.
 * ``damping_schedule`` warmup damping recurrence (reading R-2).
 * ``kfac_step``        Algorithm 1's body minus fwd/bwd/update.
-* ``refresh_interval`` / ``refresh`` / ``fim_diff`` / ``diff_percentiles`` /
-  ``stale_results`` and ``plan(stale=True)``: stale Fisher information
+* ``refresh_interval`` / ``refresh`` / ``refresh_kinds`` / ``fim_diff`` /
+  ``diff_percentiles`` / ``stale_results`` / ``grefresh_results`` and
+  ``plan(stale=True | g_only=True)``: stale Fisher information
   (NEXT-1; reading R-20).
 * ``learning_rate`` / ``momentum`` / ``apply_update`` / ``rescale_weights`` /
   ``update_layer``: the update after the AllGather (NEXT-3; R-21).
@@ -285,7 +286,7 @@ def layer_cost(layer):
     return a ** 3 + g ** 3 + 2 * g * g * a + 2 * g * a * a
 
 
-def plan(layers, world, policy=POLICY_RR, stale=False):
+def plan(layers, world, policy=POLICY_RR, stale=False, g_only=False):
     """Owner map and owner-major segment layout.
 
     owner[l]: primary owner.  RR: l mod P.  LPT: layers by (-cost, l), each to
@@ -299,6 +300,10 @@ def plan(layers, world, policy=POLICY_RR, stale=False):
     "reduce the frequency of updating (A, G, F)"; reading R-20): the same
     owners, but each owned layer carries only its ∇W segment; the A and G
     offsets are None (seg_off -1).  The AG layout is unchanged.
+
+    g_only=True: the layout of a step that refreshes G but keeps A stale
+    (S:549): each owned layer carries [∇W, G packed]; A's offset is
+    None (seg_off -1).
     """
     L, P = len(layers), int(world)
     if L < 1 or P < 1:
@@ -327,6 +332,11 @@ def plan(layers, world, policy=POLICY_RR, stale=False):
             if stale:
                 m[l] = (o_w, None, None)
                 continue
+            if g_only:
+                o_g = off
+                off = _align(off + packed_len(g))
+                m[l] = (o_w, None, o_g)
+                continue
             o_a = off
             off = _align(off + packed_len(a))
             o_g = off
@@ -353,7 +363,7 @@ def plan(layers, world, policy=POLICY_RR, stale=False):
     ag_off = np.array([owner[l] * ag_chunk + ag_local[owner[l]][l] for l in range(L)], dtype=np.int64)
     return dict(owner=np.array(owner, dtype=np.int32), owned=owned, local=local,
                 seg_off=seg_off, rs_chunk=int(rs_chunk), ag_off=ag_off, ag_chunk=int(ag_chunk),
-                world=P, L=L, stale=bool(stale))
+                world=P, L=L, stale=bool(stale), g_only=bool(g_only))
 
 
 # --------------------------------------------------------------------------
@@ -388,10 +398,11 @@ def build_send(layers, pl, rank, factors, dws):
             a, g = dims(layers[l])
             base = r * c
             send[base + o_w: base + o_w + g * a] = np.asarray(dws[l], dtype=np.float64).reshape(-1)
-            if o_a is None:  # stale layout: ∇W only
+            if o_g is None:  # stale layout: ∇W only
                 continue
             A, G = factors[l]
-            send[base + o_a: base + o_a + packed_len(a)] = pack(A)
+            if o_a is not None:  # (a G-refresh layout carries no A)
+                send[base + o_a: base + o_a + packed_len(a)] = pack(A)
             send[base + o_g: base + o_g + packed_len(g)] = pack(G)
     return send
 
@@ -626,3 +637,31 @@ def bn_precondition(F, grad, gamma_bn):
     if st:
         raise ValueError("bn_precondition: F + gamma_bn I not positive definite")
     return X @ grad
+
+
+def refresh_kinds(t, epoch, schedule="rampup", fresh_floor=500, a_multiple=1):
+    """Per-kind refresh decision: G refreshes as ``refresh``; A with its interval
+    multiplied by ``a_multiple`` ("refreshing A_{l-1} less frequently than G_l").
+    Returns (refresh_A, refresh_G); A refreshing implies G refreshing."""
+    if int(a_multiple) < 1:
+        raise ValueError("a_multiple >= 1")
+    iv = refresh_interval(epoch, schedule)
+    rg = refresh(t, epoch, fresh_floor=fresh_floor, interval=iv)
+    ra = refresh(t, epoch, fresh_floor=fresh_floor, interval=iv * int(a_multiple))
+    return ra, rg
+
+
+def grefresh_results(layers, pl_g, rank, recv, gamma, cached):
+    """Stages 4-5 of a G-refresh step on one rank (R-20): G from the [∇W, G] recv chunk, damped with
+    the cached π of the last full refresh, G_d = G + (√γ/π) I; A_d⁻¹ cached.  `cached[l] = (Ainv, pi)`."""
+    out = {}
+    for l, (o_w, _, o_g) in pl_g["local"][rank].items():
+        a, g = dims(layers[l])
+        dW = recv[o_w:o_w + g * a].reshape(g, a)
+        G = unpack(recv[o_g:o_g + packed_len(g)])
+        Ainv, pi = cached[l]
+        G_d = G + (math.sqrt(gamma) / pi) * np.eye(g)
+        Ginv, sg = inverse(G_d)
+        pre = precondition(Ginv, Ainv, dW) if sg == 0 else None
+        out[l] = dict(G=G, G_d=G_d, Ginv=Ginv, dW=dW, precond=pre, status=sg)
+    return out

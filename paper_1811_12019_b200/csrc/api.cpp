@@ -94,7 +94,7 @@ kfac_status kfac_factor_ws_bytes(const kfac_layer_desc *layer, int32_t n, int32_
 kfac_status kfac_factor_all(kfac_plan_t p, const void *const *xs, const void *const *gys, kfac_dtype dt,
                             const float *alphaA, const float *alphaG, float *rs_send, void *ws, void *stream) {
     if (p && p->stale && rs_send) return replicate_dw(p, rs_send, stream);
-    if (!p || !xs || !gys || !rs_send) return set_error(KFAC_ERR_ARG, "kfac_factor_all: NULL argument");
+    if (!p || (!xs && !p->g_only) || !gys || !rs_send) return set_error(KFAC_ERR_ARG, "kfac_factor_all: NULL argument");
     if (dt != KFAC_BF16 && dt != KFAC_FP16) return set_error(KFAC_ERR_ARG, "kfac_factor_all: dtype");
     if (p->factor_ws > 0 && !ws) return set_error(KFAC_ERR_ARG, "kfac_factor_all: workspace required");
     const int L = p->L;
@@ -104,10 +104,11 @@ kfac_status kfac_factor_all(kfac_plan_t p, const void *const *xs, const void *co
         const double rows = (double)p->n_local * g.ho * g.wo;
         aA[l] = alphaA ? alphaA[l] : (float)(1.0 / rows);
         aG[l] = alphaG ? alphaG[l] : (float)(1.0 / rows);
-        if (!xs[l] || !gys[l]) return set_error(KFAC_ERR_ARG, "kfac_factor_all: NULL input pointer");
+        if ((!p->g_only && !xs[l]) || !gys[l]) return set_error(KFAC_ERR_ARG, "kfac_factor_all: NULL input pointer");
     }
-    const bool same = p->c_dt == (int)dt && p->c_send == rs_send && p->c_ws == ws &&
-                      p->c_xs == std::vector<const void *>(xs, xs + L) &&
+    const std::vector<const void *> xv = p->g_only ? std::vector<const void *>(L, nullptr)
+                                                   : std::vector<const void *>(xs, xs + L);
+    const bool same = p->c_dt == (int)dt && p->c_send == rs_send && p->c_ws == ws && p->c_xs == xv &&
                       p->c_gys == std::vector<const void *>(gys, gys + L) && p->c_aA == aA && p->c_aG == aG;
     if (!same) {
         p->c_jobs.clear();
@@ -116,10 +117,10 @@ kfac_status kfac_factor_all(kfac_plan_t p, const void *const *xs, const void *co
             a.g = p->geoms[l];
             a.n = p->n_local;
             a.is_A = true;
-            a.src = xs[l];
-            a.out = rs_send + p->seg_off[3 * l + 1];
+            a.src = p->g_only ? nullptr : xs[l];
+            a.out = p->g_only ? nullptr : rs_send + p->seg_off[3 * l + 1];
             a.alpha = aA[l];
-            p->c_jobs.push_back(a);
+            if (!p->g_only) p->c_jobs.push_back(a);  // a G refresh keeps A stale
             FactorJob b = a;
             b.is_A = false;
             b.src = gys[l];
@@ -135,7 +136,7 @@ kfac_status kfac_factor_all(kfac_plan_t p, const void *const *xs, const void *co
         p->c_dt = (int)dt;
         p->c_send = rs_send;
         p->c_ws = ws;
-        p->c_xs.assign(xs, xs + L);
+        p->c_xs = xv;
         p->c_gys.assign(gys, gys + L);
         p->c_aA = aA;
         p->c_aG = aG;
@@ -152,6 +153,7 @@ kfac_status kfac_factor_all(kfac_plan_t p, const void *const *xs, const void *co
             const Geom &g = p->geoms[l];
             const int64_t n3[3] = {(int64_t)g.dG * g.dA, packed_len(g.dA), packed_len(g.dG)};
             for (int s3 = 0; s3 < 3; s3++) {
+                if (p->local[r][k][s3] < 0) continue;  // segment absent from this layout
                 sd.push_back({rs_send + p->seg_off[3 * l + s3], rs_send + (int64_t)r * p->rs_chunk + p->local[r][k][s3]});
                 cnt.push_back(n3[s3]);
             }
@@ -165,7 +167,7 @@ kfac_status kfac_factor_all(kfac_plan_t p, const void *const *xs, const void *co
 kfac_status kfac_factor_diff(kfac_plan_t p, int32_t rank, const float *recv_cur, const float *recv_prev, double *diff,
                              void *ws, void *stream) {
     if (!p || !recv_cur || !recv_prev || !diff || !ws) return set_error(KFAC_ERR_ARG, "kfac_factor_diff: NULL argument");
-    if (p->stale) return set_error(KFAC_ERR_STATE, "kfac_factor_diff: a stale plan carries no factors");
+    if (p->stale || p->g_only) return set_error(KFAC_ERR_STATE, "kfac_factor_diff: needs the full plan's recv chunks");
     if (rank < 0 || rank >= p->world) return set_error(KFAC_ERR_STATE, "kfac_factor_diff: rank out of range");
     const auto &ow = p->owned[rank];
     std::vector<DiffMat> mats;
@@ -250,10 +252,12 @@ kfac_status kfac_damped_inverse(kfac_plan_t p, int32_t rank, const float *recv, 
             sum_tasks += inverse_tasks(n);
         }
     int64_t off = align16(inverse_scratch_bytes((int)ow.size(), sum_nt, sum_tiles, sum_tasks));
+    if (p->g_only && !pi_out)
+        return set_error(KFAC_ERR_ARG, "kfac_damped_inverse: a G refresh reads the cached pi from pi_out");
     std::vector<InvMat> mats;
     for (size_t k = 0; k < ow.size(); k++) {
         const Geom &g = p->geoms[ow[k]];
-        for (int which = 0; which < 2; which++) {
+        for (int which = p->g_only ? 1 : 0; which < 2; which++) {
             InvMat m{};
             m.n = which == 0 ? g.dA : g.dG;
             m.packed = recv + p->local[rank][k][1 + which];
@@ -269,7 +273,7 @@ kfac_status kfac_damped_inverse(kfac_plan_t p, int32_t rank, const float *recv, 
         }
     }
     if (off > p->ws_bytes) return set_error(KFAC_ERR_STATE, "kfac_damped_inverse: workspace layout exceeds ws_bytes");
-    return inverse_launch(mats, (int)ow.size(), gamma, pair_scratch, pi_out, S(stream));
+    return inverse_launch(mats, (int)ow.size(), gamma, pair_scratch, pi_out, p->g_only ? 1 : 0, S(stream));
 }
 
 // ------------------------------------------------------------------ stage 5
@@ -294,7 +298,9 @@ kfac_status kfac_precondition(kfac_plan_t p, int32_t rank, const float *recv, fl
         off += align16(precond_ws_floats(g.dG, g.dA));
         j.sA = inv_ws + p->split_off[rank][2 * k];
         j.sG = inv_ws + p->split_off[rank][2 * k + 1];
-        j.resplit = p->stale ? 0 : 1;
+        j.resplit = p->stale ? 0 : 1;          // the A_d^-1 split: only a full step re-splits it
+        j.resplitG = p->stale ? 0 : 1;         // G_d^-1: full and G-refresh steps
+        if (p->g_only) j.resplit = 0;
         if (p->owner[l] == rank) {
             j.out = ag_buf + p->ag_off[l];
         } else {

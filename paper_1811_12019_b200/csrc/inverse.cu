@@ -61,7 +61,8 @@ struct InvParams {
     int32_t nm, steps, total_tasks, pad0_;
     double gamma;
     double *pair_scratch;  // [npairs][4]: pi, dA, dG
-    float *pi_out;
+    float *pi_out;         // pi per pair (out; in for a G refresh: the cached pi of the last full refresh)
+    int32_t g_only;        // G refresh: G matrices only, damped with the cached pi (R-20)
     // dataflow state (zeroed per inverse call): one task counter, then per matrix / column / step
     // stamps and counters -- see inverse_kernel
     int *counter;
@@ -99,7 +100,15 @@ __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b)
 // ---- prologue: traces -> pi and the damping of each (A, G) pair
 __global__ void damp_trace_kernel(const __grid_constant__ InvParams P) {
     const MatDesc &ma = P.m[blockIdx.x];
-    if (!ma.is_A) return;
+    if (!ma.is_A) {
+        if (P.g_only && threadIdx.x == 0) {  // G refresh: G_d = G + sqrt(gamma) / pi_cached I
+            const double pi = P.pi_out[ma.pair], sg = sqrt(P.gamma);
+            P.pair_scratch[4 * ma.pair + 0] = pi;
+            P.pair_scratch[4 * ma.pair + 2] = sg / pi;
+            *ma.status = 0;
+        }
+        return;
+    }
     const MatDesc *mg = nullptr;
     for (int k = 0; k < P.nm; k++)
         if (P.m[k].pair == ma.pair && !P.m[k].is_A) mg = &P.m[k];
@@ -878,7 +887,7 @@ int64_t inverse_ws_doubles(int n) {
 }
 
 kfac_status inverse_launch(const std::vector<InvMat> &mats, int npairs, float gamma, double *pair_scratch,
-                           float *pi_out, cudaStream_t st) {
+                           float *pi_out, int g_only, cudaStream_t st) {
     if (mats.empty()) return KFAC_OK;
     if ((int)mats.size() > kMaxMats) return set_error(KFAC_ERR_UNSUPPORTED, "too many owned matrices for one launch");
     static bool attr = false;
@@ -898,6 +907,7 @@ kfac_status inverse_launch(const std::vector<InvMat> &mats, int npairs, float ga
     P.gamma = (double)gamma;
     P.pair_scratch = pair_scratch;
     P.pi_out = pi_out;
+    P.g_only = g_only;
     // matrices by column blocks, descending: the matrices active at step k are a prefix
     std::vector<int> order(mats.size());
     for (size_t i = 0; i < mats.size(); i++) order[i] = (int)i;

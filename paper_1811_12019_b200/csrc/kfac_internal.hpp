@@ -105,12 +105,13 @@ struct PrecJob {
     float *tmp;           // precond_ws_floats(dG, dA) scratch (3xTF32 split operands, T^T)
     float *out;           // [dG, dA]
     float *sA, *sG;       // persistent hi / lo split of A_d^-1, G_d^-1 (precond_split_floats each, in inv_ws)
-    int32_t resplit;      // 1: split the inverses into sA / sG (full step); 0: reuse them (stale step, R-20)
+    int32_t resplit;      // 1: split A_d^-1 into sA (full step); 0: reuse it (stale / G-refresh step, R-20)
+    int32_t resplitG;     // 1: split G_d^-1 into sG (full / G-refresh step); 0: reuse it (stale step)
     int32_t dG, dA;
 };
 int64_t precond_split_floats(int n);  // [2][n][kpad(n)] hi / lo copy of one n x n inverse
 kfac_status inverse_launch(const std::vector<InvMat> &mats, int npairs, float gamma, double *pair_scratch,
-                           float *pi_out, cudaStream_t st);
+                           float *pi_out, int g_only, cudaStream_t st);
 kfac_status precond_launch(const std::vector<PrecJob> &jobs, cudaStream_t st);
 struct DiffMat {          // one packed factor of the stale-Fisher change rate (diff.cu)
     const float *cur, *prev;  // packed upper, 16-byte aligned

@@ -117,6 +117,13 @@ kfac_status plan_build(kfac_plan *p) {
                 p->local[r].push_back(o);
                 continue;
             }
+            if (p->g_only) {  // G refresh: A's cached inverse is reused, dW and G travel
+                o[1] = -1;
+                o[2] = off;
+                off = align16(off + packed_len(g.dG));
+                p->local[r].push_back(o);
+                continue;
+            }
             o[1] = off;
             off = align16(off + packed_len(g.dA));
             o[2] = off;
@@ -237,7 +244,7 @@ kfac_status kfac_plan_create(const kfac_layer_desc *layers, int32_t L, int32_t w
 
 kfac_status kfac_plan_create_stale(kfac_plan_t full, kfac_plan_t *out) {
     if (!full || !out) return set_error(KFAC_ERR_ARG, "kfac_plan_create_stale: NULL argument");
-    if (full->stale) return set_error(KFAC_ERR_STATE, "kfac_plan_create_stale: plan is already a stale plan");
+    if (full->stale || full->g_only) return set_error(KFAC_ERR_STATE, "kfac_plan_create_stale: plan is not a full plan");
     kfac_plan *p = new kfac_plan();
     p->layers = full->layers;
     p->L = full->L;
@@ -255,6 +262,27 @@ kfac_status kfac_plan_create_stale(kfac_plan_t full, kfac_plan_t *out) {
 }
 
 int32_t kfac_plan_is_stale(kfac_plan_t p) { return p && p->stale ? 1 : 0; }
+
+kfac_status kfac_plan_create_grefresh(kfac_plan_t full, kfac_plan_t *out) {
+    if (!full || !out) return set_error(KFAC_ERR_ARG, "kfac_plan_create_grefresh: NULL argument");
+    if (full->stale || full->g_only) return set_error(KFAC_ERR_STATE, "kfac_plan_create_grefresh: plan is not a full plan");
+    kfac_plan *p = new kfac_plan();
+    p->layers = full->layers;
+    p->L = full->L;
+    p->world = full->world;
+    p->n_local = full->n_local;
+    p->policy = full->policy;
+    p->g_only = true;
+    kfac_status s = plan_build(p);
+    if (s) {
+        delete p;
+        return s;
+    }
+    *out = p;
+    return KFAC_OK;
+}
+
+int32_t kfac_plan_refresh_kind(kfac_plan_t p) { return !p ? -1 : p->stale ? 2 : p->g_only ? 1 : 0; }
 
 int32_t kfac_refresh_interval(int32_t schedule, int32_t epoch) {
     if (epoch < 0) return -1;

@@ -348,7 +348,7 @@ kfac_status precond_launch(const std::vector<PrecJob> &jobs, cudaStream_t st) {
         w += 2 * (int64_t)dG * kpad(dA);
         float *sT = w;
         if (j.resplit || !j.sA) sj.push_back({j.Ainv, sA, dA, dA, dA, (int32_t)kpad(dA)});
-        if (j.resplit || !j.sG) sj.push_back({j.Ginv, sG, dG, dG, dG, (int32_t)kpad(dG)});
+        if (j.resplitG || !j.sG) sj.push_back({j.Ginv, sG, dG, dG, dG, (int32_t)kpad(dG)});
         sj.push_back({j.dW, sW, dG, dA, dA, (int32_t)kpad(dA)});
         GemmProb a{};
         kfac_status s = split_map(&a.tA, sA, dA, (int)kpad(dA));

@@ -82,6 +82,8 @@ _precondition = _sig("kfac_precondition", [_P, _i32, _P, _P, _P, _P, _P])
 _allgather = _sig("kfac_allgather_precond", [_P, _P, _P, _P])
 _plan_create_stale = _sig("kfac_plan_create_stale", [_P, ctypes.POINTER(_P)])
 _plan_is_stale = _sig("kfac_plan_is_stale", [_P])
+_plan_create_grefresh = _sig("kfac_plan_create_grefresh", [_P, ctypes.POINTER(_P)])
+_plan_refresh_kind = _sig("kfac_plan_refresh_kind", [_P])
 _refresh_interval = _sig("kfac_refresh_interval", [_i32, _i32])
 _refresh = _sig("kfac_refresh", [_i64, _i32, _i32, _i64, _i32])
 _factor_diff = _sig("kfac_factor_diff", [_P, _i32, _P, _P, _P, _P, _P])
@@ -100,7 +102,8 @@ EXPORTS = ["kfac_last_error", "kfac_version", "kfac_launch_count", "kfac_plan_cr
            "kfac_factor_G", "kfac_factor_ws_bytes", "kfac_factor_all", "kfac_reduce_scatter_factors",
            "kfac_damped_inverse", "kfac_precondition", "kfac_allgather_precond", "kfac_plan_create_stale",
            "kfac_plan_is_stale", "kfac_refresh_interval", "kfac_refresh", "kfac_factor_diff", "kfac_update", "kfac_bn_grads",
-           "kfac_bn_precondition", "kfac_bn_ws_bytes", "kfac_bn_exchange"]
+           "kfac_bn_precondition", "kfac_bn_ws_bytes", "kfac_bn_exchange",
+           "kfac_plan_create_grefresh", "kfac_plan_refresh_kind"]
 
 
 def _check(st, where):
@@ -139,17 +142,20 @@ def _stream(stream):
 class Plan:
     """kfac_plan_create / _query / _rank_layers / _destroy."""
 
-    def __init__(self, layers, world, n_local, policy=RR, stale_of=None):
+    def __init__(self, layers, world, n_local, policy=RR, stale_of=None, grefresh_of=None):
         self.layers = list(layers)
         h = _P()
         if stale_of is not None:  # kfac_plan_create_stale: the dW-only layout of `stale_of`
             _check(_plan_create_stale(stale_of.h, ctypes.byref(h)), "kfac_plan_create_stale")
+        elif grefresh_of is not None:  # kfac_plan_create_grefresh: the [dW, G] layout
+            _check(_plan_create_grefresh(grefresh_of.h, ctypes.byref(h)), "kfac_plan_create_grefresh")
         else:
             arr = (LayerDesc * len(layers))(*[layer_desc(l) for l in layers])
             _check(_plan_create(arr, len(layers), int(world), int(n_local), int(policy), ctypes.byref(h)),
                    "kfac_plan_create")
         self.h = h
         self.stale = bool(_plan_is_stale(h))
+        self.kind = int(_plan_refresh_kind(h))  # 0 full, 1 G refresh, 2 stale
         self.world, self.n_local, self.L = int(world), int(n_local), len(layers)
         self._q = None
 
@@ -189,6 +195,10 @@ class Plan:
     def stale_plan(self):
         """kfac_plan_create_stale: the plan of the steps that reuse stale factors."""
         return Plan(self.layers, self.world, self.n_local, stale_of=self)
+
+    def grefresh_plan(self):
+        """kfac_plan_create_grefresh: the plan of the steps that refresh G only."""
+        return Plan(self.layers, self.world, self.n_local, grefresh_of=self)
 
 
 def refresh_interval(schedule, epoch):
@@ -248,11 +258,11 @@ def factor_all(plan, xs, gys, rs_send, ws, alphaA=None, alphaG=None, stream=None
         _check(_factor_all(plan.h, None, None, 0, None, None, _ptr(rs_send), _ptr(ws), _stream(stream)),
                "kfac_factor_all")
         return
-    xa = (_P * L)(*[x.data_ptr() for x in xs])
+    xa = (_P * L)(*[x.data_ptr() for x in xs]) if xs is not None else None  # None: a G refresh
     ga = (_P * L)(*[g.data_ptr() for g in gys])
     aA = (ctypes.c_float * L)(*alphaA) if alphaA is not None else None
     aG = (ctypes.c_float * L)(*alphaG) if alphaG is not None else None
-    _check(_factor_all(plan.h, xa, ga, _DT[xs[0].dtype], aA, aG, _ptr(rs_send), _ptr(ws), _stream(stream)),
+    _check(_factor_all(plan.h, xa, ga, _DT[gys[0].dtype], aA, aG, _ptr(rs_send), _ptr(ws), _stream(stream)),
            "kfac_factor_all")
 
 

@@ -48,6 +48,10 @@ class KfacStep:
             self.rs_recv_prev = torch.zeros_like(self.rs_recv)  # the previous refresh's factors
             self.diff = torch.full((max(2 * n_owned, 1),), float("nan"), dtype=torch.float64, device=dev)
             self.refreshes = 0
+            self.gplan = self.plan.grefresh_plan()  # G refresh, A kept stale
+            self.gq = self.gplan.query()
+            self.g_send = torch.zeros(world * self.gq["rs_chunk"], dtype=torch.float32, device=dev)
+            self.g_recv = torch.zeros(self.gq["rs_chunk"], dtype=torch.float32, device=dev)
 
     # ---- views (zero-copy: the caller's dW lives in the send buffer)
     def dims(self, l):
@@ -121,6 +125,30 @@ class KfacStep:
                   lambda: kfac.reduce_scatter_factors(self.comm, self.splan, self.s_send, self.s_recv, stream),
                   lambda: None,
                   lambda: kfac.precondition(self.splan, self.rank, self.s_recv, self.inv_ws, self.ag_buf, self.ws,
+                                            stream),
+                  lambda: self.allgather(stream))
+        for i, f in enumerate(stages):
+            f()
+            if events is not None:
+                events[i].record(stream)
+
+    def grefresh_dw_view(self, l):
+        da, dg = self.dims(l)
+        o = self.gq["seg_off"][l][0]
+        return self.g_send[o:o + dg * da].view(dg, da)
+
+    def set_grefresh_dw(self, dws):
+        for l, d in enumerate(dws):
+            self.grefresh_dw_view(l).copy_(d, non_blocking=True)
+
+    def run_grefresh(self, gys, gamma, stream=None, events=None):
+        """A step that refreshes G but keeps A stale (R-20): G factors only, ReduceScatter of [dW, G],
+        G_d^-1 with the pi of the last full step (self.pi), the cached A_d^-1 and its split, AllGather."""
+        stages = (lambda: kfac.factor_all(self.gplan, None, gys, self.g_send, self.ws, stream=stream),
+                  lambda: kfac.reduce_scatter_factors(self.comm, self.gplan, self.g_send, self.g_recv, stream),
+                  lambda: kfac.damped_inverse(self.gplan, self.rank, self.g_recv, gamma, self.inv_ws, self.dev_status,
+                                              self.pi, self.ws, stream),
+                  lambda: kfac.precondition(self.gplan, self.rank, self.g_recv, self.inv_ws, self.ag_buf, self.ws,
                                             stream),
                   lambda: self.allgather(stream))
         for i, f in enumerate(stages):

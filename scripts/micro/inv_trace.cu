@@ -30,11 +30,11 @@ int main(int argc, char **argv) {
     double *w2 = work + inverse_ws_doubles(n);
     mats[1].packed = dp; mats[1].inv = dinv + (size_t)n * n; mats[1].work = w2; mats[1].panel = w2 + (int64_t)128 * 128;
     mats[1].status = status + 1; mats[1].n = 128; mats[1].pair = 0; mats[1].is_A = 0;
-    for (int r = 0; r < 3; r++) inverse_launch(mats, 1, 0.01f, scratch, pi, 0);
+    for (int r = 0; r < 3; r++) inverse_launch(mats, 1, 0.01f, scratch, pi, 0, 0);
     cudaDeviceSynchronize();
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
     cudaEventRecord(e0);
-    inverse_launch(mats, 1, 0.01f, scratch, pi, 0);
+    inverse_launch(mats, 1, 0.01f, scratch, pi, 0, 0);
     cudaEventRecord(e1); cudaEventSynchronize(e1);
     float ms; cudaEventElapsedTime(&ms, e0, e1);
     fprintf(stderr, "n=%d inverse %.3f ms (%s)\n", n, ms, cudaGetErrorString(cudaGetLastError()));

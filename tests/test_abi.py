@@ -125,3 +125,23 @@ def test_refresh_controller_vs_oracle(K, orc):
     assert K.refresh_interval(9, 0) == -1 and K.refresh_interval(0, -1) == -1
     with pytest.raises(ValueError):
         K.refresh(-1, 0)
+
+
+@pytest.mark.parametrize("cfg", ["single_conv", "resnet50"])
+@pytest.mark.parametrize("P", [1, 2, 5])
+def test_grefresh_plan_bit_exact_vs_oracle(K, orc, cfg, P):
+    """kfac_plan_create_grefresh: the [dW, G] layout, bit-exact against oracle.plan(g_only=True)."""
+    L, n = shapes.config(cfg)
+    full = K.Plan(L, P, n, 1)
+    gp = full.grefresh_plan()
+    assert gp.kind == 1 and full.kind == 0 and full.stale_plan().kind == 2
+    q = gp.query()
+    ref = orc.plan(L, P, 1, g_only=True)
+    assert q["rs_chunk"] == ref["rs_chunk"] and np.array_equal(np.array(q["seg_off"]), ref["seg_off"])
+    for r in range(P):
+        rl = gp.rank_layers(r)
+        assert [tuple(-1 if v is None else v for v in ref["local"][r][l]) for l in ref["owned"][r]] == \
+            [tuple(o) for o in rl["local_off"]]
+        assert rl["inv_off"] == full.rank_layers(r)["inv_off"]
+    with pytest.raises(K.KfacError, match="ERR_STATE"):
+        K.Plan(L, P, n, grefresh_of=gp)

@@ -155,3 +155,40 @@ def test_stale_step_end_to_end(K, orc, gamma):
         assert es <= 1e-5 and ee <= TOL_PREC
     with pytest.raises(K.KfacError, match="ERR_STATE"):
         K.damped_inverse(st.splan, 0, st.s_recv, gamma, st.inv_ws, st.dev_status, st.pi, st.ws)
+
+
+@pytest.mark.parametrize("gamma", [2.5e-2, 2.5e-4])
+def test_grefresh_step_end_to_end(K, orc, gamma):
+    """Full step (seed 1811), then a G refresh with new gy and dW (seed 99): G factors, [dW, G]
+    ReduceScatter, G_d^-1 with the cached pi, the cached A_d^-1 (R-20), against oracle.grefresh_results."""
+    n = 4
+    st = K.KfacStep(NET, n, stale=True)
+    xs, gys, dws = _inputs(NET, n, 1811)
+    st.set_dw([d.cuda() for d in dws])
+    st.run([x.cuda() for x in xs], [g.cuda() for g in gys], gamma)
+    _, gys2, dws2 = _inputs(NET, n, 99)
+    st.set_grefresh_dw([d.cuda() for d in dws2])
+    st.run_grefresh([g.cuda() for g in gys2], gamma)
+    torch.cuda.synchronize()
+    assert st.dev_status.cpu().abs().sum().item() == 0
+    full = orc.kfac_step(NET, _oracle_in(xs, gys, dws, n), 1, gamma)
+    gp = orc.plan(NET, 1, 0, g_only=True)
+    facs = [(None, orc.factor_G(inputs.half_bits(gys2[l]), shapes.rows(L, n), L["c_out"])) for l, L in enumerate(NET)]
+    recv = orc.reduce_scatter([orc.build_send(NET, gp, 0, facs, [d.numpy() for d in dws2])], gp)[0]
+    cached = {l: (v["Ainv"], v["pi"]) for l, v in full["results"][0].items()}
+    ref = orc.grefresh_results(NET, gp, 0, recv, gamma, cached)
+    rl = st.plan.rank_layers(0)
+    for k, l in enumerate(rl["layers"]):
+        Ai, Gi = st.inv_views(k)
+        dg = shapes.dims(NET[l])[1]
+        eg = relerr(Gi.cpu().double().numpy(), ref[l]["Ginv"])
+        ee = relerr(st.result(l).cpu().double().numpy(), ref[l]["precond"])
+        print(f"layer {l}: G-refresh Ginv err {eg:.2e}, e2e {ee:.2e}")
+        assert eg <= 2e-3 and ee <= TOL_PREC
+    # A's inverse is untouched by the G refresh: a second stale-A G refresh with the first inputs
+    # restores the full step's result
+    st.set_grefresh_dw([d.cuda() for d in dws])
+    st.run_grefresh([g.cuda() for g in gys], gamma)
+    torch.cuda.synchronize()
+    for l in range(len(NET)):
+        assert relerr(st.result(l).cpu().double().numpy(), full["results"][0][l]["precond"]) <= TOL_PREC

@@ -117,3 +117,62 @@ def test_stale_step_reproduces_full_step(orc):
         for l, v in got.items():
             assert np.array_equal(v["dW"], full["results"][r][l]["dW"])
             assert np.array_equal(v["precond"], full["results"][r][l]["precond"])
+
+
+def test_refresh_kinds(orc):
+    """A refreshes with its interval multiplied ('A-multiplier 2, G interval 10 -> A every 20')."""
+    for t in range(500, 700):
+        ra, rg = orc.refresh_kinds(t, 20, "step13", 500, a_multiple=2)  # interval 20 (P:751-755)
+        assert rg == (t % 20 == 0) and ra == (t % 40 == 0)
+        assert not ra or rg  # A implies G
+    assert orc.refresh_kinds(3, 0, "rampup", 50, a_multiple=4) == (True, True)  # fresh floor: both
+    with pytest.raises(ValueError):
+        orc.refresh_kinds(3, 0, a_multiple=0)
+
+
+@pytest.mark.parametrize("cfg", ["single_conv", "resnet50", "stress"])
+@pytest.mark.parametrize("P", [1, 2, 8])
+def test_grefresh_layout_invariants(orc, cfg, P):
+    layers, _ = shapes.config(cfg)
+    full, st = orc.plan(layers, P, 1), orc.plan(layers, P, 1, stale=True)
+    gp = orc.plan(layers, P, 1, g_only=True)
+    assert st["rs_chunk"] < gp["rs_chunk"] < full["rs_chunk"]
+    assert (gp["seg_off"][:, 1] == -1).all() and (gp["seg_off"][:, 2] >= 0).all()
+    assert np.array_equal(gp["owner"], full["owner"]) and np.array_equal(gp["ag_off"], full["ag_off"])
+    for r in range(P):
+        end = 0
+        for l in gp["owned"][r]:
+            o_w, o_a, o_g = gp["local"][r][l]
+            a, g = orc.dims(layers[l])
+            assert o_a is None and o_w % 16 == 0 and o_g % 16 == 0 and o_w >= end and o_g >= o_w + g * a
+            end = o_g + g * (g + 1) // 2
+        assert end <= gp["rs_chunk"]
+
+
+def test_grefresh_step_reproduces_full_step(orc):
+    """A G refresh with the same factors, the full step's π and A_d⁻¹ gives the full step's 𝒢 (R-20)."""
+    layers, n = shapes.config("single_conv")
+    layers = layers + [shapes.conv("c2", 8, 16, 1, 1, 0, 8), shapes.linear("fc", 24, 10, 1)]
+    P, gamma = 2, 2.5e-2
+    rank_inputs = []
+    for r in range(P):
+        xs = [inputs.half_bits(inputs.layer_x(l, i, 4, rank=r, stem=False)) for i, l in enumerate(layers)]
+        gys = [inputs.half_bits(inputs.layer_gy(l, i, 4, rank=r)) for i, l in enumerate(layers)]
+        dws = [inputs.layer_dw(l, i, rank=r).numpy() for i, l in enumerate(layers)]
+        rank_inputs.append((xs, gys, dws, 4))
+    full = orc.kfac_step(layers, rank_inputs, P, gamma)
+    gp = orc.plan(layers, P, 0, g_only=True)
+    sends = []
+    for r in range(P):
+        xs, gys, dws, nl = rank_inputs[r]
+        facs = [(None, orc.factor_G(gys[l], orc.rows(L, nl), L["c_out"])) for l, L in enumerate(layers)]
+        sends.append(orc.build_send(layers, gp, r, facs, dws))
+    recvs = orc.reduce_scatter(sends, gp)
+    for r in range(P):
+        cached = {l: (v["Ainv"], v["pi"]) for l, v in full["results"][r].items()}
+        got = orc.grefresh_results(layers, gp, r, recvs[r], gamma, cached)
+        for l, v in got.items():
+            want = full["results"][r][l]
+            assert np.array_equal(v["G"], want["G"])
+            assert np.allclose(v["G_d"], want["G_d"], rtol=1e-15, atol=0)
+            assert np.allclose(v["precond"], want["precond"], rtol=1e-12, atol=1e-15)
