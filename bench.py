@@ -285,6 +285,22 @@ def run_ours(args):
             K.factor_diff(st.plan, rank, st.rs_recv, st.rs_recv_prev, st.diff, st.ws, stream)
             dev_ev[s][1].record(stream)
         barrier()
+        # G-only refresh steps (A kept stale): G factors, [dW, G] ReduceScatter, G inverses
+        st.set_grefresh_dw([d.to(dev) for d in dws_h])
+        for _ in range(args.warmup):
+            st.run_grefresh(gys, args.gamma, stream)
+        gev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
+        barrier()
+        for s in range(args.steps):
+            if flush.numel():
+                flush.fill_(s & 0xFF)
+            gev[s][0].record(stream)
+            st.run_grefresh(gys, args.gamma, stream)
+            gev[s][1].record(stream)
+        barrier()
+        gms = torch.tensor([sum(e[0].elapsed_time(e[1]) for e in gev) / args.steps], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(gms, op=dist.ReduceOp.MAX)
         sm = torch.tensor([sum(e[0].elapsed_time(e[nst]) for e in sev)] +
                           [sum(e[i].elapsed_time(e[i + 1]) for e in sev) for i in range(nst)] +
                           [sum(e[0].elapsed_time(e[1]) for e in dev_ev)], dtype=torch.float64, device=dev)
@@ -302,6 +318,8 @@ def run_ours(args):
                  "rs_bytes_per_rank": st.sq["rs_chunk"] * 4, "full_rs_bytes_per_rank": st.q["rs_chunk"] * 4,
                  "refresh_interval": iv, "amortized_ms": round((ms + (iv - 1) * sm[0]) / iv, 3),
                  "diff_ms": round(sm[-1], 4),
+                 "grefresh_step_ms": round(gms.item(), 3),
+                 "grefresh_rs_bytes_per_rank": st.gq["rs_chunk"] * 4,
                  "diff_roofline": {"bound": "hbm", "achieved": round(dgbs, 1), "peak": hbm, "unit": "GB/s",
                                    "frac": round(dgbs / hbm, 4), "traffic": None,
                                    "kernel": "diff_partial_kernel + diff_final_kernel",
