@@ -9,7 +9,8 @@ oracle simulating the same P ranks (oracle.kfac_step):
   * every layer's preconditioned gradient in the gathered buffer (stage 6),
   * that the AllGather buffers of all ranks are bitwise identical (replica consistency);
 then a stale-factor step (NEXT-1, R-20: new dW, dW-only ReduceScatter, the
-cached inverses) against oracle.stale_results, replicas again identical; and the BN
+cached inverses) against oracle.stale_results, replicas again identical; a G-only
+refresh against oracle.grefresh_results; and the BN
 Fisher across ranks (kfac_bn_exchange + replicated kfac_bn_precondition, R-22).
 Exit code 0 on success.
 """
@@ -132,6 +133,38 @@ def main():
         print(f"mp_parity {cfg} P={world} stale step: end-to-end max err {serr:.2e}, replicas identical {ok}",
               flush=True)
         ok &= serr <= 2e-3
+    # ---- a G-only refresh (A kept stale, R-20): new gy and dW, [dW, G] ReduceScatter, cached pi and A_d^-1
+    gys3 = [inputs.layer_gy(l, i, n, rank, seed=777) for i, l in enumerate(layers)]
+    dws3 = [inputs.layer_dw(l, i, rank, seed=778) for i, l in enumerate(layers)]
+    st.set_grefresh_dw([d.to(dev) for d in dws3])
+    st.run_grefresh([g.to(dev) for g in gys3], gamma)
+    torch.cuda.synchronize()
+    bufs = [torch.empty_like(st.ag_buf) for _ in range(world)]
+    dist.all_gather(bufs, st.ag_buf)
+    all3 = [None] * world
+    dist.all_gather_object(all3, ([inputs.half_bits(g) for g in gys3], [d.numpy() for d in dws3]))
+    if rank == 0:
+        import oracle
+        for b in bufs[1:]:
+            ok &= torch.equal(b, bufs[0])
+        gp = oracle.plan(layers, world, policy, g_only=True)
+        sends = []
+        for r in range(world):
+            facs = [(None, oracle.factor_G(all3[r][0][l], shapes.rows(L, n), L["c_out"])) for l, L in enumerate(layers)]
+            sends.append(oracle.build_send(layers, gp, r, facs, all3[r][1]))
+        grecvs = oracle.reduce_scatter(sends, gp)
+        g = bufs[0].cpu().double().numpy()
+        gerr = 0.0
+        for l in range(len(layers)):
+            da, dg = shapes.dims(layers[l])
+            owner = pl["owner"][l]
+            cached = {m: (v["Ainv"], v["pi"]) for m, v in ref["results"][owner].items()}
+            want = oracle.grefresh_results(layers, gp, owner, grecvs[owner], gamma, cached)[l]["precond"]
+            gerr = max(gerr, relerr(g[pl["ag_off"][l]:pl["ag_off"][l] + dg * da], want.reshape(-1)))
+        print(f"mp_parity {cfg} P={world} G refresh: end-to-end max err {gerr:.2e}, replicas identical {ok}",
+              flush=True)
+        ok &= gerr <= 2e-3
+
     # ---- BN Fisher across ranks (NEXT-2, R-22): AllGather of S, mean of the BN grads, replicated solve
     bc, bhw = [64, 256, 6], [25, 9, 16]
     gb = torch.Generator().manual_seed(500 + rank)
