@@ -21,7 +21,6 @@ namespace {
 constexpr int kUpdThreads = 256;
 constexpr int64_t kUpdChunk = 8192;  // weights per block
 constexpr int kUpdMaxLayers = 160;
-constexpr int64_t kUpdGroupBytes = 48ll << 20;  // weights per step + rescale group (L2 is 126 MB)
 
 struct UpdParams {
     float *w[kUpdMaxLayers];
@@ -152,19 +151,9 @@ __global__ void __launch_bounds__(kUpdThreads) update_scale_kernel(const __grid_
 
 kfac_status update_launch(const std::vector<UpdJob> &jobs, float lr, float mom, int rescale, float eps, double *ws,
                           int64_t ws_bytes, cudaStream_t st) {
-    // layers go in groups of <= kUpdGroupBytes of weights (whole layers), each group's step pass then its
-    // rescale pass: the rescale re-reads weights the step pass just wrote, which then still sit in L2
-    for (size_t j0 = 0; j0 < jobs.size();) {
+    for (size_t j0 = 0; j0 < jobs.size(); j0 += kUpdMaxLayers) {
         thread_local UpdParams P;  // host staging of the parameter block, per calling thread
-        size_t j1 = j0;
-        int64_t bytes = 0;
-        while (j1 < jobs.size() && (int)(j1 - j0) < kUpdMaxLayers) {
-            const int64_t b = (int64_t)jobs[j1].dG * jobs[j1].dA * 4;
-            if (j1 > j0 && rescale && bytes + b > kUpdGroupBytes) break;
-            bytes += b;
-            j1++;
-        }
-        P.nlayers = (int)(j1 - j0);
+        P.nlayers = (int)std::min<size_t>(kUpdMaxLayers, jobs.size() - j0);
         int32_t nb = 0;
         for (int k = 0; k < P.nlayers; k++) {
             const UpdJob &u = jobs[j0 + k];
@@ -194,7 +183,6 @@ kfac_status update_launch(const std::vector<UpdJob> &jobs, float lr, float mom, 
             KFAC_LAUNCHED();
             KFAC_CUDA_TRY(cudaGetLastError());
         }
-        j0 = j1;
     }
     return KFAC_OK;
 }
