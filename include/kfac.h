@@ -327,11 +327,11 @@ KFAC_API kfac_status kfac_bn_grads(int32_t nl, const int32_t *c /* host [nl] */,
  * The full mode never forms F: F has rank <= n, and by the Woodbury identity
  *   (F + gamma_bn I)^-1 v = (v - S^T (gamma_bn n I + S S^T)^-1 S v) / gamma_bn,
  * i.e. a column-parallel fp64 Gram S S^T (all layers in one launch) and an n x n fp64
- * Cholesky solve per layer; n <= 128 (e.g. the samples of up to 4 ranks of 32 after an
- * all-gather of S).  grad / out: [2C] fp32 device (out may not alias grad).  ws: device
+ * Cholesky solve per layer; n <= 256 (the samples of up to 8 ranks of 32 after an
+ * all-gather of S; K sits in shared memory up to n = 128, in the workspace beyond).  grad / out: [2C] fp32 device (out may not alias grad).  ws: device
  * scratch of kfac_bn_ws_bytes (full mode; may be NULL for the diagonal mode).
  * Errors: KFAC_ERR_ARG (NULL, gamma_bn <= 0, n < 1, full mode without enough ws),
- * KFAC_ERR_SHAPE (c < 1), KFAC_ERR_UNSUPPORTED (full mode with n > 128).                */
+ * KFAC_ERR_SHAPE (c < 1), KFAC_ERR_UNSUPPORTED (full mode with n > 256).                */
 KFAC_API kfac_status kfac_bn_precondition(int32_t nl, const int32_t *c /* host [nl] */, int32_t n,
                                  const float *const *S /* host [nl] */, const float *const *grad /* host [nl] */,
                                  float gamma_bn, int32_t full, float *const *out /* host [nl] */, void *ws,

@@ -387,7 +387,7 @@ kfac_status kfac_bn_precondition(int32_t nl, const int32_t *c, int32_t n, const 
     if (!(gamma_bn > 0.f)) return set_error(KFAC_ERR_ARG, "kfac_bn_precondition: gamma_bn must be > 0");
     if (n < 1) return set_error(KFAC_ERR_ARG, "kfac_bn_precondition: n >= 1");
     if (full && n > kBnMaxSamples)
-        return set_error(KFAC_ERR_UNSUPPORTED, "kfac_bn_precondition: full mode supports n <= 128 samples");
+        return set_error(KFAC_ERR_UNSUPPORTED, "kfac_bn_precondition: full mode supports n <= 256 samples");
     std::vector<BnJob> jobs;
     for (int l = 0; l < nl; l++) {
         if (!Sv[l] || !grad[l] || !out[l]) return set_error(KFAC_ERR_ARG, "kfac_bn_precondition: NULL layer pointer");

@@ -55,6 +55,7 @@ struct BnPrecParams {
     double lambda;
     double *ws;  // Gram partials: per item n(n+1)/2 + n doubles
     double *y;   // [nl][n] solved y of each layer (after the partials in the workspace)
+    double *kglob;  // [nl][n][n] K in the workspace when n > kBnSmemSamples, else null
 };
 
 __device__ __forceinline__ float2 h2f(uint32_t v, int fp16) {
@@ -240,8 +241,9 @@ __global__ void __launch_bounds__(kBnThreads) bn_solve_kernel(const __grid_const
     extern __shared__ double bsm[];
     const int l = blockIdx.x, n = P.n, tid = threadIdx.x, npair = n * (n + 1) / 2;
     const double lam = P.lambda;
-    double *K = bsm;       // [n][n]
-    double *u = K + n * n;  // [n]
+    // K [n][n] in shared memory, or (n > kBnSmemSamples) in this layer's workspace slot
+    double *K = P.kglob ? P.kglob + (int64_t)l * n * n : bsm;
+    double *u = P.kglob ? bsm : K + n * n;  // [n]
     const int it0 = P.item0[l], nit = P.item0[l + 1] - it0;
     for (int q = tid; q < npair + n; q += kBnThreads) {
         double acc = 0.0;
@@ -310,10 +312,15 @@ __global__ void __launch_bounds__(kBnThreads) bn_out_kernel(const __grid_constan
 
 static int64_t gram_items(int c) { return (2 * (int64_t)c + kGramCols - 1) / kGramCols; }
 
+// K in shared memory up to this many samples; past it (up to kBnMaxSamples) each layer's K lives in
+// the workspace (L2-resident: n = 256 is 512 KB per layer)
+constexpr int kBnSmemSamples = 128;
+
 int64_t bn_ws_bytes(const std::vector<int> &cs, int n) {
     int64_t items = 0;
     for (int c : cs) items += gram_items(c);
-    return items * ((int64_t)n * (n + 1) / 2 + n) * 8 + (int64_t)cs.size() * n * 8;
+    const int64_t kglob = n > kBnSmemSamples ? (int64_t)cs.size() * n * n * 8 : 0;
+    return items * ((int64_t)n * (n + 1) / 2 + n) * 8 + kglob + (int64_t)cs.size() * n * 8;
 }
 
 kfac_status bn_grads_launch(const std::vector<BnJob> &jobs, int n, int fp16, cudaStream_t st) {
@@ -347,7 +354,7 @@ kfac_status bn_grads_launch(const std::vector<BnJob> &jobs, int n, int fp16, cud
 kfac_status bn_precond_launch(const std::vector<BnJob> &jobs, int n, int full, double lambda, double *ws,
                               int64_t ws_bytes, cudaStream_t st) {
     const int64_t gsmem = (int64_t)n * (kGramCols + 1) * 8 + kGramCols * 8;
-    const int64_t ssmem = (int64_t)n * n * 8 + (int64_t)n * 8;
+    const int64_t ssmem = (n > kBnSmemSamples ? 0 : (int64_t)n * n * 8) + (int64_t)n * 8;
     if (full) {
         KFAC_CUDA_TRY(cudaFuncSetAttribute(bn_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem));
         KFAC_CUDA_TRY(cudaFuncSetAttribute(bn_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssmem));
@@ -381,6 +388,7 @@ kfac_status bn_precond_launch(const std::vector<BnJob> &jobs, int n, int full, d
         if (!ws || bn_ws_bytes(cs, n) > ws_bytes)
             return set_error(KFAC_ERR_ARG, "kfac_bn_precondition: full mode needs kfac_bn_ws_bytes of workspace");
         P.y = ws + (bn_ws_bytes(cs, n) / 8 - (int64_t)P.nl * n);
+        P.kglob = n > kBnSmemSamples ? P.y - (int64_t)P.nl * n * n : nullptr;
         bn_gram_kernel<<<items, kBnThreads, gsmem, st>>>(P);
         KFAC_LAUNCHED();
         KFAC_CUDA_TRY(cudaGetLastError());

@@ -132,7 +132,7 @@ struct BnJob {             // one Batch Normalization layer (bn.cu)
     float *out;               // [2c]
     int32_t c, hw;
 };
-constexpr int kBnMaxSamples = 128;  // full-mode Woodbury solve in shared memory
+constexpr int kBnMaxSamples = 256;  // full-mode Woodbury solve: n x n fp64 K (8 ranks x 32 samples)
 kfac_status bn_grads_launch(const std::vector<BnJob> &jobs, int n, int fp16, cudaStream_t st);
 kfac_status bn_precond_launch(const std::vector<BnJob> &jobs, int n, int full, double lambda, double *ws,
                               int64_t ws_bytes, cudaStream_t st);

@@ -4,7 +4,7 @@ kfac_bn_grads against oracle.bn_sample_grads on the same seeded half inputs (fac
 2e-3), kfac_bn_precondition (diagonal, and full through the Woodbury identity) against
 oracle.bn_precondition of the dense (F + gamma_BN I): stage-wise on the GPU's own fp32 S (fp64
 on both sides, 1e-8) and end to end from the half inputs (2e-3), at small shapes, every
-ResNet-50 BN shape at batch 32, and the n = 128 limit.
+ResNet-50 BN shape at batch 32, n = 128 (K in shared memory) and n = 256 (K in the workspace).
 """
 import numpy as np
 import pytest
@@ -98,13 +98,14 @@ def test_bn_resnet50_shapes(K, orc):
 
 
 def test_bn_sample_limit(K, orc):
-    _run(K, orc, [64, 512], [4, 1], 128, seed=2)
-    S = [torch.zeros(129, 128, device="cuda")]
+    _run(K, orc, [64, 512], [4, 1], 128, seed=2)  # K in shared memory
+    _run(K, orc, [64, 512, 6], [4, 1, 3], 256, seed=3)  # K in the workspace (8 ranks x 32 samples)
+    S = [torch.zeros(257, 128, device="cuda")]
     g = [torch.zeros(128, device="cuda")]
     with pytest.raises(K.KfacError, match="ERR_UNSUPPORTED"):
-        K.bn_precondition([64], 129, S, g, 0.4, 1, [torch.empty(128, device="cuda")])
+        K.bn_precondition([64], 257, S, g, 0.4, 1, [torch.empty(128, device="cuda")])
     with pytest.raises(K.KfacError, match="ERR_ARG"):  # full mode without its workspace
         K.bn_precondition([64], 4, S, g, 0.4, 1, [torch.empty(128, device="cuda")])
-    K.bn_precondition([64], 129, S, g, 0.4, 0, [torch.empty(128, device="cuda")])  # diag: any n
+    K.bn_precondition([64], 257, S, g, 0.4, 0, [torch.empty(128, device="cuda")])  # diag: any n
     with pytest.raises(K.KfacError, match="ERR_ARG"):
         K.bn_precondition([64], 4, S, g, 0.0, 0, [torch.empty(128, device="cuda")])
