@@ -841,9 +841,14 @@ __global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ I
     __shared__ double T[32][33];
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     for (int t = blockIdx.x; t < npairs; t += gridDim.x) {
-        int bi = 0, rem = t;
-        while (rem >= nt - bi) rem -= nt - bi++;
-        const int bj = bi + rem;
+        // tile t of the row-major upper tile order: row bi starts at S(bi) = bi nt - bi (bi - 1) / 2
+        // (closed form + fix-up; a walk over the rows cost ~nt ALU steps per tile)
+        const double b2 = 2.0 * nt + 1.0;
+        int bi = (int)((b2 - sqrt(b2 * b2 - 8.0 * t)) * 0.5);
+        bi = max(0, min(bi, nt - 1));
+        while (bi > 0 && bi * nt - bi * (bi - 1) / 2 > t) bi--;
+        while (bi + 1 < nt && (bi + 1) * nt - (bi + 1) * bi / 2 <= t) bi++;
+        const int bj = bi + (t - (bi * nt - bi * (bi - 1) / 2));
         __syncthreads();
         for (int r = ty; r < 32; r += 8) {
             const int i = bi * 32 + r, j = bj * 32 + tx;
