@@ -246,18 +246,26 @@ OR_EXPORT int or_cholesky(const double *M, int n, double *L, int nthreads) {
     return 0;
 }
 
-/* Li = L⁻¹ for lower-triangular L, column by column (forward substitution). */
+/* Li = L⁻¹ for lower-triangular L, column by column (forward substitution).
+ * Column c is built in a contiguous buffer and then stored (a layout choice
+ * for the cache only: the arithmetic and its order are the substitution's). */
 OR_EXPORT void or_tri_inv_lower(const double *L, int n, double *Li, int nthreads) {
     memset(Li, 0, sizeof(double) * (size_t)n * n);
     set_threads(nthreads);
-#pragma omp parallel for schedule(dynamic, 4)
-    for (int c = 0; c < n; c++) {
-        Li[(size_t)c * n + c] = 1.0 / L[(size_t)c * n + c];
-        for (int i = c + 1; i < n; i++) {
-            double s = 0.0;
-            for (int k = c; k < i; k++) s += L[(size_t)i * n + k] * Li[(size_t)k * n + c];
-            Li[(size_t)i * n + c] = -s / L[(size_t)i * n + i];
+#pragma omp parallel
+    {
+        double *col = (double *)malloc(sizeof(double) * (size_t)n);
+#pragma omp for schedule(dynamic, 4)
+        for (int c = 0; c < n; c++) {
+            col[c] = 1.0 / L[(size_t)c * n + c];
+            for (int i = c + 1; i < n; i++) {
+                double s = 0.0;
+                for (int k = c; k < i; k++) s += L[(size_t)i * n + k] * col[k];
+                col[i] = -s / L[(size_t)i * n + i];
+            }
+            for (int i = c; i < n; i++) Li[(size_t)i * n + c] = col[i];
         }
+        free(col);
     }
 }
 
@@ -271,12 +279,17 @@ OR_EXPORT int or_inverse_spd(const double *M, int n, double *X, int nthreads) {
         return st;
     }
     or_tri_inv_lower(L, n, Li, nthreads);
-    /* X = Liᵀ Li : X[i][j] = sum_{k >= max(i,j)} Li[k][i] Li[k][j] */
+    /* X = Liᵀ Li : X[i][j] = sum_{k >= max(i,j)} Li[k][i] Li[k][j].  The
+     * columns of Li are read from its transpose T = Liᵀ (T[i][k] = Li[k][i]),
+     * a copy for contiguous access; same products, same order.             */
+    double *T = L; /* L is no longer needed: reuse it for Liᵀ */
+    for (int i = 0; i < n; i++)
+        for (int k = 0; k < n; k++) T[(size_t)i * n + k] = Li[(size_t)k * n + i];
 #pragma omp parallel for schedule(dynamic, 4)
     for (int i = 0; i < n; i++)
         for (int j = i; j < n; j++) {
             double s = 0.0;
-            for (int k = j; k < n; k++) s += Li[(size_t)k * n + i] * Li[(size_t)k * n + j];
+            for (int k = j; k < n; k++) s += T[(size_t)i * n + k] * T[(size_t)j * n + k];
             X[(size_t)i * n + j] = s;
             X[(size_t)j * n + i] = s;
         }
@@ -289,23 +302,34 @@ OR_EXPORT int or_inverse_spd(const double *M, int n, double *X, int nthreads) {
  * 𝒢 = G⁻¹ · ∇W · A⁻¹ with ∇W in R^{dG x dA} row-major (bias column last).  */
 OR_EXPORT void or_precondition(const double *Ginv, int dG, const double *Ainv, int dA,
                                const double *dW, double *out, int nthreads) {
+    /* Columns of Ainv and of T = ∇W·Ainv are read from transposed copies
+     * (AiT[j][k] = Ainv[k][j], TT[j][k] = T[k][j]) for contiguous access;
+     * the products and their order are those of the plain triple loops.   */
     double *T = (double *)malloc(sizeof(double) * (size_t)dG * dA);
+    double *AiT = (double *)malloc(sizeof(double) * (size_t)dA * dA);
+    double *TT = (double *)malloc(sizeof(double) * (size_t)dG * dA);
     set_threads(nthreads);
+    for (int k = 0; k < dA; k++)
+        for (int j = 0; j < dA; j++) AiT[(size_t)j * dA + k] = Ainv[(size_t)k * dA + j];
 #pragma omp parallel for schedule(static)
     for (int i = 0; i < dG; i++)
         for (int j = 0; j < dA; j++) {
             double s = 0.0;
-            for (int k = 0; k < dA; k++) s += dW[(size_t)i * dA + k] * Ainv[(size_t)k * dA + j];
+            for (int k = 0; k < dA; k++) s += dW[(size_t)i * dA + k] * AiT[(size_t)j * dA + k];
             T[(size_t)i * dA + j] = s;
         }
+    for (int k = 0; k < dG; k++)
+        for (int j = 0; j < dA; j++) TT[(size_t)j * dG + k] = T[(size_t)k * dA + j];
 #pragma omp parallel for schedule(static)
     for (int i = 0; i < dG; i++)
         for (int j = 0; j < dA; j++) {
             double s = 0.0;
-            for (int k = 0; k < dG; k++) s += Ginv[(size_t)i * dG + k] * T[(size_t)k * dA + j];
+            for (int k = 0; k < dG; k++) s += Ginv[(size_t)i * dG + k] * TT[(size_t)j * dG + k];
             out[(size_t)i * dA + j] = s;
         }
     free(T);
+    free(AiT);
+    free(TT);
 }
 
 /* Selected entries of 𝒢 one by one: out[q] = sum_{k,l} Ginv[i][k] dW[k][l] Ainv[l][j]. */

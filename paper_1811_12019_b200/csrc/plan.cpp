@@ -3,7 +3,7 @@
 // ("multiple layers are handled by each GPU ...
 // some layers will be calculated redundantly"; readings R-15, R-16).
 // Host-only C++; the oracle carries its own independent implementation and
-// tests/test_layout.py compares the two bit-exactly.
+// tests/test_abi.py (test_plan_bit_exact_vs_oracle) compares the two bit-exactly.
 #include <algorithm>
 #include <atomic>
 #include <cstring>

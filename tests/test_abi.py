@@ -145,3 +145,11 @@ def test_grefresh_plan_bit_exact_vs_oracle(K, orc, cfg, P):
         assert rl["inv_off"] == full.rank_layers(r)["inv_off"]
     with pytest.raises(K.KfacError, match="ERR_STATE"):
         K.Plan(L, P, n, grefresh_of=gp)
+
+
+def test_plan_lpt_hand_worked(K):
+    """plan.cpp's LPT owners on the hand-worked example of tests/golden/lpt_examples.json (R-15)."""
+    import json
+    e = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "lpt_examples.json")))["fc_dims_P3"]
+    layers = [shapes.linear(f"fc{i}", a, g, bias=0) for i, (a, g) in enumerate(e["dims"])]
+    assert K.Plan(layers, e["P"], 1, 1).query()["owner"] == e["owner"]

@@ -133,3 +133,31 @@ def test_redundant_owners_identical(orc):
         assert len(copies) >= 2
         for c in copies[1:]:
             assert np.array_equal(c, copies[0])
+
+
+LPT = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "lpt_examples.json")))
+
+
+@pytest.mark.parametrize("name", [k for k in LPT if k.startswith("cost")])
+def test_lpt_hand_worked_costs(orc, monkeypatch, name):
+    """R-15's LPT policy on hand-worked cost lists (tests/golden/lpt_examples.json):
+    the exact owner list and loads.  Descending order, the (-cost, l) key and the lowest-rank
+    tie-break each change the result of at least one example."""
+    e = LPT[name]
+    layers = [shapes.linear(f"l{i}", 1, 1, bias=0) for i in range(len(e["costs"]))]
+    cost = {id(layer): c for layer, c in zip(layers, e["costs"])}
+    monkeypatch.setattr(orc, "layer_cost", lambda layer: cost[id(layer)])
+    pl = orc.plan(layers, e["P"], orc.POLICY_LPT)
+    assert pl["owner"].tolist() == e["owner"]
+    load = [sum(c for c, o in zip(e["costs"], e["owner"]) if o == r) for r in range(e["P"])]
+    assert load == e["load"]
+
+
+def test_lpt_hand_worked_fc_dims(orc):
+    """The same policy with the real cost model (R-15) on hand-computed FC costs."""
+    e = LPT["fc_dims_P3"]
+    layers = [shapes.linear(f"fc{i}", a, g, bias=0) for i, (a, g) in enumerate(e["dims"])]
+    assert [orc.layer_cost(l) for l in layers] == e["costs"]
+    pl = orc.plan(layers, e["P"], orc.POLICY_LPT)
+    assert pl["owner"].tolist() == e["owner"]
+    assert pl["owned"] == [[l for l in range(len(layers)) if e["owner"][l] == r] for r in range(e["P"])]
