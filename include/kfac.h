@@ -114,8 +114,12 @@ KFAC_API int64_t kfac_launch_count(void);
  * chunk is padded to rs_chunk = max chunk (NCCL has no V variant).  The
  * AllGather chunk of rank r holds the preconditioned gradient of each layer
  * whose PRIMARY owner is r, ascending, 16-aligned, padded to ag_chunk.
+ * Limits: every factor dimension dA, dG <= 16384 (the inverse's step table);
+ * any number of layers per rank (the inverse runs in launches of <= 64 owned
+ * layers each, in stream order).
  * Errors: KFAC_ERR_ARG (NULL, L < 1, world < 1, n_local < 1, bad policy),
- * KFAC_ERR_SHAPE (a non-positive dimension, kind not 0/1).                 */
+ * KFAC_ERR_SHAPE (a non-positive dimension, kind not 0/1),
+ * KFAC_ERR_UNSUPPORTED (a factor dimension above 16384).                   */
 KFAC_API kfac_status kfac_plan_create(const kfac_layer_desc *layers /* host [L] */, int32_t L, int32_t world,
                              int32_t n_local, kfac_policy policy, kfac_plan_t *out /* host */);
 

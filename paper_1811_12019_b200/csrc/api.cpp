@@ -26,6 +26,17 @@ struct kfac_comm {
             return set_error(KFAC_ERR_NCCL, std::string(#expr) + ": " + ncclGetErrorString(_r)); \
     } while (0)
 
+// After enqueueing a collective: a communicator that has failed asynchronously (a peer died, a
+// network / NVLink error) reports it here instead of hanging later (SURVEY §5 failure detection).
+static kfac_status nccl_check_async(ncclComm_t comm) {
+    ncclResult_t a = ncclSuccess;
+    ncclResult_t r = ncclCommGetAsyncError(comm, &a);
+    if (r != ncclSuccess) return set_error(KFAC_ERR_NCCL, std::string("ncclCommGetAsyncError: ") + ncclGetErrorString(r));
+    if (a != ncclSuccess && a != ncclInProgress)
+        return set_error(KFAC_ERR_NCCL, std::string("NCCL asynchronous error: ") + ncclGetErrorString(a));
+    return KFAC_OK;
+}
+
 static cudaStream_t S(void *s) { return static_cast<cudaStream_t>(s); }
 
 static kfac_status one_factor(const kfac_layer_desc *layer, const void *src, kfac_dtype dt, int32_t n, float alpha,
@@ -106,6 +117,7 @@ kfac_status kfac_factor_all(kfac_plan_t p, const void *const *xs, const void *co
         aG[l] = alphaG ? alphaG[l] : (float)(1.0 / rows);
         if ((!p->g_only && !xs[l]) || !gys[l]) return set_error(KFAC_ERR_ARG, "kfac_factor_all: NULL input pointer");
     }
+    std::lock_guard<std::mutex> lock(p->c_mu);
     const std::vector<const void *> xv = p->g_only ? std::vector<const void *>(L, nullptr)
                                                    : std::vector<const void *>(xs, xs + L);
     const bool same = p->c_dt == (int)dt && p->c_send == rs_send && p->c_ws == ws && p->c_xs == xv &&
@@ -230,6 +242,7 @@ kfac_status kfac_reduce_scatter_factors(kfac_comm_t c, kfac_plan_t p, const floa
     }
     if (!c || c->world != p->world) return set_error(KFAC_ERR_STATE, "kfac_reduce_scatter_factors: comm/plan world mismatch");
     KFAC_NCCL_TRY(ncclReduceScatter(send, recv, (size_t)p->rs_chunk, ncclFloat32, ncclAvg, c->comm, S(stream)));
+    KFAC_TRY(nccl_check_async(c->comm));
     return KFAC_OK;
 }
 
@@ -365,12 +378,21 @@ kfac_status kfac_bn_exchange(kfac_comm_t cm, int32_t nl, const int32_t *c, int32
     for (int l = 0; l < nl; l++)
         if (!S_local[l] || !S_all[l] || !grad[l] || c[l] < 1) return set_error(KFAC_ERR_ARG, "kfac_bn_exchange: layer argument");
     KFAC_NCCL_TRY(ncclGroupStart());
-    for (int l = 0; l < nl; l++) {
+    ncclResult_t r = ncclSuccess;
+    const char *what = "";
+    for (int l = 0; l < nl && r == ncclSuccess; l++) {  // on an error, fall through to close the group
         const size_t cnt = (size_t)n_local * 2 * c[l];
-        KFAC_NCCL_TRY(ncclAllGather(S_local[l], S_all[l], cnt, ncclFloat32, cm->comm, S(stream)));
-        KFAC_NCCL_TRY(ncclAllReduce(grad[l], grad[l], (size_t)2 * c[l], ncclFloat32, ncclAvg, cm->comm, S(stream)));
+        r = ncclAllGather(S_local[l], S_all[l], cnt, ncclFloat32, cm->comm, S(stream));
+        what = "ncclAllGather";
+        if (r == ncclSuccess) {
+            r = ncclAllReduce(grad[l], grad[l], (size_t)2 * c[l], ncclFloat32, ncclAvg, cm->comm, S(stream));
+            what = "ncclAllReduce";
+        }
     }
-    KFAC_NCCL_TRY(ncclGroupEnd());
+    const ncclResult_t e = ncclGroupEnd();
+    if (r != ncclSuccess) return set_error(KFAC_ERR_NCCL, std::string(what) + ": " + ncclGetErrorString(r));
+    if (e != ncclSuccess) return set_error(KFAC_ERR_NCCL, std::string("ncclGroupEnd: ") + ncclGetErrorString(e));
+    KFAC_TRY(nccl_check_async(cm->comm));
     return KFAC_OK;
 }
 
@@ -409,6 +431,7 @@ kfac_status kfac_allgather_precond(kfac_comm_t c, kfac_plan_t p, float *ag_buf, 
     if (!c || c->world != p->world) return set_error(KFAC_ERR_STATE, "kfac_allgather_precond: comm/plan world mismatch");
     float *mine = ag_buf + (int64_t)c->rank * p->ag_chunk;
     KFAC_NCCL_TRY(ncclAllGather(mine, ag_buf, (size_t)p->ag_chunk, ncclFloat32, c->comm, S(stream)));
+    KFAC_TRY(nccl_check_async(c->comm));
     return KFAC_OK;
 }
 

@@ -148,14 +148,10 @@ kfac_status diff_launch(const std::vector<DiffMat> &mats, double *ws, int64_t ws
         if ((int64_t)nb * (int64_t)sizeof(double2) > ws_bytes)
             return set_error(KFAC_ERR_STATE, "kfac_factor_diff: workspace too small for the block partials");
         P.part = reinterpret_cast<double2 *>(ws);
-        static int grid = 0;
-        if (!grid) {
-            int dev = 0, sms = 0, per = 0;
-            KFAC_CUDA_TRY(cudaGetDevice(&dev));
-            KFAC_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-            KFAC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, diff_partial_kernel, kDiffThreads, 0));
-            grid = sms * std::max(per, 1);
-        }
+        int sms = 0, per = 0;
+        KFAC_TRY(dev_sm_count(&sms));
+        KFAC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, diff_partial_kernel, kDiffThreads, 0));
+        const int grid = sms * std::max(per, 1);
         diff_partial_kernel<<<std::min(nb, grid), kDiffThreads, 0, st>>>(P);
         KFAC_LAUNCHED();
         KFAC_CUDA_TRY(cudaGetLastError());

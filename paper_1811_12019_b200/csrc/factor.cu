@@ -33,6 +33,7 @@
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <mutex>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -738,7 +739,10 @@ typedef CUresult (*PFN_encodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32
 static PFN_encodeTiled g_encTiled = nullptr;
 static int g_driver = 0;
 
+static std::mutex g_drv_mu;
+
 static kfac_status load_driver_fns() {
+    std::lock_guard<std::mutex> lock(g_drv_mu);
     if (g_encTiled) return KFAC_OK;
     cudaDriverEntryPointQueryResult q1;
     void *f1 = nullptr;
@@ -930,18 +934,11 @@ static kfac_status setup_prob(const FactorJob &j, kfac_dtype dt, FactorProb *pr,
     return KFAC_OK;
 }
 
-static int g_num_sms = 0;
-
 kfac_status factor_prepare(const std::vector<FactorJob> &jobs, kfac_dtype dt, void *ws, int64_t ws_cap,
                            bool dry_run, FactorLaunch *out) {
     out->params.clear();
     out->ws_bytes = 0;
     if (jobs.empty()) return KFAC_OK;
-    if (!dry_run && !g_num_sms) {
-        int dev = 0;
-        KFAC_CUDA_TRY(cudaGetDevice(&dev));
-        KFAC_CUDA_TRY(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
-    }
     const int nj = (int)jobs.size();
     std::vector<FactorProb> geo(nj);
     double total = 0;  // MMA K-steps over all tile pairs
@@ -984,7 +981,11 @@ kfac_status factor_prepare(const std::vector<FactorJob> &jobs, kfac_dtype dt, vo
     for (int i = 0; i < nj; i++) order[i] = i;
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return item_cost[a] > item_cost[b]; });
     int64_t ws_off = 0, col_off = 0;
+#ifdef KFAC_DEBUG_KNOBS  // development switches (disable MMA / TMA / stores): never in a product build
     const int dbg = getenv("KFAC_DBG_MODE") ? atoi(getenv("KFAC_DBG_MODE")) : 0;
+#else
+    const int dbg = 0;
+#endif
     for (int base = 0; base < nj;) {
         out->params.emplace_back();
         FactorParams &P = out->params.back();
@@ -1021,6 +1022,7 @@ kfac_status factor_prepare(const std::vector<FactorJob> &jobs, kfac_dtype dt, vo
         P.nprobs = cnt;
         P.nmaps = nmaps;
         P.total_items = items;
+#ifdef KFAC_DEBUG_KNOBS
         if (!dry_run && getenv("KFAC_DEBUG")) {
             for (int k = 0; k < cnt; k++) {
                 const FactorProb &pr = P.probs[k];
@@ -1033,6 +1035,7 @@ kfac_status factor_prepare(const std::vector<FactorJob> &jobs, kfac_dtype dt, vo
             fprintf(stderr, "[kfac] factor launch: %d problems, %d descriptors, %d items, target %.0f k-steps/item\n",
                     P.nprobs, P.nmaps, items, target);
         }
+#endif
         base += cnt;
     }
     out->ws_bytes = need + col_need + 256;
@@ -1040,21 +1043,19 @@ kfac_status factor_prepare(const std::vector<FactorJob> &jobs, kfac_dtype dt, vo
 }
 
 kfac_status factor_launch(const FactorLaunch &fl, const std::vector<FactorJob> &jobs, cudaStream_t st) {
-    static bool attr_set = false;
-    if (!attr_set) {
-        KFAC_CUDA_TRY(cudaFuncSetAttribute(factor_syrk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));
-        attr_set = true;
-    }
+    int sms = 0;
+    KFAC_TRY(dev_sm_count(&sms));
+    KFAC_TRY(dev_func_smem((const void *)factor_syrk_kernel, (int)kSmemBytes));
     for (const FactorParams &P : fl.params) {
         if (P.total_items == 0) continue;
         int npre = 0;
         for (int p = 0; p < P.nprobs; p++) npre += P.probs[p].im2col_pre != 0;
         if (npre) {
-            im2col_kernel<<<dim3(8 * (g_num_sms ? g_num_sms : 148), npre), 256, 0, st>>>(P);
+            im2col_kernel<<<dim3(8 * sms, npre), 256, 0, st>>>(P);
             KFAC_LAUNCHED();
             KFAC_CUDA_TRY(cudaGetLastError());
         }
-        int grid = std::min(P.total_items, g_num_sms ? g_num_sms : 148);
+        int grid = std::min(P.total_items, sms);
         if (P.counter) KFAC_CUDA_TRY(cudaMemsetAsync(P.counter, 0, sizeof(int32_t), st));
         factor_syrk_kernel<<<grid, kThreads, kSmemBytes, st>>>(P);
         KFAC_LAUNCHED();
@@ -1065,7 +1066,10 @@ kfac_status factor_launch(const FactorLaunch &fl, const std::vector<FactorJob> &
             if (pr.splits > 1) fix += pr.npairs;
             if (pr.d_out != pr.d) maxbias = std::max(maxbias, pr.d + 1), nbias++;
         }
-        if (fix && !getenv("KFAC_NO_FIXUP")) {
+#ifdef KFAC_DEBUG_KNOBS
+        if (getenv("KFAC_NO_FIXUP")) fix = 0;
+#endif
+        if (fix) {
             factor_fixup_kernel<<<fix * kFixRowGroups, 256, 0, st>>>(P);
             KFAC_LAUNCHED();
             KFAC_CUDA_TRY(cudaGetLastError());

@@ -872,7 +872,6 @@ extern "C" __attribute__((visibility("default"))) int kfac_debug_inverse_trace(v
     return (int)cudaMemcpyFromSymbol(host, g_trace, sizeof(TraceRec) * n);
 }
 #endif
-static int g_inv_sms = 0;
 
 int64_t inverse_ld(int n) { return (n + 15) / 16 * 16; }
 int64_t inverse_scratch_bytes(int npairs, int64_t sum_nt, int64_t sum_tiles, int64_t sum_tasks) {
@@ -894,18 +893,24 @@ int64_t inverse_ws_doubles(int n) {
 kfac_status inverse_launch(const std::vector<InvMat> &mats, int npairs, float gamma, double *pair_scratch,
                            float *pi_out, int g_only, cudaStream_t st) {
     if (mats.empty()) return KFAC_OK;
-    if ((int)mats.size() > kMaxMats) return set_error(KFAC_ERR_UNSUPPORTED, "too many owned matrices for one launch");
-    static bool attr = false;
-    if (!g_inv_sms) {
-        int dev = 0;
-        KFAC_CUDA_TRY(cudaGetDevice(&dev));
-        KFAC_CUDA_TRY(cudaDeviceGetAttribute(&g_inv_sms, cudaDevAttrMultiProcessorCount, dev));
+    if ((int)mats.size() > kMaxMats) {
+        // more than kMaxMats owned matrices (e.g. ResNet-101 on one GPU): several launches in stream
+        // order, split at (A, G) pair boundaries (the damping couples a pair's traces); each launch
+        // re-zeroes the dataflow state, which is sized for all matrices
+        size_t b = 0;
+        while (b < mats.size()) {
+            size_t e = std::min(mats.size(), b + (size_t)kMaxMats);
+            while (e < mats.size() && e > b + 1 && mats[e].pair == mats[e - 1].pair) e--;
+            KFAC_TRY(inverse_launch(std::vector<InvMat>(mats.begin() + b, mats.begin() + e), npairs, gamma,
+                                    pair_scratch, pi_out, g_only, st));
+            b = e;
+        }
+        return KFAC_OK;
     }
-    if (!attr) {
-        KFAC_CUDA_TRY(cudaFuncSetAttribute(pivot_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPivSmem));
-        KFAC_CUDA_TRY(cudaFuncSetAttribute(inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kUpdSmem));
-        attr = true;
-    }
+    int sms = 0;
+    KFAC_TRY(dev_sm_count(&sms));
+    KFAC_TRY(dev_func_smem((const void *)pivot_kernel, kPivSmem));
+    KFAC_TRY(dev_func_smem((const void *)inverse_kernel, kUpdSmem));
     InvParams P;
     memset(&P, 0, sizeof(P));
     P.nm = (int)mats.size();
@@ -972,7 +977,7 @@ kfac_status inverse_launch(const std::vector<InvMat> &mats, int npairs, float ga
     pivot_kernel<<<P.nm, 256, kPivSmem, st>>>(P);
     KFAC_LAUNCHED();
     KFAC_CUDA_TRY(cudaGetLastError());
-    inverse_kernel<<<std::min(P.total_tasks, g_inv_sms), 256, kUpdSmem, st>>>(P);
+    inverse_kernel<<<std::min(P.total_tasks, sms), 256, kUpdSmem, st>>>(P);
     KFAC_LAUNCHED();
     KFAC_CUDA_TRY(cudaGetLastError());
     const int max32 = (maxn + 31) / 32;

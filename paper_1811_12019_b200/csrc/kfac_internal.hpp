@@ -24,6 +24,17 @@ extern std::atomic<int64_t> g_launches;  // kernels launched (kfac_launch_count)
             return ::kfac::set_error(KFAC_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
     } while (0)
 
+// per-device launch setup, thread-safe (a process may drive several GPUs from several threads):
+// the current device's SM count, and the >48 KB dynamic shared memory opt-in of `func` on it
+kfac_status dev_sm_count(int *sms);
+kfac_status dev_func_smem(const void *func, int bytes);
+
+#define KFAC_TRY(expr)                     \
+    do {                                   \
+        kfac_status _s = (expr);           \
+        if (_s != KFAC_OK) return _s;      \
+    } while (0)
+
 inline int64_t packed_len(int64_t d) { return d * (d + 1) / 2; }
 inline int64_t align16(int64_t v) { return (v + 15) / 16 * 16; }
 
@@ -143,6 +154,7 @@ kfac_status replicate_launch(const std::vector<std::pair<const float *, float *>
                              const std::vector<int64_t> &counts, cudaStream_t st);
 
 constexpr int kPanel = 128;  // sweep block size of the inverse
+constexpr int kMaxInverseDim = 128 * kPanel;  // 16384: the sweep's step table (kfac_plan_create rejects larger)
 int64_t inverse_ws_doubles(int n);  // fp64 working matrix + panels of one n x n inverse
 // pair data (pi, damping) + the dataflow state of the persistent sweep; over the owned matrices,
 // sum_nt = sum of nt = ceil(n / kPanel), sum_tiles = sum of nt (nt + 1) / 2

@@ -1,6 +1,7 @@
 // kfac_plan.hpp -- the opaque plan / communicator objects behind the C-ABI.
 #pragma once
 #include <array>
+#include <mutex>
 #include <vector>
 
 #include "kfac_internal.hpp"
@@ -20,7 +21,9 @@ struct kfac_plan {
     std::vector<std::vector<int64_t>> inv_off;  // per rank: 2 per owned layer
     std::vector<std::vector<int64_t>> split_off;  // per rank: 2 per owned layer (3xTF32 split cache, after the inverses)
     std::vector<int64_t> inv_floats;
-    // cached grouped factor launch (re-encoded when the pointers change)
+    // cached grouped factor launch (re-encoded when the pointers change); c_mu serialises
+    // concurrent kfac_factor_all calls on one plan (the ABI allows calls from several threads)
+    std::mutex c_mu;
     std::vector<const void *> c_xs, c_gys;
     std::vector<float> c_aA, c_aG;
     float *c_send = nullptr;

@@ -10,6 +10,10 @@
 #include <numeric>
 #include <string>
 
+#include <map>
+#include <mutex>
+#include <set>
+
 #include "kfac_plan.hpp"
 
 namespace kfac {
@@ -20,6 +24,35 @@ std::atomic<int64_t> g_launches{0};
 kfac_status set_error(kfac_status st, const std::string &msg) {
     g_last_error = msg;
     return st;
+}
+
+// ---- per-device launch setup (the SM count and the shared memory opt-in are per device)
+static std::mutex g_dev_mu;
+static std::map<int, int> g_dev_sms;
+static std::set<std::pair<int, const void *>> g_dev_attr;
+
+kfac_status dev_sm_count(int *sms) {
+    int dev = 0;
+    KFAC_CUDA_TRY(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(g_dev_mu);
+    auto it = g_dev_sms.find(dev);
+    if (it == g_dev_sms.end()) {
+        int v = 0;
+        KFAC_CUDA_TRY(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev));
+        it = g_dev_sms.emplace(dev, v).first;
+    }
+    *sms = it->second;
+    return KFAC_OK;
+}
+
+kfac_status dev_func_smem(const void *func, int bytes) {
+    int dev = 0;
+    KFAC_CUDA_TRY(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(g_dev_mu);
+    if (g_dev_attr.count({dev, func})) return KFAC_OK;
+    KFAC_CUDA_TRY(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    g_dev_attr.insert({dev, func});
+    return KFAC_OK;
 }
 
 kfac_status make_geom(const kfac_layer_desc &d, Geom *g) {
@@ -66,6 +99,9 @@ kfac_status plan_build(kfac_plan *p) {
     for (int l = 0; l < L; l++) {
         kfac_status s = make_geom(p->layers[l], &p->geoms[l]);
         if (s) return s;
+        if (p->geoms[l].dA > kMaxInverseDim || p->geoms[l].dG > kMaxInverseDim)
+            return set_error(KFAC_ERR_UNSUPPORTED, "layer " + std::to_string(l) + ": a factor dimension exceeds " +
+                                                       std::to_string(kMaxInverseDim) + " (inverse limit)");
     }
     // ownership
     p->owner.assign(L, 0);

@@ -256,7 +256,6 @@ typedef CUresult (*PFN_encTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t,
                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 static PFN_encTiled g_enc = nullptr;
-static int g_gsms = 0;
 
 static kfac_status split_map(CUtensorMap *m, float *base, int rows, int Kp) {
     if (!g_enc) {
@@ -301,14 +300,9 @@ static kfac_status launch_splits(const std::vector<SplitJob> &js, cudaStream_t s
 }
 
 static kfac_status launch_gemms(std::vector<GemmProb> &gs, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
-        KFAC_CUDA_TRY(cudaFuncSetAttribute(gemm_3xtf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GSmem));
-        int dev = 0;
-        KFAC_CUDA_TRY(cudaGetDevice(&dev));
-        KFAC_CUDA_TRY(cudaDeviceGetAttribute(&g_gsms, cudaDevAttrMultiProcessorCount, dev));
-        attr = true;
-    }
+    int sms = 0;
+    KFAC_TRY(dev_sm_count(&sms));
+    KFAC_TRY(dev_func_smem((const void *)gemm_3xtf32_kernel, (int)GSmem));
     // heaviest problems first (static striding)
     std::stable_sort(gs.begin(), gs.end(), [](const GemmProb &a, const GemmProb &b) {
         return (int64_t)a.M * a.N * a.K > (int64_t)b.M * b.N * b.K;
@@ -326,7 +320,7 @@ static kfac_status launch_gemms(std::vector<GemmProb> &gs, cudaStream_t st) {
         }
         P.total = items;
         if (!items) continue;
-        gemm_3xtf32_kernel<<<std::min(items, g_gsms), GThreads, GSmem, st>>>(P);
+        gemm_3xtf32_kernel<<<std::min(items, sms), GThreads, GSmem, st>>>(P);
         KFAC_LAUNCHED();
         KFAC_CUDA_TRY(cudaGetLastError());
     }

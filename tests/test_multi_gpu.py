@@ -15,7 +15,9 @@ def _ngpu():
 
 
 @pytest.mark.parametrize("cfg,policy,nproc", [("small", 0, 2), ("small", 1, 2), ("one_layer", 0, 2),
-                                              ("small", 1, 4)])
+                                              ("small", 1, 4), ("resnet50", 1, 2), ("resnet50", 1, 4),
+                                              ("stress", 1, 2), ("stress", 1, 4)])
+@pytest.mark.timeout(3600)
 def test_mp_parity(cfg, policy, nproc):
     if _ngpu() < nproc:
         pytest.skip(f"needs {nproc} GPUs, have {_ngpu()}")
@@ -24,7 +26,7 @@ def test_mp_parity(cfg, policy, nproc):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr=127.0.0.1", "--master-port=29631", os.path.join(ROOT, "tests", "mp_parity.py"), cfg,
            str(policy)]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=3000, cwd=ROOT)
     print(r.stdout[-2000:], r.stderr[-2000:])
     assert r.returncode == 0
     assert "mp_parity" in r.stdout
