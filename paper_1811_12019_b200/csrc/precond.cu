@@ -7,8 +7,11 @@
 //     𝒢   = G_d^-1 * T         (A-op G_d^-1 [dG x dG], B-op T^T [dA x dG])
 // Precision: single-pass TF32 / bf16 miss the 2e-3 bound on
 // activation-consistent gradients, so every product is a 3xTF32 split
-//     a*b ~ hi(a)hi(b) + hi(a)lo(b) + lo(a)hi(b),  lo(x) = x - tf32(x)
-// on tcgen05.mma kind::tf32 with fp32 accumulation in TMEM (fp32-class error).
+//     a*b ~ hi(a)hi(b) + hi(a)lo(b) + lo(a)hi(b),  hi = rn_tf32(x), lo = rn_tf32(x - hi)
+// on tcgen05.mma kind::tf32 with fp32 accumulation in TMEM (fp32-class error).  The tensor
+// core's fp32 accumulation does not round to nearest, and over K = 4608 its error grows well
+// past an fp32 GEMM's, so TMEM holds only 256-element K segments that the epilogue sums in
+// registers with round-to-nearest adds.
 // The operands are staged as [2][rows][K] (hi, lo) by a split kernel (the
 // first GEMM's epilogue writes T^T already split); TMA loads 32-element K
 // boxes (SW128, K-major) of hi and lo for both operands.
@@ -22,6 +25,7 @@ namespace kfac {
 
 constexpr int GM = 128, GN = 128, GK = 32;  // tile M, N; K elements per stage (128 B rows)
 constexpr int GStages = 3;
+constexpr int GSeg = 8;                     // K chunks (256 elements) per TMEM accumulation segment
 constexpr int GThreads = 192;               // warps 0-3 epilogue, 4 MMA, 5 TMA
 constexpr int kMaxG = 96;
 constexpr int GOp = GM * GK * 4;            // 16 KB per operand half per stage
@@ -41,8 +45,10 @@ struct GemmParams {
     GemmProb p[kMaxG];
 };
 
-__device__ __forceinline__ float tf32_trunc(float x) {
-    return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+// round to the nearest tf32 value (ties away from zero); the result is exact in tf32, so the
+// MMA's own operand truncation leaves it unchanged
+__device__ __forceinline__ float tf32_rn(float x) {
+    return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
 
 __device__ __forceinline__ void mma_tf32_ss(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
@@ -122,47 +128,51 @@ __global__ void __launch_bounds__(GThreads, 1) gemm_3xtf32_kernel(const __grid_c
             }
         }
     } else if (warp == 4) {
-        uint32_t stage = 0, phase = 0, tph0 = 0, tph1 = 0;
+        // K is accumulated in TMEM segments of GSeg chunks; the epilogue adds each segment into
+        // fp32 registers (round to nearest) while the MMAs of the next one run in the other buffer
+        uint32_t stage = 0, phase = 0, tph = 0;
         int buf = 0;
         for (int item = blockIdx.x; item < total; item += gridDim.x) {
             int pi, m0, n0;
             gdecode(P, item, pi, m0, n0);
             const int kch = (P.p[pi].K + GK - 1) / GK;
-            const uint32_t tacc = tmem_base + buf * GN;
-            if (lane == 0) {
-                mbar_wait(&tempty[buf], (buf ? tph1 : tph0) ^ 1);
-                tc_fence_after();
-                for (int kc = 0; kc < kch; kc++) {
-                    mbar_wait(&full[stage], phase);
+            for (int k0 = 0; k0 < kch; k0 += GSeg) {
+                const uint32_t tacc = tmem_base + buf * GN;
+                if (lane == 0) {
+                    mbar_wait(&tempty[buf], ((tph >> buf) & 1) ^ 1);
                     tc_fence_after();
-                    const uint32_t s = smem_u32(smem + (size_t)stage * GStageBytes);
-                    const uint32_t ah = s, al = s + GOp, bh = s + 2 * GOp, bl = s + 3 * GOp;
+                    for (int kc = k0; kc < kch && kc < k0 + GSeg; kc++) {
+                        mbar_wait(&full[stage], phase);
+                        tc_fence_after();
+                        const uint32_t s = smem_u32(smem + (size_t)stage * GStageBytes);
+                        const uint32_t ah = s, al = s + GOp, bh = s + 2 * GOp, bl = s + 3 * GOp;
 #pragma unroll
-                    for (int k = 0; k < GK / 8; k++) {  // K = 8 tf32 per MMA = 32 bytes within the SW128 atom
-                        const uint32_t ko = k * 32;
-                        const uint64_t dah = umma_desc(ah + ko, 16, 1024, UMMA_SW128);
-                        const uint64_t dal = umma_desc(al + ko, 16, 1024, UMMA_SW128);
-                        const uint64_t dbh = umma_desc(bh + ko, 16, 1024, UMMA_SW128);
-                        const uint64_t dbl = umma_desc(bl + ko, 16, 1024, UMMA_SW128);
-                        const uint32_t acc0 = (kc > 0 || k > 0) ? 1u : 0u;
-                        mma_tf32_ss(tacc, dal, dbh, kIdescTF32, acc0);  // small terms first
-                        mma_tf32_ss(tacc, dah, dbl, kIdescTF32, 1u);
-                        mma_tf32_ss(tacc, dah, dbh, kIdescTF32, 1u);
+                        for (int k = 0; k < GK / 8; k++) {  // K = 8 tf32 per MMA = 32 bytes within the SW128 atom
+                            const uint32_t ko = k * 32;
+                            const uint64_t dah = umma_desc(ah + ko, 16, 1024, UMMA_SW128);
+                            const uint64_t dal = umma_desc(al + ko, 16, 1024, UMMA_SW128);
+                            const uint64_t dbh = umma_desc(bh + ko, 16, 1024, UMMA_SW128);
+                            const uint64_t dbl = umma_desc(bl + ko, 16, 1024, UMMA_SW128);
+                            const uint32_t acc0 = (kc > k0 || k > 0) ? 1u : 0u;
+                            mma_tf32_ss(tacc, dal, dbh, kIdescTF32, acc0);  // small terms first
+                            mma_tf32_ss(tacc, dah, dbl, kIdescTF32, 1u);
+                            mma_tf32_ss(tacc, dah, dbh, kIdescTF32, 1u);
+                        }
+                        mma_commit(&empty[stage]);
+                        if (++stage == GStages) {
+                            stage = 0;
+                            phase ^= 1;
+                        }
                     }
-                    mma_commit(&empty[stage]);
-                    if (++stage == GStages) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
+                    mma_commit(&tfull[buf]);
                 }
-                mma_commit(&tfull[buf]);
+                __syncwarp();
+                tph ^= 1u << buf;
+                buf ^= 1;
             }
-            __syncwarp();
-            if (buf) tph1 ^= 1; else tph0 ^= 1;
-            buf ^= 1;
         }
-    } else {  // epilogue warps 0-3
-        uint32_t tph0 = 0, tph1 = 0;
+    } else {  // epilogue warps 0-3: thread = one output row, 128 fp32 register accumulators
+        uint32_t tph = 0;
         int buf = 0;
         const int row = warp * 32 + lane;
         for (int item = blockIdx.x; item < total; item += gridDim.x) {
@@ -171,19 +181,31 @@ __global__ void __launch_bounds__(GThreads, 1) gemm_3xtf32_kernel(const __grid_c
             const GemmProb &g = P.p[pi];
             float *C = g.C, *Clo = g.Clo;
             const int M = g.M, N = g.N, ldc = g.ldc;
-            mbar_wait(&tfull[buf], buf ? tph1 : tph0);
-            tc_fence_after();
-            const uint32_t tacc = tmem_base + buf * GN + ((uint32_t)(warp * 32) << 16);
-            for (int q = 0; q < GN / 32; q++) {
-                uint32_t r[32];
-                tmem_ld_32x32b_x32(tacc + q * 32, r);
-                tmem_ld_wait();
+            const int kch = (g.K + GK - 1) / GK;
+            float acc[GN];
 #pragma unroll
-                for (int i = 0; i < 32; i++) stage_buf[row * GLd + i] = __uint_as_float(r[i]);
-                if (q == GN / 32 - 1) {
-                    tc_fence_before();
-                    mbar_arrive(&tempty[buf]);
+            for (int i = 0; i < GN; i++) acc[i] = 0.f;
+            for (int k0 = 0; k0 < kch; k0 += GSeg) {
+                mbar_wait(&tfull[buf], (tph >> buf) & 1);
+                tc_fence_after();
+                const uint32_t tacc = tmem_base + buf * GN + ((uint32_t)(warp * 32) << 16);
+#pragma unroll
+                for (int q = 0; q < GN / 32; q++) {
+                    uint32_t r[32];
+                    tmem_ld_32x32b_x32(tacc + q * 32, r);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int i = 0; i < 32; i++) acc[q * 32 + i] += __uint_as_float(r[i]);
                 }
+                tc_fence_before();
+                mbar_arrive(&tempty[buf]);
+                tph ^= 1u << buf;
+                buf ^= 1;
+            }
+#pragma unroll
+            for (int q = 0; q < GN / 32; q++) {
+#pragma unroll
+                for (int i = 0; i < 32; i++) stage_buf[row * GLd + i] = acc[q * 32 + i];
                 named_bar_sync(2, 128);
                 const int j = n0 + q * 32 + lane;
                 for (int rr = warp; rr < GM; rr += 4) {
@@ -191,10 +213,10 @@ __global__ void __launch_bounds__(GThreads, 1) gemm_3xtf32_kernel(const __grid_c
                     if (i >= M) break;
                     if (j < N) {
                         const float v = stage_buf[rr * GLd + lane];
-                        if (Clo) {  // split output for the next product: hi = tf32(v), lo = v - hi
-                            const float hi = tf32_trunc(v);
+                        if (Clo) {  // split output for the next product: hi = tf32(v), lo = tf32(v - hi)
+                            const float hi = tf32_rn(v);
                             C[(int64_t)i * ldc + j] = hi;
-                            Clo[(int64_t)i * ldc + j] = v - hi;
+                            Clo[(int64_t)i * ldc + j] = tf32_rn(v - hi);
                         } else {
                             C[(int64_t)i * ldc + j] = v;
                         }
@@ -205,8 +227,6 @@ __global__ void __launch_bounds__(GThreads, 1) gemm_3xtf32_kernel(const __grid_c
                 }
                 named_bar_sync(2, 128);
             }
-            if (buf) tph1 ^= 1; else tph0 ^= 1;
-            buf ^= 1;
         }
     }
     tc_fence_before();
@@ -217,7 +237,7 @@ __global__ void __launch_bounds__(GThreads, 1) gemm_3xtf32_kernel(const __grid_c
     }
 }
 
-// split fp32 rows [rows][K] (row stride ld_src) into [2][rows][Kp]: hi = x, lo = x - tf32(x)
+// split fp32 rows [rows][K] (row stride ld_src) into [2][rows][Kp]: hi = tf32(x), lo = tf32(x - hi)
 struct SplitJob {
     const float *src;
     float *dst;
@@ -242,8 +262,8 @@ __global__ void __launch_bounds__(256) split_kernel(const __grid_constant__ Spli
             for (int e = 0; e < 4; e++) {
                 const int k = 4 * q + e;
                 x[e] = k < J.K ? __ldg(src + k) : 0.f;
-                h[e] = tf32_trunc(x[e]);  // exact tf32 value, whatever rounding the MMA applies
-                l[e] = x[e] - h[e];
+                h[e] = tf32_rn(x[e]);
+                l[e] = tf32_rn(x[e] - h[e]);  // |x - h - l| <= 2^-22 |x|
             }
             hi[q] = make_float4(h[0], h[1], h[2], h[3]);
             lo[q] = make_float4(l[0], l[1], l[2], l[3]);

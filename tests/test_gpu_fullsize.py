@@ -6,7 +6,7 @@ Every stage is compared densely, layer by layer (Algorithm 1
   a1/a2 factors   rs_recv's packed A, G vs oracle.factor_A / factor_G           <= 2e-3
   a5 damping      pi vs oracle.damp on the same fp32 factors                    <= 1e-6 rel
   a6 inverse      A_d^-1, G_d^-1 vs oracle.inverse of the SAME fp32 damped matrices <= 1e-5
-  a7 precondition 𝒢 vs oracle.precondition(GPU G_d^-1, GPU A_d^-1, ∇W)           <= 2e-3 (expect ~1e-6)
+  a7 precondition 𝒢 vs oracle.precondition(GPU G_d^-1, GPU A_d^-1, ∇W)           <= 2e-3 (expect ~1e-6..3e-5)
   end to end      𝒢 vs oracle (factors -> damp -> inverse -> precondition, all fp64) <= 2e-3
 (relative Frobenius errors over full matrices, BASELINE.json north_star tolerances).  The
 oracle's work is large at these sizes (RN50: ~0.8 TFLOP of factors, 2 x 0.45 TFLOP of
@@ -85,7 +85,7 @@ def test_fullsize_step_parity(K, orc, cfg, gamma):
     status = st.dev_status.cpu().tolist()
     pis = st.pi.cpu().double().numpy()
     ref_f = oracle_factors(orc, cfg)
-    worst = {k: (0.0, None) for k in ("factor", "pi", "inverse", "precond", "e2e")}
+    worst = {k: (0.0, None) for k in ("factor", "pi", "inverse", "precond", "precond_vs_fp32", "e2e")}
 
     def note(kind, e, where):
         if e > worst[kind][0]:
@@ -119,9 +119,16 @@ def test_fullsize_step_parity(K, orc, cfg, gamma):
             assert e <= TOL_INV, (name, "AG"[which], e)
         # a7 on the GPU's own inverses
         got = st.result(l).cpu().double().numpy()
-        e = relerr(got, orc.precondition(Gi, Ai, dW))
+        want = orc.precondition(Gi, Ai, dW)
+        e = relerr(got, want)
         note("precond", e, name)
-        assert e <= TOL_PREC and e <= 1e-5, (name, e)  # 3xTF32 is fp32-class (R-13)
+        assert e <= TOL_PREC, (name, e)
+        # R-13: 3xTF32 is fp32-class.  Cancellation in A_d^-1 (kappa ~ 2e3) lifts any fp32 product chain
+        # above 1e-5 on some layers, so the yardstick is plain fp32 GEMMs of the same operands (CPU)
+        f32 = (torch.from_numpy(Gi).float() @ torch.from_numpy(dW).float()) @ torch.from_numpy(Ai).float()
+        e32 = relerr(f32.double().numpy(), want)
+        note("precond_vs_fp32", e / max(e32, 1e-12), name)
+        assert e <= max(1e-5, 4 * e32), (name, e, e32)
         # end to end: the all-fp64 oracle pipeline from the same half inputs
         Ad64, Gd64, _ = orc.damp(A64, G64, gamma)
         Ai64, sa = orc.inverse(Ad64)
