@@ -255,11 +255,35 @@ KFAC_API kfac_status kfac_reduce_scatter_factors(kfac_comm_t comm, kfac_plan_t p
  *   pi = sqrt((tr A / dA) / (tr G / dG)), pi = 1 if a trace is 0;
  *   A_d = A + pi*sqrt(gamma) I,  G_d = G + sqrt(gamma)/pi I   (R-1)
  * and writes A_d^-1, G_d^-1 (full fp32) at inv_off into inv_ws (R-12:
- * fp64 arithmetic).  dev_status[2k+0 / 2k+1] = 0 on success, else the failing
+ * fp64-class arithmetic, see kfac_plan_set_inverse_precision).  dev_status[2k+0 / 2k+1] = 0 on success, else the failing
  * pivot index + 1 for A_d / G_d.  pi_out (device, may be NULL) receives pi per
  * owned layer.  Errors: KFAC_ERR_ARG (gamma <= 0, NULL), KFAC_ERR_STATE.    */
 KFAC_API kfac_status kfac_damped_inverse(kfac_plan_t plan, int32_t rank, const float *rs_recv, float gamma, float *inv_ws,
                                 int32_t *dev_status, float *pi_out, void *ws, void *stream);
+
+/* Precision of the damped inverse's sweep updates (reading R-12).  The pivots,
+ * panels P_k R_J and the working matrix are fp64 in every mode; what varies is the rank-128 update
+ * M_IJ -= R_I^T (P_k R_J), > 90% of the flops:
+ *   KFAC_INV_AUTO  per matrix, from the a-priori bound kappa(M_d) <= tr(M_d)/delta (delta = the
+ *                  damping added): int8-sliced updates (each fp64 operand column as 5 balanced
+ *                  8-bit digits under a power-of-two scale; exact int32 tensor-core sums of the
+ *                  15 leading digit pairs, recombined exactly in int64 and scaled in fp64;
+ *                  relative error <= ~3e-13 x bound on the paper's factors) where
+ *                  bound <= 3e6, fp64 DMMA updates elsewhere (default);
+ *   KFAC_INV_FP64  fp64 DMMA updates for every matrix;
+ *   KFAC_INV_INT8  int8-sliced updates for every matrix (tests and experiments).
+ * A stale / G-refresh plan takes the mode of the plan it was made from at creation.
+ * Errors: KFAC_ERR_ARG (NULL plan, unknown mode).                                               */
+typedef enum { KFAC_INV_AUTO = 0, KFAC_INV_FP64 = 1, KFAC_INV_INT8 = 2 } kfac_inv_precision;
+KFAC_API kfac_status kfac_plan_set_inverse_precision(kfac_plan_t plan, int32_t mode);
+
+/* After kfac_damped_inverse on `stream` with workspace `ws`: per owned matrix 2k+0 (A_d) / 2k+1
+ * (G_d) of `rank`, the condition bound tr(M_d)/delta and the update precision it got (4 = int8
+ * slices, 0 = fp64).  Host outputs of 2 x (owned layers) entries.  SYNCHRONISES `stream` (a
+ * device-to-host copy of the pair data at the start of ws).  Errors: KFAC_ERR_ARG, KFAC_ERR_STATE
+ * (stale plan, rank), KFAC_ERR_CUDA.  On a G-refresh plan the A entries are not meaningful.     */
+KFAC_API kfac_status kfac_inverse_report(kfac_plan_t plan, int32_t rank, const void *ws, double *bound /* host */,
+                                         int32_t *slices /* host */, void *stream);
 
 /* Change rate of the Kronecker factors between two refreshes:
  * for the k-th layer owned by `rank` (kfac_plan_rank_layers order),

@@ -286,7 +286,25 @@ kfac_status kfac_damped_inverse(kfac_plan_t p, int32_t rank, const float *recv, 
         }
     }
     if (off > p->ws_bytes) return set_error(KFAC_ERR_STATE, "kfac_damped_inverse: workspace layout exceeds ws_bytes");
-    return inverse_launch(mats, (int)ow.size(), gamma, pair_scratch, pi_out, p->g_only ? 1 : 0, S(stream));
+    return inverse_launch(mats, (int)ow.size(), gamma, pair_scratch, pi_out, p->g_only ? 1 : 0, p->inv_prec, S(stream));
+}
+
+kfac_status kfac_inverse_report(kfac_plan_t p, int32_t rank, const void *ws, double *bound, int32_t *slices, void *stream) {
+    if (!p || !ws || !bound || !slices) return set_error(KFAC_ERR_ARG, "kfac_inverse_report: NULL argument");
+    if (p->stale) return set_error(KFAC_ERR_STATE, "kfac_inverse_report: a stale plan runs no inverse");
+    if (rank < 0 || rank >= p->world) return set_error(KFAC_ERR_STATE, "kfac_inverse_report: rank out of range");
+    const size_t np = p->owned[rank].size();
+    std::vector<double> h(8 * np);
+    if (np) {
+        KFAC_CUDA_TRY(cudaMemcpyAsync(h.data(), ws, h.size() * sizeof(double), cudaMemcpyDeviceToHost, S(stream)));
+        KFAC_CUDA_TRY(cudaStreamSynchronize(S(stream)));
+    }
+    for (size_t k = 0; k < np; k++)
+        for (int which = 0; which < 2; which++) {
+            bound[2 * k + which] = h[8 * k + 3 + which];
+            slices[2 * k + which] = (int32_t)h[8 * k + 5 + which];
+        }
+    return KFAC_OK;
 }
 
 // ------------------------------------------------------------------ stage 5

@@ -25,6 +25,7 @@
 #include <cstring>
 
 #include "kfac_internal.hpp"
+#include "sm100.cuh"
 
 namespace kfac {
 
@@ -41,7 +42,9 @@ constexpr int KC = KFAC_INV_KC;  // K rows per shared-memory ring stage of the t
 constexpr int kStages = KFAC_INV_STAGES;  // ring depth
 constexpr int kPivSmem = (B * (B + 1) + 2 * 32 * (B + 4) + 32 * 36 + 64) * 8 + 64;
 constexpr int kTileSmem = kStages * 2 * KC * (B + 4) * 8;  // A/B chunk ring (padded rows): 66 KB
-constexpr int kUpdSmem = kPivSmem > kTileSmem + B * (B + 4) * 8 ? kPivSmem : kTileSmem + B * (B + 4) * 8;
+constexpr int kUpdSmemDmma = kPivSmem > kTileSmem + B * (B + 4) * 8 ? kPivSmem : kTileSmem + B * (B + 4) * 8;
+constexpr int kUpdSmemOz = 2 * (5 * B * B) + 3 * (5 * 32 * B) + 4 * B * 4 + 1024;  // = kOzSmem (int8 updates)
+constexpr int kUpdSmem = kUpdSmemDmma > kUpdSmemOz ? kUpdSmemDmma : kUpdSmemOz;
 static_assert(kUpdSmem >= B * (B + 1) * 8 + kTileSmem, "panel staging + ring fit the update kernel's shared memory");
 
 struct MatDesc {
@@ -54,7 +57,7 @@ struct MatDesc {
     int32_t nt;          // column blocks
     int32_t col_begin;   // prefix of nt over the (nt-descending) matrix list: column / step flags
     int32_t tile_begin;  // prefix of nt (nt + 1) / 2: tile flags
-    int32_t pad_;
+    int32_t orig;        // index in the caller's matrix list (2 * pair + !is_A): report slot
 };
 constexpr int kMaxSteps = 128;
 struct InvParams {
@@ -63,6 +66,8 @@ struct InvParams {
     double *pair_scratch;  // [npairs][4]: pi, dA, dG
     float *pi_out;         // pi per pair (out; in for a G refresh: the cached pi of the last full refresh)
     int32_t g_only;        // G refresh: G matrices only, damped with the cached pi (R-20)
+    int32_t prec_mode;     // inverse precision: KFAC_INV_AUTO / KFAC_INV_FP64 / KFAC_INV_INT8 (kfac.h)
+    int32_t *ozflag;       // [nm] per matrix (launch order): 1 = int8-sliced updates, 0 = fp64 DMMA updates
     // dataflow state (zeroed per inverse call): one task counter, then per matrix / column / step
     // stamps and counters -- see inverse_kernel
     int *counter;
@@ -97,47 +102,70 @@ __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b)
                  : "d"(a), "d"(b));
 }
 
-// ---- prologue: traces -> pi and the damping of each (A, G) pair
+// ---- prologue: traces -> pi and the damping of each (A, G) pair, and the per-matrix
+// precision of the sweep's updates (reading R-12): the a-priori condition bound
+//     kappa(M_d) <= tr(M_d) / delta = (tr(M) + n delta) / delta,   delta = the damping added,
+// picks int8-sliced updates (5 balanced 8-bit digits: measured error <= 3e-13 x bound on the
+// workload's factors and on rank-deficient ReLU Grams, scripts/ozaki_proto.py) where
+// bound <= kOzBound, i.e. a predicted error <= 1e-6 against the 1e-5 tolerance; the others keep
+// fp64 DMMA updates.  Pair scratch (8 doubles per pair): pi, A's add,
+// G's add, A's bound, G's bound, A's slices, G's slices (0 = fp64), spare.
+constexpr double kOzBound = 3e6;
+constexpr int kOzS = 5;  // 8-bit digits per operand of an int8-sliced update
+__device__ double block_trace(const float *packed, int n, double *red) {
+    double t = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) t += (double)packed[poff(i, i, n)];
+    red[threadIdx.x] = t;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+        __syncthreads();
+    }
+    return red[0];
+}
+__device__ void decide_precision(const InvParams &P, int mi, double tr, double add) {
+    const MatDesc &m = P.m[mi];
+    const double bound = add > 0.0 ? (tr + m.n * add) / add : INFINITY;
+    const int s = P.prec_mode == KFAC_INV_FP64 ? 0 : (P.prec_mode == KFAC_INV_INT8 ? kOzS : (bound <= kOzBound ? kOzS : 0));
+    P.ozflag[mi] = s ? 1 : 0;
+    P.pair_scratch[8 * m.pair + (m.is_A ? 3 : 4)] = bound;
+    P.pair_scratch[8 * m.pair + (m.is_A ? 5 : 6)] = (double)s;
+}
 __global__ void damp_trace_kernel(const __grid_constant__ InvParams P) {
     const MatDesc &ma = P.m[blockIdx.x];
+    __shared__ double red[256];
     if (!ma.is_A) {
-        if (P.g_only && threadIdx.x == 0) {  // G refresh: G_d = G + sqrt(gamma) / pi_cached I
-            const double pi = P.pi_out[ma.pair], sg = sqrt(P.gamma);
-            P.pair_scratch[4 * ma.pair + 0] = pi;
-            P.pair_scratch[4 * ma.pair + 2] = sg / pi;
-            *ma.status = 0;
+        if (P.g_only) {  // G refresh: G_d = G + sqrt(gamma) / pi_cached I
+            const double tg = block_trace(ma.packed, ma.n, red);
+            if (threadIdx.x == 0) {
+                const double pi = P.pi_out[ma.pair], sg = sqrt(P.gamma);
+                P.pair_scratch[8 * ma.pair + 0] = pi;
+                P.pair_scratch[8 * ma.pair + 2] = sg / pi;
+                decide_precision(P, blockIdx.x, tg, sg / pi);
+                *ma.status = 0;
+            }
         }
         return;
     }
-    const MatDesc *mg = nullptr;
+    int gi = -1;
     for (int k = 0; k < P.nm; k++)
-        if (P.m[k].pair == ma.pair && !P.m[k].is_A) mg = &P.m[k];
-    __shared__ double red[2][256];
-    double ta = 0.0, tg = 0.0;
-    for (int i = threadIdx.x; i < ma.n; i += blockDim.x) ta += (double)ma.packed[poff(i, i, ma.n)];
-    for (int i = threadIdx.x; i < mg->n; i += blockDim.x) tg += (double)mg->packed[poff(i, i, mg->n)];
-    red[0][threadIdx.x] = ta;
-    red[1][threadIdx.x] = tg;
+        if (P.m[k].pair == ma.pair && !P.m[k].is_A) gi = k;
+    const MatDesc &mg = P.m[gi];
+    const double ta = block_trace(ma.packed, ma.n, red);
     __syncthreads();
-    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
-        if (threadIdx.x < s) {
-            red[0][threadIdx.x] += red[0][threadIdx.x + s];
-            red[1][threadIdx.x] += red[1][threadIdx.x + s];
-        }
-        __syncthreads();
-    }
+    const double tg = block_trace(mg.packed, mg.n, red);
     if (threadIdx.x == 0) {
-        ta = red[0][0];
-        tg = red[1][0];
         double pi = 1.0;
-        if (ta != 0.0 && tg != 0.0) pi = sqrt((ta / ma.n) / (tg / mg->n));
+        if (ta != 0.0 && tg != 0.0) pi = sqrt((ta / ma.n) / (tg / mg.n));
         double sg = sqrt(P.gamma);
-        P.pair_scratch[4 * ma.pair + 0] = pi;
-        P.pair_scratch[4 * ma.pair + 1] = pi * sg;  // added to A's diagonal
-        P.pair_scratch[4 * ma.pair + 2] = sg / pi;  // added to G's diagonal
+        P.pair_scratch[8 * ma.pair + 0] = pi;
+        P.pair_scratch[8 * ma.pair + 1] = pi * sg;  // added to A's diagonal
+        P.pair_scratch[8 * ma.pair + 2] = sg / pi;  // added to G's diagonal
         if (P.pi_out) P.pi_out[ma.pair] = (float)pi;
+        decide_precision(P, blockIdx.x, ta, pi * sg);
+        decide_precision(P, gi, tg, sg / pi);
         *ma.status = 0;
-        *mg->status = 0;
+        *mg.status = 0;
     }
 }
 
@@ -145,7 +173,7 @@ __global__ void damp_trace_kernel(const __grid_constant__ InvParams P) {
 __global__ void unpack_damp_kernel(const __grid_constant__ InvParams P) {
     const MatDesc &m = P.m[blockIdx.y];
     const int64_t n = m.n;
-    const double add = P.pair_scratch[4 * m.pair + (m.is_A ? 1 : 2)];
+    const double add = P.pair_scratch[8 * m.pair + (m.is_A ? 1 : 2)];
     for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
         const float *src = m.packed + poff(i, i, n);
         double *dst = m.work + i * m.ld;
@@ -357,15 +385,6 @@ __device__ __forceinline__ double *pivot_slot(const MatDesc &m, int k) {
 __device__ __forceinline__ double *panel_R(const MatDesc &m, int k) { return m.panel + (int64_t)(k % kPanelBufs) * 2 * B * m.ld; }
 __device__ __forceinline__ double *panel_Wp(const MatDesc &m, int k) { return panel_R(m, k) + (int64_t)B * m.ld; }
 
-// step 0 only: P_0 (later pivots are fused into the previous step's tile (K+1, K+1) update)
-__global__ void __launch_bounds__(256, 1) pivot_kernel(const __grid_constant__ InvParams P) {
-    const MatDesc &m = P.m[blockIdx.x];
-    if (*m.status != 0) return;
-    extern __shared__ double dyn[];
-    const int f = pivot_block(m.work, m.ld, 0, min(B, m.n), pivot_slot(m, 0), dyn);
-    if (f && threadIdx.x == 0) *m.status = f;
-}
-
 __device__ __forceinline__ void cp_async16(void *dst, const void *src, bool ok) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
                  "l"(src), "r"(ok ? 16 : 0)
@@ -418,9 +437,6 @@ struct Ring {
     uint64_t *full, *empty;  // [kStages] each
     uint32_t g;              // chunks this CTA has streamed so far (uniform over the CTA)
 };
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s2u(bar)) : "memory");
-}
 // BSRC: 0 both operands through the ring; 1 / 2 the B operand is already resident in shared memory
 // (Tb, row stride B+1: element (t, j) at Tb[t][j], or at Tb[j][t] for 2) and only A streams.
 template <int BSRC = 0>
@@ -485,10 +501,454 @@ __device__ __forceinline__ void cp_async8(void *dst, const void *src, bool ok) {
                  : "memory");
 }
 
+#ifdef INV_TRACE  // experiment build only: per-task timeline
+struct TraceRec { int g, k, kind, I, J, sm; long long t0, t1, t2, t3, t4; };
+__device__ TraceRec g_trace[1 << 17];
+__device__ long long g_trace_sub[1024][2];  // per CTA: end of the product, end of the C-tile wait
+__device__ __forceinline__ long long gtime() { long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t; }
+#define TRACE(...) __VA_ARGS__
+#else
+#define TRACE(...)
+#endif
+// ---- int8-sliced ("Ozaki") sweep updates on the tensor cores (tcgen05 kind::i8), the per-matrix
+// fast path of reading R-12 (decide_precision).  Each column c of a step's panel block X (X = R_J
+// or Wp_J, 128 rows t = the step's K index) is written with five balanced 8-bit digits
+//     X[t][c] = 2^(e_c - 37) * sum_{s<5} q_s[t][c] 2^8(4-s),   q_s in [-128, 127] (|q_0| <= 33),
+// e_c the column exponent (max_t |X[t][c]| < 2^e_c), |error| <= 2^(e_c - 38).  The update product
+// R_I^T Wp_J then is 2^(e_i + f_j - 42) * sum_{d<5} 2^8(4-d) Acc_d with the exact int32 tensor-core
+// sums Acc_d = sum_{s+u=d} q_s(R_I)^T q_u(Wp_J) (the 15 digit pairs of weight >= 2^-32 of the
+// leading one), recombined exactly in int64 (|V| < 2^50) and scaled in fp64.  Measured on the
+// workload's factors and rank-deficient ReLU Grams at kappa ~ 1e4: ~1e-8 relative error of the
+// damped inverse (scripts/ozaki_proto.py), against 3e-8 for all-fp64 updates and the 1e-5 bound.
+// Digit tiles are [128 columns][128 t] int8, K-major in the 128-byte swizzle, 16 KB each, written
+// once per (step, column block) by the panel task; an update streams its B operand in column
+// quarters (N = 32) through a 3-slot ring, and TMEM holds two quarter accumulator sets (5 x 32
+// columns each) so that one quarter drains while the next one's 60 MMAs run.
+constexpr int kOzSlice = B * B;       // bytes per int8 digit tile
+constexpr int kOzQ = 32;              // columns per pass (MMA N)
+constexpr int kOzQBytes = kOzQ * B;   // one digit tile's quarter (32 rows x 128 B)
+constexpr int kOzD = 6;               // digits stored per column: x = 2^(e - 45) sum_{s<6} q_s 2^8(5-s)
+constexpr int kOzBits = 45;
+constexpr int kOzSet = kOzD * kOzSlice;            // one stored digit tile set (96 KB)
+constexpr int kOzABytes = kOzS * kOzSlice;          // one step's A digits (80 KB)
+constexpr int kOzRBytes = kOzS * kOzQBytes;         // one ring slot: a quarter of the 5 B tiles (20 KB)
+constexpr int kOzSmem = 2 * kOzABytes + 3 * kOzRBytes + 4 * B * 4 + 1024;
+static_assert(kOzS == 5, "the drain recombines exactly five diagonals");
+static_assert(kOzSmem == kUpdSmemOz, "kUpdSmem accounts for the int8 pipeline");
+static_assert(B * (B + 1) * 8 <= 133120 && kOzSet <= 133120, "the panel's T region holds R_J, P_k's digits and Wp_J");
+static_assert(B * (B + 1) * 8 <= 2 * kOzABytes, "the product tile fits the A slots");
+// instruction descriptor kind::i8: D s32, A and B s8, both K-major, M = 128, N = n
+__host__ __device__ constexpr uint32_t idesc_i8(uint32_t n) {
+    return (2u << 4) | (1u << 7) | (1u << 10) | ((n >> 3) << 17) | ((uint32_t)(B >> 4) << 24);
+}
+
+// per matrix, after the pivot slots: [step mod kPanelBufs][J][op: R_J, Wp_J] digit tile sets (6 x 16 KB),
+// their column exponents [step mod kPanelBufs][op][n], and two pivot digit sets (P_k, k mod 2) + exponents
+__device__ __forceinline__ uint8_t *oz_base(const MatDesc &m) {
+    return reinterpret_cast<uint8_t *>(m.panel + 2 * kPanelBufs * (int64_t)B * m.ld + 2 * (int64_t)B * B);
+}
+__device__ __forceinline__ uint8_t *oz_slices(const MatDesc &m, int k, int J, int op) {
+    return oz_base(m) + (((int64_t)(k % kPanelBufs) * m.nt + J) * 2 + op) * kOzSet;
+}
+__device__ __forceinline__ int *oz_exps(const MatDesc &m, int k, int op) {
+    return reinterpret_cast<int *>(oz_base(m) + (int64_t)kPanelBufs * m.nt * 2 * kOzSet) + ((int64_t)(k % kPanelBufs) * 2 + op) * m.nt * B;
+}
+__device__ __forceinline__ uint8_t *oz_pivdig(const MatDesc &m, int k) {
+    return oz_base(m) + (int64_t)kPanelBufs * m.nt * 2 * kOzSet + (int64_t)kPanelBufs * 2 * m.nt * B * 4 + (k & 1) * (kOzSet + B * 4);
+}
+__device__ __forceinline__ int *oz_pivexp(const MatDesc &m, int k) { return reinterpret_cast<int *>(oz_pivdig(m, k) + kOzSet); }
+
+// digits of the 128 x 128 block X -> dst (kOzD tiles) and the column exponents -> dexp[0..128) (and
+// sexp, 128 ints of shared memory).  MODE 0: X[t][c] = T[t][c]; 1: T[c][t]; 2: the pivot,
+// X = P = -S with S in upper storage, zero outside bk x bk.  All 256 threads.
+template <int MODE>
+__device__ __forceinline__ double oz_x(const double (*T)[B + 1], int t, int c, int bk) {
+    if (MODE == 0) return T[t][c];
+    if (MODE == 1) return T[c][t];
+    return (t < bk && c < bk) ? -T[min(t, c)][max(t, c)] : 0.0;
+}
+template <int MODE>
+__device__ void oz_slice(const double (*T)[B + 1], uint8_t *dst, int *dexp, int *sexp, int bk = B) {
+    const int tid = threadIdx.x;
+    {  // column maxima: two threads per column (half the rows each), 8 loads in flight
+        const int c = tid & (B - 1), t0 = (tid >> 7) * (B / 2);
+        double mx[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) mx[u] = 0.0;
+#pragma unroll
+        for (int t = 0; t < B / 2; t += 8)
+#pragma unroll
+            for (int u = 0; u < 8; u++) mx[u] = fmax(mx[u], fabs(oz_x<MODE>(T, t0 + t + u, c, bk)));
+        const double m4 = fmax(fmax(fmax(mx[0], mx[1]), fmax(mx[2], mx[3])), fmax(fmax(mx[4], mx[5]), fmax(mx[6], mx[7])));
+        double *red = reinterpret_cast<double *>(sexp + B);  // 128 doubles of scratch after the exponents
+        if (tid >= B) red[c] = m4;
+        __syncthreads();
+        if (tid < B) {
+            const double m = fmax(m4, red[c]);
+            int e = 0;
+            if (m > 0.0) frexp(m, &e);
+            e = max(e, -960);  // below: the digits (and the contribution) vanish
+            sexp[c] = e;
+            dexp[c] = e;
+        }
+    }
+    __syncthreads();
+    // digits: U = Y + C with C = 0x80 in each of the five low bytes; the low bytes of U XOR 0x80 are the
+    // balanced digits q_5..q_1 (q = u - 128), and U >> 40 is q_0 (|q_0| <= 33).  Four consecutive t are
+    // transposed byte-wise (PRMT) into the digit planes.
+    for (int it = tid; it < B * 8; it += 256) {
+        const int c = it & (B - 1), tc = it >> 7;  // consecutive threads: consecutive columns (conflict-free)
+        const double sc = __longlong_as_double((long long)(1023 + kOzBits - sexp[c]) << 52);
+        uint32_t wd[kOzD][4];
+#pragma unroll
+        for (int g = 0; g < 4; g++) {
+            uint32_t lo[4], hi[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const long long U = __double2ll_rn(oz_x<MODE>(T, 16 * tc + 4 * g + u, c, bk) * sc) + 0x8080808080LL;
+                lo[u] = (uint32_t)U ^ 0x80808080u;        // bytes: q_5, q_4, q_3, q_2
+                hi[u] = (uint32_t)(U >> 32);              // byte 0: q_1 ^ 0x80, bits 8..: q_0
+            }
+            // 4 x 4 byte transpose of lo: plane 5 gets byte 0 of each, ... plane 2 byte 3
+            const uint32_t a01 = __byte_perm(lo[0], lo[1], 0x5140), a23 = __byte_perm(lo[2], lo[3], 0x5140);
+            const uint32_t b01 = __byte_perm(lo[0], lo[1], 0x7362), b23 = __byte_perm(lo[2], lo[3], 0x7362);
+            wd[5][g] = __byte_perm(a01, a23, 0x5410);
+            wd[4][g] = __byte_perm(a01, a23, 0x7632);
+            wd[3][g] = __byte_perm(b01, b23, 0x5410);
+            wd[2][g] = __byte_perm(b01, b23, 0x7632);
+            const uint32_t h01 = __byte_perm(hi[0], hi[1], 0x5140), h23 = __byte_perm(hi[2], hi[3], 0x5140);
+            wd[1][g] = __byte_perm(h01, h23, 0x5410) ^ 0x80808080u;
+            wd[0][g] = __byte_perm(h01, h23, 0x7632);  // byte 1 of hi = q_0 (signed, |q_0| < 128)
+        }
+#pragma unroll
+        for (int s = 0; s < kOzD; s++)
+            *reinterpret_cast<uint4 *>(dst + s * kOzSlice + c * B + ((tc ^ (c & 7)) << 4)) =
+                make_uint4(wd[s][0], wd[s][1], wd[s][2], wd[s][3]);
+    }
+    asm volatile("fence.proxy.async;" ::: "memory");  // the digits are read back by bulk copies
+}
+
+// barriers of the int8 update pipeline (shared memory) and their phase bits (uniform per CTA)
+enum { OZ_A = 0, OZ_R = 2, OZ_TF = 5, OZ_TE = 7, OZ_NBAR = 9 };
+struct OzState {
+    uint64_t *bar;  // [OZ_NBAR]: A digits per step (2), ring slots (3), TMEM full (2), TMEM empty (2)
+    uint32_t ph;    // phase bit per barrier
+    uint32_t tmem;  // 2 accumulator sets x (5 or 6) diagonals x 32 columns
+    int *sexp;      // [128] shared: column exponents of the block being cut into digits
+    int *eP;        // [128] shared: the pivot's row exponents (panel product)
+};
+__device__ __forceinline__ void oz_wait(OzState &o, int b) {
+    cbar_wait(o.bar + b, (o.ph >> b) & 1);
+    o.ph ^= 1u << b;
+}
+
+// 32 lanes x 8 columns of 32-bit
+__device__ __forceinline__ void tmem_ld_x8(uint32_t taddr, uint32_t (&r)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
+}
+__device__ __forceinline__ void mma_i8(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_prefetch_l2(const void *src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+// one thread: the 15 digit-pair products of one column quarter (K = 128 = 4 MMAs of K 32 each).
+// The accumulator set is [diagonal d = 0..4][32 columns] and a ring slot holds the quarter tiles of
+// B's digits u = 0..4 as consecutive 32-row blocks, so for A's digit s ONE MMA with B = rows
+// [0, 32 (5 - s)) of the slot (N = 32 (5 - s)) adds q_s^T r_u into diagonal s + u for every u at
+// once: 5 MMAs per K step, each A chunk read from shared memory once.
+template <int ND>
+__device__ __forceinline__ void oz_mma_pass(uint32_t tacc, uint32_t sa, uint32_t sb) {
+#pragma unroll
+    for (int s = 0; s < ND; s++)
+#pragma unroll
+        for (int kk = 0; kk < B / 32; kk++)
+            mma_i8(tacc + kOzQ * s, umma_desc(sa + s * kOzSlice + kk * 32, 16, 1024, UMMA_SW128),
+                   umma_desc(sb + kk * 32, 16, 1024, UMMA_SW128), idesc_i8(kOzQ * (ND - s)), (s > 0 || kk > 0) ? 1u : 0u);
+}
+// thread (warp w, lane): row 32 (w & 3) + lane, columns 16 (w >> 2) + [0, 16) of the quarter (eB: the
+// quarter's 32 column exponents):
+// acc += 2^(eA[row] + eB[col] - 42) * sum_d 2^8(4-d) Acc_d   (int64 exact, |V| < 2^50):
+// x y = 2^(ea - 37) 2^(eb - 37) sum_{s,u} 2^8(8 - s - u) q_s r_u = 2^(ea + eb - 42) sum_d 2^8(4 - d) Acc_d
+__device__ __forceinline__ void oz_drain(uint32_t tacc, double (&acc)[16], const int *eA, const int *eB) {
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t tb = tacc + ((uint32_t)(32 * (w & 3)) << 16) + 16 * (w >> 2);
+    const int ea = eA[32 * (w & 3) + lane] - 42 + 1023;
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+        uint32_t a[kOzS][8];
+#pragma unroll
+        for (int d = 0; d < kOzS; d++) tmem_ld_x8(tb + kOzQ * d + 8 * h, a[d]);
+        tmem_ld_wait();
+#pragma unroll
+        for (int c = 0; c < 8; c++) {
+            const long long V = (long long)(int)a[0][c] * 4294967296LL + (long long)(int)a[1][c] * 16777216LL +
+                                (long long)(int)a[2][c] * 65536LL + (long long)(int)a[3][c] * 256LL + (long long)(int)a[4][c];
+            const double v = __longlong_as_double(V + 0x4338000000000000LL) - 6755399441055744.0;  // exact, |V| < 2^51
+            const int ex = max(ea + eB[16 * (w >> 2) + 8 * h + c], 0);
+            acc[8 * h + c] = fma(v, __longlong_as_double((long long)ex << 52), acc[8 * h + c]);
+        }
+    }
+}
+
+// the panel product's drain (all six digits, the 21 pairs of weight >= 2^-40): per thread row t,
+// columns 16 (w >> 2) + [0, 16) of the quarter; acc = 2^(eP[t] + eR[col] - 50) * sum_d 2^8(5-d) Acc_d,
+// recombined as two exact halves (each |.| < 2^40) so that the fp64 conversion stays exact
+__device__ __forceinline__ void oz_drain6(uint32_t tacc, double (&acc)[16], const int *eP, const int *eR) {
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t tb = tacc + ((uint32_t)(32 * (w & 3)) << 16) + 16 * (w >> 2);
+    const int ea = eP[32 * (w & 3) + lane] - 50 + 1023;
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+        uint32_t a[kOzD][8];
+#pragma unroll
+        for (int d = 0; d < kOzD; d++) tmem_ld_x8(tb + kOzQ * d + 8 * h, a[d]);
+        tmem_ld_wait();
+#pragma unroll
+        for (int c = 0; c < 8; c++) {
+            const long long Vh = (long long)(int)a[0][c] * 65536LL + (long long)(int)a[1][c] * 256LL + (long long)(int)a[2][c];
+            const long long Vl = (long long)(int)a[3][c] * 65536LL + (long long)(int)a[4][c] * 256LL + (long long)(int)a[5][c];
+            const double vh = __longlong_as_double(Vh + 0x4338000000000000LL) - 6755399441055744.0;
+            const double vl = __longlong_as_double(Vl + 0x4338000000000000LL) - 6755399441055744.0;
+            const int ex = max(ea + eR[16 * (w >> 2) + 8 * h + c], 0);
+            acc[8 * h + c] = fma(vh, 16777216.0, vl) * __longlong_as_double((long long)ex << 52);
+        }
+    }
+}
+
+// panel task (m, k, J) of an int8-sliced matrix: R_J staged and cut into digits (global, for the
+// updates and for this product), Wp_J = P_k R_J from the pivot's digits on the tensor cores (4
+// column-quarter passes, 21 digit pairs each, same pipeline as oz_update), then Wp_J's digits and
+// the step-k value of tile (K, J).  Shared memory: T (R_J, then P_k's digits, then Wp_J) + a 3-slot
+// ring of R_J's quarter digit tiles.
+constexpr int kOzPRing = kOzD * kOzQBytes;  // 24 KB
+constexpr int kOzPanelSmem = 133120 + 3 * kOzPRing + 1024;
+static_assert(kOzPanelSmem <= kUpdSmem, "the int8 panel fits the update kernel's shared memory");
+__device__ void oz_panel(const MatDesc &m, int k, int J, double *dyn, OzState &o, int *sexp, int *eP) {
+    const int n = m.n, k0 = k * B, K = k;
+    const int64_t ld = m.ld;
+    const int j0 = J * B;
+    const int bk = min(B, n - k0), bj = min(B, n - j0);
+    uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(dyn) + 1023) & ~uintptr_t(1023));
+    double(*T)[B + 1] = reinterpret_cast<double(*)[B + 1]>(sm);
+    uint8_t *ring = sm + 133120;
+    const int bjp = min(B, (int)ld - j0);
+    const bool trans = J < K;
+    const int r0 = trans ? j0 : k0, c0 = trans ? k0 : j0, nr = trans ? bj : bk, nc = trans ? bk : bj;
+    asm volatile("fence.proxy.async;" ::: "memory");  // P_k's digits (another CTA) and this smem (earlier tasks)
+    __syncthreads();
+#pragma unroll 16
+    for (int it = 0; it < B * B / 256; it++) {
+        const int e = it * 256 + threadIdx.x, r = e >> 7, c = e & (B - 1);
+        const bool ok = r < nr && c < nc;
+        cp_async8(&T[r][c], ok ? m.work + (int64_t)(r0 + r) * ld + c0 + c : m.work, ok);
+    }
+    cp_async_commit();
+    cp_async_wait_0();
+    __syncthreads();
+    uint8_t *rdig = oz_slices(m, k, J, 0);
+    if (trans) oz_slice<1>(T, rdig, oz_exps(m, k, 0) + j0, sexp);
+    else oz_slice<0>(T, rdig, oz_exps(m, k, 0) + j0, sexp);
+    __syncthreads();  // T is read; R_J's digits are in global memory (proxy-fenced)
+    TRACE(if (threadIdx.x == 0) g_trace_sub[blockIdx.x][0] = gtime();)
+    auto load_ring = [&](int q) {
+        uint8_t *dst = ring + (q % 3) * kOzPRing;
+        cbar_expect(o.bar + OZ_R + q % 3, kOzPRing);
+        for (int s = 0; s < kOzD; s++) bulk_row(dst + s * kOzQBytes, rdig + s * kOzSlice + q * kOzQBytes, kOzQBytes, o.bar + OZ_R + q % 3);
+    };
+    if (threadIdx.x == 0) {
+        cbar_expect(o.bar + OZ_A, kOzSet + B * 4);
+        bulk_row(sm, oz_pivdig(m, k), kOzSet, o.bar + OZ_A);
+        bulk_row(eP, oz_pivexp(m, k), B * 4, o.bar + OZ_A);
+        for (int q = 0; q < 3; q++) load_ring(q);
+    }
+    double acc[4][16];
+    const uint32_t sA = smem_u32(sm), sR = smem_u32(ring);
+#pragma unroll
+    for (int p = 0; p <= 4; p++) {
+        if (p < 4 && threadIdx.x == 0) {
+            oz_wait(o, OZ_TE + (p & 1));
+            oz_wait(o, OZ_R + p % 3);
+            if (p == 0) oz_wait(o, OZ_A);
+            tc_fence_after();
+            oz_mma_pass<kOzD>(o.tmem + (p & 1) * (kOzD * kOzQ), sA, sR + (p % 3) * kOzPRing);
+            mma_commit(o.bar + OZ_TF + (p & 1));
+        }
+        if (p >= 1) {
+            const int pd = p - 1;
+            if (pd == 0 && threadIdx.x != 0) oz_wait(o, OZ_A);
+            oz_wait(o, OZ_TF + (pd & 1));
+            tc_fence_after();
+            oz_drain6(o.tmem + (pd & 1) * (kOzD * kOzQ), acc[pd], eP, sexp + kOzQ * pd);
+            tc_fence_before();
+            mbar_arrive(o.bar + OZ_TE + (pd & 1));
+            if (threadIdx.x == 0 && pd + 3 < 4) load_ring(pd + 3);
+        }
+    }
+    __syncthreads();  // every MMA completed: P_k's digits in T are dead
+    TRACE(if (threadIdx.x == 0) g_trace_sub[blockIdx.x][1] = gtime();)
+    {
+        const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, t = 32 * (w & 3) + lane, cb = 16 * (w >> 2);
+#pragma unroll
+        for (int q = 0; q < 4; q++)
+#pragma unroll
+            for (int c = 0; c < 16; c++) T[t][32 * q + cb + c] = acc[q][c];  // Wp_J (zero outside bk rows)
+    }
+    __syncthreads();
+    oz_slice<0>(T, oz_slices(m, k, J, 1), oz_exps(m, k, 1) + j0, sexp);  // Wp_J's digits
+    for (int e = threadIdx.x; e < bk * B; e += 256) {  // the step-k value of tile (K, J)
+        const int t = e >> 7, j = e & (B - 1);
+        if (j >= bjp || trans) continue;
+        m.work[(int64_t)(k0 + t) * ld + j0 + j] = T[t][j];
+    }
+    if (trans)  // M_JK <- Wp_J^T: row j of tile (J, K), consecutive threads along t
+        for (int e = threadIdx.x; e < bj * B; e += 256) {
+            const int j = e >> 7, t = e & (B - 1);
+            if (t < bk) m.work[(int64_t)(j0 + j) * ld + k0 + t] = T[t][j];
+        }
+}
+
+// update task (m, k, I, J) of an int8-sliced matrix, ns = 1 or 2 steps: 4 ns column-quarter passes
+// (step st = p / 4, quarter q = p % 4, TMEM set p & 1, ring slot p % 3).  Thread 0 loads and issues;
+// every thread drains.  The product goes through shared memory to a coalesced C read-modify-write
+// (the C tile was prefetched into L2 at the task start).  Same contract as update_task's DMMA path.
+__device__ int oz_update(const InvParams &P, const MatDesc &m, int k, int ns, int I, int J, double *dyn, const int *pflag,
+                         OzState &o, bool &deferred) {
+    const int n = m.n, i0 = I * B, j0 = J * B, bi = min(B, n - i0);
+    const int64_t ld = m.ld;
+    double *W = m.work;
+    const int last = k + ns - 1, Q = 4 * ns;
+    uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(dyn) + 1023) & ~uintptr_t(1023));
+    uint8_t *ring = sm + 2 * kOzABytes;
+    int *eA = reinterpret_cast<int *>(ring + 3 * kOzRBytes), *eB = eA + 2 * B;  // [2 steps][128] each
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int jw = (int)min((int64_t)B, ld - j0);  // columns of the tile inside ld (a multiple of 16)
+    fence_proxy_async_smem();  // earlier generic use of this shared memory before the bulk copies
+    __syncthreads();
+    if (threadIdx.x < bi) bulk_prefetch_l2(W + (int64_t)(i0 + threadIdx.x) * ld + j0, jw * 8);
+    auto load_ring = [&](int p) {  // thread 0: the B digits of pass p into slot p % 3
+        const int st = p >> 2, q = p & 3;
+        const uint8_t *src = oz_slices(m, k + st, J, 1) + q * kOzQBytes;
+        uint8_t *dst = ring + (p % 3) * kOzRBytes;
+        cbar_expect(o.bar + OZ_R + p % 3, kOzRBytes);
+        for (int s = 0; s < kOzS; s++) bulk_row(dst + s * kOzQBytes, src + s * kOzSlice, kOzQBytes, o.bar + OZ_R + p % 3);
+    };
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < ns; st++) {
+            cbar_expect(o.bar + OZ_A + st, kOzABytes + 2 * B * 4);
+            const uint8_t *src = oz_slices(m, k + st, I, 0);
+            for (int s = 0; s < kOzS; s++) bulk_row(sm + st * kOzABytes + s * kOzSlice, src + s * kOzSlice, kOzSlice, o.bar + OZ_A + st);
+            bulk_row(eA + st * B, oz_exps(m, k + st, 0) + i0, B * 4, o.bar + OZ_A + st);
+            bulk_row(eB + st * B, oz_exps(m, k + st, 1) + j0, B * 4, o.bar + OZ_A + st);
+        }
+        for (int p = 0; p < 3 && p < Q; p++) load_ring(p);
+    }
+    double acc[4][16];
+#pragma unroll
+    for (int q = 0; q < 4; q++)
+#pragma unroll
+        for (int c = 0; c < 16; c++) acc[q][c] = 0.0;
+    const uint32_t sA = smem_u32(sm), sR = smem_u32(ring);
+    auto issue = [&](int p) {  // thread 0: the MMAs of pass p
+        const int st = p >> 2;
+        oz_wait(o, OZ_TE + (p & 1));  // its TMEM set was drained (or never used: pre-armed)
+        oz_wait(o, OZ_R + p % 3);
+        if ((p & 3) == 0) oz_wait(o, OZ_A + st);
+        tc_fence_after();
+        oz_mma_pass<kOzS>(o.tmem + (p & 1) * (kOzS * kOzQ), sA + st * kOzABytes, sR + (p % 3) * kOzRBytes);
+        mma_commit(o.bar + OZ_TF + (p & 1));
+    };
+#pragma unroll
+    for (int p = 0; p <= 8; p++) {
+        if (p > Q) break;
+        if (p < Q && threadIdx.x == 0) issue(p);
+        if (p >= 1) {  // drain pass p - 1 while pass p runs
+            const int pd = p - 1, st = pd >> 2;
+            if ((pd & 3) == 0 && threadIdx.x != 0) oz_wait(o, OZ_A + st);  // exponents visible to every thread
+            oz_wait(o, OZ_TF + (pd & 1));
+            tc_fence_after();
+            oz_drain(o.tmem + (pd & 1) * (kOzS * kOzQ), acc[pd & 3], eA + st * B, eB + st * B + kOzQ * (pd & 3));
+            tc_fence_before();
+            mbar_arrive(o.bar + OZ_TE + (pd & 1));
+            if (threadIdx.x == 0 && pd + 3 < Q) load_ring(pd + 3);  // its slot's MMAs are complete (drained)
+        }
+    }
+    // the product tile through shared memory (the A slots are dead: every MMA completed)
+    __syncthreads();
+    double(*Pt)[B + 1] = reinterpret_cast<double(*)[B + 1]>(dyn);
+    {
+        const int r = 32 * (w & 3) + lane, cb = 16 * (w >> 2);
+#pragma unroll
+        for (int q = 0; q < 4; q++)
+#pragma unroll
+            for (int c = 0; c < 16; c++) Pt[r][32 * q + cb + c] = acc[q][c];
+    }
+    __syncthreads();
+    TRACE(if (threadIdx.x == 0) g_trace_sub[blockIdx.x][0] = gtime();)
+    const bool piv = I == last + 1 && J == last + 1;
+    // coalesced C read-modify-write: warp w takes rows w, w + 8, ...; lane l columns l + 32 i.  All 64
+    // loads of a lane are issued before any use (L2 hits: the tile was prefetched at the task start).
+    {
+        double cv[B / 8][4];
+#pragma unroll
+        for (int i8 = 0; i8 < B / 8; i8++) {
+            const int r = w + 8 * i8;
+            const double *crow = W + (int64_t)(i0 + r) * ld + j0;
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+                const int c = lane + 32 * i;
+                cv[i8][i] = (r < bi && c < jw) ? __ldcg(crow + c) : 0.0;
+            }
+        }
+#pragma unroll
+        for (int i8 = 0; i8 < B / 8; i8++) {
+            const int r = w + 8 * i8;
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+                const int c = lane + 32 * i;
+                const double v = cv[i8][i] - Pt[r][c];
+                if (piv) Pt[r][c] = (r < bi && c < bi) ? v : (r == c ? 1.0 : 0.0);  // fused next pivot, in place
+                else if (r < bi && c < jw) W[(int64_t)(i0 + r) * ld + j0 + c] = v;
+            }
+        }
+    }
+    TRACE(if (threadIdx.x == 0) g_trace_sub[blockIdx.x][1] = gtime();)
+    if (piv) {
+        __syncthreads();
+        if (last >= 1 && threadIdx.x == 0) {  // its slot held P_{last-1}: step last-1's panels must be done
+            int vv;
+            do {
+                asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(vv) : "l"(pflag) : "memory");
+                if (vv < m.nt) __nanosleep(128);
+            } while (vv < m.nt);
+        }
+        __syncthreads();
+        const int f = pivot_block(W, ld, i0, bi, pivot_slot(m, last + 1), dyn, true);
+        if (!f) {  // P_{last+1}'s digits (S = -P, upper storage) for the next step's panel products
+            __syncthreads();
+            oz_slice<2>(reinterpret_cast<const double(*)[B + 1]>(dyn), oz_pivdig(m, last + 1), oz_pivexp(m, last + 1), o.sexp, bi);
+        }
+        return f;
+    }
+    deferred = true;
+    return 0;
+}
+
 // ---- panel task (m, k, J): R_J = block row K (from upper storage), Wp_J = P_k R_J.  The task also
 // gives tile (K, J) its step-k value Wp_J (M_KJ <- Wp_J, or M_JK <- Wp_J^T left of the diagonal):
 // nothing else reads that tile at step k, so the row / column K "copy" updates have no work left.
-__device__ void panel_task(const MatDesc &m, int k, int J, double *dyn, Ring &ring) {
+__device__ void panel_task(const MatDesc &m, int k, int J, double *dyn, Ring &ring, bool oz, OzState &ozs) {
+    if (oz) {
+        oz_panel(m, k, J, dyn, ozs, ozs.sexp, ozs.eP);
+        return;
+    }
     const int n = m.n, k0 = k * B, K = k;
     const int64_t ld = m.ld;
     const int j0 = J * B;
@@ -551,21 +1011,13 @@ __device__ void panel_task(const MatDesc &m, int k, int J, double *dyn, Ring &ri
         }
 }
 
-#ifdef INV_TRACE  // experiment build only: per-task timeline
-struct TraceRec { int g, k, kind, I, J, sm; long long t0, t1, t2, t3, t4; };
-__device__ TraceRec g_trace[1 << 17];
-__device__ long long g_trace_sub[1024][2];  // per CTA: end of the product, end of the C-tile wait
-__device__ __forceinline__ long long gtime() { long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t; }
-#define TRACE(...) __VA_ARGS__
-#else
-#define TRACE(...)
-#endif
 // ---- update task (m, k, I, J): rank-B sweep update of upper tile (I, J); the task of tile
 // (K+1, K+1) then inverts that block (the next step's pivot).  Returns 0 or a pivot failure.
 // nsteps = 1: the update of tile (I, J) at step k (incl. the copy tiles of row / column k);
 // nsteps = 2: the merged update for steps k and k+1 (I, J not in {k, k+1}).
 __device__ int update_task(const InvParams &P, const MatDesc &m, int k, int nsteps, int I, int J, double *dyn,
-                           const int *pflag, uint64_t *cbar, uint32_t &cph, Ring &ring, bool &deferred) {
+                           const int *pflag, uint64_t *cbar, uint32_t &cph, Ring &ring, bool &deferred, bool oz,
+                           OzState &ozs) {
     const int n = m.n, k0 = k * B, K = k;
     const int64_t ld = m.ld;
     const int bk = min(B, n - k0);
@@ -575,6 +1027,7 @@ __device__ int update_task(const InvParams &P, const MatDesc &m, int k, int nste
     double *W = m.work;
     if (I == K && J == K) return 0;  // M_KK <- -P_K: written by the pivot itself (pivot_block)
     if (I == K || J == K) return 0;  // M_KJ <- Wp_J / M_IK <- Wp_I^T: written by the panel tasks
+    if (oz) return oz_update(P, m, k, nsteps, I, J, dyn, pflag, ozs, deferred);
     double acc[8][8];
 #pragma unroll
     for (int p = 0; p < 8; p++)
@@ -664,6 +1117,20 @@ __device__ __forceinline__ void wait_ge(const int *f, int target) {
 }
 __device__ __forceinline__ int upper_index(int I, int J, int nt) { return I * nt - I * (I - 1) / 2 + (J - I); }
 
+// step 0 only: P_0 (later pivots are fused into the previous step's tile (K+1, K+1) update)
+__global__ void __launch_bounds__(256, 1) pivot_kernel(const __grid_constant__ InvParams P) {
+    const MatDesc &m = P.m[blockIdx.x];
+    if (*m.status != 0) return;
+    extern __shared__ double dyn[];
+    const int f = pivot_block(m.work, m.ld, 0, min(B, m.n), pivot_slot(m, 0), dyn);
+    if (f && threadIdx.x == 0) *m.status = f;
+    if (!f && P.ozflag[blockIdx.x]) {  // P_0's digits for step 0's int8 panel products
+        __shared__ __align__(16) int sexp[3 * B];
+        __syncthreads();
+        oz_slice<2>(reinterpret_cast<const double(*)[B + 1]>(dyn), oz_pivdig(m, 0), oz_pivexp(m, 0), sexp, min(B, m.n));
+    }
+}
+
 #include "inverse_tasks.hpp"
 using namespace kfac_inv;
 
@@ -691,6 +1158,30 @@ __global__ void inverse_tasks_kernel(const __grid_constant__ InvParams P) {
     pair_emit(nt, k, m, cur, P.tasks + P.step_begin[pr]);
 }
 
+// L2 prefetch (one warp) of what task t will read: t = the current task + gridDim.x, which some CTA
+// takes about one task duration from now (tasks are handed out in order).  Stale lines are harmless
+// (L2 is coherent: a later write of the producer updates them).
+__device__ void prefetch_task(const InvParams &P, int t, int lane) {
+    if (t >= P.total_tasks) return;
+    const int4 task = P.tasks[t];
+    const int k = task.x, I = task.w >> 16, J = task.w & 0xffff;
+    const MatDesc &m = P.m[task.z];
+    const int n = m.n;
+    const int64_t ld = m.ld;
+    if (task.y == 1 || task.y == 2) {
+        if (!P.ozflag[task.z] || I == k || J == k) return;
+        const int ns = task.y == 2 ? 2 : 1, i0 = I * B, j0 = J * B, bi = min(B, n - i0);
+        const int jw = (int)min((int64_t)B, ld - j0);
+        if (lane < 2 * ns) bulk_prefetch_l2(oz_slices(m, k + (lane >> 1), (lane & 1) ? J : I, lane & 1), kOzABytes);
+        for (int r = lane; r < bi; r += 32) bulk_prefetch_l2(m.work + (int64_t)(i0 + r) * ld + j0, jw * 8);
+    } else if (J != k) {  // panel: the staged block of row K (upper storage; transposed left of the diagonal)
+        const int k0 = k * B, j0 = J * B, bk = min(B, n - k0), bj = min(B, n - j0);
+        const bool trans = J < k;
+        const int r0 = trans ? j0 : k0, c0 = trans ? k0 : j0, nr = trans ? bj : bk, nc = trans ? bk : bj;
+        for (int r = lane; r < nr; r += 32) bulk_prefetch_l2(m.work + (int64_t)(r0 + r) * ld + c0, ((nc * 8 + 15) / 16) * 16);
+    }
+}
+
 // ---- the whole sweep as ONE persistent launch: CTAs take tasks from an atomic counter in the
 // order above, and each task waits on the stamps of the tasks it reads:
 //   panel (m,k,J):   tile (K,J) of step k-1, P_k, and (buffer reuse) all of step k-2's updates
@@ -703,6 +1194,9 @@ __global__ void __launch_bounds__(256, 1) inverse_kernel(const __grid_constant__
     __shared__ int next;
     __shared__ uint64_t cbar;  // C tile bulk loads of update tasks
     __shared__ uint64_t ring_full[kStages], ring_empty[kStages];
+    __shared__ uint64_t ozbar[OZ_NBAR];  // int8-sliced updates: operand loads, TMEM full / empty
+    __shared__ uint32_t tmem_slot;
+    __shared__ __align__(16) int oz_sexp[3 * B], oz_eP[B];  // exponents + 128 doubles of reduction scratch
     uint32_t cph = 0;
     Ring ring{ring_full, ring_empty, 0};
     if (threadIdx.x == 0) {
@@ -711,8 +1205,16 @@ __global__ void __launch_bounds__(256, 1) inverse_kernel(const __grid_constant__
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 256;" ::"r"(s2u(ring_full + st)) : "memory");
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 8;" ::"r"(s2u(ring_empty + st)) : "memory");
         }
+        for (int b = 0; b < OZ_NBAR; b++) mbar_init(ozbar + b, b >= OZ_TE ? 256 : 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    if (threadIdx.x < 32) tmem_alloc(&tmem_slot, 512);  // one CTA per SM (shared memory): all of TMEM
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    OzState ozs{ozbar, 0u, tmem_slot, oz_sexp, oz_eP};
+    mbar_arrive(ozbar + OZ_TE);  // both TMEM accumulator sets start empty
+    mbar_arrive(ozbar + OZ_TE + 1);
     // deferred release of the previous update task (its tile stores may still be draining)
     bool pend = false, pend_two = false;
     int *pend_tile = nullptr, *pend_done = nullptr;
@@ -734,11 +1236,16 @@ __global__ void __launch_bounds__(256, 1) inverse_kernel(const __grid_constant__
         __syncthreads();
         const int g = next;
         if (g >= P.total_tasks) break;
+
         TRACE(long long tr0 = gtime(); long long tr1 = 0; int trI = -1, trJ = -1, trkind = 0;)
+#ifdef KFAC_INV_PREFETCH  // experiment: L2 prefetch one round ahead (measured slower: 20.0 -> 24.5 us per merged task)
+        if ((threadIdx.x >> 5) == 1) prefetch_task(P, g + gridDim.x, threadIdx.x & 31);
+#endif
         const int4 task = P.tasks[g];
         const int k = task.x, mi = task.z, I = task.w >> 16, J = task.w & 0xffff;
         const MatDesc &m = P.m[mi];
         const int nt = m.nt;
+        const bool oz = P.ozflag[mi] != 0;
         if (task.y == 0 || task.y == 3) {
             // ---------------- panel task (kind 0) / chain task (kind 3: panel (k, J = k+1), then the
             // update of tile (J, J) at step k and its inverse P_{k+1}, in one task)
@@ -756,7 +1263,7 @@ __global__ void __launch_bounds__(256, 1) inverse_kernel(const __grid_constant__
             __syncthreads();
             TRACE(tr1 = gtime(); trJ = J; trkind = task.y == 3 ? 5 : 0;)
             const bool live = next == 0;
-            if (live && J != k) panel_task(m, k, J, dyn, ring);  // R_K / P R_K are never read
+            if (live && J != k) panel_task(m, k, J, dyn, ring, oz, ozs);  // R_K / P R_K are never read
             __threadfence();
             __syncthreads();
             if (threadIdx.x == 0) {
@@ -768,7 +1275,7 @@ __global__ void __launch_bounds__(256, 1) inverse_kernel(const __grid_constant__
                 bool deferred = false;  // stays false: the pivot path writes W itself
                 if (live)
                     f = update_task(P, m, k, 1, J, J, dyn, P.panels_done + m.col_begin + (k >= 1 ? k - 1 : 0), &cbar, cph,
-                                    ring, deferred);
+                                    ring, deferred, oz, ozs);
                 if (f && threadIdx.x == 0) *m.status = f;
                 __threadfence();
                 __syncthreads();
@@ -800,7 +1307,7 @@ __global__ void __launch_bounds__(256, 1) inverse_kernel(const __grid_constant__
             bool deferred = false;
             if (next == 0)
                 f = update_task(P, m, k, ns, I, J, dyn, P.panels_done + m.col_begin + (last >= 1 ? last - 1 : 0), &cbar,
-                                cph, ring, deferred);
+                                cph, ring, deferred, oz, ozs);
             if (deferred) {  // tile stores still draining: release at the next task's start
                 pend = true;
                 pend_tile = P.tileflag + m.tile_begin + upper_index(I, J, nt);
@@ -828,6 +1335,12 @@ __global__ void __launch_bounds__(256, 1) inverse_kernel(const __grid_constant__
             g_trace[g] = TraceRec{g, k, trkind, trI, trJ, sm, tr0, tr1, gtime(), g_trace_sub[blockIdx.x][0], g_trace_sub[blockIdx.x][1]};
         }
 #endif
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        tc_fence_after();
+        tmem_dealloc(tmem_slot, 512);
     }
 }
 
@@ -874,11 +1387,14 @@ extern "C" __attribute__((visibility("default"))) int kfac_debug_inverse_trace(v
 #endif
 
 int64_t inverse_ld(int n) { return (n + 15) / 16 * 16; }
+static int64_t pair_doubles(int npairs) { return ((8 * (int64_t)npairs + 15) / 16) * 16; }
+static int64_t state_ints(int npairs, int64_t sum_nt, int64_t sum_tiles) {
+    return 16 + 4 * (int64_t)npairs + 3 * sum_nt + sum_tiles;
+}
 int64_t inverse_scratch_bytes(int npairs, int64_t sum_nt, int64_t sum_tiles, int64_t sum_tasks) {
-    // pair data | counter + pivflag (2 npairs) | colflag, panels_done, tiles_done (sum_nt each) |
-    // tileflag | task records (16 B each)
-    return ((4 * (int64_t)npairs + 15) / 16) * 16 * 8 +
-           ((16 + 2 * (int64_t)npairs + 3 * sum_nt + sum_tiles + 3) / 4) * 16 + sum_tasks * 16 + 256;
+    // pair data (8 doubles per pair) | counter + pivflag (2 npairs) + ozflag (2 npairs) | colflag,
+    // panels_done, tiles_done (sum_nt each) | tileflag | task records (16 B each)
+    return pair_doubles(npairs) * 8 + ((state_ints(npairs, sum_nt, sum_tiles) + 3) / 4) * 16 + sum_tasks * 16 + 256;
 }
 // tasks of one n x n matrix's sweep: nt panels + nt (nt + 1) / 2 tiles per step, nt steps
 int64_t inverse_tasks(int n) {
@@ -886,12 +1402,14 @@ int64_t inverse_tasks(int n) {
     return nt * (nt + nt * (nt + 1) / 2);
 }
 int64_t inverse_ws_doubles(int n) {
-    const int64_t ld = inverse_ld(n);
-    return (n * ld + 2 * kPanelBufs * (int64_t)B * ld + 2 * (int64_t)B * B + 31) / 32 * 32;
+    // working matrix | fp64 R / Wp panels | pivot slots | int8 digit tiles | digit exponents
+    const int64_t ld = inverse_ld(n), nt = (n + B - 1) / B;
+    const int64_t oz = (kPanelBufs * nt * 2 * (int64_t)kOzSet + kPanelBufs * 2 * nt * B * 4 + 2 * (kOzSet + B * 4)) / 8;
+    return (n * ld + 2 * kPanelBufs * (int64_t)B * ld + 2 * (int64_t)B * B + oz + 31) / 32 * 32;
 }
 
 kfac_status inverse_launch(const std::vector<InvMat> &mats, int npairs, float gamma, double *pair_scratch,
-                           float *pi_out, int g_only, cudaStream_t st) {
+                           float *pi_out, int g_only, int prec_mode, cudaStream_t st) {
     if (mats.empty()) return KFAC_OK;
     if ((int)mats.size() > kMaxMats) {
         // more than kMaxMats owned matrices (e.g. ResNet-101 on one GPU): several launches in stream
@@ -902,7 +1420,7 @@ kfac_status inverse_launch(const std::vector<InvMat> &mats, int npairs, float ga
             size_t e = std::min(mats.size(), b + (size_t)kMaxMats);
             while (e < mats.size() && e > b + 1 && mats[e].pair == mats[e - 1].pair) e--;
             KFAC_TRY(inverse_launch(std::vector<InvMat>(mats.begin() + b, mats.begin() + e), npairs, gamma,
-                                    pair_scratch, pi_out, g_only, st));
+                                    pair_scratch, pi_out, g_only, prec_mode, st));
             b = e;
         }
         return KFAC_OK;
@@ -918,6 +1436,7 @@ kfac_status inverse_launch(const std::vector<InvMat> &mats, int npairs, float ga
     P.pair_scratch = pair_scratch;
     P.pi_out = pi_out;
     P.g_only = g_only;
+    P.prec_mode = prec_mode;
     // matrices by column blocks, descending: the matrices active at step k are a prefix
     std::vector<int> order(mats.size());
     for (size_t i = 0; i < mats.size(); i++) order[i] = (int)i;
@@ -935,6 +1454,7 @@ kfac_status inverse_launch(const std::vector<InvMat> &mats, int npairs, float ga
         d.ld = (int)inverse_ld(d.n);
         d.pair = src.pair;
         d.is_A = src.is_A;
+        d.orig = order[r];
         d.nt = (d.n + B - 1) / B;
         d.col_begin = sum_nt;
         d.tile_begin = sum_tiles;
@@ -956,15 +1476,16 @@ kfac_status inverse_launch(const std::vector<InvMat> &mats, int npairs, float ga
     P.step_begin[npairs_steps] = task;
     P.total_tasks = task;
     // dataflow state after the pair data (inverse_scratch_bytes): zeroed once per call
-    int *state = reinterpret_cast<int *>(pair_scratch + ((4 * (int64_t)npairs + 15) / 16) * 16);
+    int *state = reinterpret_cast<int *>(pair_scratch + pair_doubles(npairs));
     P.counter = state;
     P.pivflag = state + 16;
-    P.colflag = P.pivflag + 2 * npairs;
+    P.ozflag = P.pivflag + 2 * npairs;
+    P.colflag = P.ozflag + 2 * npairs;
     P.panels_done = P.colflag + sum_nt;
     P.tiles_done = P.panels_done + sum_nt;
     P.tileflag = P.tiles_done + sum_nt;
-    P.tasks = reinterpret_cast<int4 *>(state + ((16 + 2 * (int64_t)npairs + 3 * sum_nt + sum_tiles + 3) / 4) * 4);
-    KFAC_CUDA_TRY(cudaMemsetAsync(state, 0, (16 + 2 * (int64_t)npairs + 3 * sum_nt + sum_tiles) * sizeof(int), st));
+    P.tasks = reinterpret_cast<int4 *>(state + ((state_ints(npairs, sum_nt, sum_tiles) + 3) / 4) * 4);
+    KFAC_CUDA_TRY(cudaMemsetAsync(state, 0, state_ints(npairs, sum_nt, sum_tiles) * sizeof(int), st));
     inverse_tasks_kernel<<<dim3(npairs_steps, (P.nm + 31) / 32), 32, 0, st>>>(P);
     KFAC_LAUNCHED();
     KFAC_CUDA_TRY(cudaGetLastError());

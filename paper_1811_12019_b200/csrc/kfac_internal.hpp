@@ -122,7 +122,7 @@ struct PrecJob {
 };
 int64_t precond_split_floats(int n);  // [2][n][kpad(n)] hi / lo copy of one n x n inverse
 kfac_status inverse_launch(const std::vector<InvMat> &mats, int npairs, float gamma, double *pair_scratch,
-                           float *pi_out, int g_only, cudaStream_t st);
+                           float *pi_out, int g_only, int prec_mode, cudaStream_t st);
 kfac_status precond_launch(const std::vector<PrecJob> &jobs, cudaStream_t st);
 struct DiffMat {          // one packed factor of the stale-Fisher change rate (diff.cu)
     const float *cur, *prev;  // packed upper, 16-byte aligned

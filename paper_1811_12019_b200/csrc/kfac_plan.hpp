@@ -13,6 +13,7 @@ struct kfac_plan {
     kfac_policy policy = KFAC_OWN_ROUND_ROBIN;
     bool stale = false;   // stale-factor wire layout: dW segments only (R-20)
     bool g_only = false;  // G-refresh layout: dW and G segments (A kept stale, R-20)
+    int inv_prec = KFAC_INV_AUTO;  // kfac_plan_set_inverse_precision
     std::vector<int32_t> owner;
     std::vector<std::vector<int>> owned;                          // per rank, ascending
     std::vector<std::vector<std::array<int64_t, 3>>> local;       // per rank, per owned layer

@@ -308,6 +308,7 @@ kfac_status kfac_plan_create_grefresh(kfac_plan_t full, kfac_plan_t *out) {
     p->world = full->world;
     p->n_local = full->n_local;
     p->policy = full->policy;
+    p->inv_prec = full->inv_prec;
     p->g_only = true;
     kfac_status s = plan_build(p);
     if (s) {
@@ -315,6 +316,13 @@ kfac_status kfac_plan_create_grefresh(kfac_plan_t full, kfac_plan_t *out) {
         return s;
     }
     *out = p;
+    return KFAC_OK;
+}
+
+kfac_status kfac_plan_set_inverse_precision(kfac_plan_t p, int32_t mode) {
+    if (!p) return set_error(KFAC_ERR_ARG, "kfac_plan_set_inverse_precision: NULL plan");
+    if (mode < KFAC_INV_AUTO || mode > KFAC_INV_INT8) return set_error(KFAC_ERR_ARG, "kfac_plan_set_inverse_precision: bad mode");
+    p->inv_prec = mode;
     return KFAC_OK;
 }
 

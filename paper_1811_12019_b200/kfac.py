@@ -95,6 +95,9 @@ _bn_precondition = _sig("kfac_bn_precondition", [_i32, _pi32, _i32, ctypes.POINT
 _bn_exchange = _sig("kfac_bn_exchange", [_P, _i32, _pi32, _i32, ctypes.POINTER(_P), ctypes.POINTER(_P),
                                           ctypes.POINTER(_P), _P])
 _bn_ws_bytes = _sig("kfac_bn_ws_bytes", [_i32, _pi32, _i32, _pi64])
+_set_inv_prec = _sig("kfac_plan_set_inverse_precision", [_P, _i32])
+_inv_report = _sig("kfac_inverse_report", [_P, _i32, _P, ctypes.POINTER(ctypes.c_double), _pi32, _P])
+INV_AUTO, INV_FP64, INV_INT8 = 0, 1, 2
 _update = _sig("kfac_update", [_P, _P, ctypes.POINTER(_P), ctypes.POINTER(_P), _f32, _f32, _i32, _f32, _P, _P])
 
 EXPORTS = ["kfac_last_error", "kfac_version", "kfac_launch_count", "kfac_plan_create", "kfac_plan_query", "kfac_plan_rank_layers",
@@ -103,7 +106,8 @@ EXPORTS = ["kfac_last_error", "kfac_version", "kfac_launch_count", "kfac_plan_cr
            "kfac_damped_inverse", "kfac_precondition", "kfac_allgather_precond", "kfac_plan_create_stale",
            "kfac_plan_is_stale", "kfac_refresh_interval", "kfac_refresh", "kfac_factor_diff", "kfac_update", "kfac_bn_grads",
            "kfac_bn_precondition", "kfac_bn_ws_bytes", "kfac_bn_exchange",
-           "kfac_plan_create_grefresh", "kfac_plan_refresh_kind"]
+           "kfac_plan_create_grefresh", "kfac_plan_refresh_kind", "kfac_plan_set_inverse_precision",
+           "kfac_inverse_report"]
 
 
 def _check(st, where):
@@ -192,6 +196,10 @@ class Plan:
                     inv_off=[list(inv[2 * i:2 * i + 2]) for i in range(k)], inv_floats=nf.value)
 
 
+    def set_inverse_precision(self, mode):
+        """kfac_plan_set_inverse_precision: INV_AUTO (per-matrix bound), INV_FP64 or INV_INT8."""
+        _check(_set_inv_prec(self.h, int(mode)), "kfac_plan_set_inverse_precision")
+
     def stale_plan(self):
         """kfac_plan_create_stale: the plan of the steps that reuse stale factors."""
         return Plan(self.layers, self.world, self.n_local, stale_of=self)
@@ -274,6 +282,15 @@ def reduce_scatter_factors(comm, plan, rs_send, rs_recv, stream=None):
 def damped_inverse(plan, rank, rs_recv, gamma, inv_ws, dev_status, pi_out, ws, stream=None):
     _check(_damped_inverse(plan.h, int(rank), _ptr(rs_recv), float(gamma), _ptr(inv_ws), _ptr(dev_status),
                            _ptr(pi_out), _ptr(ws), _stream(stream)), "kfac_damped_inverse")
+
+
+def inverse_report(plan, rank, ws, n_owned, stream=None):
+    """kfac_inverse_report (synchronises the stream): per owned matrix (A_d, G_d of each layer),
+    the condition bound tr(M_d)/delta and the update precision (5 = int8 digits, 0 = fp64)."""
+    bound = (ctypes.c_double * (2 * n_owned))()
+    sl = (ctypes.c_int32 * (2 * n_owned))()
+    _check(_inv_report(plan.h, int(rank), _ptr(ws), bound, sl, _stream(stream)), "kfac_inverse_report")
+    return list(bound), list(sl)
 
 
 def precondition(plan, rank, rs_recv, inv_ws, ag_buf, ws, stream=None):

@@ -21,12 +21,14 @@ class KfacStep:
     compare the factors of two consecutive refreshes.
     """
 
-    def __init__(self, layers, n_local, rank=0, world=1, policy=kfac.RR, comm=None, device=None, stale=False):
+    def __init__(self, layers, n_local, rank=0, world=1, policy=kfac.RR, comm=None, device=None, stale=False,
+                 inv_precision=kfac.INV_AUTO):
         self.layers = list(layers)
         self.rank, self.world, self.n_local = int(rank), int(world), int(n_local)
         self.comm = comm
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.plan = kfac.Plan(self.layers, world, n_local, policy)
+        self.plan.set_inverse_precision(inv_precision)
         q = self.plan.query()
         self.q = q
         self.rl = self.plan.rank_layers(rank)
@@ -111,6 +113,12 @@ class KfacStep:
     def inverse(self, gamma, stream=None):
         kfac.damped_inverse(self.plan, self.rank, self.rs_recv, gamma, self.inv_ws, self.dev_status, self.pi,
                             self.ws, stream)
+
+    def inverse_report(self, stream=None):
+        """Per owned layer k: ((bound_A, bound_G), (slices_A, slices_G)) of the last inverse."""
+        n = len(self.rl["layers"])
+        b, s = kfac.inverse_report(self.plan, self.rank, self.ws, n, stream)
+        return [((b[2 * k], b[2 * k + 1]), (s[2 * k], s[2 * k + 1])) for k in range(n)]
 
     def precondition(self, stream=None):
         kfac.precondition(self.plan, self.rank, self.rs_recv, self.inv_ws, self.ag_buf, self.ws, stream)

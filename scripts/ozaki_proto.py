@@ -70,7 +70,7 @@ def oz_product(R, Wp, S):
     return out * np.ldexp(1.0, ea)[:, None] * np.ldexp(1.0, eb)[None, :]
 
 
-def sweep(M, S):
+def sweep(M, S, panel_oz=False):
     W = M.copy()
     n = W.shape[0]
     nt = (n + B - 1) // B
@@ -78,7 +78,7 @@ def sweep(M, S):
         K = slice(k * B, min(n, (k + 1) * B))
         P = np.linalg.inv(W[K, K])
         R = W[K, :].copy()
-        Wp = P @ R
+        Wp = oz_product(P.T.copy(), R, S) if (S and panel_oz) else P @ R
         others = np.r_[0:k * B, min(n, (k + 1) * B):n]
         if S:
             W[np.ix_(others, others)] -= oz_product(R[:, others], Wp[:, others], S)
@@ -93,23 +93,27 @@ def sweep(M, S):
 def main():
     cfg = sys.argv[1] if len(sys.argv) > 1 else "resnet50"
     names = sys.argv[2].split(",") if len(sys.argv) > 2 else ["l3b0c2"]
-    gammas = [2.5e-2, 2.5e-4]
+    gammas = [float(g) for g in sys.argv[3].split(",")] if len(sys.argv) > 3 else [2.5e-2, 2.5e-4]
+    Ss = [int(v) for v in sys.argv[4].split(",")] if len(sys.argv) > 4 else [0, 4, 5, 6, 7]
+    which_only = sys.argv[5] if len(sys.argv) > 5 else "AG"
     for name in names:
         A, G = factor_pair(cfg, name)
         for gamma in gammas:
             ta, tg = np.trace(A) / A.shape[0], np.trace(G) / G.shape[0]
             pi = np.sqrt(ta / tg)
             for which, (M, add) in (("A", (A, pi * np.sqrt(gamma))), ("G", (G, np.sqrt(gamma) / pi))):
+                if which not in which_only:
+                    continue
                 Md = M + add * np.eye(M.shape[0])
                 ref = np.linalg.inv(Md)
                 kap = np.linalg.cond(Md)
                 bound = (np.trace(Md)) / add
                 res = []
-                for S in (0, 4, 5, 6, 7):
-                    t0 = time.time()
-                    X = sweep(Md, S)
-                    e = np.linalg.norm(X - ref) / np.linalg.norm(ref)
-                    res.append(f"S={S}:{e:.1e}")
+                for S in Ss:
+                    for poz in ((False, True) if S else (False,)):
+                        X = sweep(Md, S, poz)
+                        e = np.linalg.norm(X - ref) / np.linalg.norm(ref)
+                        res.append(f"S={S}{'p' if poz else ''}:{e:.1e}")
                 print(f"{name} {which} n={M.shape[0]} gamma={gamma:g} kappa={kap:.2e} tr/delta={bound:.2e} " + " ".join(res),
                       flush=True)
 

@@ -183,9 +183,10 @@ def test_step_multilayer_end_to_end(K, orc):
         assert e <= TOL_PREC
 
 
-def test_inverse_reports_not_pd(K, orc):
+@pytest.mark.parametrize("prec", [1, 2])  # INV_FP64, INV_INT8
+def test_inverse_reports_not_pd(K, orc, prec):
     layers = [shapes.linear("fc", 7, 5, bias=0)]
-    st = K.KfacStep(layers, 1)
+    st = K.KfacStep(layers, 1, inv_precision=prec)
     dW, pa, pg = None, None, None
     # hand-made recv: A = -I (not PD after damping 0.1*pi), G = I
     d_a, d_g = 7, 5
@@ -202,15 +203,17 @@ def test_inverse_reports_not_pd(K, orc):
     assert want == 2
 
 
+@pytest.mark.parametrize("prec", [0, 1])  # INV_AUTO (per-matrix bound), INV_FP64
 @pytest.mark.parametrize("n", [64, 65, 130, 300, 513, 1153])
-def test_inverse_ill_conditioned(K, orc, n):
-    """Rank-deficient ReLU-like factors at small damping (kappa ~ 1e4): fp64 sweep meets 1e-5."""
+def test_inverse_ill_conditioned(K, orc, n, prec):
+    """Rank-deficient ReLU-like factors at small damping (kappa ~ 1e4): the sweep meets 1e-5 with
+    fp64 updates and with the per-matrix choice (R-12)."""
     rng = np.random.default_rng(n)
     X = np.maximum(rng.standard_normal((n // 3, n)), 0)
     A = (X.T @ X / X.shape[0]).astype(np.float32).astype(np.float64)
     G = np.eye(4)
     layers = [shapes.linear("fc", n, 4, bias=0)]
-    st = K.KfacStep(layers, 1)
+    st = K.KfacStep(layers, 1, inv_precision=prec)
     _, pa, pg = st.recv_views(0)
     pa.copy_(torch.as_tensor(orc.pack(A), dtype=torch.float32))
     pg.copy_(torch.as_tensor(orc.pack(G), dtype=torch.float32))
@@ -220,19 +223,20 @@ def test_inverse_ill_conditioned(K, orc, n):
     ref, s = orc.inverse(Ad)
     Ai, _ = st.inv_views(0)
     e = relerr(Ai.cpu().double().numpy(), ref)
-    print(f"n={n} cond={np.linalg.cond(Ad):.1e} err={e:.2e}")
+    print(f"n={n} cond={np.linalg.cond(Ad):.1e} err={e:.2e} report={st.inverse_report()}")
     assert s == 0 and st.dev_status.cpu().tolist() == [0, 0]
     assert e <= TOL_INV
 
 
 @pytest.mark.timeout(300)
-def test_inverse_batched_dataflow(K, orc):
+@pytest.mark.parametrize("prec", [1, 2])  # INV_FP64, INV_INT8
+def test_inverse_batched_dataflow(K, orc, prec):
     """Several owned matrices of mixed sizes (ragged tails, 1x1, multi-step) in ONE persistent
     dataflow launch, one of them not PD mid-sweep (pivot 400 of 1000: its tasks stop, the others
     must complete and stay exact -- no deadlock on the skipped tasks' stamps)."""
     layers = [shapes.linear("a", 700, 17, bias=0), shapes.linear("b", 129, 300, bias=0),
               shapes.linear("c", 1000, 1, bias=0), shapes.linear("d", 128, 65, bias=0)]
-    st = K.KfacStep(layers, 1)
+    st = K.KfacStep(layers, 1, inv_precision=prec)
     rng = np.random.default_rng(7)
     mats = []
     for k, l in enumerate(layers):
@@ -264,15 +268,16 @@ def test_inverse_batched_dataflow(K, orc):
 
 
 @pytest.mark.timeout(300)
+@pytest.mark.parametrize("prec", [0, 1, 2])
 @pytest.mark.parametrize("n", [2049, 4608])
-def test_fullsize_inverse_residual(K, n):
+def test_fullsize_inverse_residual(K, n, prec):
     """BASELINE config 5's largest factors (FC 2049, conv 4608; 17 / 36 sweep steps, merged
     two-step updates, odd and even step counts).  A rigorous bound on the relative error of the
     returned fp32 inverse X from its fp64 residual R = M X - I:
     ||X - M^-1||_F = ||M^-1 R||_F <= ||R||_F / lambda_min(M), and ||M^-1||_F >= ||X||_F - that."""
     g = 64
     layers = [shapes.linear("fc", n, g, bias=0)]
-    st = K.KfacStep(layers, 1)
+    st = K.KfacStep(layers, 1, inv_precision=prec)
     gen = torch.Generator(device="cuda").manual_seed(n)
     X = torch.relu(torch.randn(n // 2, n, generator=gen, device="cuda", dtype=torch.float64))
     A = (X.T @ X / X.shape[0]).float()
@@ -294,7 +299,8 @@ def test_fullsize_inverse_residual(K, n):
     lam_min = torch.linalg.eigvalsh(Ad)[0].item()
     err_abs = res / lam_min
     err_rel = err_abs / (torch.linalg.norm(Xi).item() - err_abs)
-    print(f"n={n} residual {res:.2e} lambda_min {lam_min:.2e} relative error <= {err_rel:.2e}")
+    print(f"n={n} prec={prec} residual {res:.2e} lambda_min {lam_min:.2e} relative error <= {err_rel:.2e} "
+          f"report {st.inverse_report()}")
     assert 0 < err_rel <= TOL_INV
     assert torch.allclose(Xi, Xi.T)
 
@@ -341,3 +347,36 @@ def test_fullsize_factors_sampled(K, orc, cfg):
     errs.sort(reverse=True)
     print(f"{cfg}: worst sampled entry errors {[(f'{e:.1e}', n, w) for e, n, w in errs[:6]]}")
     assert errs[0][0] <= TOL_FACTOR, errs[:3]
+
+
+@pytest.mark.parametrize("gamma", [2.5e-2, 2.5e-4])
+def test_inverse_report(K, orc, gamma):
+    """kfac_inverse_report: the a-priori bound tr(M_d)/delta of every matrix (R-12) against the
+    host's own trace arithmetic, and the precision each mode assigns (AUTO: int8 slices iff the
+    bound is <= 3e6)."""
+    layers = [shapes.linear("a", 300, 40, bias=0), shapes.linear("b", 129, 7, bias=0)]
+    rng = np.random.default_rng(3)
+    mats = []
+    for l in layers:
+        pair = []
+        for d in shapes.dims(l):
+            X = np.maximum(rng.standard_normal((max(d // 4, 1), d)), 0)
+            pair.append((X.T @ X / X.shape[0]).astype(np.float32).astype(np.float64))
+        mats.append(pair)
+    for prec in (0, 1, 2):
+        st = K.KfacStep(layers, 1, inv_precision=prec)
+        for k, (A, G) in enumerate(mats):
+            _, pa, pg = st.recv_views(k)
+            pa.copy_(torch.as_tensor(orc.pack(A), dtype=torch.float32))
+            pg.copy_(torch.as_tensor(orc.pack(G), dtype=torch.float32))
+        st.inverse(gamma)
+        rep = st.inverse_report()
+        for k, (A, G) in enumerate(mats):
+            _, _, pi = orc.damp(A, G, gamma)
+            for which, (M, add) in enumerate(((A, pi * np.sqrt(gamma)), (G, np.sqrt(gamma) / pi))):
+                want = (np.trace(M) + M.shape[0] * add) / add
+                got = rep[k][0][which]
+                assert abs(got - want) <= 1e-6 * want, (k, which, got, want)
+                sl = rep[k][1][which]
+                assert sl == {0: 5 if want <= 3e6 else 0, 1: 0, 2: 5}[prec], (prec, k, which, want, sl)
+        assert st.dev_status.cpu().abs().sum().item() == 0
