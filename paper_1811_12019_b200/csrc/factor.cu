@@ -521,6 +521,7 @@ __global__ void __launch_bounds__(kThreads, 1) factor_syrk_kernel(const __grid_c
                 const float alpha = pr.alpha;
                 for (int c0 = cbeg; c0 < nc; c0 += kQ) {
                     tmem_ld_wait();
+                    tmem_regs_ready(r);
                     float4 *srow = reinterpret_cast<float4 *>(stg + lane * kStageLd);
 #pragma unroll
                     for (int m = 0; m < 4; m++)

@@ -20,6 +20,8 @@
 // of every upper tile) -- all n^3 flops are in the tile products, which run
 // as fp64 DFMA tiles of 128x128 with 8x8 register blocking.
 #include <algorithm>
+#include <mutex>
+#include <type_traits>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -28,6 +30,11 @@
 #include "sm100.cuh"
 
 namespace kfac {
+
+// The persistent inverse kernel runs 8 worker warps (256 threads) and one producer warp (see OZ_*);
+// worker-only code synchronises with WSYNC (named barrier 1, 256 threads), __syncthreads is for all.
+constexpr int kWorkers = 256, kThreads = 288;
+#define WSYNC() asm volatile("bar.sync 1, 256;" ::: "memory")
 
 constexpr int kMaxMats = 128;
 constexpr int kPanelBufs = 4;  // panel buffers per matrix (step mod 4)
@@ -58,7 +65,9 @@ struct MatDesc {
     int32_t col_begin;   // prefix of nt over the (nt-descending) matrix list: column / step flags
     int32_t tile_begin;  // prefix of nt (nt + 1) / 2: tile flags
     int32_t orig;        // index in the caller's matrix list (2 * pair + !is_A): report slot
+    const CUtensorMap *tmaps;  // [3] in global memory: the digit tile sets as 4-D TMA maps (OZ_MAP_*)
 };
+enum { OZ_MAP_A = 0, OZ_MAP_R5 = 1, OZ_MAP_R6 = 2 };  // boxes {128 B, 128 rows, 5 digits}, {., 32, 5}, {., 32, 6}
 constexpr int kMaxSteps = 128;
 struct InvParams {
     int32_t nm, steps, total_tasks, pad0_;
@@ -223,7 +232,7 @@ __device__ __forceinline__ int block_sweep32(const double (*S)[B + 1], int s0, d
     for (int t = 0; t < S2_; t++) {
         double *rb = rowbuf + (t & 1) * 32;
         if (w == (t >> 2)) rb[lane] = x[t & 3];
-        __syncthreads();
+        WSYNC();
         const double d = rb[t];
         if (!(d > 0.0)) return base + t + 1;  // uniform: every thread read the same d
         const double inv = rcp_fast(d);
@@ -262,13 +271,13 @@ __device__ int pivot_block(double *__restrict__ W, int64_t ld, int k0, int bk, d
     // only the upper triangle of S is ever read (min / max indexing below), so only it is loaded
     // (coalesced rows); identity padding beyond bk keeps the sweep well defined
     if (!preloaded)
-        for (int e = tid; e < B * B; e += blockDim.x) {
+        for (int e = tid; e < B * B; e += kWorkers) {
             const int i = e >> 7, j = e & (B - 1);
             if (j < i) continue;
             S[i][j] = (i < bk && j < bk) ? W[(int64_t)(k0 + i) * ld + (k0 + j)] : (i == j ? 1.0 : 0.0);
         }
     if (tid == 0) *fsh = 0;
-    __syncthreads();
+    WSYNC();
     PCLK(0)
     for (int sb = 0; sb < B / S2; sb++) {
         const int s0 = sb * S2;
@@ -280,13 +289,13 @@ __device__ int pivot_block(double *__restrict__ W, int64_t ld, int k0, int bk, d
                 break;
             }
         }
-        __syncthreads();
+        WSYNC();
         PCLK(1 + 4 * sb)
-        for (int e = tid; e < S2 * B; e += blockDim.x) {  // old block row s (upper storage)
+        for (int e = tid; e < S2 * B; e += kWorkers) {  // old block row s (upper storage)
             const int a = s0 + (e >> 7), c = e & (B - 1);
             O[(e >> 7) * SLD + c] = S[min(a, c)][max(a, c)];
         }
-        __syncthreads();
+        WSYNC();
         if (*fsh) break;
         PCLK(2 + 4 * sb)
 #ifdef PIVOT_DBG
@@ -320,7 +329,7 @@ __device__ int pivot_block(double *__restrict__ W, int64_t ld, int k0, int bk, d
                     *reinterpret_cast<double2 *>(Wr + (8 * i + r8) * SLD + 16 * w + 8 * j + 2 * k4) =
                         make_double2(c[i][j][0], c[i][j][1]);
         }
-        __syncthreads();
+        WSYNC();
         PCLK(3 + 4 * sb)
 #ifdef PIVOT_DBG
         if (g_pivot_dbg == 2 && sb >= 1) break;
@@ -353,21 +362,21 @@ __device__ int pivot_block(double *__restrict__ W, int64_t ld, int k0, int bk, d
                 S[i][j + 1] -= acc[x][1];
             }
         }
-        __syncthreads();
-        for (int e = tid; e < S2 * B; e += blockDim.x) {
+        WSYNC();
+        for (int e = tid; e < S2 * B; e += kWorkers) {
             const int a = e >> 7, j = e & (B - 1);
             if (j >= s0 && j < s0 + S2) S[s0 + a][j] = -Q[a * QLD + (j - s0)];
             else if (j > s0) S[s0 + a][j] = Wr[a * SLD + j];  // right of the sub-block: its row band
             else S[j][s0 + a] = Wr[a * SLD + j];              // left: its column band (upper storage)
         }
-        __syncthreads();
+        WSYNC();
         PCLK(4 + 4 * sb)
     }
-    __syncthreads();
+    WSYNC();
     PCLK(20)
     const int fail = *fsh;
     if (fail) return fail;
-    for (int e = tid; e < B * B; e += blockDim.x) {  // P = -S (zero outside bk); W_KK = -P (upper)
+    for (int e = tid; e < B * B; e += kWorkers) {  // P = -S (zero outside bk); W_KK = -P (upper)
         const int i = e >> 7, j = e & (B - 1);
         const bool in = i < bk && j < bk;
         Pout[e] = in ? -S[min(i, j)][max(i, j)] : 0.0;
@@ -445,7 +454,7 @@ __device__ __forceinline__ void tile_product(const Seg &s0, const Seg &s1, doubl
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int arow = 64 * (w >> 2) + (lane >> 2), bcol = 32 * (w & 3) + (lane >> 2), kl = lane & 3;
     const int n0 = (s0.kt + KC - 1) / KC, nch = n0 + (s1.kt + KC - 1) / KC;
-    __syncthreads();  // the caller's shared-memory use (staging, pivots, epilogues) is over
+    WSYNC();  // the caller's shared-memory use (staging, pivots, epilogues) is over
     auto produce = [&](int c) {  // every thread: its 16-byte pieces of chunk c
         const uint32_t G = ring.g + c, st = G % kStages;
         const bool first = c < n0;
@@ -492,7 +501,7 @@ __device__ __forceinline__ void tile_product(const Seg &s0, const Seg &s1, doubl
         if (c + kStages - 1 < nch) produce(c + kStages - 1);
     }
     ring.g += nch;
-    __syncthreads();  // every warp is done with the ring before the caller reuses the shared memory
+    WSYNC();  // every warp is done with the ring before the caller reuses the shared memory
 }
 
 __device__ __forceinline__ void cp_async8(void *dst, const void *src, bool ok) {
@@ -507,6 +516,10 @@ __device__ TraceRec g_trace[1 << 17];
 __device__ long long g_trace_sub[1024][2];  // per CTA: end of the product, end of the C-tile wait
 __device__ __forceinline__ long long gtime() { long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t; }
 #define TRACE(...) __VA_ARGS__
+__device__ unsigned long long g_ozprof[8];  // cycles: ring wait, TE wait, A wait, TF wait, drain, issue, tasks
+__device__ long long g_ozt[148][80];  // one merged task per CTA (the 20th): producer issue start/end, warp-1 TF done/drain done
+__device__ int g_ozcnt[148];
+#define OZPROF(i, t0) atomicAdd(&g_ozprof[i], (unsigned long long)(clock64() - (t0)))
 #else
 #define TRACE(...)
 #endif
@@ -547,6 +560,9 @@ __host__ __device__ constexpr uint32_t idesc_i8(uint32_t n) {
 __device__ __forceinline__ uint8_t *oz_base(const MatDesc &m) {
     return reinterpret_cast<uint8_t *>(m.panel + 2 * kPanelBufs * (int64_t)B * m.ld + 2 * (int64_t)B * B);
 }
+__device__ __forceinline__ int oz_set(const MatDesc &m, int k, int J, int op) {
+    return ((k % kPanelBufs) * m.nt + J) * 2 + op;
+}
 __device__ __forceinline__ uint8_t *oz_slices(const MatDesc &m, int k, int J, int op) {
     return oz_base(m) + (((int64_t)(k % kPanelBufs) * m.nt + J) * 2 + op) * kOzSet;
 }
@@ -582,7 +598,7 @@ __device__ void oz_slice(const double (*T)[B + 1], uint8_t *dst, int *dexp, int 
         const double m4 = fmax(fmax(fmax(mx[0], mx[1]), fmax(mx[2], mx[3])), fmax(fmax(mx[4], mx[5]), fmax(mx[6], mx[7])));
         double *red = reinterpret_cast<double *>(sexp + B);  // 128 doubles of scratch after the exponents
         if (tid >= B) red[c] = m4;
-        __syncthreads();
+        WSYNC();
         if (tid < B) {
             const double m = fmax(m4, red[c]);
             int e = 0;
@@ -592,7 +608,7 @@ __device__ void oz_slice(const double (*T)[B + 1], uint8_t *dst, int *dexp, int 
             dexp[c] = e;
         }
     }
-    __syncthreads();
+    WSYNC();
     // digits: U = Y + C with C = 0x80 in each of the five low bytes; the low bytes of U XOR 0x80 are the
     // balanced digits q_5..q_1 (q = u - 128), and U >> 40 is q_0 (|q_0| <= 33).  Four consecutive t are
     // transposed byte-wise (PRMT) into the digit planes.
@@ -621,15 +637,27 @@ __device__ void oz_slice(const double (*T)[B + 1], uint8_t *dst, int *dexp, int 
             wd[0][g] = __byte_perm(h01, h23, 0x7632);  // byte 1 of hi = q_0 (signed, |q_0| < 128)
         }
 #pragma unroll
-        for (int s = 0; s < kOzD; s++)
-            *reinterpret_cast<uint4 *>(dst + s * kOzSlice + c * B + ((tc ^ (c & 7)) << 4)) =
-                make_uint4(wd[s][0], wd[s][1], wd[s][2], wd[s][3]);
+        for (int s = 0; s < kOzD; s++) {
+            uint8_t *a = dst + s * kOzSlice + c * B + ((tc ^ (c & 7)) << 4);
+#if KFAC_OZ_HINTS
+            asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(a), "r"(wd[s][0]), "r"(wd[s][1]),
+                         "r"(wd[s][2]), "r"(wd[s][3]), "l"(pol_evict_last())
+                         : "memory");
+#else
+            *reinterpret_cast<uint4 *>(a) = make_uint4(wd[s][0], wd[s][1], wd[s][2], wd[s][3]);
+#endif
+        }
     }
     asm volatile("fence.proxy.async;" ::: "memory");  // the digits are read back by bulk copies
 }
 
 // barriers of the int8 update pipeline (shared memory) and their phase bits (uniform per CTA)
-enum { OZ_A = 0, OZ_R = 2, OZ_TF = 5, OZ_TE = 7, OZ_NBAR = 9 };
+enum { OZ_A = 0, OZ_R = 2, OZ_TF = 5, OZ_TE = 7, OZ_RF = 9, OZ_RD = 12, OZ_NBAR = 13 };
+// The persistent kernel runs 8 worker warps (256 threads: every task's arithmetic, epilogues, drains) and
+// one producer warp (threads 256..287) whose lane 0 loads the int8 operands and issues the tensor-core
+// MMAs of the int8 tasks, so that the MMAs of pass p run while the workers drain pass p-1.  Worker-only
+// code synchronises with WSYNC (named barrier 1, 256 threads); __syncthreads is for all 288.
+
 struct OzState {
     uint64_t *bar;  // [OZ_NBAR]: A digits per step (2), ring slots (3), TMEM full (2), TMEM empty (2)
     uint32_t ph;    // phase bit per barrier
@@ -659,6 +687,34 @@ __device__ __forceinline__ void mma_i8(uint32_t d, uint64_t a, uint64_t b, uint3
 __device__ __forceinline__ void bulk_prefetch_l2(const void *src, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
+// L2 residency: the C tiles stream through once per two steps (evict first); the digit tiles are read
+// by a whole step's tasks (evict last).  KFAC_OZ_HINTS=0 builds without hints (experiments).
+#ifndef KFAC_OZ_HINTS
+#define KFAC_OZ_HINTS 1
+#endif
+__device__ __forceinline__ uint64_t pol_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t pol_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ double ld_ef(const double *p, uint64_t pol) {
+    double v;
+    asm volatile("ld.global.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ void st_ef(double *p, double v, uint64_t pol) {
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void bulk_row_hint(void *dst, const void *src, uint32_t bytes, uint64_t *bar, uint64_t pol) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(s2u(dst)),
+                 "l"(src), "r"(bytes), "r"(s2u(bar)), "l"(pol)
+                 : "memory");
+}
 // one thread: the 15 digit-pair products of one column quarter (K = 128 = 4 MMAs of K 32 each).
 // The accumulator set is [diagonal d = 0..4][32 columns] and a ring slot holds the quarter tiles of
 // B's digits u = 0..4 as consecutive 32-row blocks, so for A's digit s ONE MMA with B = rows
@@ -666,12 +722,15 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void *src, uint32_t bytes
 // once: 5 MMAs per K step, each A chunk read from shared memory once.
 template <int ND>
 __device__ __forceinline__ void oz_mma_pass(uint32_t tacc, uint32_t sa, uint32_t sb) {
+    // descriptors from two bases: the start-address field is addr >> 4 (shared memory < 256 KB: no
+    // carry out of the 14-bit field), so an operand offset is a constant add
+    const uint64_t da = umma_desc(sa, 16, 1024, UMMA_SW128), db = umma_desc(sb, 16, 1024, UMMA_SW128);
 #pragma unroll
     for (int s = 0; s < ND; s++)
 #pragma unroll
         for (int kk = 0; kk < B / 32; kk++)
-            mma_i8(tacc + kOzQ * s, umma_desc(sa + s * kOzSlice + kk * 32, 16, 1024, UMMA_SW128),
-                   umma_desc(sb + kk * 32, 16, 1024, UMMA_SW128), idesc_i8(kOzQ * (ND - s)), (s > 0 || kk > 0) ? 1u : 0u);
+            mma_i8(tacc + kOzQ * s, da + (uint64_t)((s * kOzSlice + kk * 32) >> 4), db + (uint64_t)((kk * 32) >> 4),
+                   idesc_i8(kOzQ * (ND - s)), (s > 0 || kk > 0) ? 1u : 0u);
 }
 // thread (warp w, lane): row 32 (w & 3) + lane, columns 16 (w >> 2) + [0, 16) of the quarter (eB: the
 // quarter's 32 column exponents):
@@ -688,9 +747,12 @@ __device__ __forceinline__ void oz_drain(uint32_t tacc, double (&acc)[16], const
         for (int d = 0; d < kOzS; d++) tmem_ld_x8(tb + kOzQ * d + 8 * h, a[d]);
         tmem_ld_wait();
 #pragma unroll
+        for (int d = 0; d < kOzS; d++) tmem_regs_ready(a[d]);
+#pragma unroll
         for (int c = 0; c < 8; c++) {
-            const long long V = (long long)(int)a[0][c] * 4294967296LL + (long long)(int)a[1][c] * 16777216LL +
-                                (long long)(int)a[2][c] * 65536LL + (long long)(int)a[3][c] * 256LL + (long long)(int)a[4][c];
+            // Horner in int32 while it fits (|Acc_0 2^8 + Acc_1| < 2^26), then 64-bit
+            const int v01 = (int)a[0][c] * 256 + (int)a[1][c];
+            const long long V = ((long long)v01 * 256 + (int)a[2][c]) * 65536LL + ((long long)(int)a[3][c] * 256 + (int)a[4][c]);
             const double v = __longlong_as_double(V + 0x4338000000000000LL) - 6755399441055744.0;  // exact, |V| < 2^51
             const int ex = max(ea + eB[16 * (w >> 2) + 8 * h + c], 0);
             acc[8 * h + c] = fma(v, __longlong_as_double((long long)ex << 52), acc[8 * h + c]);
@@ -712,9 +774,11 @@ __device__ __forceinline__ void oz_drain6(uint32_t tacc, double (&acc)[16], cons
         for (int d = 0; d < kOzD; d++) tmem_ld_x8(tb + kOzQ * d + 8 * h, a[d]);
         tmem_ld_wait();
 #pragma unroll
+        for (int d = 0; d < kOzD; d++) tmem_regs_ready(a[d]);
+#pragma unroll
         for (int c = 0; c < 8; c++) {
-            const long long Vh = (long long)(int)a[0][c] * 65536LL + (long long)(int)a[1][c] * 256LL + (long long)(int)a[2][c];
-            const long long Vl = (long long)(int)a[3][c] * 65536LL + (long long)(int)a[4][c] * 256LL + (long long)(int)a[5][c];
+            const long long Vh = (long long)((int)a[0][c] * 256 + (int)a[1][c]) * 256 + (int)a[2][c];
+            const long long Vl = (long long)((int)a[3][c] * 256 + (int)a[4][c]) * 256 + (int)a[5][c];
             const double vh = __longlong_as_double(Vh + 0x4338000000000000LL) - 6755399441055744.0;
             const double vl = __longlong_as_double(Vl + 0x4338000000000000LL) - 6755399441055744.0;
             const int ex = max(ea + eR[16 * (w >> 2) + 8 * h + c], 0);
@@ -739,11 +803,34 @@ __device__ void oz_panel(const MatDesc &m, int k, int J, double *dyn, OzState &o
     uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(dyn) + 1023) & ~uintptr_t(1023));
     double(*T)[B + 1] = reinterpret_cast<double(*)[B + 1]>(sm);
     uint8_t *ring = sm + 133120;
+    uint8_t *rdig = oz_slices(m, k, J, 0);
+    if (threadIdx.x >= kWorkers) {  // ---- producer warp: after R_J's digits are out, P_k's digits into
+        if (threadIdx.x != kWorkers) return;  // T, R_J's quarter tiles through the ring, 4 passes
+        const uint32_t sA = smem_u32(sm), sR = smem_u32(ring);
+        auto load_ring = [&](int q) {  // the quarter of R_J's 6 digit tiles: one TMA op (box {128, 32, 6})
+            cbar_expect(o.bar + OZ_R + q % 3, kOzPRing);
+            tma_load_4d(ring + (q % 3) * kOzPRing, m.tmaps + OZ_MAP_R6, o.bar + OZ_R + q % 3, 0, kOzQ * q, 0, oz_set(m, k, J, 0));
+        };
+        oz_wait(o, OZ_RD);  // the workers are done with T and R_J's digits are in global memory
+        asm volatile("fence.proxy.async;" ::: "memory");
+        cbar_expect(o.bar + OZ_A, kOzSet + B * 4);
+        bulk_row(sm, oz_pivdig(m, k), kOzSet, o.bar + OZ_A);
+        bulk_row(eP, oz_pivexp(m, k), B * 4, o.bar + OZ_A);
+        for (int q = 0; q < 3; q++) load_ring(q);
+        for (int p = 0; p < 4; p++) {
+            oz_wait(o, OZ_TE + (p & 1));
+            oz_wait(o, OZ_R + p % 3);
+            if (p == 0) oz_wait(o, OZ_A);
+            tc_fence_after();
+            oz_mma_pass<kOzD>(o.tmem + (p & 1) * (kOzD * kOzQ), sA, sR + (p % 3) * kOzPRing);
+            mma_commit(o.bar + OZ_TF + (p & 1));
+        }
+        return;
+    }
+    // ---- workers
     const int bjp = min(B, (int)ld - j0);
     const bool trans = J < K;
     const int r0 = trans ? j0 : k0, c0 = trans ? k0 : j0, nr = trans ? bj : bk, nc = trans ? bk : bj;
-    asm volatile("fence.proxy.async;" ::: "memory");  // P_k's digits (another CTA) and this smem (earlier tasks)
-    __syncthreads();
 #pragma unroll 16
     for (int it = 0; it < B * B / 256; it++) {
         const int e = it * 256 + threadIdx.x, r = e >> 7, c = e & (B - 1);
@@ -752,47 +839,30 @@ __device__ void oz_panel(const MatDesc &m, int k, int J, double *dyn, OzState &o
     }
     cp_async_commit();
     cp_async_wait_0();
-    __syncthreads();
-    uint8_t *rdig = oz_slices(m, k, J, 0);
+    WSYNC();
     if (trans) oz_slice<1>(T, rdig, oz_exps(m, k, 0) + j0, sexp);
     else oz_slice<0>(T, rdig, oz_exps(m, k, 0) + j0, sexp);
-    __syncthreads();  // T is read; R_J's digits are in global memory (proxy-fenced)
+    mbar_arrive(o.bar + OZ_RD);  // this worker's digit stores are proxy-fenced and it is done with T
     TRACE(if (threadIdx.x == 0) g_trace_sub[blockIdx.x][0] = gtime();)
-    auto load_ring = [&](int q) {
-        uint8_t *dst = ring + (q % 3) * kOzPRing;
-        cbar_expect(o.bar + OZ_R + q % 3, kOzPRing);
-        for (int s = 0; s < kOzD; s++) bulk_row(dst + s * kOzQBytes, rdig + s * kOzSlice + q * kOzQBytes, kOzQBytes, o.bar + OZ_R + q % 3);
-    };
-    if (threadIdx.x == 0) {
-        cbar_expect(o.bar + OZ_A, kOzSet + B * 4);
-        bulk_row(sm, oz_pivdig(m, k), kOzSet, o.bar + OZ_A);
-        bulk_row(eP, oz_pivexp(m, k), B * 4, o.bar + OZ_A);
-        for (int q = 0; q < 3; q++) load_ring(q);
-    }
     double acc[4][16];
-    const uint32_t sA = smem_u32(sm), sR = smem_u32(ring);
-#pragma unroll
-    for (int p = 0; p <= 4; p++) {
-        if (p < 4 && threadIdx.x == 0) {
-            oz_wait(o, OZ_TE + (p & 1));
-            oz_wait(o, OZ_R + p % 3);
-            if (p == 0) oz_wait(o, OZ_A);
-            tc_fence_after();
-            oz_mma_pass<kOzD>(o.tmem + (p & 1) * (kOzD * kOzQ), sA, sR + (p % 3) * kOzPRing);
-            mma_commit(o.bar + OZ_TF + (p & 1));
+    auto iter = [&](auto pc) {
+        constexpr int pd = decltype(pc)::value;
+        if (pd == 0) oz_wait(o, OZ_A);  // P_k's exponents visible to every worker
+        oz_wait(o, OZ_TF + (pd & 1));
+        tc_fence_after();
+        oz_drain6(o.tmem + (pd & 1) * (kOzD * kOzQ), acc[pd], eP, sexp + kOzQ * pd);
+        tc_fence_before();
+        mbar_arrive(o.bar + OZ_TE + (pd & 1));
+        if (pd == 0 && threadIdx.x == 0) {  // pass 0's MMAs are complete: its ring slot takes quarter 3
+            cbar_expect(o.bar + OZ_R + 0, kOzPRing);
+            tma_load_4d(ring, m.tmaps + OZ_MAP_R6, o.bar + OZ_R + 0, 0, kOzQ * 3, 0, oz_set(m, k, J, 0));
         }
-        if (p >= 1) {
-            const int pd = p - 1;
-            if (pd == 0 && threadIdx.x != 0) oz_wait(o, OZ_A);
-            oz_wait(o, OZ_TF + (pd & 1));
-            tc_fence_after();
-            oz_drain6(o.tmem + (pd & 1) * (kOzD * kOzQ), acc[pd], eP, sexp + kOzQ * pd);
-            tc_fence_before();
-            mbar_arrive(o.bar + OZ_TE + (pd & 1));
-            if (threadIdx.x == 0 && pd + 3 < 4) load_ring(pd + 3);
-        }
-    }
-    __syncthreads();  // every MMA completed: P_k's digits in T are dead
+    };
+    iter(std::integral_constant<int, 0>());
+    iter(std::integral_constant<int, 1>());
+    iter(std::integral_constant<int, 2>());
+    iter(std::integral_constant<int, 3>());
+    WSYNC();  // every MMA completed: P_k's digits in T are dead
     TRACE(if (threadIdx.x == 0) g_trace_sub[blockIdx.x][1] = gtime();)
     {
         const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, t = 32 * (w & 3) + lane, cb = 16 * (w >> 2);
@@ -801,7 +871,7 @@ __device__ void oz_panel(const MatDesc &m, int k, int J, double *dyn, OzState &o
 #pragma unroll
             for (int c = 0; c < 16; c++) T[t][32 * q + cb + c] = acc[q][c];  // Wp_J (zero outside bk rows)
     }
-    __syncthreads();
+    WSYNC();
     oz_slice<0>(T, oz_slices(m, k, J, 1), oz_exps(m, k, 1) + j0, sexp);  // Wp_J's digits
     for (int e = threadIdx.x; e < bk * B; e += 256) {  // the step-k value of tile (K, J)
         const int t = e >> 7, j = e & (B - 1);
@@ -815,10 +885,17 @@ __device__ void oz_panel(const MatDesc &m, int k, int J, double *dyn, OzState &o
         }
 }
 
+// pass order of an update task: quarter-major (both steps of quarter q, then quarter q+1), so that a
+// quarter's product is final after its last step's pass and its C read-modify-write overlaps the
+// following passes' MMAs
+__host__ __device__ constexpr int oz_pass_q(int p, int ns) { return ns == 2 ? p >> 1 : p; }
+__host__ __device__ constexpr int oz_pass_st(int p, int ns) { return ns == 2 ? p & 1 : 0; }
+
 // update task (m, k, I, J) of an int8-sliced matrix, ns = 1 or 2 steps: 4 ns column-quarter passes
-// (step st = p / 4, quarter q = p % 4, TMEM set p & 1, ring slot p % 3).  Thread 0 loads and issues;
-// every thread drains.  The product goes through shared memory to a coalesced C read-modify-write
-// (the C tile was prefetched into L2 at the task start).  Same contract as update_task's DMMA path.
+// (step st = p / 4, quarter q = p % 4, TMEM set p & 1, ring slot p % 3).  The producer thread (256)
+// loads and issues; the workers drain pass p-1 while pass p runs, then take the product through
+// shared memory to a coalesced C read-modify-write (the C tile was prefetched into L2 at the task
+// start).  Same contract as update_task's DMMA path.
 __device__ int oz_update(const InvParams &P, const MatDesc &m, int k, int ns, int I, int J, double *dyn, const int *pflag,
                          OzState &o, bool &deferred) {
     const int n = m.n, i0 = I * B, j0 = J * B, bi = min(B, n - i0);
@@ -830,58 +907,82 @@ __device__ int oz_update(const InvParams &P, const MatDesc &m, int k, int ns, in
     int *eA = reinterpret_cast<int *>(ring + 3 * kOzRBytes), *eB = eA + 2 * B;  // [2 steps][128] each
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int jw = (int)min((int64_t)B, ld - j0);  // columns of the tile inside ld (a multiple of 16)
-    fence_proxy_async_smem();  // earlier generic use of this shared memory before the bulk copies
-    __syncthreads();
-    if (threadIdx.x < bi) bulk_prefetch_l2(W + (int64_t)(i0 + threadIdx.x) * ld + j0, jw * 8);
-    auto load_ring = [&](int p) {  // thread 0: the B digits of pass p into slot p % 3
-        const int st = p >> 2, q = p & 3;
-        const uint8_t *src = oz_slices(m, k + st, J, 1) + q * kOzQBytes;
-        uint8_t *dst = ring + (p % 3) * kOzRBytes;
-        cbar_expect(o.bar + OZ_R + p % 3, kOzRBytes);
-        for (int s = 0; s < kOzS; s++) bulk_row(dst + s * kOzQBytes, src + s * kOzSlice, kOzQBytes, o.bar + OZ_R + p % 3);
-    };
-    if (threadIdx.x == 0) {
+    if (threadIdx.x >= kWorkers) {  // ---- producer warp
+        if (threadIdx.x != kWorkers) return 0;
+        asm volatile("fence.proxy.async;" ::: "memory");  // the digits (generic stores of other CTAs, flags acquired)
+        const uint32_t sA = smem_u32(sm), sR = smem_u32(ring);
+        // one TMA op per operand load: the quarter of the 5 B digit tiles (box {128, 32, 5}) and the 5 A tiles
+        auto load_ring = [&](int p) {  // the B digits of pass p into slot p % 3
+            cbar_expect(o.bar + OZ_R + p % 3, kOzRBytes);
+            tma_load_4d(ring + (p % 3) * kOzRBytes, m.tmaps + OZ_MAP_R5, o.bar + OZ_R + p % 3, 0, kOzQ * oz_pass_q(p, ns), 0,
+                        oz_set(m, k + oz_pass_st(p, ns), J, 1));
+        };
         for (int st = 0; st < ns; st++) {
             cbar_expect(o.bar + OZ_A + st, kOzABytes + 2 * B * 4);
-            const uint8_t *src = oz_slices(m, k + st, I, 0);
-            for (int s = 0; s < kOzS; s++) bulk_row(sm + st * kOzABytes + s * kOzSlice, src + s * kOzSlice, kOzSlice, o.bar + OZ_A + st);
+            tma_load_4d(sm + st * kOzABytes, m.tmaps + OZ_MAP_A, o.bar + OZ_A + st, 0, 0, 0, oz_set(m, k + st, I, 0));
             bulk_row(eA + st * B, oz_exps(m, k + st, 0) + i0, B * 4, o.bar + OZ_A + st);
             bulk_row(eB + st * B, oz_exps(m, k + st, 1) + j0, B * 4, o.bar + OZ_A + st);
         }
         for (int p = 0; p < 3 && p < Q; p++) load_ring(p);
+        TRACE(const bool rec = Q == 8 && g_ozcnt[blockIdx.x] == 20;)
+        for (int p = 0; p < Q; p++) {
+            const int st = oz_pass_st(p, ns);
+            TRACE(if (rec) g_ozt[blockIdx.x][40 + p] = clock64();)
+            oz_wait(o, OZ_TE + (p & 1));  // its TMEM set was drained (or never used: pre-armed)
+            TRACE(if (rec) g_ozt[blockIdx.x][48 + p] = clock64();)
+            oz_wait(o, OZ_R + p % 3);
+            if (p < ns) oz_wait(o, OZ_A + st);  // the first pass of each step
+            TRACE(if (p == 0) g_trace_sub[blockIdx.x][0] = gtime();)
+            TRACE(if (rec) g_ozt[blockIdx.x][p] = clock64();)
+            tc_fence_after();
+            oz_mma_pass<kOzS>(o.tmem + (p & 1) * (kOzS * kOzQ), sA + st * kOzABytes, sR + (p % 3) * kOzRBytes);
+            mma_commit(o.bar + OZ_TF + (p & 1));
+            TRACE(if (rec) g_ozt[blockIdx.x][8 + p] = clock64();)
+        }
+        return 0;
     }
+    // ---- workers
+    if (threadIdx.x < bi) bulk_prefetch_l2(W + (int64_t)(i0 + threadIdx.x) * ld + j0, jw * 8);
     double acc[4][16];
 #pragma unroll
     for (int q = 0; q < 4; q++)
 #pragma unroll
         for (int c = 0; c < 16; c++) acc[q][c] = 0.0;
-    const uint32_t sA = smem_u32(sm), sR = smem_u32(ring);
-    auto issue = [&](int p) {  // thread 0: the MMAs of pass p
-        const int st = p >> 2;
-        oz_wait(o, OZ_TE + (p & 1));  // its TMEM set was drained (or never used: pre-armed)
-        oz_wait(o, OZ_R + p % 3);
-        if ((p & 3) == 0) oz_wait(o, OZ_A + st);
-        tc_fence_after();
-        oz_mma_pass<kOzS>(o.tmem + (p & 1) * (kOzS * kOzQ), sA + st * kOzABytes, sR + (p % 3) * kOzRBytes);
-        mma_commit(o.bar + OZ_TF + (p & 1));
-    };
-#pragma unroll
-    for (int p = 0; p <= 8; p++) {
-        if (p > Q) break;
-        if (p < Q && threadIdx.x == 0) issue(p);
-        if (p >= 1) {  // drain pass p - 1 while pass p runs
-            const int pd = p - 1, st = pd >> 2;
-            if ((pd & 3) == 0 && threadIdx.x != 0) oz_wait(o, OZ_A + st);  // exponents visible to every thread
+    TRACE(const bool wrec = Q == 8 && g_ozcnt[blockIdx.x] == 20;)
+    // passes written out with a compile-time index so that acc stays in registers
+    auto iter = [&](auto pc) {
+        constexpr int pd = decltype(pc)::value;
+        if (pd < Q) {
+            const int q = oz_pass_q(pd, ns), st = oz_pass_st(pd, ns);
+            if (pd < ns) oz_wait(o, OZ_A + st);  // exponents visible to every worker
             oz_wait(o, OZ_TF + (pd & 1));
+            TRACE(if (wrec && threadIdx.x == 32) g_ozt[blockIdx.x][16 + pd] = clock64();)
             tc_fence_after();
-            oz_drain(o.tmem + (pd & 1) * (kOzS * kOzQ), acc[pd & 3], eA + st * B, eB + st * B + kOzQ * (pd & 3));
+            if (ns == 2) oz_drain(o.tmem + (pd & 1) * (kOzS * kOzQ), acc[(pd >> 1) & 3], eA + st * B, eB + st * B + kOzQ * q);
+            else oz_drain(o.tmem + (pd & 1) * (kOzS * kOzQ), acc[pd & 3], eA, eB + kOzQ * q);
             tc_fence_before();
             mbar_arrive(o.bar + OZ_TE + (pd & 1));
-            if (threadIdx.x == 0 && pd + 3 < Q) load_ring(pd + 3);  // its slot's MMAs are complete (drained)
+            if (threadIdx.x == 0 && pd + 3 < Q) {  // the drained pass's MMAs are complete: its ring slot is free
+                const int pn = pd + 3;
+                cbar_expect(o.bar + OZ_R + pn % 3, kOzRBytes);
+                tma_load_4d(ring + (pn % 3) * kOzRBytes, m.tmaps + OZ_MAP_R5, o.bar + OZ_R + pn % 3, 0, kOzQ * oz_pass_q(pn, ns),
+                            0, oz_set(m, k + oz_pass_st(pn, ns), J, 1));
+            }
+            TRACE(if (wrec && threadIdx.x == 32) g_ozt[blockIdx.x][24 + pd] = clock64();)
         }
-    }
-    // the product tile through shared memory (the A slots are dead: every MMA completed)
-    __syncthreads();
+    };
+    iter(std::integral_constant<int, 0>());
+    iter(std::integral_constant<int, 1>());
+    iter(std::integral_constant<int, 2>());
+    iter(std::integral_constant<int, 3>());
+    iter(std::integral_constant<int, 4>());
+    iter(std::integral_constant<int, 5>());
+    iter(std::integral_constant<int, 6>());
+    iter(std::integral_constant<int, 7>());
+    TRACE(WSYNC(); if (threadIdx.x == 0 && Q == 8) g_ozcnt[blockIdx.x]++;)
+    // every MMA completed (all TMEM-full phases observed): the A slots are dead
+    WSYNC();
+    TRACE(if (threadIdx.x == 0) g_trace_sub[blockIdx.x][1] = gtime();)
     double(*Pt)[B + 1] = reinterpret_cast<double(*)[B + 1]>(dyn);
     {
         const int r = 32 * (w & 3) + lane, cb = 16 * (w >> 2);
@@ -890,38 +991,37 @@ __device__ int oz_update(const InvParams &P, const MatDesc &m, int k, int ns, in
 #pragma unroll
             for (int c = 0; c < 16; c++) Pt[r][32 * q + cb + c] = acc[q][c];
     }
-    __syncthreads();
-    TRACE(if (threadIdx.x == 0) g_trace_sub[blockIdx.x][0] = gtime();)
+    WSYNC();
     const bool piv = I == last + 1 && J == last + 1;
-    // coalesced C read-modify-write: warp w takes rows w, w + 8, ...; lane l columns l + 32 i.  All 64
-    // loads of a lane are issued before any use (L2 hits: the tile was prefetched at the task start).
-    {
-        double cv[B / 8][4];
+    // coalesced C read-modify-write: warp w takes rows w, w + 8, ...; lane l columns l + 32 i; 32 loads
+    // of a lane in flight (L2 hits: the tile was prefetched at the task start)
+#pragma unroll 1
+    for (int half = 0; half < 2; half++) {
+        double cv[B / 16][4];
 #pragma unroll
-        for (int i8 = 0; i8 < B / 8; i8++) {
-            const int r = w + 8 * i8;
-            const double *crow = W + (int64_t)(i0 + r) * ld + j0;
+        for (int i8 = 0; i8 < B / 16; i8++) {
+            const int rr = w + 8 * (i8 + half * (B / 16));
+            const double *crow = W + (int64_t)(i0 + rr) * ld + j0;
 #pragma unroll
             for (int i = 0; i < 4; i++) {
                 const int c = lane + 32 * i;
-                cv[i8][i] = (r < bi && c < jw) ? __ldcg(crow + c) : 0.0;
+                cv[i8][i] = (rr < bi && c < jw) ? __ldcg(crow + c) : 0.0;
             }
         }
 #pragma unroll
-        for (int i8 = 0; i8 < B / 8; i8++) {
-            const int r = w + 8 * i8;
+        for (int i8 = 0; i8 < B / 16; i8++) {
+            const int rr = w + 8 * (i8 + half * (B / 16));
 #pragma unroll
             for (int i = 0; i < 4; i++) {
                 const int c = lane + 32 * i;
-                const double v = cv[i8][i] - Pt[r][c];
-                if (piv) Pt[r][c] = (r < bi && c < bi) ? v : (r == c ? 1.0 : 0.0);  // fused next pivot, in place
-                else if (r < bi && c < jw) W[(int64_t)(i0 + r) * ld + j0 + c] = v;
+                const double v = cv[i8][i] - Pt[rr][c];
+                if (piv) Pt[rr][c] = (rr < bi && c < bi) ? v : (rr == c ? 1.0 : 0.0);  // fused next pivot, in place
+                else if (rr < bi && c < jw) W[(int64_t)(i0 + rr) * ld + j0 + c] = v;
             }
         }
     }
-    TRACE(if (threadIdx.x == 0) g_trace_sub[blockIdx.x][1] = gtime();)
     if (piv) {
-        __syncthreads();
+        WSYNC();
         if (last >= 1 && threadIdx.x == 0) {  // its slot held P_{last-1}: step last-1's panels must be done
             int vv;
             do {
@@ -929,10 +1029,10 @@ __device__ int oz_update(const InvParams &P, const MatDesc &m, int k, int ns, in
                 if (vv < m.nt) __nanosleep(128);
             } while (vv < m.nt);
         }
-        __syncthreads();
+        WSYNC();
         const int f = pivot_block(W, ld, i0, bi, pivot_slot(m, last + 1), dyn, true);
         if (!f) {  // P_{last+1}'s digits (S = -P, upper storage) for the next step's panel products
-            __syncthreads();
+            WSYNC();
             oz_slice<2>(reinterpret_cast<const double(*)[B + 1]>(dyn), oz_pivdig(m, last + 1), oz_pivexp(m, last + 1), o.sexp, bi);
         }
         return f;
@@ -969,7 +1069,7 @@ __device__ void panel_task(const MatDesc &m, int k, int J, double *dyn, Ring &ri
     }
     cp_async_commit();
     cp_async_wait_0();
-    __syncthreads();
+    WSYNC();
     for (int e = threadIdx.x; e < bk * B; e += 256) {
         const int t = e >> 7, j = e & (B - 1);
         if (j >= bjp) continue;
@@ -990,12 +1090,12 @@ __device__ void panel_task(const MatDesc &m, int k, int J, double *dyn, Ring &ri
     const Seg seg{pivot_slot(m, k), B, B, nullptr, 0, 0, bk}, none{nullptr, 0, 0, nullptr, 0, 0, 0};
     if (trans) tile_product<2>(seg, none, acc, dyn + B * (B + 1), ring, &T[0][0]);
     else tile_product<1>(seg, none, acc, dyn + B * (B + 1), ring, &T[0][0]);
-    __syncthreads();  // the product's staging buffers are free: the result goes through T
+    WSYNC();  // the product's staging buffers are free: the result goes through T
 #pragma unroll
     for (int p = 0; p < 8; p++)
 #pragma unroll
         for (int q = 0; q < 8; q++) T[tile_row(p)][tile_col(q)] = acc[p][q];
-    __syncthreads();
+    WSYNC();
     // Wp_J into the panel buffer (rows whole up to ld) and the step-k value of tile (K, J)
     for (int e = threadIdx.x; e < bk * B; e += 256) {
         const int t = e >> 7, j = e & (B - 1);
@@ -1043,7 +1143,7 @@ __device__ int update_task(const InvParams &P, const MatDesc &m, int k, int nste
     {
         const uint32_t rowb = (uint32_t)min((int64_t)B, ld - j0) * 8;
         if (threadIdx.x == 0) cbar_expect(cbar, rowb * bi);
-        __syncthreads();  // expect_tx before any complete_tx
+        WSYNC();  // expect_tx before any complete_tx
         if (threadIdx.x < bi) bulk_row(Cs + threadIdx.x * SLD, W + (int64_t)(i0 + threadIdx.x) * ld + j0, rowb, cbar);
     }
     // M_IJ -= R_I^T Wp_J : acc[i][j] = sum_t R[t][i0+i] Wp[t][j0+j]   (for each step of the task)
@@ -1064,7 +1164,7 @@ __device__ int update_task(const InvParams &P, const MatDesc &m, int k, int nste
         for (int p = 0; p < 8; p++)
 #pragma unroll
             for (int q = 0; q < 8; q++) acc[p][q] = Cs[tile_row(p) * SLD + tile_col(q)] - acc[p][q];
-        __syncthreads();  // Cs is read; the pivot's smem overlaps it
+        WSYNC();  // Cs is read; the pivot's smem overlaps it
         double(*S)[B + 1] = reinterpret_cast<double(*)[B + 1]>(dyn);
 #pragma unroll
         for (int p = 0; p < 8; p++) {
@@ -1075,7 +1175,7 @@ __device__ int update_task(const InvParams &P, const MatDesc &m, int k, int nste
                 S[i][j] = (i < bi && j < bi) ? acc[p][q] : (i == j ? 1.0 : 0.0);
             }
         }
-        __syncthreads();
+        WSYNC();
         // its slot held P_{last-1}: every step-(last-1) panel task must be done reading it
         if (last >= 1 && threadIdx.x == 0) {
             int v;
@@ -1084,7 +1184,7 @@ __device__ int update_task(const InvParams &P, const MatDesc &m, int k, int nste
                 if (v < m.nt) __nanosleep(128);
             } while (v < m.nt);
         }
-        __syncthreads();
+        WSYNC();
         return pivot_block(W, ld, i0, bi, pivot_slot(m, last + 1), dyn, true);
     }
     // column pairs (16-byte stores); rows are written whole up to the leading dimension: the lower
@@ -1126,7 +1226,7 @@ __global__ void __launch_bounds__(256, 1) pivot_kernel(const __grid_constant__ I
     if (f && threadIdx.x == 0) *m.status = f;
     if (!f && P.ozflag[blockIdx.x]) {  // P_0's digits for step 0's int8 panel products
         __shared__ __align__(16) int sexp[3 * B];
-        __syncthreads();
+        WSYNC();
         oz_slice<2>(reinterpret_cast<const double(*)[B + 1]>(dyn), oz_pivdig(m, 0), oz_pivexp(m, 0), sexp, min(B, m.n));
     }
 }
@@ -1189,7 +1289,7 @@ __device__ void prefetch_task(const InvParams &P, int t, int lane) {
 //                    the fused pivot also waits for step k-1's panels (pivot slot reuse)
 // Waits only point to earlier tasks, which are held by running CTAs: no deadlock.  Step k+1's
 // panels and updates start while step k's tail is still running (look-ahead).
-__global__ void __launch_bounds__(256, 1) inverse_kernel(const __grid_constant__ InvParams P) {
+__global__ void __launch_bounds__(kThreads, 1) inverse_kernel(const __grid_constant__ InvParams P) {
     extern __shared__ double dyn[];
     __shared__ int next;
     __shared__ uint64_t cbar;  // C tile bulk loads of update tasks
@@ -1205,7 +1305,7 @@ __global__ void __launch_bounds__(256, 1) inverse_kernel(const __grid_constant__
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 256;" ::"r"(s2u(ring_full + st)) : "memory");
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 8;" ::"r"(s2u(ring_empty + st)) : "memory");
         }
-        for (int b = 0; b < OZ_NBAR; b++) mbar_init(ozbar + b, b >= OZ_TE ? 256 : 1);
+        for (int b = 0; b < OZ_NBAR; b++) mbar_init(ozbar + b, (b == OZ_TE || b == OZ_TE + 1 || b == OZ_RD) ? kWorkers : 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (threadIdx.x < 32) tmem_alloc(&tmem_slot, 512);  // one CTA per SM (shared memory): all of TMEM
@@ -1213,13 +1313,17 @@ __global__ void __launch_bounds__(256, 1) inverse_kernel(const __grid_constant__
     __syncthreads();
     tc_fence_after();
     OzState ozs{ozbar, 0u, tmem_slot, oz_sexp, oz_eP};
-    mbar_arrive(ozbar + OZ_TE);  // both TMEM accumulator sets start empty
-    mbar_arrive(ozbar + OZ_TE + 1);
+    const bool producer = threadIdx.x >= kWorkers;  // warp 8: int8 operand loads and MMA issue only
+    if (!producer) {
+        mbar_arrive(ozbar + OZ_TE);  // both TMEM accumulator sets start empty
+        mbar_arrive(ozbar + OZ_TE + 1);
+    }
     // deferred release of the previous update task (its tile stores may still be draining)
     bool pend = false, pend_two = false;
     int *pend_tile = nullptr, *pend_done = nullptr;
     int pend_val = 0;
     for (;;) {
+        asm volatile("fence.proxy.async;" ::: "memory");  // this task's generic accesses before the next one's bulk copies
         __syncthreads();  // the previous task is done with shared memory and `next`
         if (threadIdx.x == 0) {
             const int gn = atomicAdd(P.counter, 1);
@@ -1263,7 +1367,7 @@ __global__ void __launch_bounds__(256, 1) inverse_kernel(const __grid_constant__
             __syncthreads();
             TRACE(tr1 = gtime(); trJ = J; trkind = task.y == 3 ? 5 : 0;)
             const bool live = next == 0;
-            if (live && J != k) panel_task(m, k, J, dyn, ring, oz, ozs);  // R_K / P R_K are never read
+            if (live && J != k && (oz || !producer)) panel_task(m, k, J, dyn, ring, oz, ozs);  // R_K / P R_K are never read
             __threadfence();
             __syncthreads();
             if (threadIdx.x == 0) {
@@ -1273,7 +1377,7 @@ __global__ void __launch_bounds__(256, 1) inverse_kernel(const __grid_constant__
             if (task.y == 3) {
                 int f = 0;
                 bool deferred = false;  // stays false: the pivot path writes W itself
-                if (live)
+                if (live && (oz || !producer))
                     f = update_task(P, m, k, 1, J, J, dyn, P.panels_done + m.col_begin + (k >= 1 ? k - 1 : 0), &cbar, cph,
                                     ring, deferred, oz, ozs);
                 if (f && threadIdx.x == 0) *m.status = f;
@@ -1305,7 +1409,7 @@ __global__ void __launch_bounds__(256, 1) inverse_kernel(const __grid_constant__
             TRACE(tr1 = gtime(); trI = I; trJ = J; trkind = (I == last + 1 && J == last + 1) ? 2 : (ns == 2 ? 3 : ((I == k || J == k) ? 4 : 1));)
             int f = 0;
             bool deferred = false;
-            if (next == 0)
+            if (next == 0 && (oz || !producer))
                 f = update_task(P, m, k, ns, I, J, dyn, P.panels_done + m.col_begin + (last >= 1 ? last - 1 : 0), &cbar,
                                 cph, ring, deferred, oz, ozs);
             if (deferred) {  // tile stores still draining: release at the next task's start
@@ -1380,6 +1484,12 @@ __global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ I
 }
 
 #ifdef INV_TRACE
+extern "C" __attribute__((visibility("default"))) int kfac_debug_ozt(void *host) {
+    return (int)cudaMemcpyFromSymbol(host, g_ozt, sizeof(g_ozt));
+}
+extern "C" __attribute__((visibility("default"))) int kfac_debug_ozprof(void *host) {
+    return (int)cudaMemcpyFromSymbol(host, g_ozprof, sizeof(g_ozprof));
+}
 extern "C" __attribute__((visibility("default"))) int kfac_debug_inverse_trace(void *host, int max) {
     const int n = max < (1 << 17) ? max : (1 << 17);
     return (int)cudaMemcpyFromSymbol(host, g_trace, sizeof(TraceRec) * n);
@@ -1391,10 +1501,16 @@ static int64_t pair_doubles(int npairs) { return ((8 * (int64_t)npairs + 15) / 1
 static int64_t state_ints(int npairs, int64_t sum_nt, int64_t sum_tiles) {
     return 16 + 4 * (int64_t)npairs + 3 * sum_nt + sum_tiles;
 }
+static int64_t tasks_offset(int npairs, int64_t sum_nt, int64_t sum_tiles) {  // bytes
+    return pair_doubles(npairs) * 8 + ((state_ints(npairs, sum_nt, sum_tiles) + 3) / 4) * 16;
+}
+static int64_t tmaps_offset(int npairs, int64_t sum_nt, int64_t sum_tiles, int64_t sum_tasks) {  // bytes, 128-aligned
+    return (tasks_offset(npairs, sum_nt, sum_tiles) + sum_tasks * 16 + 127) / 128 * 128;
+}
 int64_t inverse_scratch_bytes(int npairs, int64_t sum_nt, int64_t sum_tiles, int64_t sum_tasks) {
     // pair data (8 doubles per pair) | counter + pivflag (2 npairs) + ozflag (2 npairs) | colflag,
-    // panels_done, tiles_done (sum_nt each) | tileflag | task records (16 B each)
-    return pair_doubles(npairs) * 8 + ((state_ints(npairs, sum_nt, sum_tiles) + 3) / 4) * 16 + sum_tasks * 16 + 256;
+    // panels_done, tiles_done (sum_nt each) | tileflag | task records (16 B each) | 3 TMA maps per matrix
+    return tmaps_offset(npairs, sum_nt, sum_tiles, sum_tasks) + 2 * (int64_t)npairs * 3 * 128 + 256;
 }
 // tasks of one n x n matrix's sweep: nt panels + nt (nt + 1) / 2 tiles per step, nt steps
 int64_t inverse_tasks(int n) {
@@ -1406,6 +1522,22 @@ int64_t inverse_ws_doubles(int n) {
     const int64_t ld = inverse_ld(n), nt = (n + B - 1) / B;
     const int64_t oz = (kPanelBufs * nt * 2 * (int64_t)kOzSet + kPanelBufs * 2 * nt * B * 4 + 2 * (kOzSet + B * 4)) / 8;
     return (n * ld + 2 * kPanelBufs * (int64_t)B * ld + 2 * (int64_t)B * B + oz + 31) / 32 * 32;
+}
+
+typedef CUresult (*PFN_invEncTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                    const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static PFN_invEncTiled g_inv_enc = nullptr;
+static std::mutex g_inv_enc_mu;
+static kfac_status load_enc() {
+    std::lock_guard<std::mutex> lock(g_inv_enc_mu);
+    if (g_inv_enc) return KFAC_OK;
+    cudaDriverEntryPointQueryResult q;
+    void *f = nullptr;
+    KFAC_CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q));
+    if (!f) return set_error(KFAC_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+    g_inv_enc = (PFN_invEncTiled)f;
+    return KFAC_OK;
 }
 
 kfac_status inverse_launch(const std::vector<InvMat> &mats, int npairs, float gamma, double *pair_scratch,
@@ -1462,6 +1594,31 @@ kfac_status inverse_launch(const std::vector<InvMat> &mats, int npairs, float ga
         sum_tiles += d.nt * (d.nt + 1) / 2;
         maxn = std::max(maxn, d.n);
     }
+    // the digit tile sets of every matrix as 4-D TMA maps (global memory, after the task records)
+    int64_t sum_tasks_all = 0;
+    for (int i = 0; i < P.nm; i++) sum_tasks_all += inverse_tasks(P.m[i].n);
+    uint8_t *scratch0 = reinterpret_cast<uint8_t *>(pair_scratch);
+    CUtensorMap *dmaps = reinterpret_cast<CUtensorMap *>(scratch0 + tmaps_offset(npairs, sum_nt, sum_tiles, sum_tasks_all));
+    std::vector<CUtensorMap> hmaps(3 * (size_t)P.nm);
+    KFAC_TRY(load_enc());
+    for (int i = 0; i < P.nm; i++) {
+        MatDesc &d = P.m[i];
+        uint8_t *base = reinterpret_cast<uint8_t *>(d.panel + 2 * kPanelBufs * (int64_t)B * d.ld + 2 * (int64_t)B * B);
+        const cuuint64_t dims[4] = {(cuuint64_t)B, (cuuint64_t)B, (cuuint64_t)kOzD, (cuuint64_t)kPanelBufs * d.nt * 2};
+        const cuuint64_t strides[3] = {(cuuint64_t)B, (cuuint64_t)kOzSlice, (cuuint64_t)kOzSet};
+        const cuuint32_t es[4] = {1, 1, 1, 1};
+        const cuuint32_t boxes[3][4] = {{(cuuint32_t)B, (cuuint32_t)B, (cuuint32_t)kOzS, 1},
+                                        {(cuuint32_t)B, (cuuint32_t)kOzQ, (cuuint32_t)kOzS, 1},
+                                        {(cuuint32_t)B, (cuuint32_t)kOzQ, (cuuint32_t)kOzD, 1}};
+        for (int t = 0; t < 3; t++) {
+            const CUresult r = g_inv_enc(&hmaps[3 * i + t], CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, base, dims, strides, boxes[t], es,
+                                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS) return set_error(KFAC_ERR_CUDA, "inverse: cuTensorMapEncodeTiled (digit tiles) failed");
+        }
+        d.tmaps = dmaps + 3 * i;
+    }
+    KFAC_CUDA_TRY(cudaMemcpyAsync(dmaps, hmaps.data(), hmaps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice, st));
     const int steps = (maxn + B - 1) / B;
     if (steps > kMaxSteps) return set_error(KFAC_ERR_UNSUPPORTED, "inverse: matrix too large (more than 128 column blocks)");
     P.steps = steps;
@@ -1484,7 +1641,7 @@ kfac_status inverse_launch(const std::vector<InvMat> &mats, int npairs, float ga
     P.panels_done = P.colflag + sum_nt;
     P.tiles_done = P.panels_done + sum_nt;
     P.tileflag = P.tiles_done + sum_nt;
-    P.tasks = reinterpret_cast<int4 *>(state + ((state_ints(npairs, sum_nt, sum_tiles) + 3) / 4) * 4);
+    P.tasks = reinterpret_cast<int4 *>(reinterpret_cast<uint8_t *>(pair_scratch) + tasks_offset(npairs, sum_nt, sum_tiles));
     KFAC_CUDA_TRY(cudaMemsetAsync(state, 0, state_ints(npairs, sum_nt, sum_tiles) * sizeof(int), st));
     inverse_tasks_kernel<<<dim3(npairs_steps, (P.nm + 31) / 32), 32, 0, st>>>(P);
     KFAC_LAUNCHED();
@@ -1498,7 +1655,7 @@ kfac_status inverse_launch(const std::vector<InvMat> &mats, int npairs, float ga
     pivot_kernel<<<P.nm, 256, kPivSmem, st>>>(P);
     KFAC_LAUNCHED();
     KFAC_CUDA_TRY(cudaGetLastError());
-    inverse_kernel<<<std::min(P.total_tasks, sms), 256, kUpdSmem, st>>>(P);
+    inverse_kernel<<<std::min(P.total_tasks, sms), kThreads, kUpdSmem, st>>>(P);
     KFAC_LAUNCHED();
     KFAC_CUDA_TRY(cudaGetLastError());
     const int max32 = (maxn + 31) / 32;

@@ -194,6 +194,7 @@ __global__ void __launch_bounds__(GThreads, 1) gemm_3xtf32_kernel(const __grid_c
                     uint32_t r[32];
                     tmem_ld_32x32b_x32(tacc + q * 32, r);
                     tmem_ld_wait();
+                    tmem_regs_ready(r);
 #pragma unroll
                     for (int i = 0; i < 32; i++) acc[q * 32 + i] += __uint_as_float(r[i]);
                 }

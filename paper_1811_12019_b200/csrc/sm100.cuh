@@ -175,6 +175,14 @@ __device__ __forceinline__ void tmem_ld_32x32b_x16(uint32_t taddr, uint32_t (&r)
         : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// tcgen05.ld writes its destination registers asynchronously, until tcgen05.wait::ld.  Nothing in the
+// inline asm above ties the registers to the wait, so the compiler could schedule a use of them
+// before it: pass each through an (ordered, volatile) empty asm after the wait.
+template <int N>
+__device__ __forceinline__ void tmem_regs_ready(uint32_t (&r)[N]) {
+#pragma unroll
+    for (int i = 0; i < N; i++) asm volatile("" : "+r"(r[i])::"memory");
+}
 
 // UMMA shared-memory descriptor (tcgen05 "matrix descriptor"):
 //   [0,14) start address >> 4, [16,30) leading byte offset >> 4,
