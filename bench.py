@@ -183,32 +183,73 @@ def cpu_full_step(layers, n, xs, gys, dws, gamma, threads=0):
     return ms, {k: round(v, 2) for k, v in st.items()}, threads if threads > 0 else oracle.max_threads()
 
 
+def stage_work(l, n):
+    """Oracle work per stage of one layer (multiply-adds): factors, inverse, precondition."""
+    da, dg = shapes.dims(l)
+    return (shapes.rows(l, n) * (da * da + dg * dg), da ** 3 + dg ** 3, dg * da * (da + dg))
+
+
+def cpu_subset_step(layers, n, subset, gamma, seed=1811, threads=0):
+    """The full, unsampled oracle pipeline (all n images) on the layers in `subset`, scaled to the
+    whole step stage by stage by the exact work ratio.  Returns (scaled ms, measured s, {stage: s})."""
+    import oracle
+    oracle.build()
+    t = [0.0, 0.0, 0.0]
+    for i in subset:
+        l = layers[i]
+        x = inputs.half_bits(inputs.layer_x(l, i, n, 0, seed))
+        gy = inputs.half_bits(inputs.layer_gy(l, i, n, 0, seed))
+        dw = inputs.layer_dw(l, i, 0, seed).double().numpy()
+        t0 = time.perf_counter()
+        A = oracle.factor_A(l, x, n, threads=threads)
+        G = oracle.factor_G(gy, shapes.rows(l, n), l["c_out"], threads=threads)
+        t1 = time.perf_counter()
+        Ad, Gd, _ = oracle.damp(A, G, gamma)
+        Ai, _ = oracle.inverse(Ad, threads)
+        Gi, _ = oracle.inverse(Gd, threads)
+        t2 = time.perf_counter()
+        oracle.precondition(Gi, Ai, dw, threads)
+        t3 = time.perf_counter()
+        t[0] += t1 - t0
+        t[1] += t2 - t1
+        t[2] += t3 - t2
+    w_all = [sum(stage_work(l, n)[q] for l in layers) for q in range(3)]
+    w_sub = [sum(stage_work(layers[i], n)[q] for i in subset) for q in range(3)]
+    scaled = sum(t[q] * w_all[q] / max(w_sub[q], 1) for q in range(3)) * 1e3
+    return scaled, sum(t), {"factors": round(t[0], 2), "inverse": round(t[1], 2), "precondition": round(t[2], 2)}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     layers, n = shapes.config(args.config)
-    small = 1024 if args.config in ("resnet50", "resnet18_cifar") else 10 ** 9
-    if args.config == "stress":
-        small = 1000
+    # each step runs the full oracle pipeline on 1/S of the layers (subsets of similar work mix: layers by
+    # descending work, dealt round-robin), scaled stage by stage to the whole step; consecutive steps
+    # visit consecutive subsets, so K >= S steps cover every layer
+    S = min(8, len(layers))
+    order = sorted(range(len(layers)), key=lambda i: -sum(stage_work(layers[i], n)))
+    subsets = [sorted(order[j::S]) for j in range(S)]
     for _ in range(args.warmup):
-        cpu_sample(layers[:1], 1, 64)  # cheap warm-up (library load, page-in)
+        cpu_subset_step(layers, 1, [order[-1]], args.gamma, args.seed)  # cheap warm-up (library load, page-in)
+    import oracle
     vals, meas = [], []
-    desc = cores = scale = None
-    for _ in range(args.steps):
-        v, desc, cores, m, scale = cpu_sample(layers, n, small)
+    for st in range(args.steps):
+        v, m, _ = cpu_subset_step(layers, n, subsets[st % S], args.gamma, args.seed)
         vals.append(v)
         meas.append(m)
     ms = statistics.mean(vals)
+    cores = oracle.max_threads()
+    desc = (f"step i = the full oracle pipeline (all {n} images, real inputs) on layer subset i mod {S} "
+            f"(~1/{S} of the layers, similar work mix), scaled stage by stage by the exact work ratio")
     out = {"metric": METRIC, "value": round(ms, 3), "unit": "ms", "impl": "reference", "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": False,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": {"workload": args.config, "global_batch": n * args.gpus, "per_gpu_batch": n},
            "cpu_baseline": {"value": round(ms, 3), "unit": "ms", "cores": cores, "kind": "oracle", "sample": desc,
                             "sampled": True, "measured_s_per_step": round(statistics.mean(meas), 2),
-                            "scale": round(scale, 2),
-                            "note": "each step is a bounded sample scaled to one full step (the full unsampled oracle "
-                                    "step is the cpu_baseline of the ours arm)"},
+                            "scale": round(ms / 1e3 / max(statistics.mean(meas), 1e-9), 2),
+                            "note": "the full unsampled oracle step is the cpu_baseline of the ours arm"},
            "e2e": {"value": round(ms, 3), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
     return 0
@@ -547,16 +588,41 @@ def run_ours(args):
                 "kernel": "factor_syrk_kernel (+fixup, bias)", "flops_counting": "upper triangle, rows*d*(d+1)",
                 "hbm_gbs": round(w["factor_bytes"] / fac_s / 1e9, 1), "peak_src": pk["src"] + " sustained"}
     inv_tf = w["inverse_flops"] / (st_ms["inverse"] / 1e3) / 1e12
+    # per-matrix precision of the sweep (kfac_inverse_report, reading R-12): int8-digit matrices run
+    # 15 digit-pair MMAs per 128^3 update tile and 21 per panel product on the int8 tensor cores, the
+    # others n^3 fp64 flops on DMMA.  Executed int8 ops per matrix of nt blocks: sum over steps of
+    # (nt - 1) panels x 21 + nt (nt - 1) / 2 update tiles x 15, times 2 * 128^3.
+    rep = st.inverse_report()
+    i8_ops, f64_flops, n_i8 = 0, 0, 0
+    for k, li in enumerate(st.rl["layers"]):
+        for which, d in enumerate(shapes.dims(layers[li])):
+            if rep[k][1][which]:
+                nt_ = (d + 127) // 128
+                i8_ops += nt_ * ((nt_ - 1) * 21 + nt_ * (nt_ - 1) // 2 * 15) * 2 * 128 ** 3
+                n_i8 += 1
+            else:
+                f64_flops += d ** 3
+    i8_peak = pk["bf16_tflops_sustained"] * 2.0  # int8 dense = 2x bf16 (B200 nominal 4.5 / 2.25 P)
+    i8_tops = i8_ops / (st_ms["inverse"] / 1e3) / 1e12
     prec_peak = pk["bf16_tflops_sustained"] * 0.5 / 3.0
     prec_tf = w["precond_flops"] / (st_ms["precondition"] / 1e3) / 1e12
     rs_bytes = st.q["rs_chunk"] * 4 * (world - 1)
     roofs = {
         "factors": fac_roof,
-        "inverse": {"bound": "tensor", "achieved": round(inv_tf, 3), "peak": round(FP64_PEAK_TFLOPS, 1),
-                    "unit": "TFLOP/s", "frac": round(inv_tf / FP64_PEAK_TFLOPS, 4), "traffic": None,
-                    "kernel": "inverse_kernel (persistent fp64 block sweep on DMMA; + pivot, finalize)",
-                    "flops_counting": "n^3 per matrix",
-                    "peak_src": "derived fp64 148x64x2x1.965GHz (DMMA measured 37.1, scripts/micro/dmma_bench.cu)"},
+        "inverse": ({"bound": "tensor", "achieved": round(i8_tops, 2), "peak": round(i8_peak, 1), "unit": "TOPS",
+                     "frac": round(i8_tops / i8_peak, 4), "traffic": None,
+                     "kernel": "inverse_kernel (persistent block sweep: int8-digit tcgen05 updates / panels, fp64 pivots)",
+                     "ops_counting": "executed int8 MMA ops: 15 digit pairs per 128^3 update tile, 21 per panel product",
+                     "int8_matrices": n_i8, "fp64_matrices": len(rep) * 2 - n_i8,
+                     "fp64_equivalent_tflops": round(inv_tf, 2),
+                     "fp64_equivalent_frac_of_dmma_peak": round(inv_tf / FP64_PEAK_TFLOPS, 3),
+                     "peak_src": pk["src"] + " bf16 sustained x 2 (int8 dense = 2x bf16)"}
+                    if n_i8 else
+                    {"bound": "tensor", "achieved": round(inv_tf, 3), "peak": round(FP64_PEAK_TFLOPS, 1),
+                     "unit": "TFLOP/s", "frac": round(inv_tf / FP64_PEAK_TFLOPS, 4), "traffic": None,
+                     "kernel": "inverse_kernel (persistent fp64 block sweep on DMMA; + pivot, finalize)",
+                     "flops_counting": "n^3 per matrix",
+                     "peak_src": "derived fp64 148x64x2x1.965GHz (DMMA measured 37.1, scripts/micro/dmma_bench.cu)"}),
         "precondition": {"bound": "tensor", "achieved": round(prec_tf, 3), "peak": round(prec_peak, 1),
                          "unit": "TFLOP/s", "frac": round(prec_tf / prec_peak, 4), "traffic": None,
                          "kernel": "gemm_3xtf32_kernel (tcgen05 kind::tf32, 3 products per fp32 product)",

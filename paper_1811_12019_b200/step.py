@@ -34,7 +34,9 @@ class KfacStep:
         self.rl = self.plan.rank_layers(rank)
         dev = self.device
         self.rs_send = torch.zeros(world * q["rs_chunk"], dtype=torch.float32, device=dev)
-        self.rs_recv = torch.zeros(q["rs_chunk"], dtype=torch.float32, device=dev)
+        # world 1: the mean ReduceScatter is the identity, so the receive buffer IS the send buffer
+        # (kfac_reduce_scatter_factors does nothing when send == recv)
+        self.rs_recv = self.rs_send if world == 1 else torch.zeros(q["rs_chunk"], dtype=torch.float32, device=dev)
         self.ag_buf = torch.zeros(world * q["ag_chunk"], dtype=torch.float32, device=dev)
         self.inv_ws = torch.zeros(max(self.rl["inv_floats"], 1), dtype=torch.float32, device=dev)
         self.ws = torch.zeros(max(q["ws_bytes"], 16), dtype=torch.uint8, device=dev)
