@@ -302,7 +302,8 @@ def run_ours(args):
     policy = K.LPT if args.policy == "lpt" else K.RR
     st = K.KfacStep(layers, n, rank=rank, world=world, policy=policy, comm=comm, device=dev,
                     stale=not args.no_stale, inv_precision={"auto": K.INV_AUTO, "fp64": K.INV_FP64,
-                                                            "int8": K.INV_INT8}[args.inv_precision])
+                                                            "int8": K.INV_INT8}[args.inv_precision],
+                    rs_mode={"padded": K.RS_PADDED, "per_owner": K.RS_PER_OWNER}[args.rs_mode])
     # synthetic inputs of this rank (global-sample seeded), pinned host copies for the e2e leg
     t0 = time.time()
     # x and gy of all layers live in ONE flat buffer (per-layer views 256-byte aligned), host (pinned)
@@ -705,6 +706,8 @@ def main():
     ap.add_argument("--policy", default="lpt", choices=["lpt", "rr"])
     ap.add_argument("--gamma", type=float, default=2.5e-2)  # gamma^(0), Table 3
     ap.add_argument("--seed", type=int, default=1811)
+    ap.add_argument("--rs-mode", default="padded", choices=["padded", "per_owner"],
+                    help="ReduceScatter: one padded ncclReduceScatter or per-owner grouped ncclReduce (kfac_plan_set_rs_mode)")
     ap.add_argument("--inv-precision", default="auto", choices=["auto", "fp64", "int8"],
                     help="damped-inverse update precision (kfac_plan_set_inverse_precision, reading R-12)")
     ap.add_argument("--no-e2e", action="store_true")

@@ -250,6 +250,17 @@ KFAC_API kfac_status kfac_factor_all(kfac_plan_t plan, const void *const *xs /* 
 KFAC_API kfac_status kfac_reduce_scatter_factors(kfac_comm_t comm, kfac_plan_t plan, const float *rs_send,
                                         float *rs_recv, void *stream);
 
+/* How kfac_reduce_scatter_factors moves the owner-major buffer:
+ *   KFAC_RS_PADDED     one ncclReduceScatter(avg) of world x rs_chunk (every rank's chunk padded to the
+ *                      largest; default);
+ *   KFAC_RS_PER_OWNER  an ncclGroup of one ncclReduce(avg) per owner, rooted at it, over exactly the
+ *                      floats its chunk uses (the ReduceScatterV of the paper: no padding; rs_recv
+ *                      beyond the owner's payload is left untouched).
+ * Same result on every element the layout uses.  Stale / G-refresh plans take the mode of the plan
+ * they were made from.  Errors: KFAC_ERR_ARG.                                                      */
+typedef enum { KFAC_RS_PADDED = 0, KFAC_RS_PER_OWNER = 1 } kfac_rs_mode;
+KFAC_API kfac_status kfac_plan_set_rs_mode(kfac_plan_t plan, int32_t mode);
+
 /* ------------------------------------------------------------------ stage 4
  * For every layer owned by `rank` (kfac_plan_rank_layers order, k-th layer):
  *   pi = sqrt((tr A / dA) / (tr G / dG)), pi = 1 if a trace is 0;

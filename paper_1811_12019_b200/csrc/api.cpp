@@ -241,7 +241,20 @@ kfac_status kfac_reduce_scatter_factors(kfac_comm_t c, kfac_plan_t p, const floa
         return KFAC_OK;
     }
     if (!c || c->world != p->world) return set_error(KFAC_ERR_STATE, "kfac_reduce_scatter_factors: comm/plan world mismatch");
-    KFAC_NCCL_TRY(ncclReduceScatter(send, recv, (size_t)p->rs_chunk, ncclFloat32, ncclAvg, c->comm, S(stream)));
+    if (p->rs_mode == KFAC_RS_PER_OWNER) {
+        // one ncclReduce(avg) per owner, rooted at it, over exactly its chunk's payload (no padding)
+        KFAC_NCCL_TRY(ncclGroupStart());
+        ncclResult_t r = ncclSuccess;
+        for (int o = 0; o < p->world && r == ncclSuccess; o++)  // on an error, fall through to close the group
+            if (p->rs_used[o] > 0)
+                r = ncclReduce(send + (int64_t)o * p->rs_chunk, recv, (size_t)p->rs_used[o], ncclFloat32, ncclAvg, o, c->comm,
+                               S(stream));
+        const ncclResult_t e = ncclGroupEnd();
+        if (r != ncclSuccess) return set_error(KFAC_ERR_NCCL, std::string("ncclReduce: ") + ncclGetErrorString(r));
+        if (e != ncclSuccess) return set_error(KFAC_ERR_NCCL, std::string("ncclGroupEnd: ") + ncclGetErrorString(e));
+    } else {
+        KFAC_NCCL_TRY(ncclReduceScatter(send, recv, (size_t)p->rs_chunk, ncclFloat32, ncclAvg, c->comm, S(stream)));
+    }
     KFAC_TRY(nccl_check_async(c->comm));
     return KFAC_OK;
 }
@@ -280,6 +293,7 @@ kfac_status kfac_damped_inverse(kfac_plan_t p, int32_t rank, const float *recv, 
             m.panel = m.work + (int64_t)m.n * ld;
             off += inverse_ws_doubles(m.n) * 8;
             m.status = dev_status + 2 * k + which;
+            m.split = inv_ws + p->split_off[rank][2 * k + which];  // the precondition's 3xTF32 operand, written here
             m.pair = (int)k;
             m.is_A = which == 0;
             mats.push_back(m);
@@ -329,9 +343,8 @@ kfac_status kfac_precondition(kfac_plan_t p, int32_t rank, const float *recv, fl
         off += align16(precond_ws_floats(g.dG, g.dA));
         j.sA = inv_ws + p->split_off[rank][2 * k];
         j.sG = inv_ws + p->split_off[rank][2 * k + 1];
-        j.resplit = p->stale ? 0 : 1;          // the A_d^-1 split: only a full step re-splits it
-        j.resplitG = p->stale ? 0 : 1;         // G_d^-1: full and G-refresh steps
-        if (p->g_only) j.resplit = 0;
+        j.resplit = 0;   // the inverses' tf32 hi / lo splits are written by kfac_damped_inverse (finalize_kernel)
+        j.resplitG = 0;  // and cached in inv_ws for stale / G-refresh steps (R-20)
         if (p->owner[l] == rank) {
             j.out = ag_buf + p->ag_off[l];
         } else {

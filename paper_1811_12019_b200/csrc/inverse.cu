@@ -66,6 +66,7 @@ struct MatDesc {
     int32_t tile_begin;  // prefix of nt (nt + 1) / 2: tile flags
     int32_t orig;        // index in the caller's matrix list (2 * pair + !is_A): report slot
     const CUtensorMap *tmaps;  // [3] in global memory: the digit tile sets as 4-D TMA maps (OZ_MAP_*)
+    float *split;              // [2][n][round4(n)] tf32 hi / lo of the inverse for the precondition, or null
 };
 enum { OZ_MAP_A = 0, OZ_MAP_R5 = 1, OZ_MAP_R6 = 2 };  // boxes {128 B, 128 rows, 5 digits}, {., 32, 5}, {., 32, 6}
 constexpr int kMaxSteps = 128;
@@ -652,14 +653,19 @@ __device__ void oz_slice(const double (*T)[B + 1], uint8_t *dst, int *dexp, int 
 }
 
 // barriers of the int8 update pipeline (shared memory) and their phase bits (uniform per CTA)
-enum { OZ_A = 0, OZ_R = 2, OZ_TF = 5, OZ_TE = 7, OZ_RF = 9, OZ_RD = 12, OZ_NBAR = 13 };
+enum { OZ_A = 0, OZ_R = 2, OZ_TF = 5, OZ_TE = 8, OZ_RD = 11, OZ_NBAR = 12 };
+#ifndef KFAC_OZ_SETS
+#define KFAC_OZ_SETS 3
+#endif
+constexpr int kOzSets = KFAC_OZ_SETS;  // TMEM accumulator sets of an update (3 x 5 x 32 columns); a panel uses 2 (2 x 6 x 32)
+static_assert(kOzSets * kOzS * kOzQ <= 512 && 2 * kOzD * kOzQ <= 512, "accumulator sets fit TMEM");
 // The persistent kernel runs 8 worker warps (256 threads: every task's arithmetic, epilogues, drains) and
 // one producer warp (threads 256..287) whose lane 0 loads the int8 operands and issues the tensor-core
 // MMAs of the int8 tasks, so that the MMAs of pass p run while the workers drain pass p-1.  Worker-only
 // code synchronises with WSYNC (named barrier 1, 256 threads); __syncthreads is for all 288.
 
 struct OzState {
-    uint64_t *bar;  // [OZ_NBAR]: A digits per step (2), ring slots (3), TMEM full (2), TMEM empty (2)
+    uint64_t *bar;  // [OZ_NBAR]: A digits per step (2), ring slots (3), TMEM full (3), TMEM empty (3), R_J digits out
     uint32_t ph;    // phase bit per barrier
     uint32_t tmem;  // 2 accumulator sets x (5 or 6) diagonals x 32 columns
     int *sexp;      // [128] shared: column exponents of the block being cut into digits
@@ -813,6 +819,7 @@ __device__ void oz_panel(const MatDesc &m, int k, int J, double *dyn, OzState &o
         };
         oz_wait(o, OZ_RD);  // the workers are done with T and R_J's digits are in global memory
         asm volatile("fence.proxy.async;" ::: "memory");
+        asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(m.tmaps + OZ_MAP_R6) : "memory");
         cbar_expect(o.bar + OZ_A, kOzSet + B * 4);
         bulk_row(sm, oz_pivdig(m, k), kOzSet, o.bar + OZ_A);
         bulk_row(eP, oz_pivexp(m, k), B * 4, o.bar + OZ_A);
@@ -910,6 +917,8 @@ __device__ int oz_update(const InvParams &P, const MatDesc &m, int k, int ns, in
     if (threadIdx.x >= kWorkers) {  // ---- producer warp
         if (threadIdx.x != kWorkers) return 0;
         asm volatile("fence.proxy.async;" ::: "memory");  // the digits (generic stores of other CTAs, flags acquired)
+        for (int t = 0; t < 2; t++)  // the maps were written by tmap_store_kernel (generic proxy)
+            asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(m.tmaps + t) : "memory");
         const uint32_t sA = smem_u32(sm), sR = smem_u32(ring);
         // one TMA op per operand load: the quarter of the 5 B digit tiles (box {128, 32, 5}) and the 5 A tiles
         auto load_ring = [&](int p) {  // the B digits of pass p into slot p % 3
@@ -928,15 +937,15 @@ __device__ int oz_update(const InvParams &P, const MatDesc &m, int k, int ns, in
         for (int p = 0; p < Q; p++) {
             const int st = oz_pass_st(p, ns);
             TRACE(if (rec) g_ozt[blockIdx.x][40 + p] = clock64();)
-            oz_wait(o, OZ_TE + (p & 1));  // its TMEM set was drained (or never used: pre-armed)
+            oz_wait(o, OZ_TE + p % kOzSets);  // its TMEM set was drained (or never used: pre-armed)
             TRACE(if (rec) g_ozt[blockIdx.x][48 + p] = clock64();)
             oz_wait(o, OZ_R + p % 3);
             if (p < ns) oz_wait(o, OZ_A + st);  // the first pass of each step
             TRACE(if (p == 0) g_trace_sub[blockIdx.x][0] = gtime();)
             TRACE(if (rec) g_ozt[blockIdx.x][p] = clock64();)
             tc_fence_after();
-            oz_mma_pass<kOzS>(o.tmem + (p & 1) * (kOzS * kOzQ), sA + st * kOzABytes, sR + (p % 3) * kOzRBytes);
-            mma_commit(o.bar + OZ_TF + (p & 1));
+            oz_mma_pass<kOzS>(o.tmem + (p % kOzSets) * (kOzS * kOzQ), sA + st * kOzABytes, sR + (p % 3) * kOzRBytes);
+            mma_commit(o.bar + OZ_TF + p % kOzSets);
             TRACE(if (rec) g_ozt[blockIdx.x][8 + p] = clock64();)
         }
         return 0;
@@ -955,13 +964,13 @@ __device__ int oz_update(const InvParams &P, const MatDesc &m, int k, int ns, in
         if (pd < Q) {
             const int q = oz_pass_q(pd, ns), st = oz_pass_st(pd, ns);
             if (pd < ns) oz_wait(o, OZ_A + st);  // exponents visible to every worker
-            oz_wait(o, OZ_TF + (pd & 1));
+            oz_wait(o, OZ_TF + pd % kOzSets);
             TRACE(if (wrec && threadIdx.x == 32) g_ozt[blockIdx.x][16 + pd] = clock64();)
             tc_fence_after();
-            if (ns == 2) oz_drain(o.tmem + (pd & 1) * (kOzS * kOzQ), acc[(pd >> 1) & 3], eA + st * B, eB + st * B + kOzQ * q);
-            else oz_drain(o.tmem + (pd & 1) * (kOzS * kOzQ), acc[pd & 3], eA, eB + kOzQ * q);
+            if (ns == 2) oz_drain(o.tmem + (pd % kOzSets) * (kOzS * kOzQ), acc[(pd >> 1) & 3], eA + st * B, eB + st * B + kOzQ * q);
+            else oz_drain(o.tmem + (pd % kOzSets) * (kOzS * kOzQ), acc[pd & 3], eA, eB + kOzQ * q);
             tc_fence_before();
-            mbar_arrive(o.bar + OZ_TE + (pd & 1));
+            mbar_arrive(o.bar + OZ_TE + pd % kOzSets);
             if (threadIdx.x == 0 && pd + 3 < Q) {  // the drained pass's MMAs are complete: its ring slot is free
                 const int pn = pd + 3;
                 cbar_expect(o.bar + OZ_R + pn % 3, kOzRBytes);
@@ -1305,7 +1314,7 @@ __global__ void __launch_bounds__(kThreads, 1) inverse_kernel(const __grid_const
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 256;" ::"r"(s2u(ring_full + st)) : "memory");
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 8;" ::"r"(s2u(ring_empty + st)) : "memory");
         }
-        for (int b = 0; b < OZ_NBAR; b++) mbar_init(ozbar + b, (b == OZ_TE || b == OZ_TE + 1 || b == OZ_RD) ? kWorkers : 1);
+        for (int b = 0; b < OZ_NBAR; b++) mbar_init(ozbar + b, ((b >= OZ_TE && b < OZ_TE + kOzSets) || b == OZ_RD) ? kWorkers : 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (threadIdx.x < 32) tmem_alloc(&tmem_slot, 512);  // one CTA per SM (shared memory): all of TMEM
@@ -1315,8 +1324,7 @@ __global__ void __launch_bounds__(kThreads, 1) inverse_kernel(const __grid_const
     OzState ozs{ozbar, 0u, tmem_slot, oz_sexp, oz_eP};
     const bool producer = threadIdx.x >= kWorkers;  // warp 8: int8 operand loads and MMA issue only
     if (!producer) {
-        mbar_arrive(ozbar + OZ_TE);  // both TMEM accumulator sets start empty
-        mbar_arrive(ozbar + OZ_TE + 1);
+        for (int b = 0; b < kOzSets; b++) mbar_arrive(ozbar + OZ_TE + b);  // the TMEM accumulator sets start empty
     }
     // deferred release of the previous update task (its tile stores may still be draining)
     bool pend = false, pend_two = false;
@@ -1450,9 +1458,22 @@ __global__ void __launch_bounds__(kThreads, 1) inverse_kernel(const __grid_const
 
 // ---- epilogue: inv = -M (symmetric, full fp32) from the upper storage.  Each upper 32 x 32 tile is
 // read once (coalesced, through shared memory) and written to both of its output blocks.
+// the precondition's 3xTF32 operand (precond.cu split_kernel's format): hi = rn_tf32(v), lo = rn_tf32(v - hi),
+// planes [2][n][kp], kp = n rounded up to 4 (the padding columns zero)
+__device__ __forceinline__ float tf32_rn_inv(float x) {
+    return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+}
+__device__ __forceinline__ void split_store(float *split, int n, int kp, int i, int j, float v) {
+    const float hi = tf32_rn_inv(v);
+    split[(int64_t)i * kp + j] = hi;
+    split[(int64_t)n * kp + (int64_t)i * kp + j] = tf32_rn_inv(v - hi);
+}
 __global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ InvParams P) {
     const MatDesc &m = P.m[blockIdx.y];
-    const int n = m.n;
+    const int n = m.n, kp = (n + 3) / 4 * 4;
+    if (m.split && blockIdx.x == 0 && kp > n)
+        for (int i = threadIdx.x; i < n; i += blockDim.x)
+            for (int j = n; j < kp; j++) m.split[(int64_t)i * kp + j] = m.split[(int64_t)n * kp + (int64_t)i * kp + j] = 0.f;
     const int64_t ld = m.ld;
     const int nt = (n + 31) / 32, npairs = nt * (nt + 1) / 2;
     __shared__ double T[32][33];
@@ -1474,10 +1495,18 @@ __global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ I
         __syncthreads();
         for (int r = ty; r < 32; r += 8) {
             const int i = bi * 32 + r, j = bj * 32 + tx;
-            if (i < n && j < n) m.inv[(int64_t)i * n + j] = (float)(-((bi < bj || r <= tx) ? T[r][tx] : T[tx][r]));
+            if (i < n && j < n) {
+                const float v = (float)(-((bi < bj || r <= tx) ? T[r][tx] : T[tx][r]));
+                m.inv[(int64_t)i * n + j] = v;
+                if (m.split) split_store(m.split, n, kp, i, j, v);
+            }
             if (bi < bj) {
                 const int i2 = bj * 32 + r, j2 = bi * 32 + tx;
-                if (i2 < n && j2 < n) m.inv[(int64_t)i2 * n + j2] = (float)(-T[tx][r]);
+                if (i2 < n && j2 < n) {
+                    const float v = (float)(-T[tx][r]);
+                    m.inv[(int64_t)i2 * n + j2] = v;
+                    if (m.split) split_store(m.split, n, kp, i2, j2, v);
+                }
             }
         }
     }
@@ -1522,6 +1551,22 @@ int64_t inverse_ws_doubles(int n) {
     const int64_t ld = inverse_ld(n), nt = (n + B - 1) / B;
     const int64_t oz = (kPanelBufs * nt * 2 * (int64_t)kOzSet + kPanelBufs * 2 * nt * B * 4 + 2 * (kOzSet + B * 4)) / 8;
     return (n * ld + 2 * kPanelBufs * (int64_t)B * ld + 2 * (int64_t)B * B + oz + 31) / 32 * 32;
+}
+
+// the digit tile maps of one inverse launch, written to global memory by a kernel (parameter space
+// holds up to 32 KB); the TMA reads them through the tensormap proxy (released here, acquired by the
+// producer before its first use)
+constexpr int kMapChunk = 192;
+struct alignas(64) MapChunk {
+    int32_t n, pad[15];
+    CUtensorMap maps[kMapChunk];
+};
+__global__ void tmap_store_kernel(const __grid_constant__ MapChunk C, CUtensorMap *dst) {
+    const uint4 *src = reinterpret_cast<const uint4 *>(C.maps);
+    uint4 *d = reinterpret_cast<uint4 *>(dst);
+    for (int i = threadIdx.x; i < C.n * (int)(sizeof(CUtensorMap) / 16); i += blockDim.x) d[i] = src[i];
+    __syncthreads();
+    asm volatile("fence.proxy.tensormap::generic.release.gpu;" ::: "memory");
 }
 
 typedef CUresult (*PFN_invEncTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
@@ -1587,6 +1632,7 @@ kfac_status inverse_launch(const std::vector<InvMat> &mats, int npairs, float ga
         d.pair = src.pair;
         d.is_A = src.is_A;
         d.orig = order[r];
+        d.split = src.split;
         d.nt = (d.n + B - 1) / B;
         d.col_begin = sum_nt;
         d.tile_begin = sum_tiles;
@@ -1618,7 +1664,16 @@ kfac_status inverse_launch(const std::vector<InvMat> &mats, int npairs, float ga
         }
         d.tmaps = dmaps + 3 * i;
     }
-    KFAC_CUDA_TRY(cudaMemcpyAsync(dmaps, hmaps.data(), hmaps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice, st));
+    // stream-ordered upload through kernel parameters (no host synchronisation, unlike a pageable copy)
+    for (size_t b = 0; b < hmaps.size(); b += kMapChunk) {
+        MapChunk c;
+        memset(&c, 0, sizeof(c));
+        c.n = (int)std::min<size_t>(kMapChunk, hmaps.size() - b);
+        memcpy(c.maps, hmaps.data() + b, c.n * sizeof(CUtensorMap));
+        tmap_store_kernel<<<1, 256, 0, st>>>(c, dmaps + b);
+        KFAC_LAUNCHED();
+        KFAC_CUDA_TRY(cudaGetLastError());
+    }
     const int steps = (maxn + B - 1) / B;
     if (steps > kMaxSteps) return set_error(KFAC_ERR_UNSUPPORTED, "inverse: matrix too large (more than 128 column blocks)");
     P.steps = steps;

@@ -105,6 +105,7 @@ struct InvMat {        // one damped factor to invert
     double *work;         // n*n fp64 working matrix
     double *panel;        // 8 * kPanel * ld + 2 * kPanel^2 fp64 (R, P R per step mod 4; two pivots)
     int32_t *status;      // device status word
+    float *split;         // [2][n][round4(n)] tf32 hi / lo split of the inverse (the precondition's operand), or null
     int32_t n;
     int32_t pair;         // index of the (A, G) pair this matrix belongs to
     int32_t is_A;

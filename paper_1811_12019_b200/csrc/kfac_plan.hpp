@@ -14,6 +14,8 @@ struct kfac_plan {
     bool stale = false;   // stale-factor wire layout: dW segments only (R-20)
     bool g_only = false;  // G-refresh layout: dW and G segments (A kept stale, R-20)
     int inv_prec = KFAC_INV_AUTO;  // kfac_plan_set_inverse_precision
+    int rs_mode = KFAC_RS_PADDED;  // kfac_plan_set_rs_mode
+    std::vector<int64_t> rs_used;  // per rank: floats of its chunk the layout uses (<= rs_chunk)
     std::vector<int32_t> owner;
     std::vector<std::vector<int>> owned;                          // per rank, ascending
     std::vector<std::vector<std::array<int64_t, 3>>> local;       // per rank, per owned layer

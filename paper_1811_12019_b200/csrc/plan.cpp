@@ -140,6 +140,7 @@ kfac_status plan_build(kfac_plan *p) {
     }
     // RS layout
     p->local.assign(P, {});
+    p->rs_used.assign(P, 0);
     int64_t maxc = 0;
     for (int r = 0; r < P; r++) {
         int64_t off = 0;
@@ -167,6 +168,7 @@ kfac_status plan_build(kfac_plan *p) {
             p->local[r].push_back(o);
         }
         maxc = std::max(maxc, off);
+        p->rs_used[r] = off;
     }
     p->rs_chunk = maxc;
     p->seg_off.assign(3 * (size_t)L, 0);
@@ -287,6 +289,8 @@ kfac_status kfac_plan_create_stale(kfac_plan_t full, kfac_plan_t *out) {
     p->world = full->world;
     p->n_local = full->n_local;
     p->policy = full->policy;
+    p->rs_mode = full->rs_mode;
+    p->inv_prec = full->inv_prec;
     p->stale = true;
     kfac_status s = plan_build(p);
     if (s) {
@@ -308,6 +312,7 @@ kfac_status kfac_plan_create_grefresh(kfac_plan_t full, kfac_plan_t *out) {
     p->world = full->world;
     p->n_local = full->n_local;
     p->policy = full->policy;
+    p->rs_mode = full->rs_mode;
     p->inv_prec = full->inv_prec;
     p->g_only = true;
     kfac_status s = plan_build(p);
@@ -316,6 +321,13 @@ kfac_status kfac_plan_create_grefresh(kfac_plan_t full, kfac_plan_t *out) {
         return s;
     }
     *out = p;
+    return KFAC_OK;
+}
+
+kfac_status kfac_plan_set_rs_mode(kfac_plan_t p, int32_t mode) {
+    if (!p) return set_error(KFAC_ERR_ARG, "kfac_plan_set_rs_mode: NULL plan");
+    if (mode != KFAC_RS_PADDED && mode != KFAC_RS_PER_OWNER) return set_error(KFAC_ERR_ARG, "kfac_plan_set_rs_mode: bad mode");
+    p->rs_mode = mode;
     return KFAC_OK;
 }
 

@@ -98,6 +98,8 @@ _bn_ws_bytes = _sig("kfac_bn_ws_bytes", [_i32, _pi32, _i32, _pi64])
 _set_inv_prec = _sig("kfac_plan_set_inverse_precision", [_P, _i32])
 _inv_report = _sig("kfac_inverse_report", [_P, _i32, _P, ctypes.POINTER(ctypes.c_double), _pi32, _P])
 INV_AUTO, INV_FP64, INV_INT8 = 0, 1, 2
+_set_rs_mode = _sig("kfac_plan_set_rs_mode", [_P, _i32])
+RS_PADDED, RS_PER_OWNER = 0, 1
 _update = _sig("kfac_update", [_P, _P, ctypes.POINTER(_P), ctypes.POINTER(_P), _f32, _f32, _i32, _f32, _P, _P])
 
 EXPORTS = ["kfac_last_error", "kfac_version", "kfac_launch_count", "kfac_plan_create", "kfac_plan_query", "kfac_plan_rank_layers",
@@ -107,7 +109,7 @@ EXPORTS = ["kfac_last_error", "kfac_version", "kfac_launch_count", "kfac_plan_cr
            "kfac_plan_is_stale", "kfac_refresh_interval", "kfac_refresh", "kfac_factor_diff", "kfac_update", "kfac_bn_grads",
            "kfac_bn_precondition", "kfac_bn_ws_bytes", "kfac_bn_exchange",
            "kfac_plan_create_grefresh", "kfac_plan_refresh_kind", "kfac_plan_set_inverse_precision",
-           "kfac_inverse_report"]
+           "kfac_inverse_report", "kfac_plan_set_rs_mode"]
 
 
 def _check(st, where):
@@ -199,6 +201,10 @@ class Plan:
     def set_inverse_precision(self, mode):
         """kfac_plan_set_inverse_precision: INV_AUTO (per-matrix bound), INV_FP64 or INV_INT8."""
         _check(_set_inv_prec(self.h, int(mode)), "kfac_plan_set_inverse_precision")
+
+    def set_rs_mode(self, mode):
+        """kfac_plan_set_rs_mode: RS_PADDED (one ReduceScatter) or RS_PER_OWNER (grouped per-owner Reduce)."""
+        _check(_set_rs_mode(self.h, int(mode)), "kfac_plan_set_rs_mode")
 
     def stale_plan(self):
         """kfac_plan_create_stale: the plan of the steps that reuse stale factors."""

@@ -22,13 +22,14 @@ class KfacStep:
     """
 
     def __init__(self, layers, n_local, rank=0, world=1, policy=kfac.RR, comm=None, device=None, stale=False,
-                 inv_precision=kfac.INV_AUTO):
+                 inv_precision=kfac.INV_AUTO, rs_mode=kfac.RS_PADDED):
         self.layers = list(layers)
         self.rank, self.world, self.n_local = int(rank), int(world), int(n_local)
         self.comm = comm
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.plan = kfac.Plan(self.layers, world, n_local, policy)
         self.plan.set_inverse_precision(inv_precision)
+        self.plan.set_rs_mode(rs_mode)
         q = self.plan.query()
         self.q = q
         self.rl = self.plan.rank_layers(rank)

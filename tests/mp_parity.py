@@ -52,6 +52,7 @@ def unpack(p, d):
 def main():
     cfg = sys.argv[1] if len(sys.argv) > 1 else "small"
     policy = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+    rs_mode = int(sys.argv[3]) if len(sys.argv) > 3 else 0  # 0 padded ReduceScatter, 1 per-owner grouped Reduce
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
@@ -68,7 +69,7 @@ def main():
     comm = K.Comm(bytes(uid.cpu().numpy().tobytes()), rank, world, local)
     layers, n = NETS[cfg]()
     gamma = 2.5e-2
-    st = K.KfacStep(layers, n, rank=rank, world=world, policy=policy, comm=comm, device=dev, stale=True)
+    st = K.KfacStep(layers, n, rank=rank, world=world, policy=policy, comm=comm, device=dev, stale=True, rs_mode=rs_mode)
     xs = [inputs.layer_x(l, i, n, rank) for i, l in enumerate(layers)]
     gys = [inputs.layer_gy(l, i, n, rank) for i, l in enumerate(layers)]
     dws = [inputs.layer_dw(l, i, rank) for i, l in enumerate(layers)]
@@ -118,7 +119,7 @@ def main():
             owner = pl["owner"][l]
             e = relerr(g[off:off + dg * da], ref["results"][owner][l]["precond"].reshape(-1))
             err = max(err, e)
-        print(f"mp_parity {cfg} P={world} policy={policy}: stage3 err {stage3:.2e}, end-to-end max err {err:.2e}, "
+        print(f"mp_parity {cfg} P={world} policy={policy} rs_mode={rs_mode}: stage3 err {stage3:.2e}, end-to-end max err {err:.2e}, "
               f"replicas identical {ok}", flush=True)
         ok &= err <= 2e-3
     if big:  # the stale / G-refresh / BN legs are covered by the small nets
