@@ -706,7 +706,7 @@ def main():
     ap.add_argument("--policy", default="lpt", choices=["lpt", "rr"])
     ap.add_argument("--gamma", type=float, default=2.5e-2)  # gamma^(0), Table 3
     ap.add_argument("--seed", type=int, default=1811)
-    ap.add_argument("--rs-mode", default="padded", choices=["padded", "per_owner"],
+    ap.add_argument("--rs-mode", default="per_owner", choices=["padded", "per_owner"],
                     help="ReduceScatter: one padded ncclReduceScatter or per-owner grouped ncclReduce (kfac_plan_set_rs_mode)")
     ap.add_argument("--inv-precision", default="auto", choices=["auto", "fp64", "int8"],
                     help="damped-inverse update precision (kfac_plan_set_inverse_precision, reading R-12)")

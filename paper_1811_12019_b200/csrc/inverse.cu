@@ -1039,6 +1039,7 @@ __device__ int oz_update(const InvParams &P, const MatDesc &m, int k, int ns, in
             } while (vv < m.nt);
         }
         WSYNC();
+        TRACE(if (threadIdx.x == 0) g_trace_sub[blockIdx.x][1] = gtime();)
         const int f = pivot_block(W, ld, i0, bi, pivot_slot(m, last + 1), dyn, true);
         if (!f) {  // P_{last+1}'s digits (S = -P, upper storage) for the next step's panel products
             WSYNC();
@@ -1376,6 +1377,7 @@ __global__ void __launch_bounds__(kThreads, 1) inverse_kernel(const __grid_const
             TRACE(tr1 = gtime(); trJ = J; trkind = task.y == 3 ? 5 : 0;)
             const bool live = next == 0;
             if (live && J != k && (oz || !producer)) panel_task(m, k, J, dyn, ring, oz, ozs);  // R_K / P R_K are never read
+            TRACE(if (task.y == 3 && threadIdx.x == 0) g_trace_sub[blockIdx.x][0] = gtime();)
             __threadfence();
             __syncthreads();
             if (threadIdx.x == 0) {

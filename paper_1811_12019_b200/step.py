@@ -22,7 +22,7 @@ class KfacStep:
     """
 
     def __init__(self, layers, n_local, rank=0, world=1, policy=kfac.RR, comm=None, device=None, stale=False,
-                 inv_precision=kfac.INV_AUTO, rs_mode=kfac.RS_PADDED):
+                 inv_precision=kfac.INV_AUTO, rs_mode=kfac.RS_PER_OWNER):
         self.layers = list(layers)
         self.rank, self.world, self.n_local = int(rank), int(world), int(n_local)
         self.comm = comm

@@ -25,7 +25,7 @@ for kd, L in sorted(kinds.items()):
     print(f"kind {kd}: n={len(L)} mean {sum(L)/len(L):.1f} us, max {max(L):.1f}")
 # update tasks with sub-phase stamps (INV_TRACE builds of the current kernel): start -> product
 # end -> C-tile wait end -> task end
-for kd in (0, 1, 3):
+for kd in (0, 1, 3, 5):
     sub = [r for r in rows if r[2] == kd and len(r) >= 11 and r[9] >= r[7] and r[10] >= r[9] and r[8] >= r[10]]
     if sub:
         n = len(sub)
