@@ -37,6 +37,7 @@ constexpr int kWorkers = 256, kThreads = 288;
 #define WSYNC() asm volatile("bar.sync 1, 256;" ::: "memory")
 
 constexpr int kMaxMats = 128;
+constexpr int kUnpRows = 8, kFinTiles = 16;
 constexpr int kPanelBufs = 4;  // panel buffers per matrix (step mod 4)
 constexpr int B = kPanel;     // 128
 #ifndef KFAC_INV_KC  // experiment overrides (KFAC_NVCC_EXTRA)
@@ -88,6 +89,10 @@ struct InvParams {
     int *tileflag;     // [sum tiles] k + 1 once tile (I, J) holds its step-k value
     int4 *tasks;       // [total_tasks] task records (gen_step_tasks), built on the device per call
     int32_t step_begin[kMaxSteps + 1];  // first record of each pair's list (inverse_tasks.hpp)
+    // flattened grids of the prologue / epilogue kernels: blocks [unp_begin[r], unp_begin[r+1]) unpack matrix r
+    // (kUnpRows rows each), [fin_begin[r], fin_begin[r+1]) finalize it (kFinTiles 32 x 32 tile pairs each)
+    int32_t unp_begin[kMaxMats + 1];
+    int32_t fin_begin[kMaxMats + 1];
     MatDesc m[kMaxMats];
 };
 
@@ -180,11 +185,23 @@ __global__ void damp_trace_kernel(const __grid_constant__ InvParams P) {
 }
 
 // packed fp32 -> fp64 working matrix (upper triangle), damped diagonal
+// the matrix a block of a flattened grid belongs to (prefix table, binary search; uniform per block)
+__device__ __forceinline__ int flat_matrix(const int32_t *begin, int nm, int b) {
+    int lo = 0, hi = nm - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (begin[mid] <= b) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
 __global__ void unpack_damp_kernel(const __grid_constant__ InvParams P) {
-    const MatDesc &m = P.m[blockIdx.y];
+    const int r = flat_matrix(P.unp_begin, P.nm, blockIdx.x);
+    const MatDesc &m = P.m[r];
     const int64_t n = m.n;
     const double add = P.pair_scratch[8 * m.pair + (m.is_A ? 1 : 2)];
-    for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+    const int64_t i0 = (int64_t)(blockIdx.x - P.unp_begin[r]) * kUnpRows;
+    for (int64_t i = i0; i < min(n, i0 + kUnpRows); i++) {
         const float *src = m.packed + poff(i, i, n);
         double *dst = m.work + i * m.ld;
         for (int64_t j = i + threadIdx.x; j < n; j += blockDim.x) {
@@ -1471,16 +1488,17 @@ __device__ __forceinline__ void split_store(float *split, int n, int kp, int i, 
     split[(int64_t)n * kp + (int64_t)i * kp + j] = tf32_rn_inv(v - hi);
 }
 __global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ InvParams P) {
-    const MatDesc &m = P.m[blockIdx.y];
+    const int rm = flat_matrix(P.fin_begin, P.nm, blockIdx.x), bx = blockIdx.x - P.fin_begin[rm];
+    const MatDesc &m = P.m[rm];
     const int n = m.n, kp = (n + 3) / 4 * 4;
-    if (m.split && blockIdx.x == 0 && kp > n)
+    if (m.split && bx == 0 && kp > n)
         for (int i = threadIdx.x; i < n; i += blockDim.x)
             for (int j = n; j < kp; j++) m.split[(int64_t)i * kp + j] = m.split[(int64_t)n * kp + (int64_t)i * kp + j] = 0.f;
     const int64_t ld = m.ld;
     const int nt = (n + 31) / 32, npairs = nt * (nt + 1) / 2;
     __shared__ double T[32][33];
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-    for (int t = blockIdx.x; t < npairs; t += gridDim.x) {
+    for (int t = bx * kFinTiles; t < min(npairs, (bx + 1) * kFinTiles); t++) {
         // tile t of the row-major upper tile order: row bi starts at S(bi) = bi nt - bi (bi - 1) / 2
         // (closed form + fix-up; a walk over the rows cost ~nt ALU steps per tile)
         const double b2 = 2.0 * nt + 1.0;
@@ -1587,6 +1605,19 @@ static kfac_status load_enc() {
     return KFAC_OK;
 }
 
+// one non-blocking side stream per device (created on first use)
+static kfac_status side_stream(cudaStream_t *out) {
+    static std::mutex mu;
+    static cudaStream_t streams[64] = {};
+    int dev = 0;
+    KFAC_CUDA_TRY(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 64) return set_error(KFAC_ERR_UNSUPPORTED, "inverse: device index >= 64");
+    std::lock_guard<std::mutex> lock(mu);
+    if (!streams[dev]) KFAC_CUDA_TRY(cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking));
+    *out = streams[dev];
+    return KFAC_OK;
+}
+
 kfac_status inverse_launch(const std::vector<InvMat> &mats, int npairs, float gamma, double *pair_scratch,
                            float *pi_out, int g_only, int prec_mode, cudaStream_t st) {
     if (mats.empty()) return KFAC_OK;
@@ -1641,6 +1672,12 @@ kfac_status inverse_launch(const std::vector<InvMat> &mats, int npairs, float ga
         sum_nt += d.nt;
         sum_tiles += d.nt * (d.nt + 1) / 2;
         maxn = std::max(maxn, d.n);
+    }
+    P.unp_begin[0] = P.fin_begin[0] = 0;
+    for (int i = 0; i < P.nm; i++) {
+        const int n = P.m[i].n, t32 = (n + 31) / 32;
+        P.unp_begin[i + 1] = P.unp_begin[i] + (n + kUnpRows - 1) / kUnpRows;
+        P.fin_begin[i + 1] = P.fin_begin[i] + (t32 * (t32 + 1) / 2 + kFinTiles - 1) / kFinTiles;
     }
     // the digit tile sets of every matrix as 4-D TMA maps (global memory, after the task records)
     int64_t sum_tasks_all = 0;
@@ -1700,23 +1737,35 @@ kfac_status inverse_launch(const std::vector<InvMat> &mats, int npairs, float ga
     P.tileflag = P.tiles_done + sum_nt;
     P.tasks = reinterpret_cast<int4 *>(reinterpret_cast<uint8_t *>(pair_scratch) + tasks_offset(npairs, sum_nt, sum_tiles));
     KFAC_CUDA_TRY(cudaMemsetAsync(state, 0, state_ints(npairs, sum_nt, sum_tiles) * sizeof(int), st));
-    inverse_tasks_kernel<<<dim3(npairs_steps, (P.nm + 31) / 32), 32, 0, st>>>(P);
+    // the task list is data-independent: it is built on a side stream while damping, unpack and the
+    // step-0 pivots run on `st`
+    cudaStream_t side = nullptr;
+    KFAC_TRY(side_stream(&side));
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    KFAC_CUDA_TRY(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    KFAC_CUDA_TRY(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    KFAC_CUDA_TRY(cudaEventRecord(ev_fork, st));
+    KFAC_CUDA_TRY(cudaStreamWaitEvent(side, ev_fork, 0));
+    inverse_tasks_kernel<<<dim3(npairs_steps, (P.nm + 31) / 32), 32, 0, side>>>(P);
     KFAC_LAUNCHED();
     KFAC_CUDA_TRY(cudaGetLastError());
+    KFAC_CUDA_TRY(cudaEventRecord(ev_join, side));
     damp_trace_kernel<<<P.nm, 256, 0, st>>>(P);
     KFAC_LAUNCHED();
     KFAC_CUDA_TRY(cudaGetLastError());
-    unpack_damp_kernel<<<dim3(std::min(maxn, 1024), P.nm), 256, 0, st>>>(P);
+    unpack_damp_kernel<<<P.unp_begin[P.nm], 256, 0, st>>>(P);
     KFAC_LAUNCHED();
     KFAC_CUDA_TRY(cudaGetLastError());
     pivot_kernel<<<P.nm, 256, kPivSmem, st>>>(P);
     KFAC_LAUNCHED();
     KFAC_CUDA_TRY(cudaGetLastError());
+    KFAC_CUDA_TRY(cudaStreamWaitEvent(st, ev_join, 0));
+    cudaEventDestroy(ev_fork);  // released once they complete
+    cudaEventDestroy(ev_join);
     inverse_kernel<<<std::min(P.total_tasks, sms), kThreads, kUpdSmem, st>>>(P);
     KFAC_LAUNCHED();
     KFAC_CUDA_TRY(cudaGetLastError());
-    const int max32 = (maxn + 31) / 32;
-    finalize_kernel<<<dim3(std::min(max32 * (max32 + 1) / 2, 592), P.nm), 256, 0, st>>>(P);
+    finalize_kernel<<<P.fin_begin[P.nm], 256, 0, st>>>(P);
     KFAC_LAUNCHED();
     KFAC_CUDA_TRY(cudaGetLastError());
     return KFAC_OK;
