@@ -37,7 +37,7 @@ constexpr int kWorkers = 256, kThreads = 288;
 #define WSYNC() asm volatile("bar.sync 1, 256;" ::: "memory")
 
 constexpr int kMaxMats = 128;
-constexpr int kUnpRows = 8, kFinTiles = 16;
+constexpr int kUnpRows = 8, kFinTiles = 4, kFinT = 64;  // finalize: 4 tile pairs of 64 x 64 per block
 constexpr int kPanelBufs = 4;  // panel buffers per matrix (step mod 4)
 constexpr int B = kPanel;     // 128
 #ifndef KFAC_INV_KC  // experiment overrides (KFAC_NVCC_EXTRA)
@@ -204,8 +204,9 @@ __global__ void unpack_damp_kernel(const __grid_constant__ InvParams P) {
     for (int64_t i = i0; i < min(n, i0 + kUnpRows); i++) {
         const float *src = m.packed + poff(i, i, n);
         double *dst = m.work + i * m.ld;
+#pragma unroll 4
         for (int64_t j = i + threadIdx.x; j < n; j += blockDim.x) {
-            double v = (double)src[j - i];
+            double v = (double)__ldcs(src + (j - i));  // read once: streaming
             if (j == i) v += add;
             dst[j] = v;
         }
@@ -1475,7 +1476,7 @@ __global__ void __launch_bounds__(kThreads, 1) inverse_kernel(const __grid_const
     }
 }
 
-// ---- epilogue: inv = -M (symmetric, full fp32) from the upper storage.  Each upper 32 x 32 tile is
+// ---- epilogue: inv = -M (symmetric, full fp32) from the upper storage.  Each upper 64 x 64 tile is
 // read once (coalesced, through shared memory) and written to both of its output blocks.
 // the precondition's 3xTF32 operand (precond.cu split_kernel's format): hi = rn_tf32(v), lo = rn_tf32(v - hi),
 // planes [2][n][kp], kp = n rounded up to 4 (the padding columns zero)
@@ -1495,9 +1496,10 @@ __global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ I
         for (int i = threadIdx.x; i < n; i += blockDim.x)
             for (int j = n; j < kp; j++) m.split[(int64_t)i * kp + j] = m.split[(int64_t)n * kp + (int64_t)i * kp + j] = 0.f;
     const int64_t ld = m.ld;
-    const int nt = (n + 31) / 32, npairs = nt * (nt + 1) / 2;
-    __shared__ double T[32][33];
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int nt = (n + kFinT - 1) / kFinT, npairs = nt * (nt + 1) / 2;
+    __shared__ double T[kFinT][kFinT + 1];
+    const int tx = threadIdx.x & (kFinT - 1), ty = threadIdx.x / kFinT;  // 64 columns x 4 row groups
+    constexpr int RG = 256 / kFinT;
     for (int t = bx * kFinTiles; t < min(npairs, (bx + 1) * kFinTiles); t++) {
         // tile t of the row-major upper tile order: row bi starts at S(bi) = bi nt - bi (bi - 1) / 2
         // (closed form + fix-up; a walk over the rows cost ~nt ALU steps per tile)
@@ -1508,20 +1510,23 @@ __global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ I
         while (bi + 1 < nt && (bi + 1) * nt - (bi + 1) * bi / 2 <= t) bi++;
         const int bj = bi + (t - (bi * nt - bi * (bi - 1) / 2));
         __syncthreads();
-        for (int r = ty; r < 32; r += 8) {
-            const int i = bi * 32 + r, j = bj * 32 + tx;
+#pragma unroll
+        for (int k = 0; k < kFinT / RG; k++) {  // 16 loads of a thread in flight
+            const int r = ty + RG * k, i = bi * kFinT + r, j = bj * kFinT + tx;
             T[r][tx] = (i < n && j < n) ? m.work[(int64_t)i * ld + j] : 0.0;
         }
         __syncthreads();
-        for (int r = ty; r < 32; r += 8) {
-            const int i = bi * 32 + r, j = bj * 32 + tx;
+#pragma unroll 4
+        for (int k = 0; k < kFinT / RG; k++) {
+            const int r = ty + RG * k;
+            const int i = bi * kFinT + r, j = bj * kFinT + tx;
             if (i < n && j < n) {
                 const float v = (float)(-((bi < bj || r <= tx) ? T[r][tx] : T[tx][r]));
                 m.inv[(int64_t)i * n + j] = v;
                 if (m.split) split_store(m.split, n, kp, i, j, v);
             }
             if (bi < bj) {
-                const int i2 = bj * 32 + r, j2 = bi * 32 + tx;
+                const int i2 = bj * kFinT + r, j2 = bi * kFinT + tx;
                 if (i2 < n && j2 < n) {
                     const float v = (float)(-T[tx][r]);
                     m.inv[(int64_t)i2 * n + j2] = v;
@@ -1675,9 +1680,9 @@ kfac_status inverse_launch(const std::vector<InvMat> &mats, int npairs, float ga
     }
     P.unp_begin[0] = P.fin_begin[0] = 0;
     for (int i = 0; i < P.nm; i++) {
-        const int n = P.m[i].n, t32 = (n + 31) / 32;
+        const int n = P.m[i].n, tf = (n + kFinT - 1) / kFinT;
         P.unp_begin[i + 1] = P.unp_begin[i] + (n + kUnpRows - 1) / kUnpRows;
-        P.fin_begin[i + 1] = P.fin_begin[i] + (t32 * (t32 + 1) / 2 + kFinTiles - 1) / kFinTiles;
+        P.fin_begin[i + 1] = P.fin_begin[i] + (tf * (tf + 1) / 2 + kFinTiles - 1) / kFinTiles;
     }
     // the digit tile sets of every matrix as 4-D TMA maps (global memory, after the task records)
     int64_t sum_tasks_all = 0;
