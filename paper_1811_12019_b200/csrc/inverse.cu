@@ -673,10 +673,11 @@ __device__ void oz_slice(const double (*T)[B + 1], uint8_t *dst, int *dexp, int 
 // barriers of the int8 update pipeline (shared memory) and their phase bits (uniform per CTA)
 enum { OZ_A = 0, OZ_R = 2, OZ_TF = 5, OZ_TE = 8, OZ_RD = 11, OZ_NBAR = 12 };
 #ifndef KFAC_OZ_SETS
-#define KFAC_OZ_SETS 3
+#define KFAC_OZ_SETS 2
 #endif
 constexpr int kOzSets = KFAC_OZ_SETS;  // TMEM accumulator sets of an update (3 x 5 x 32 columns); a panel uses 2 (2 x 6 x 32)
-static_assert(kOzSets * kOzS * kOzQ <= 512 && 2 * kOzD * kOzQ <= 512, "accumulator sets fit TMEM");
+static_assert(kOzSets * kOzS * kOzQ + 3 * 64 <= 512 && 2 * kOzD * kOzQ <= 512,
+              "accumulator sets + three parked quarters (update) / two sets (panel) fit TMEM");
 // The persistent kernel runs 8 worker warps (256 threads: every task's arithmetic, epilogues, drains) and
 // one producer warp (threads 256..287) whose lane 0 loads the int8 operands and issues the tensor-core
 // MMAs of the int8 tasks, so that the MMAs of pass p run while the workers drain pass p-1.  Worker-only
@@ -699,6 +700,17 @@ __device__ __forceinline__ void tmem_ld_x8(uint32_t taddr, uint32_t (&r)[8]) {
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                  : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
                  : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st_x32(uint32_t taddr, const uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+        "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+        "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+        : "memory");
 }
 __device__ __forceinline__ void mma_i8(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
     asm volatile(
@@ -970,23 +982,25 @@ __device__ int oz_update(const InvParams &P, const MatDesc &m, int k, int ns, in
     }
     // ---- workers
     if (threadIdx.x < bi) bulk_prefetch_l2(W + (int64_t)(i0 + threadIdx.x) * ld + j0, jw * 8);
-    double acc[4][16];
-#pragma unroll
-    for (int q = 0; q < 4; q++)
-#pragma unroll
-        for (int c = 0; c < 16; c++) acc[q][c] = 0.0;
+    // acc: the current quarter's product (fp64, this thread's 16 columns); a finished quarter is parked in
+    // TMEM beyond the accumulator sets (2 words per value) so that only one quarter lives in registers
+    double acc[16];
+    const uint32_t tpark = o.tmem + ((uint32_t)(32 * (w & 3)) << 16) + kOzSets * kOzS * kOzQ + 32 * (w >> 2);
     TRACE(const bool wrec = Q == 8 && g_ozcnt[blockIdx.x] == 20;)
-    // passes written out with a compile-time index so that acc stays in registers
+    // passes written out with a compile-time index (static register indices)
     auto iter = [&](auto pc) {
         constexpr int pd = decltype(pc)::value;
         if (pd < Q) {
             const int q = oz_pass_q(pd, ns), st = oz_pass_st(pd, ns);
             if (pd < ns) oz_wait(o, OZ_A + st);  // exponents visible to every worker
+            if (st == 0) {
+#pragma unroll
+                for (int c = 0; c < 16; c++) acc[c] = 0.0;
+            }
             oz_wait(o, OZ_TF + pd % kOzSets);
             TRACE(if (wrec && threadIdx.x == 32) g_ozt[blockIdx.x][16 + pd] = clock64();)
             tc_fence_after();
-            if (ns == 2) oz_drain(o.tmem + (pd % kOzSets) * (kOzS * kOzQ), acc[(pd >> 1) & 3], eA + st * B, eB + st * B + kOzQ * q);
-            else oz_drain(o.tmem + (pd % kOzSets) * (kOzS * kOzQ), acc[pd & 3], eA, eB + kOzQ * q);
+            oz_drain(o.tmem + (pd % kOzSets) * (kOzS * kOzQ), acc, eA + st * B, eB + st * B + kOzQ * q);
             tc_fence_before();
             mbar_arrive(o.bar + OZ_TE + pd % kOzSets);
             if (threadIdx.x == 0 && pd + 3 < Q) {  // the drained pass's MMAs are complete: its ring slot is free
@@ -994,6 +1008,15 @@ __device__ int oz_update(const InvParams &P, const MatDesc &m, int k, int ns, in
                 cbar_expect(o.bar + OZ_R + pn % 3, kOzRBytes);
                 tma_load_4d(ring + (pn % 3) * kOzRBytes, m.tmaps + OZ_MAP_R5, o.bar + OZ_R + pn % 3, 0, kOzQ * oz_pass_q(pn, ns),
                             0, oz_set(m, k + oz_pass_st(pn, ns), J, 1));
+            }
+            if (st == ns - 1 && q < 3) {  // quarter q is final: park it
+                uint32_t rr[32];
+#pragma unroll
+                for (int c = 0; c < 16; c++) {
+                    rr[2 * c] = (uint32_t)__double2loint(acc[c]);
+                    rr[2 * c + 1] = (uint32_t)__double2hiint(acc[c]);
+                }
+                tmem_st_x32(tpark + 64 * q, rr);
             }
             TRACE(if (wrec && threadIdx.x == 32) g_ozt[blockIdx.x][24 + pd] = clock64();)
         }
@@ -1006,17 +1029,27 @@ __device__ int oz_update(const InvParams &P, const MatDesc &m, int k, int ns, in
     iter(std::integral_constant<int, 5>());
     iter(std::integral_constant<int, 6>());
     iter(std::integral_constant<int, 7>());
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     TRACE(WSYNC(); if (threadIdx.x == 0 && Q == 8) g_ozcnt[blockIdx.x]++;)
     // every MMA completed (all TMEM-full phases observed): the A slots are dead
+    tc_fence_before();
     WSYNC();
+    tc_fence_after();
     TRACE(if (threadIdx.x == 0) g_trace_sub[blockIdx.x][1] = gtime();)
     double(*Pt)[B + 1] = reinterpret_cast<double(*)[B + 1]>(dyn);
     {
         const int r = 32 * (w & 3) + lane, cb = 16 * (w >> 2);
 #pragma unroll
-        for (int q = 0; q < 4; q++)
+        for (int q = 0; q < 3; q++) {
+            uint32_t rr[32];
+            tmem_ld_32x32b_x32(tpark + 64 * q, rr);
+            tmem_ld_wait();
+            tmem_regs_ready(rr);
 #pragma unroll
-            for (int c = 0; c < 16; c++) Pt[r][32 * q + cb + c] = acc[q][c];
+            for (int c = 0; c < 16; c++) Pt[r][32 * q + cb + c] = __hiloint2double((int)rr[2 * c + 1], (int)rr[2 * c]);
+        }
+#pragma unroll
+        for (int c = 0; c < 16; c++) Pt[r][96 + cb + c] = acc[c];
     }
     WSYNC();
     const bool piv = I == last + 1 && J == last + 1;
