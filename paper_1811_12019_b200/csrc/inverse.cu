@@ -206,7 +206,7 @@ __global__ void unpack_damp_kernel(const __grid_constant__ InvParams P) {
         double *dst = m.work + i * m.ld;
 #pragma unroll 4
         for (int64_t j = i + threadIdx.x; j < n; j += blockDim.x) {
-            double v = (double)__ldcs(src + (j - i));  // read once: streaming
+            double v = (double)src[j - i];
             if (j == i) v += add;
             dst[j] = v;
         }
@@ -676,8 +676,8 @@ enum { OZ_A = 0, OZ_R = 2, OZ_TF = 5, OZ_TE = 8, OZ_RD = 11, OZ_NBAR = 12 };
 #define KFAC_OZ_SETS 2
 #endif
 constexpr int kOzSets = KFAC_OZ_SETS;  // TMEM accumulator sets of an update (3 x 5 x 32 columns); a panel uses 2 (2 x 6 x 32)
-static_assert(kOzSets * kOzS * kOzQ + 3 * 64 <= 512 && 2 * kOzD * kOzQ <= 512,
-              "accumulator sets + three parked quarters (update) / two sets (panel) fit TMEM");
+static_assert(kOzSets * kOzS * kOzQ + 3 * 64 <= 512 && 2 * kOzD * kOzQ + 2 * 64 <= 512,
+              "accumulator sets + parked quarters fit TMEM (update: 3 quarters, panel: 2)");
 // The persistent kernel runs 8 worker warps (256 threads: every task's arithmetic, epilogues, drains) and
 // one producer warp (threads 256..287) whose lane 0 loads the int8 operands and issues the tensor-core
 // MMAs of the int8 tasks, so that the MMAs of pass p run while the workers drain pass p-1.  Worker-only
@@ -881,13 +881,25 @@ __device__ void oz_panel(const MatDesc &m, int k, int J, double *dyn, OzState &o
     else oz_slice<0>(T, rdig, oz_exps(m, k, 0) + j0, sexp);
     mbar_arrive(o.bar + OZ_RD);  // this worker's digit stores are proxy-fenced and it is done with T
     TRACE(if (threadIdx.x == 0) g_trace_sub[blockIdx.x][0] = gtime();)
+    // quarters 0 and 1 of Wp_J are parked in TMEM beyond the two accumulator sets (2 words per value),
+    // quarters 2 and 3 stay in registers
     double acc[4][16];
+    const uint32_t tpark = o.tmem + ((uint32_t)(32 * ((threadIdx.x >> 5) & 3)) << 16) + 2 * kOzD * kOzQ + 32 * (threadIdx.x >> 7);
     auto iter = [&](auto pc) {
         constexpr int pd = decltype(pc)::value;
         if (pd == 0) oz_wait(o, OZ_A);  // P_k's exponents visible to every worker
         oz_wait(o, OZ_TF + (pd & 1));
         tc_fence_after();
         oz_drain6(o.tmem + (pd & 1) * (kOzD * kOzQ), acc[pd], eP, sexp + kOzQ * pd);
+        if (pd < 2) {
+            uint32_t rr[32];
+#pragma unroll
+            for (int c = 0; c < 16; c++) {
+                rr[2 * c] = (uint32_t)__double2loint(acc[pd][c]);
+                rr[2 * c + 1] = (uint32_t)__double2hiint(acc[pd][c]);
+            }
+            tmem_st_x32(tpark + 64 * pd, rr);
+        }
         tc_fence_before();
         mbar_arrive(o.bar + OZ_TE + (pd & 1));
         if (pd == 0 && threadIdx.x == 0) {  // pass 0's MMAs are complete: its ring slot takes quarter 3
@@ -899,12 +911,24 @@ __device__ void oz_panel(const MatDesc &m, int k, int J, double *dyn, OzState &o
     iter(std::integral_constant<int, 1>());
     iter(std::integral_constant<int, 2>());
     iter(std::integral_constant<int, 3>());
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    tc_fence_before();
     WSYNC();  // every MMA completed: P_k's digits in T are dead
+    tc_fence_after();
     TRACE(if (threadIdx.x == 0) g_trace_sub[blockIdx.x][1] = gtime();)
     {
         const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, t = 32 * (w & 3) + lane, cb = 16 * (w >> 2);
 #pragma unroll
-        for (int q = 0; q < 4; q++)
+        for (int q = 0; q < 2; q++) {
+            uint32_t rr[32];
+            tmem_ld_32x32b_x32(tpark + 64 * q, rr);
+            tmem_ld_wait();
+            tmem_regs_ready(rr);
+#pragma unroll
+            for (int c = 0; c < 16; c++) T[t][32 * q + cb + c] = __hiloint2double((int)rr[2 * c + 1], (int)rr[2 * c]);
+        }
+#pragma unroll
+        for (int q = 2; q < 4; q++)
 #pragma unroll
             for (int c = 0; c < 16; c++) T[t][32 * q + cb + c] = acc[q][c];  // Wp_J (zero outside bk rows)
     }
