@@ -14,7 +14,9 @@ parts of the method in plain Python:
                        readings R-15, R-16) -- an implementation independent
                        of the library's plan.cpp, compared bit-exactly.
 * ``reduce_scatter``   ReduceScatterV(mean) simulated in-process, summation in
-                       ascending rank order then x 1/P (R-11).
+                       ascending rank order then x 1/P (P:319-326; R-11; S:457-465);
+                       optionally with the fp16 factor wire (``wire_fp16``,
+                       NEXT-4(ii), reading R-23).
 * ``all_gather``       AllGatherV of the primary owners' 𝒢.
 * ``damping_schedule`` warmup damping recurrence (reading R-2).
 * ``kfac_step``        Algorithm 1's body minus fwd/bwd/update.
@@ -369,13 +371,52 @@ def plan(layers, world, policy=POLICY_RR, stale=False, g_only=False):
 # --------------------------------------------------------------------------
 # a4 / a8: simulated collectives (R-11, R-16)
 # --------------------------------------------------------------------------
-def reduce_scatter(sends, pl):
-    """ReduceScatterV(mean): rank r receives chunk r of Σ_{q=0..P-1} send_q (ascending), × 1/P."""
+def wire_fp16(x, scale=1.0):
+    """The fp16 wire value of x (NEXT-4(ii); reading R-9 of P:92-93, "half precision floating point
+    numbers for both computation [and communication]"; R-23): x·scale rounded to the
+    nearest IEEE binary16 value, ties to even (overflow to ±inf, gradual underflow), then ÷ scale.
+    `scale` is a power of two, so both scalings are exact and only the rounding changes x."""
+    s = float(scale)
+    m, _ = math.frexp(s)
+    if s <= 0 or m != 0.5:
+        raise ValueError("wire scale must be a positive power of two")
+    with np.errstate(over="ignore"):  # overflow to ±inf is the format's answer
+        return np.asarray(np.asarray(x, dtype=np.float64) * s).astype(np.float16).astype(np.float64) / s
+
+
+def _wire_mask(pl, n_elems):
+    """Per element of one rank's send buffer: 0 = ∇W (fp32 on the wire), 1 = A, 2 = G."""
     P, c = pl["world"], pl["rs_chunk"]
+    kind = np.zeros(P * c, dtype=np.int8)
+    for r in range(P):
+        for l, (o_w, o_a, o_g) in pl["local"][r].items():
+            for k, o in ((1, o_a), (2, o_g)):
+                if o is not None:
+                    kind[r * c + o: r * c + o + packed_len(n_elems[l][k - 1])] = k
+    return kind
+
+
+def reduce_scatter(sends, pl, wire=None, layers=None):
+    """ReduceScatterV(mean): rank r receives chunk r of Σ_{q=0..P-1} send_q (ascending), × 1/P.
+
+    wire=(scale_A, scale_G) (NEXT-4(ii), R-23; needs `layers`): the factor segments travel as fp16 —
+    every rank's A / G elements are replaced by wire_fp16(·, scale), their mean is taken in fp64 and
+    rounded to the wire once more (the owner receives a binary16 word); ∇W travels in fp32 (exact mean)."""
+    P, c = pl["world"], pl["rs_chunk"]
+    if wire is not None:
+        kind = _wire_mask(pl, [dims(L) for L in layers])
+        sc = [None, float(wire[0]), float(wire[1])]
+        sends = [np.asarray(s, dtype=np.float64).copy() for s in sends]
+        for s in sends:
+            for k in (1, 2):
+                s[kind == k] = wire_fp16(s[kind == k], sc[k])
     acc = np.zeros(P * c, dtype=np.float64)
     for q in range(P):
         acc += np.asarray(sends[q], dtype=np.float64)
     acc *= 1.0 / P
+    if wire is not None:
+        for k in (1, 2):
+            acc[kind == k] = wire_fp16(acc[kind == k], sc[k])
     return [acc[r * c:(r + 1) * c].copy() for r in range(P)]
 
 
@@ -424,8 +465,9 @@ def owned_results(layers, pl, rank, recv, gamma, threads=0):
     return out
 
 
-def kfac_step(layers, rank_inputs, world, gamma, policy=POLICY_RR, fmt="bf16", threads=0):
+def kfac_step(layers, rank_inputs, world, gamma, policy=POLICY_RR, fmt="bf16", threads=0, wire=None):
     """Simulate all P ranks.  rank_inputs[r] = (x_bits list, gy_bits list, dW list, n_local).
+    wire: None (fp32 wire) or (scale_A, scale_G) of the fp16 factor wire (reduce_scatter).
 
     Returns dict(plan, sends, recvs, results (per rank), gathered (per rank AG buffer)).
     """
@@ -440,7 +482,7 @@ def kfac_step(layers, rank_inputs, world, gamma, policy=POLICY_RR, fmt="bf16", t
             G = factor_G(gys[l], rws, layer["c_out"], fmt=fmt, threads=threads)
             factors.append((A, G))
         sends.append(build_send(layers, pl, r, factors, dws))
-    recvs = reduce_scatter(sends, pl)
+    recvs = reduce_scatter(sends, pl, wire=wire, layers=layers)
     results = [owned_results(layers, pl, r, recvs[r], gamma, threads) for r in range(world)]
     slots = []
     for r in range(world):
