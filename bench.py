@@ -303,7 +303,8 @@ def run_ours(args):
     st = K.KfacStep(layers, n, rank=rank, world=world, policy=policy, comm=comm, device=dev,
                     stale=not args.no_stale, inv_precision={"auto": K.INV_AUTO, "fp64": K.INV_FP64,
                                                             "int8": K.INV_INT8}[args.inv_precision],
-                    rs_mode={"padded": K.RS_PADDED, "per_owner": K.RS_PER_OWNER}[args.rs_mode])
+                    rs_mode={"padded": K.RS_PADDED, "per_owner": K.RS_PER_OWNER}[args.rs_mode],
+                    wire={"fp32": K.WIRE_FP32, "fp16": K.WIRE_FP16}[args.wire])
     # synthetic inputs of this rank (global-sample seeded), pinned host copies for the e2e leg
     t0 = time.time()
     # x and gy of all layers live in ONE flat buffer (per-layer views 256-byte aligned), host (pinned)
@@ -669,7 +670,8 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": args.config, "global_batch": n * world, "per_gpu_batch": n,
                        "parallelism": f"dp{world}+layer-sharded inverse/precondition ({args.policy})",
-                       "gamma": args.gamma, "l2": ("inputs %.2f GB > 126 MB L2" % (in_bytes / 1e9)) if not flush.numel()
+                       "gamma": args.gamma, "rs_mode": args.rs_mode, "wire": args.wire,
+                       "inv_precision": args.inv_precision, "l2": ("inputs %.2f GB > 126 MB L2" % (in_bytes / 1e9)) if not flush.numel()
                        else "L2 flushed (256 MB write) between steps"},
             "factor_tflops": round(fac_tflops, 2),
             "images_per_s": round(n * world / (ms / 1e3), 1),
@@ -708,6 +710,8 @@ def main():
     ap.add_argument("--seed", type=int, default=1811)
     ap.add_argument("--rs-mode", default="per_owner", choices=["padded", "per_owner"],
                     help="ReduceScatter: one padded ncclReduceScatter or per-owner grouped ncclReduce (kfac_plan_set_rs_mode)")
+    ap.add_argument("--wire", default="fp32", choices=["fp32", "fp16"],
+                    help="factor wire of the ReduceScatter (kfac_plan_set_wire; fp16 = NEXT-4(ii), scales 1)")
     ap.add_argument("--inv-precision", default="auto", choices=["auto", "fp64", "int8"],
                     help="damped-inverse update precision (kfac_plan_set_inverse_precision, reading R-12)")
     ap.add_argument("--no-e2e", action="store_true")

@@ -250,6 +250,32 @@ KFAC_API kfac_status kfac_factor_all(kfac_plan_t plan, const void *const *xs /* 
 KFAC_API kfac_status kfac_reduce_scatter_factors(kfac_comm_t comm, kfac_plan_t plan, const float *rs_send,
                                         float *rs_recv, void *stream);
 
+/* kfac_reduce_scatter_factors_ws: the same ReduceScatterV with a workspace `ws` (device, at least
+ * ws_bytes from kfac_plan_query AFTER kfac_plan_set_wire), which an fp16-wire plan needs for its
+ * staging (below); ws may be NULL for an fp32-wire plan.  kfac_reduce_scatter_factors is this call
+ * with ws = NULL and returns KFAC_ERR_ARG on a plan whose wire needs staging.                       */
+KFAC_API kfac_status kfac_reduce_scatter_factors_ws(kfac_comm_t comm, kfac_plan_t plan, const float *rs_send,
+                                                    float *rs_recv, void *ws, void *stream);
+
+/* Wire format of the factor segments in the ReduceScatterV (NEXT-4(ii); "half precision
+ * floating point numbers for both computation [and communication]"; reading R-23):
+ *   KFAC_WIRE_FP32  the packed A / G travel as the fp32 the factor kernels wrote (default);
+ *   KFAC_WIRE_FP16  each rank's A (G) element x travels as binary16(x * scale_A (scale_G)), round to
+ *                   nearest even; the collective averages the fp16 words (NCCL, fp16 arithmetic:
+ *                   up to world - 1 further roundings) and the owner receives fp16 * 1/scale in
+ *                   rs_recv.  Halves the factor payload; dW always travels in fp32.  The scales
+ *                   are powers of two chosen by the caller (like loss scaling) so that every
+ *                   |x| * scale stays below 65504 / world (overflow gives inf, which the inverse
+ *                   reports as a failed pivot) and above the fp16 subnormal range where accuracy
+ *                   matters.  At world = 1 the round trip is still applied (the same values as at
+ *                   any world size up to the averaging).
+ * Changes ws_bytes (the staging: world x (fp32 dW region + fp16 factor region) + one of each);
+ * query the plan after this call.  Stale / G-refresh plans take the wire of the plan they were
+ * made from.  Errors: KFAC_ERR_ARG (NULL plan, unknown wire, a scale that is not a power of two
+ * in [2^-61, 2^59]).                                                                               */
+typedef enum { KFAC_WIRE_FP32 = 0, KFAC_WIRE_FP16 = 1 } kfac_wire;
+KFAC_API kfac_status kfac_plan_set_wire(kfac_plan_t plan, int32_t wire, float scale_A, float scale_G);
+
 /* How kfac_reduce_scatter_factors moves the owner-major buffer:
  *   KFAC_RS_PADDED     one ncclReduceScatter(avg) of world x rs_chunk (every rank's chunk padded to the
  *                      largest; default);

@@ -728,6 +728,25 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void *src, uint32_t bytes
 #ifndef KFAC_OZ_HINTS
 #define KFAC_OZ_HINTS 1
 #endif
+// C -= P through the L2: W_row += (-P)_row as one bulk reduce-add per row (fp64 adds performed at L2;
+// W + (-P) is the same IEEE result as W - P).  Per-thread bulk groups: the issuing thread waits for
+// the source reads before the staging is reused and for completion before the tile is released.
+__device__ __forceinline__ void bulk_red_add_f64(double *dst, const void *src, uint32_t bytes) {
+    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;" ::"l"(dst), "r"(s2u(src)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() {
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    asm volatile("fence.proxy.async.global;" ::: "memory");  // the async-proxy writes before the generic release
+}
+#ifndef KFAC_OZ_BULK_RMW
+#define KFAC_OZ_BULK_RMW 1
+#endif
+constexpr int kPn = B + 2;  // staging row stride of the bulk path (16-byte aligned rows)
+
 __device__ __forceinline__ uint64_t pol_evict_first() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -1060,6 +1079,32 @@ __device__ int oz_update(const InvParams &P, const MatDesc &m, int k, int ns, in
     WSYNC();
     tc_fence_after();
     TRACE(if (threadIdx.x == 0) g_trace_sub[blockIdx.x][1] = gtime();)
+    const bool piv = I == last + 1 && J == last + 1;
+    if (KFAC_OZ_BULK_RMW && !piv) {
+        // stage -P (rows 16-byte aligned) and hand the read-modify-write of C to the L2: warp 0's lanes
+        // issue 4 row reductions each; the workers are free as soon as the staging is written
+        double(*Pn)[kPn] = reinterpret_cast<double(*)[kPn]>(dyn);
+        const int r = 32 * (w & 3) + lane, cb = 16 * (w >> 2);
+#pragma unroll
+        for (int q = 0; q < 3; q++) {
+            uint32_t rr[32];
+            tmem_ld_32x32b_x32(tpark + 64 * q, rr);
+            tmem_ld_wait();
+            tmem_regs_ready(rr);
+#pragma unroll
+            for (int c = 0; c < 16; c++) Pn[r][32 * q + cb + c] = -__hiloint2double((int)rr[2 * c + 1], (int)rr[2 * c]);
+        }
+#pragma unroll
+        for (int c = 0; c < 16; c++) Pn[r][96 + cb + c] = -acc[c];
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic staging writes -> bulk reads
+        WSYNC();
+        if (w == 0) {
+            for (int rr = lane; rr < bi; rr += 32) bulk_red_add_f64(W + (int64_t)(i0 + rr) * ld + j0, &Pn[rr][0], jw * 8);
+            bulk_commit();
+        }
+        deferred = true;
+        return 0;
+    }
     double(*Pt)[B + 1] = reinterpret_cast<double(*)[B + 1]>(dyn);
     {
         const int r = 32 * (w & 3) + lane, cb = 16 * (w >> 2);
@@ -1076,7 +1121,6 @@ __device__ int oz_update(const InvParams &P, const MatDesc &m, int k, int ns, in
         for (int c = 0; c < 16; c++) Pt[r][96 + cb + c] = acc[c];
     }
     WSYNC();
-    const bool piv = I == last + 1 && J == last + 1;
     // coalesced C read-modify-write: warp w takes rows w, w + 8, ...; lane l columns l + 32 i; 32 loads
     // of a lane in flight (L2 hits: the tile was prefetched at the task start)
 #pragma unroll 1
@@ -1407,6 +1451,11 @@ __global__ void __launch_bounds__(kThreads, 1) inverse_kernel(const __grid_const
     int *pend_tile = nullptr, *pend_done = nullptr;
     int pend_val = 0;
     for (;;) {
+        if (threadIdx.x < 32) {  // an update's bulk C reductions (warp 0): staging read before it is reused,
+            bulk_wait_read();    // writes complete before the tile's release below
+            if (pend) bulk_wait_all();
+            __syncwarp();
+        }
         asm volatile("fence.proxy.async;" ::: "memory");  // this task's generic accesses before the next one's bulk copies
         __syncthreads();  // the previous task is done with shared memory and `next`
         if (threadIdx.x == 0) {

@@ -130,6 +130,17 @@ struct DiffMat {          // one packed factor of the stale-Fisher change rate (
     double *out;
     int32_t n;
 };
+struct WireSeg {            // one segment of the fp16 factor wire (wire.cu)
+    int64_t src;              // float offset in the owner's chunk of rs_send / rs_recv
+    int64_t dst;              // element offset in the owner's fp32 (kind 0) or fp16 (kind 1, 2) wire region
+    int64_t len;              // elements
+    int32_t kind;             // 0 dW (fp32), 1 A, 2 G (fp16 x scale)
+    int32_t owner;
+};
+kfac_status wire_pack(const std::vector<WireSeg> &segs, const float *rs_send, int64_t rs_chunk, float *f32,
+                      int64_t f32_stride, void *f16, int64_t f16_stride, float scale_A, float scale_G, cudaStream_t st);
+kfac_status wire_unpack(const std::vector<WireSeg> &segs, const float *f32, const void *f16, float *rs_recv,
+                        float scale_A, float scale_G, cudaStream_t st);
 struct UpdJob {            // one layer of the post-AllGather update (update.cu)
     float *w, *w_prev;        // [dG, dA] row-major fp32, caller-owned
     const float *g;           // preconditioned gradient in the AllGather buffer

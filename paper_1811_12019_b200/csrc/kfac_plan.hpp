@@ -16,6 +16,15 @@ struct kfac_plan {
     int inv_prec = KFAC_INV_AUTO;  // kfac_plan_set_inverse_precision
     int rs_mode = KFAC_RS_PADDED;  // kfac_plan_set_rs_mode
     std::vector<int64_t> rs_used;  // per rank: floats of its chunk the layout uses (<= rs_chunk)
+    // fp16 factor wire (kfac_plan_set_wire; wire.cu): per owner a fp32 dW region and a fp16 factor region
+    int wire = KFAC_WIRE_FP32;
+    float wire_scale[2] = {1.f, 1.f};              // A, G (powers of two)
+    std::vector<kfac::WireSeg> wire_segs;          // owner-major
+    std::vector<int32_t> wire_seg_begin;           // per owner: first segment (world + 1 entries)
+    std::vector<int64_t> wire_f32_used, wire_f16_used;  // per owner: elements of its regions in use
+    int64_t wire_f32_chunk = 0, wire_f16_chunk = 0;     // region sizes per owner (max over owners)
+    int64_t wire_off[4] = {0, 0, 0, 0};            // ws byte offsets: send fp32, send fp16, recv fp32, recv fp16
+    int64_t ws_base = 0;                           // ws_bytes without the wire staging
     std::vector<int32_t> owner;
     std::vector<std::vector<int>> owned;                          // per rank, ascending
     std::vector<std::vector<std::array<int64_t, 3>>> local;       // per rank, per owned layer
@@ -38,4 +47,5 @@ struct kfac_plan {
 
 namespace kfac {
 kfac_status plan_build(kfac_plan *p);
+void wire_build(kfac_plan *p);  // the fp16 wire layout + staging (called by plan_build and kfac_plan_set_wire)
 }

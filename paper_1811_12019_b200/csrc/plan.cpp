@@ -6,6 +6,7 @@
 // tests/test_abi.py (test_plan_bit_exact_vs_oracle) compares the two bit-exactly.
 #include <algorithm>
 #include <atomic>
+#include <cmath>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -245,8 +246,52 @@ kfac_status plan_build(kfac_plan *p) {
     if (s) return s;
     p->factor_ws = fl.ws_bytes;
     ws = std::max(ws, fl.ws_bytes);
-    p->ws_bytes = align16(ws) + 256;
+    p->ws_base = align16(ws) + 256;
+    wire_build(p);
     return KFAC_OK;
+}
+
+void wire_build(kfac_plan *p) {
+    const int P = p->world;
+    p->wire_segs.clear();
+    p->wire_seg_begin.assign(P + 1, 0);
+    p->wire_f32_used.assign(P, 0);
+    p->wire_f16_used.assign(P, 0);
+    p->wire_f32_chunk = p->wire_f16_chunk = 0;
+    p->ws_bytes = p->ws_base;
+    if (p->wire != KFAC_WIRE_FP16) return;
+    for (int r = 0; r < P; r++) {
+        p->wire_seg_begin[r] = (int32_t)p->wire_segs.size();
+        int64_t o32 = 0, o16 = 0;
+        for (size_t k = 0; k < p->owned[r].size(); k++) {
+            const Geom &g = p->geoms[p->owned[r][k]];
+            const auto &loc = p->local[r][k];
+            p->wire_segs.push_back(WireSeg{loc[0], o32, (int64_t)g.dG * g.dA, 0, r});
+            o32 = align16(o32 + (int64_t)g.dG * g.dA);
+            for (int which = 0; which < 2; which++) {
+                if (loc[1 + which] < 0) continue;  // stale / G-refresh layouts
+                const int64_t len = packed_len(which == 0 ? g.dA : g.dG);
+                p->wire_segs.push_back(WireSeg{loc[1 + which], o16, len, 1 + which, r});
+                o16 = align16(o16 + len);
+            }
+        }
+        p->wire_f32_used[r] = o32;
+        p->wire_f16_used[r] = o16;
+        p->wire_f32_chunk = std::max(p->wire_f32_chunk, o32);
+        p->wire_f16_chunk = std::max(p->wire_f16_chunk, o16);
+    }
+    p->wire_seg_begin[P] = (int32_t)p->wire_segs.size();
+    auto a256 = [](int64_t v) { return (v + 255) / 256 * 256; };
+    int64_t off = 0;
+    p->wire_off[0] = off;
+    off = a256(off + (int64_t)P * p->wire_f32_chunk * 4);
+    p->wire_off[1] = off;
+    off = a256(off + (int64_t)P * p->wire_f16_chunk * 2);
+    p->wire_off[2] = off;
+    off = a256(off + p->wire_f32_chunk * 4);
+    p->wire_off[3] = off;
+    off = a256(off + p->wire_f16_chunk * 2);
+    if (p->wire_f16_chunk > 0) p->ws_bytes = std::max(p->ws_base, off + 256);
 }
 
 }  // namespace kfac
@@ -291,6 +336,9 @@ kfac_status kfac_plan_create_stale(kfac_plan_t full, kfac_plan_t *out) {
     p->policy = full->policy;
     p->rs_mode = full->rs_mode;
     p->inv_prec = full->inv_prec;
+    p->wire = full->wire;
+    p->wire_scale[0] = full->wire_scale[0];
+    p->wire_scale[1] = full->wire_scale[1];
     p->stale = true;
     kfac_status s = plan_build(p);
     if (s) {
@@ -314,6 +362,9 @@ kfac_status kfac_plan_create_grefresh(kfac_plan_t full, kfac_plan_t *out) {
     p->policy = full->policy;
     p->rs_mode = full->rs_mode;
     p->inv_prec = full->inv_prec;
+    p->wire = full->wire;
+    p->wire_scale[0] = full->wire_scale[0];
+    p->wire_scale[1] = full->wire_scale[1];
     p->g_only = true;
     kfac_status s = plan_build(p);
     if (s) {
@@ -328,6 +379,21 @@ kfac_status kfac_plan_set_rs_mode(kfac_plan_t p, int32_t mode) {
     if (!p) return set_error(KFAC_ERR_ARG, "kfac_plan_set_rs_mode: NULL plan");
     if (mode != KFAC_RS_PADDED && mode != KFAC_RS_PER_OWNER) return set_error(KFAC_ERR_ARG, "kfac_plan_set_rs_mode: bad mode");
     p->rs_mode = mode;
+    return KFAC_OK;
+}
+
+kfac_status kfac_plan_set_wire(kfac_plan_t p, int32_t wire, float scale_A, float scale_G) {
+    if (!p) return set_error(KFAC_ERR_ARG, "kfac_plan_set_wire: NULL plan");
+    if (wire != KFAC_WIRE_FP32 && wire != KFAC_WIRE_FP16) return set_error(KFAC_ERR_ARG, "kfac_plan_set_wire: bad wire");
+    for (float s : {scale_A, scale_G}) {
+        int e = 0;
+        if (!(s > 0.f) || !std::isfinite(s) || std::frexp(s, &e) != 0.5f || e < -60 || e > 60)
+            return set_error(KFAC_ERR_ARG, "kfac_plan_set_wire: scales must be powers of two in [2^-61, 2^59]");
+    }
+    p->wire = wire;
+    p->wire_scale[0] = scale_A;
+    p->wire_scale[1] = scale_G;
+    wire_build(p);
     return KFAC_OK;
 }
 

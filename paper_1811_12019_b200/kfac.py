@@ -100,6 +100,9 @@ _inv_report = _sig("kfac_inverse_report", [_P, _i32, _P, ctypes.POINTER(ctypes.c
 INV_AUTO, INV_FP64, INV_INT8 = 0, 1, 2
 _set_rs_mode = _sig("kfac_plan_set_rs_mode", [_P, _i32])
 RS_PADDED, RS_PER_OWNER = 0, 1
+_set_wire = _sig("kfac_plan_set_wire", [_P, _i32, _f32, _f32])
+WIRE_FP32, WIRE_FP16 = 0, 1
+_reduce_scatter_ws = _sig("kfac_reduce_scatter_factors_ws", [_P, _P, _P, _P, _P, _P])
 _update = _sig("kfac_update", [_P, _P, ctypes.POINTER(_P), ctypes.POINTER(_P), _f32, _f32, _i32, _f32, _P, _P])
 
 EXPORTS = ["kfac_last_error", "kfac_version", "kfac_launch_count", "kfac_plan_create", "kfac_plan_query", "kfac_plan_rank_layers",
@@ -109,7 +112,7 @@ EXPORTS = ["kfac_last_error", "kfac_version", "kfac_launch_count", "kfac_plan_cr
            "kfac_plan_is_stale", "kfac_refresh_interval", "kfac_refresh", "kfac_factor_diff", "kfac_update", "kfac_bn_grads",
            "kfac_bn_precondition", "kfac_bn_ws_bytes", "kfac_bn_exchange",
            "kfac_plan_create_grefresh", "kfac_plan_refresh_kind", "kfac_plan_set_inverse_precision",
-           "kfac_inverse_report", "kfac_plan_set_rs_mode"]
+           "kfac_inverse_report", "kfac_plan_set_rs_mode", "kfac_plan_set_wire", "kfac_reduce_scatter_factors_ws"]
 
 
 def _check(st, where):
@@ -206,6 +209,11 @@ class Plan:
         """kfac_plan_set_rs_mode: RS_PADDED (one ReduceScatter) or RS_PER_OWNER (grouped per-owner Reduce)."""
         _check(_set_rs_mode(self.h, int(mode)), "kfac_plan_set_rs_mode")
 
+    def set_wire(self, wire, scale_A=1.0, scale_G=1.0):
+        """kfac_plan_set_wire: WIRE_FP32 or WIRE_FP16 (factor segments as fp16 x power-of-two scale).
+        Changes ws_bytes: query the plan afterwards."""
+        _check(_set_wire(self.h, int(wire), float(scale_A), float(scale_G)), "kfac_plan_set_wire")
+
     def stale_plan(self):
         """kfac_plan_create_stale: the plan of the steps that reuse stale factors."""
         return Plan(self.layers, self.world, self.n_local, stale_of=self)
@@ -280,9 +288,14 @@ def factor_all(plan, xs, gys, rs_send, ws, alphaA=None, alphaG=None, stream=None
            "kfac_factor_all")
 
 
-def reduce_scatter_factors(comm, plan, rs_send, rs_recv, stream=None):
-    _check(_reduce_scatter(comm.h if comm is not None else None, plan.h, _ptr(rs_send), _ptr(rs_recv),
-                           _stream(stream)), "kfac_reduce_scatter_factors")
+def reduce_scatter_factors(comm, plan, rs_send, rs_recv, stream=None, ws=None):
+    """kfac_reduce_scatter_factors, or kfac_reduce_scatter_factors_ws when `ws` is given (fp16 wire)."""
+    c = comm.h if comm is not None else None
+    if ws is None:
+        _check(_reduce_scatter(c, plan.h, _ptr(rs_send), _ptr(rs_recv), _stream(stream)), "kfac_reduce_scatter_factors")
+    else:
+        _check(_reduce_scatter_ws(c, plan.h, _ptr(rs_send), _ptr(rs_recv), _ptr(ws), _stream(stream)),
+               "kfac_reduce_scatter_factors_ws")
 
 
 def damped_inverse(plan, rank, rs_recv, gamma, inv_ws, dev_status, pi_out, ws, stream=None):

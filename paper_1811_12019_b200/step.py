@@ -22,7 +22,7 @@ class KfacStep:
     """
 
     def __init__(self, layers, n_local, rank=0, world=1, policy=kfac.RR, comm=None, device=None, stale=False,
-                 inv_precision=kfac.INV_AUTO, rs_mode=kfac.RS_PER_OWNER):
+                 inv_precision=kfac.INV_AUTO, rs_mode=kfac.RS_PER_OWNER, wire=kfac.WIRE_FP32, wire_scale=(1.0, 1.0)):
         self.layers = list(layers)
         self.rank, self.world, self.n_local = int(rank), int(world), int(n_local)
         self.comm = comm
@@ -30,6 +30,7 @@ class KfacStep:
         self.plan = kfac.Plan(self.layers, world, n_local, policy)
         self.plan.set_inverse_precision(inv_precision)
         self.plan.set_rs_mode(rs_mode)
+        self.plan.set_wire(wire, *wire_scale)  # before the query: the fp16 wire stages in ws
         q = self.plan.query()
         self.q = q
         self.rl = self.plan.rank_layers(rank)
@@ -111,7 +112,7 @@ class KfacStep:
         kfac.factor_all(self.plan, xs, gys, self.rs_send, self.ws, alphaA, alphaG, stream)
 
     def reduce_scatter(self, stream=None):
-        kfac.reduce_scatter_factors(self.comm, self.plan, self.rs_send, self.rs_recv, stream)
+        kfac.reduce_scatter_factors(self.comm, self.plan, self.rs_send, self.rs_recv, stream, ws=self.ws)
 
     def inverse(self, gamma, stream=None):
         kfac.damped_inverse(self.plan, self.rank, self.rs_recv, gamma, self.inv_ws, self.dev_status, self.pi,
@@ -133,7 +134,8 @@ class KfacStep:
         """A step with stale factors (R-20): dW (set_stale_dw) -> ReduceScatter of the dW-only layout ->
         precondition with the inverses cached by the last full step -> AllGather.  No factor, no inverse."""
         stages = (lambda: kfac.factor_all(self.splan, None, None, self.s_send, self.ws, stream=stream),
-                  lambda: kfac.reduce_scatter_factors(self.comm, self.splan, self.s_send, self.s_recv, stream),
+                  lambda: kfac.reduce_scatter_factors(self.comm, self.splan, self.s_send, self.s_recv, stream,
+                                                      ws=self.ws),
                   lambda: None,
                   lambda: kfac.precondition(self.splan, self.rank, self.s_recv, self.inv_ws, self.ag_buf, self.ws,
                                             stream),
@@ -156,7 +158,8 @@ class KfacStep:
         """A step that refreshes G but keeps A stale (R-20): G factors only, ReduceScatter of [dW, G],
         G_d^-1 with the pi of the last full step (self.pi), the cached A_d^-1 and its split, AllGather."""
         stages = (lambda: kfac.factor_all(self.gplan, None, gys, self.g_send, self.ws, stream=stream),
-                  lambda: kfac.reduce_scatter_factors(self.comm, self.gplan, self.g_send, self.g_recv, stream),
+                  lambda: kfac.reduce_scatter_factors(self.comm, self.gplan, self.g_send, self.g_recv, stream,
+                                                      ws=self.ws),
                   lambda: kfac.damped_inverse(self.gplan, self.rank, self.g_recv, gamma, self.inv_ws, self.dev_status,
                                               self.pi, self.ws, stream),
                   lambda: kfac.precondition(self.gplan, self.rank, self.g_recv, self.inv_ws, self.ag_buf, self.ws,

@@ -53,6 +53,8 @@ def main():
     cfg = sys.argv[1] if len(sys.argv) > 1 else "small"
     policy = int(sys.argv[2]) if len(sys.argv) > 2 else 0
     rs_mode = int(sys.argv[3]) if len(sys.argv) > 3 else 0  # 0 padded ReduceScatter, 1 per-owner grouped Reduce
+    wire = int(sys.argv[4]) if len(sys.argv) > 4 else 0  # 1: fp16 factor wire (NEXT-4(ii), R-23)
+    wsc = (2.0, 4.0) if wire else None  # non-unit power-of-two scales
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
@@ -69,7 +71,8 @@ def main():
     comm = K.Comm(bytes(uid.cpu().numpy().tobytes()), rank, world, local)
     layers, n = NETS[cfg]()
     gamma = 2.5e-2
-    st = K.KfacStep(layers, n, rank=rank, world=world, policy=policy, comm=comm, device=dev, stale=True, rs_mode=rs_mode)
+    st = K.KfacStep(layers, n, rank=rank, world=world, policy=policy, comm=comm, device=dev, stale=True, rs_mode=rs_mode,
+                    wire=wire, wire_scale=wsc or (1.0, 1.0))
     xs = [inputs.layer_x(l, i, n, rank) for i, l in enumerate(layers)]
     gys = [inputs.layer_gy(l, i, n, rank) for i, l in enumerate(layers)]
     dws = [inputs.layer_dw(l, i, rank) for i, l in enumerate(layers)]
@@ -99,7 +102,7 @@ def main():
         import oracle
         for b in bufs[1:]:
             ok &= torch.equal(b, bufs[0])
-        ref = oracle.kfac_step(layers, allin, world, gamma, policy=policy)
+        ref = oracle.kfac_step(layers, allin, world, gamma, policy=policy, wire=wsc)
         pl = ref["plan"]
         for r in range(world):
             rl = st.plan.rank_layers(r)
@@ -119,7 +122,7 @@ def main():
             owner = pl["owner"][l]
             e = relerr(g[off:off + dg * da], ref["results"][owner][l]["precond"].reshape(-1))
             err = max(err, e)
-        print(f"mp_parity {cfg} P={world} policy={policy} rs_mode={rs_mode}: stage3 err {stage3:.2e}, end-to-end max err {err:.2e}, "
+        print(f"mp_parity {cfg} P={world} policy={policy} rs_mode={rs_mode} wire={wire}: stage3 err {stage3:.2e}, end-to-end max err {err:.2e}, "
               f"replicas identical {ok}", flush=True)
         ok &= err <= 2e-3
     if big:  # the stale / G-refresh / BN legs are covered by the small nets
@@ -173,7 +176,7 @@ def main():
         for r in range(world):
             facs = [(None, oracle.factor_G(all3[r][0][l], shapes.rows(L, n), L["c_out"])) for l, L in enumerate(layers)]
             sends.append(oracle.build_send(layers, gp, r, facs, all3[r][1]))
-        grecvs = oracle.reduce_scatter(sends, gp)
+        grecvs = oracle.reduce_scatter(sends, gp, wire=wsc, layers=layers)
         g = bufs[0].cpu().double().numpy()
         gerr = 0.0
         for l in range(len(layers)):
