@@ -400,8 +400,8 @@ def reduce_scatter(sends, pl, wire=None, layers=None):
     """ReduceScatterV(mean): rank r receives chunk r of Σ_{q=0..P-1} send_q (ascending), × 1/P.
 
     wire=(scale_A, scale_G) (NEXT-4(ii), R-23; needs `layers`): the factor segments travel as fp16 —
-    every rank's A / G elements are replaced by wire_fp16(·, scale), their mean is taken in fp64 and
-    rounded to the wire once more (the owner receives a binary16 word); ∇W travels in fp32 (exact mean)."""
+    every rank's A / G elements are replaced by wire_fp16(·, scale) and the owner takes the mean of
+    the P wire values it receives (in fp64 here); ∇W travels in fp32 (exact mean)."""
     P, c = pl["world"], pl["rs_chunk"]
     if wire is not None:
         kind = _wire_mask(pl, [dims(L) for L in layers])
@@ -414,9 +414,6 @@ def reduce_scatter(sends, pl, wire=None, layers=None):
     for q in range(P):
         acc += np.asarray(sends[q], dtype=np.float64)
     acc *= 1.0 / P
-    if wire is not None:
-        for k in (1, 2):
-            acc[kind == k] = wire_fp16(acc[kind == k], sc[k])
     return [acc[r * c:(r + 1) * c].copy() for r in range(P)]
 
 

@@ -82,15 +82,14 @@ def test_reduce_scatter_wire(orc, P):
             assert np.array_equal(got[r][o_w:o_w + g * a], exact[r][o_w:o_w + g * a])
             for o, n, s in ((o_a, a, sc[0]), (o_g, g, sc[1])):
                 seg = slice(o, o + n * (n + 1) // 2)
-                # the definition: mean of every rank's wire value, itself put on the wire
-                want = np.zeros(n * (n + 1) // 2)
-                for q in range(P):
-                    want += orc.wire_fp16(sends[q][r * pl["rs_chunk"]:][seg], s)
-                want = orc.wire_fp16(want / P, s)
-                assert np.array_equal(got[r][seg], want)
-                # and within one wire rounding of the exact mean per contribution
-                assert np.all(np.abs(got[r][seg] - exact[r][seg]) <= 2.0 ** -11 * (
-                    np.abs(exact[r][seg]) + sum(np.abs(sends[q][r * pl["rs_chunk"]:][seg]) for q in range(P)) / P) + 1e-300)
+                # within one wire rounding per contribution of the exact mean (|wire(x) - x| <= 2^-11 |x|)
+                bound = 2.0 ** -11 * sum(np.abs(sends[q][r * pl["rs_chunk"]:][seg]) for q in range(P)) / P
+                assert np.all(np.abs(got[r][seg] - exact[r][seg]) <= bound)
+                # every contribution is on the fp16 grid: P * mean * scale is a sum of P binary16 values,
+                # an integer multiple of 2^-24 (the smallest subnormal) -- and not the unrounded sum
+                tot = got[r][seg] * P * s
+                assert np.all(np.abs(tot * 2.0 ** 24 - np.round(tot * 2.0 ** 24)) <= 1e-6 * np.abs(tot * 2.0 ** 24))
+                assert not np.array_equal(got[r][seg], exact[r][seg])
     if P == 1:  # one rank: the wire is one rounding of the factor
         for l, (o_w, o_a, o_g) in pl["local"][0].items():
             a, g = orc.dims(layers[l])
