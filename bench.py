@@ -357,11 +357,19 @@ def run_ours(args):
     step_ms = [e[0].elapsed_time(e[nst]) for e in ev]
     stage_ms = [[e[i].elapsed_time(e[i + 1]) for e in ev] for i in range(nst)]
     mine = torch.tensor([sum(step_ms)] + [sum(x) for x in stage_ms], dtype=torch.float64, device=dev)
+    per_rank = [mine.clone() for _ in range(world)]
     if world > 1:
+        dist.all_gather(per_rank, mine)  # every rank's own stage split (the critical rank's below)
         dist.all_reduce(mine, op=dist.ReduceOp.MAX)
     tot = mine.cpu().tolist()
     ms = tot[0] / args.steps
     st_ms = {nm: tot[1 + i] / args.steps for i, nm in enumerate(names)}
+    # the critical rank: the last to reach the AllGather (longest stages 1-5); its AllGather is the
+    # collective's own cost, where stage_ms (the per-stage max over ranks) charges the AllGather of the
+    # ranks that arrive early with their wait for it
+    pr = [t.cpu().tolist() for t in per_rank]
+    crit = max(range(world), key=lambda r: pr[r][0] - pr[r][len(names)])
+    crit_ms = {nm: round(pr[crit][1 + i] / args.steps, 3) for i, nm in enumerate(names)}
 
     # ---- stale-Fisher steps (NEXT-1; R-20): dW-only ReduceScatter, cached inverses, no factor
     # or inverse work; and the Diff kernel a refresh step adds.  Same timing rules.
@@ -676,6 +684,7 @@ def run_ours(args):
             "factor_tflops": round(fac_tflops, 2),
             "images_per_s": round(n * world / (ms / 1e3), 1),
             "stage_ms": {k: round(v, 3) for k, v in st_ms.items()},
+            "stage_ms_critical_rank": dict(crit_ms, rank=crit),
             "roofline": dict(roofs[dom], stage=dom),
             "roofline_factors": fac_roof,
             "roofline_stages": roofs,

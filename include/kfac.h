@@ -261,18 +261,19 @@ KFAC_API kfac_status kfac_reduce_scatter_factors_ws(kfac_comm_t comm, kfac_plan_
  * floating point numbers for both computation [and communication]"; reading R-23):
  *   KFAC_WIRE_FP32  the packed A / G travel as the fp32 the factor kernels wrote (default);
  *   KFAC_WIRE_FP16  each rank's A (G) element x travels as binary16(x * scale_A (scale_G)), round to
- *                   nearest even; the collective averages the fp16 words (NCCL, fp16 arithmetic:
- *                   up to world - 1 further roundings) and the owner receives fp16 * 1/scale in
- *                   rs_recv.  Halves the factor payload; dW always travels in fp32.  The scales
- *                   are powers of two chosen by the caller (like loss scaling) so that every
- *                   |x| * scale stays below 65504 / world (overflow gives inf, which the inverse
- *                   reports as a failed pivot) and above the fp16 subnormal range where accuracy
- *                   matters.  At world = 1 the round trip is still applied (the same values as at
- *                   any world size up to the averaging).
- * Changes ws_bytes (the staging: world x (fp32 dW region + fp16 factor region) + one of each);
- * query the plan after this call.  Stale / G-refresh plans take the wire of the plan they were
- * made from.  Errors: KFAC_ERR_ARG (NULL plan, unknown wire, a scale that is not a power of two
- * in [2^-61, 2^59]).                                                                               */
+ *                   nearest even; the fp16 words are gathered to the owner (grouped ncclSend /
+ *                   ncclRecv, no arithmetic in flight), which writes their mean (fp32 sum in rank
+ *                   order, / world) * 1/scale into rs_recv.  Halves the factor payload; dW always
+ *                   travels in fp32 (ncclReduce / ReduceScatter avg as kfac_plan_set_rs_mode says).
+ *                   The scales are powers of two chosen by the caller (like loss scaling) so that
+ *                   every |x| * scale stays below 65504 (overflow gives inf, which the inverse reports
+ *                   as a failed pivot) and above the fp16 subnormal range where accuracy matters.  At
+ *                   world = 1 the round trip is still applied (the same rounding at every world size).
+ * Changes ws_bytes (the staging: world x (fp32 dW region + fp16 factor region) for the send and one
+ * fp32 + world fp16 regions for the receive); query the plan after this call.  Stale / G-refresh
+ * plans take the wire of the plan they were made from.  Errors: KFAC_ERR_ARG (NULL plan, unknown
+ * wire, a scale that is not a power of two in [2^-61, 2^59]), KFAC_ERR_UNSUPPORTED (fp16 wire with
+ * more than 16 ranks).                                                                              */
 typedef enum { KFAC_WIRE_FP32 = 0, KFAC_WIRE_FP16 = 1 } kfac_wire;
 KFAC_API kfac_status kfac_plan_set_wire(kfac_plan_t plan, int32_t wire, float scale_A, float scale_G);
 

@@ -233,44 +233,44 @@ void kfac_comm_destroy(kfac_comm_t c) {
 }
 
 // ------------------------------------------------------------------ stage 3
-// fp16 factor wire (NEXT-4(ii), R-23): pack -> NCCL over the fp32 / fp16 regions -> unpack (wire.cu)
+// fp16 factor wire (NEXT-4(ii), R-23): pack -> NCCL (fp32 dW reduce, fp16 factor gather) -> unpack (wire.cu)
 static kfac_status reduce_scatter_wire(kfac_comm_t c, kfac_plan_t p, const float *send, float *recv, void *ws,
                                        cudaStream_t st) {
     uint8_t *w = static_cast<uint8_t *>(ws);
-    const int P = p->world;
+    const int P = p->world, me = P == 1 ? 0 : c->rank;
+    const int64_t c32 = p->wire_f32_chunk, c16 = p->wire_f16_chunk;
     float *s32 = reinterpret_cast<float *>(w + p->wire_off[0]);
-    void *s16 = w + p->wire_off[1];
+    uint16_t *s16 = reinterpret_cast<uint16_t *>(w + p->wire_off[1]);
     float *r32 = P == 1 ? s32 : reinterpret_cast<float *>(w + p->wire_off[2]);
-    void *r16 = P == 1 ? s16 : static_cast<void *>(w + p->wire_off[3]);
-    KFAC_TRY(wire_pack(p->wire_segs, send, p->rs_chunk, s32, p->wire_f32_chunk, s16, p->wire_f16_chunk,
-                       p->wire_scale[0], p->wire_scale[1], st));
+    uint16_t *r16 = reinterpret_cast<uint16_t *>(w + p->wire_off[3]);  // [P][c16]: the words from rank q at q * c16
+    KFAC_TRY(wire_pack(p->wire_segs, send, p->rs_chunk, s32, c32, s16, c16, p->wire_scale[0], p->wire_scale[1], st));
     if (P > 1) {
-        const int64_t c32 = p->wire_f32_chunk, c16 = p->wire_f16_chunk;
         KFAC_NCCL_TRY(ncclGroupStart());
         ncclResult_t r = ncclSuccess;
         if (p->rs_mode == KFAC_RS_PER_OWNER) {
-            for (int o = 0; o < P && r == ncclSuccess; o++) {  // on an error, fall through to close the group
+            for (int o = 0; o < P && r == ncclSuccess; o++)  // on an error, fall through to close the group
                 if (p->wire_f32_used[o] > 0)
                     r = ncclReduce(s32 + (int64_t)o * c32, r32, (size_t)p->wire_f32_used[o], ncclFloat32, ncclAvg, o,
                                    c->comm, st);
-                if (r == ncclSuccess && p->wire_f16_used[o] > 0)
-                    r = ncclReduce(static_cast<uint16_t *>(s16) + (int64_t)o * c16, r16, (size_t)p->wire_f16_used[o],
-                                   ncclFloat16, ncclAvg, o, c->comm, st);
-            }
-        } else {
-            if (c32 > 0) r = ncclReduceScatter(s32, r32, (size_t)c32, ncclFloat32, ncclAvg, c->comm, st);
-            if (r == ncclSuccess && c16 > 0) r = ncclReduceScatter(s16, r16, (size_t)c16, ncclFloat16, ncclAvg, c->comm, st);
+        } else if (c32 > 0) {
+            r = ncclReduceScatter(s32, r32, (size_t)c32, ncclFloat32, ncclAvg, c->comm, st);
+        }
+        for (int q = 0; q < P && r == ncclSuccess; q++) {  // gather: owner q's fp16 region of every rank to q
+            if (q == me) continue;
+            if (p->wire_f16_used[q] > 0) r = ncclSend(s16 + (int64_t)q * c16, (size_t)p->wire_f16_used[q], ncclFloat16, q, c->comm, st);
+            if (r == ncclSuccess && p->wire_f16_used[me] > 0)
+                r = ncclRecv(r16 + (int64_t)q * c16, (size_t)p->wire_f16_used[me], ncclFloat16, q, c->comm, st);
         }
         const ncclResult_t e = ncclGroupEnd();
         if (r != ncclSuccess) return set_error(KFAC_ERR_NCCL, std::string("wire collective: ") + ncclGetErrorString(r));
         if (e != ncclSuccess) return set_error(KFAC_ERR_NCCL, std::string("ncclGroupEnd: ") + ncclGetErrorString(e));
         KFAC_TRY(nccl_check_async(c->comm));
     }
-    // the receiving rank's segments: the owner `rank` of this process (P == 1: rank 0)
-    const int me = P == 1 ? 0 : c->rank;
+    std::vector<const void *> src(P);
+    for (int q = 0; q < P; q++) src[q] = q == me ? static_cast<const void *>(s16 + (int64_t)me * c16) : r16 + (int64_t)q * c16;
     const std::vector<WireSeg> mine(p->wire_segs.begin() + p->wire_seg_begin[me],
                                     p->wire_segs.begin() + p->wire_seg_begin[me + 1]);
-    return wire_unpack(mine, r32, r16, recv, p->wire_scale[0], p->wire_scale[1], st);
+    return wire_unpack(mine, r32, src.data(), P, recv, p->wire_scale[0], p->wire_scale[1], st);
 }
 
 kfac_status kfac_reduce_scatter_factors(kfac_comm_t c, kfac_plan_t p, const float *send, float *recv, void *stream) {

@@ -530,9 +530,9 @@ __device__ __forceinline__ void cp_async8(void *dst, const void *src, bool ok) {
 }
 
 #ifdef INV_TRACE  // experiment build only: per-task timeline
-struct TraceRec { int g, k, kind, I, J, sm; long long t0, t1, t2, t3, t4; };
+struct TraceRec { int g, k, kind, I, J, sm; long long t0, t1, t2, t3, t4, t5, t6, t7, t8; };
 __device__ TraceRec g_trace[1 << 17];
-__device__ long long g_trace_sub[1024][2];  // per CTA: end of the product, end of the C-tile wait
+__device__ long long g_trace_sub[1024][6];  // per CTA: [0, 1] end of the product / of the C-tile wait; [2..5] panel phases
 __device__ __forceinline__ long long gtime() { long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t; }
 #define TRACE(...) __VA_ARGS__
 __device__ unsigned long long g_ozprof[8];  // cycles: ring wait, TE wait, A wait, TF wait, drain, issue, tasks
@@ -896,6 +896,7 @@ __device__ void oz_panel(const MatDesc &m, int k, int J, double *dyn, OzState &o
     cp_async_commit();
     cp_async_wait_0();
     WSYNC();
+    TRACE(if (threadIdx.x == 0) g_trace_sub[blockIdx.x][2] = gtime();)
     if (trans) oz_slice<1>(T, rdig, oz_exps(m, k, 0) + j0, sexp);
     else oz_slice<0>(T, rdig, oz_exps(m, k, 0) + j0, sexp);
     mbar_arrive(o.bar + OZ_RD);  // this worker's digit stores are proxy-fenced and it is done with T
@@ -952,7 +953,9 @@ __device__ void oz_panel(const MatDesc &m, int k, int J, double *dyn, OzState &o
             for (int c = 0; c < 16; c++) T[t][32 * q + cb + c] = acc[q][c];  // Wp_J (zero outside bk rows)
     }
     WSYNC();
+    TRACE(if (threadIdx.x == 0) g_trace_sub[blockIdx.x][3] = gtime();)
     oz_slice<0>(T, oz_slices(m, k, J, 1), oz_exps(m, k, 1) + j0, sexp);  // Wp_J's digits
+    TRACE(WSYNC(); if (threadIdx.x == 0) g_trace_sub[blockIdx.x][4] = gtime();)
     for (int e = threadIdx.x; e < bk * B; e += 256) {  // the step-k value of tile (K, J)
         const int t = e >> 7, j = e & (B - 1);
         if (j >= bjp || trans) continue;
@@ -1570,7 +1573,9 @@ __global__ void __launch_bounds__(kThreads, 1) inverse_kernel(const __grid_const
         if (threadIdx.x == 0 && g < (1 << 17)) {
             int sm;
             asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
-            g_trace[g] = TraceRec{g, k, trkind, trI, trJ, sm, tr0, tr1, gtime(), g_trace_sub[blockIdx.x][0], g_trace_sub[blockIdx.x][1]};
+            g_trace[g] = TraceRec{g, k, trkind, trI, trJ, sm, tr0, tr1, gtime(), g_trace_sub[blockIdx.x][0], g_trace_sub[blockIdx.x][1],
+                                  g_trace_sub[blockIdx.x][2], g_trace_sub[blockIdx.x][3], g_trace_sub[blockIdx.x][4],
+                                  g_trace_sub[blockIdx.x][5]};
         }
 #endif
     }

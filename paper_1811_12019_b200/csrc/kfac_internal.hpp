@@ -139,8 +139,8 @@ struct WireSeg {            // one segment of the fp16 factor wire (wire.cu)
 };
 kfac_status wire_pack(const std::vector<WireSeg> &segs, const float *rs_send, int64_t rs_chunk, float *f32,
                       int64_t f32_stride, void *f16, int64_t f16_stride, float scale_A, float scale_G, cudaStream_t st);
-kfac_status wire_unpack(const std::vector<WireSeg> &segs, const float *f32, const void *f16, float *rs_recv,
-                        float scale_A, float scale_G, cudaStream_t st);
+kfac_status wire_unpack(const std::vector<WireSeg> &segs, const float *f32, const void *const *f16, int npeers,
+                        float *rs_recv, float scale_A, float scale_G, cudaStream_t st);
 struct UpdJob {            // one layer of the post-AllGather update (update.cu)
     float *w, *w_prev;        // [dG, dA] row-major fp32, caller-owned
     const float *g;           // preconditioned gradient in the AllGather buffer

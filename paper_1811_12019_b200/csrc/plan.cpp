@@ -289,8 +289,8 @@ void wire_build(kfac_plan *p) {
     off = a256(off + (int64_t)P * p->wire_f16_chunk * 2);
     p->wire_off[2] = off;
     off = a256(off + p->wire_f32_chunk * 4);
-    p->wire_off[3] = off;
-    off = a256(off + p->wire_f16_chunk * 2);
+    p->wire_off[3] = off;  // the fp16 factor regions gathered from every rank
+    off = a256(off + (int64_t)P * p->wire_f16_chunk * 2);
     if (p->wire_f16_chunk > 0) p->ws_bytes = std::max(p->ws_base, off + 256);
 }
 
@@ -385,6 +385,7 @@ kfac_status kfac_plan_set_rs_mode(kfac_plan_t p, int32_t mode) {
 kfac_status kfac_plan_set_wire(kfac_plan_t p, int32_t wire, float scale_A, float scale_G) {
     if (!p) return set_error(KFAC_ERR_ARG, "kfac_plan_set_wire: NULL plan");
     if (wire != KFAC_WIRE_FP32 && wire != KFAC_WIRE_FP16) return set_error(KFAC_ERR_ARG, "kfac_plan_set_wire: bad wire");
+    if (wire == KFAC_WIRE_FP16 && p->world > 16) return set_error(KFAC_ERR_UNSUPPORTED, "kfac_plan_set_wire: fp16 wire up to 16 ranks");
     for (float s : {scale_A, scale_G}) {
         int e = 0;
         if (!(s > 0.f) || !std::isfinite(s) || std::frexp(s, &e) != 0.5f || e < -60 || e > 60)

@@ -6,11 +6,14 @@
 //
 //   pack    rs_send (fp32, every owner's chunk) -> staging: per owner a dW region (fp32, copied) and a
 //           factor region (the packed A / G segments as binary16 of x * scale, round to nearest even);
-//   NCCL    Reduce(avg) per owner (or two ReduceScatters) of the fp32 and the fp16 regions;
-//   unpack  the owner's received regions -> rs_recv at the plan's offsets (fp16 * 1/scale, exact).
+//   NCCL    Reduce(avg) per owner (or one ReduceScatter) of the fp32 dW regions; the fp16 factor
+//           regions are GATHERED to their owner (grouped ncclSend / ncclRecv: the same bytes per rank
+//           as a ring ReduceScatter, (P - 1) / P of the payload, but no fp16 arithmetic in flight);
+//   unpack  the owner's regions -> rs_recv at the plan's offsets: dW copied, each factor element the
+//           mean of its P fp16 wire words, summed in fp32 in rank order, / P, * 1/scale.
 //
 // Both passes are HBM-bound streaming copies: 4 B read + 2 B written per factor element (pack),
-// 2 B + 4 B (unpack), 4 + 4 B per dW element.  Segments start on 16-element boundaries, so every
+// 2P B + 4 B (unpack), 4 + 4 B per dW element.  Segments start on 16-element boundaries, so every
 // thread moves 4 elements per access (16 B fp32 / 8 B fp16); only a segment's last group is ragged.
 #include <cuda_fp16.h>
 
@@ -24,16 +27,18 @@ constexpr int kWireThreads = 256;
 constexpr int64_t kWireTile = 4096;  // elements per tile (16 per thread)
 constexpr int kWireMaxSegs = 240;
 
+constexpr int kWirePeers = 16;  // ranks of an fp16 wire (the unpack sums one fp16 word per rank)
+
 struct WireParams {
     const float *src_f32;    // pack: rs_send; unpack: received fp32 region
-    const __half *src_f16;   // unpack: received fp16 region
+    const __half *src_f16[kWirePeers];  // unpack: the fp16 factor region received from each rank
     float *dst_f32;          // pack: fp32 send region; unpack: rs_recv
     __half *dst_f16;         // pack: fp16 send region
     int64_t send_stride;     // pack: floats per owner chunk of rs_send (rs_chunk)
     int64_t f32_stride;      // pack: elements per owner in the fp32 region
     int64_t f16_stride;      // pack: elements per owner in the fp16 region
     float scale[3];          // per kind: 1 (dW), scale_A, scale_G  (unpack: the reciprocals)
-    int32_t nsegs, unpack;
+    int32_t nsegs, unpack, npeers;
     int32_t tile_begin[kWireMaxSegs + 1];
     WireSeg segs[kWireMaxSegs];
 };
@@ -74,15 +79,28 @@ __device__ __forceinline__ void unpack_group(const WireParams &P, const WireSeg 
         }
         return;
     }
-    const float inv = P.scale[s.kind];
-    const __half *src = P.src_f16 + s.dst + i;
+    // the mean of the P wire words: fp32 sum in rank order (exact while the P values span < 2^13 in
+    // magnitude), one division by P, then the exact power-of-two unscaling
+    const float inv = P.scale[s.kind], np = (float)P.npeers;
     if (n == 4) {
-        const uint2 u = *reinterpret_cast<const uint2 *>(src);
-        const float2 lo = __half22float2(*reinterpret_cast<const __half2 *>(&u.x));
-        const float2 hi = __half22float2(*reinterpret_cast<const __half2 *>(&u.y));
-        *reinterpret_cast<float4 *>(dst) = make_float4(lo.x * inv, lo.y * inv, hi.x * inv, hi.y * inv);
+        float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int q = 0; q < P.npeers; q++) {
+            const uint2 u = __ldcs(reinterpret_cast<const uint2 *>(P.src_f16[q] + s.dst + i));
+            const float2 lo = __half22float2(*reinterpret_cast<const __half2 *>(&u.x));
+            const float2 hi = __half22float2(*reinterpret_cast<const __half2 *>(&u.y));
+            a.x += lo.x;
+            a.y += lo.y;
+            a.z += hi.x;
+            a.w += hi.y;
+        }
+        *reinterpret_cast<float4 *>(dst) = make_float4(__fdiv_rn(a.x, np) * inv, __fdiv_rn(a.y, np) * inv,
+                                                       __fdiv_rn(a.z, np) * inv, __fdiv_rn(a.w, np) * inv);
     } else {
-        for (int j = 0; j < n; j++) dst[j] = __half2float(src[j]) * inv;
+        for (int j = 0; j < n; j++) {
+            float a = 0.f;
+            for (int q = 0; q < P.npeers; q++) a += __half2float(P.src_f16[q][s.dst + i + j]);
+            dst[j] = __fdiv_rn(a, np) * inv;
+        }
     }
 }
 
@@ -146,11 +164,13 @@ kfac_status wire_pack(const std::vector<WireSeg> &segs, const float *rs_send, in
     return wire_run(segs, P, st);
 }
 
-kfac_status wire_unpack(const std::vector<WireSeg> &segs, const float *f32, const void *f16, float *rs_recv,
-                        float scale_A, float scale_G, cudaStream_t st) {
+kfac_status wire_unpack(const std::vector<WireSeg> &segs, const float *f32, const void *const *f16, int npeers,
+                        float *rs_recv, float scale_A, float scale_G, cudaStream_t st) {
+    if (npeers < 1 || npeers > kWirePeers) return set_error(KFAC_ERR_UNSUPPORTED, "fp16 wire: at most 16 ranks");
     WireParams P{};
     P.src_f32 = f32;
-    P.src_f16 = static_cast<const __half *>(f16);
+    for (int q = 0; q < npeers; q++) P.src_f16[q] = static_cast<const __half *>(f16[q]);
+    P.npeers = npeers;
     P.dst_f32 = rs_recv;
     P.scale[0] = 1.f;
     P.scale[1] = 1.f / scale_A;  // exact: the scales are powers of two

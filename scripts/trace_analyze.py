@@ -33,6 +33,14 @@ for kd in (0, 1, 3, 5):
         cw = sum(r[10] - r[9] for r in sub) / n / 1e3
         ep = sum(r[8] - r[10] for r in sub) / n / 1e3
         print(f"kind {kd} phases: product {pr:.1f} us, C wait {cw:.1f} us, epilogue+flags {ep:.1f} us (n={n})")
+# panel (kind 0) phases: deps -> R_J staged -> R_J digits out -> passes done -> Wp_J staged -> Wp_J digits -> end
+sub = [r for r in rows if r[2] == 0 and len(r) >= 15 and r[11] >= r[7] and r[9] >= r[11] and r[10] >= r[9]
+       and r[12] >= r[10] and r[13] >= r[12] and r[8] >= r[13]]
+if sub:
+    n = len(sub)
+    ph = [(r[11] - r[7], r[9] - r[11], r[10] - r[9], r[12] - r[10], r[13] - r[12], r[8] - r[13]) for r in sub]
+    names = ["stage R_J", "slice R_J", "passes", "stage Wp_J", "slice Wp_J", "W tile + flags"]
+    print("kind 0 detail: " + ", ".join(f"{nm} {sum(p[i] for p in ph) / n / 1e3:.1f} us" for i, nm in enumerate(names)) + f" (n={n})")
 # utilisation over time: fraction of CTAs busy (work phase) per 5% of the kernel
 T = max(r[8] for r in rows) - t0
 bins = [0.0] * 20

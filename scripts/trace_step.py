@@ -15,11 +15,11 @@ for _ in range(3):
     st.run(xs, gys, 2.5e-2)
 torch.cuda.synchronize()
 lib = K.kfac._lib
-buf = np.zeros((1 << 17) * 16, dtype=np.int32)  # TraceRec: 6 ints + 5 int64 = 64 B
+buf = np.zeros((1 << 17) * 24, dtype=np.int32)  # TraceRec: 6 ints + 9 int64 = 96 B
 lib.kfac_debug_inverse_trace(buf.ctypes.data_as(ctypes.c_void_p), 1 << 17)
-rec = buf.view(np.uint8).reshape(-1, 64)
+rec = buf.view(np.uint8).reshape(-1, 96)
 ints = rec[:, :24].copy().view(np.int32).reshape(-1, 6)
-ts = rec[:, 24:].copy().view(np.int64).reshape(-1, 5)
+ts = rec[:, 24:].copy().view(np.int64).reshape(-1, 9)
 with open(sys.argv[1], "w") as f:
     for i in range(len(ints)):
         if ts[i, 2]:

@@ -54,7 +54,7 @@ def main():
     policy = int(sys.argv[2]) if len(sys.argv) > 2 else 0
     rs_mode = int(sys.argv[3]) if len(sys.argv) > 3 else 0  # 0 padded ReduceScatter, 1 per-owner grouped Reduce
     wire = int(sys.argv[4]) if len(sys.argv) > 4 else 0  # 1: fp16 factor wire (NEXT-4(ii), R-23)
-    wsc = (2.0, 4.0) if wire else None  # non-unit power-of-two scales
+    wsc = (2.0, 4.0) if wire else None  # non-unit power-of-two scales (oracle: mean of the fp16 wire values, R-23)
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
