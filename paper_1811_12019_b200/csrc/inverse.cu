@@ -602,6 +602,12 @@ __device__ __forceinline__ double oz_x(const double (*T)[B + 1], int t, int c, i
     if (MODE == 1) return T[c][t];
     return (t < bk && c < bk) ? -T[min(t, c)][max(t, c)] : 0.0;
 }
+// U = rint(x * sc) + 0x8080808080 without an fp64 -> int64 conversion: fma(x, sc, 1.5 * 2^52) rounds the
+// exact product (|x sc| < 2^45) to an integer in one step (ties to even, like __double2ll_rn), and the
+// bit pattern minus that of 1.5 * 2^52 is the integer
+__device__ __forceinline__ long long oz_round_bias(double x, double sc) {
+    return __double_as_longlong(fma(x, sc, 6755399441055744.0)) - (0x4338000000000000LL - 0x8080808080LL);
+}
 template <int MODE>
 __device__ void oz_slice(const double (*T)[B + 1], uint8_t *dst, int *dexp, int *sexp, int bk = B) {
     const int tid = threadIdx.x;
@@ -640,7 +646,7 @@ __device__ void oz_slice(const double (*T)[B + 1], uint8_t *dst, int *dexp, int 
             uint32_t lo[4], hi[4];
 #pragma unroll
             for (int u = 0; u < 4; u++) {
-                const long long U = __double2ll_rn(oz_x<MODE>(T, 16 * tc + 4 * g + u, c, bk) * sc) + 0x8080808080LL;
+                const long long U = oz_round_bias(oz_x<MODE>(T, 16 * tc + 4 * g + u, c, bk), sc);
                 lo[u] = (uint32_t)U ^ 0x80808080u;        // bytes: q_5, q_4, q_3, q_2
                 hi[u] = (uint32_t)(U >> 32);              // byte 0: q_1 ^ 0x80, bits 8..: q_0
             }
@@ -658,13 +664,7 @@ __device__ void oz_slice(const double (*T)[B + 1], uint8_t *dst, int *dexp, int 
 #pragma unroll
         for (int s = 0; s < kOzD; s++) {
             uint8_t *a = dst + s * kOzSlice + c * B + ((tc ^ (c & 7)) << 4);
-#if KFAC_OZ_HINTS
-            asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(a), "r"(wd[s][0]), "r"(wd[s][1]),
-                         "r"(wd[s][2]), "r"(wd[s][3]), "l"(pol_evict_last())
-                         : "memory");
-#else
             *reinterpret_cast<uint4 *>(a) = make_uint4(wd[s][0], wd[s][1], wd[s][2], wd[s][3]);
-#endif
         }
     }
     asm volatile("fence.proxy.async;" ::: "memory");  // the digits are read back by bulk copies
