@@ -398,7 +398,7 @@ __device__ int pivot_block(double *__restrict__ W, int64_t ld, int k0, int bk, d
     for (int e = tid; e < B * B; e += kWorkers) {  // P = -S (zero outside bk); W_KK = -P (upper)
         const int i = e >> 7, j = e & (B - 1);
         const bool in = i < bk && j < bk;
-        Pout[e] = in ? -S[min(i, j)][max(i, j)] : 0.0;
+        if (Pout) Pout[e] = in ? -S[min(i, j)][max(i, j)] : 0.0;  // (int8 matrices: their panels read P's digits)
         if (in && j >= i) W[(int64_t)(k0 + i) * ld + k0 + j] = S[i][j];
     }
     return 0;
@@ -602,6 +602,9 @@ __device__ __forceinline__ double oz_x(const double (*T)[B + 1], int t, int c, i
     if (MODE == 1) return T[c][t];
     return (t < bk && c < bk) ? -T[min(t, c)][max(t, c)] : 0.0;
 }
+#ifndef KFAC_OZ_SLICE_LANES
+#define KFAC_OZ_SLICE_LANES 4  // measured per cut: 1 lane 8.0 us, 2 lanes 5.4 us, 4 lanes 5.2 us (RN50 panels)
+#endif
 // U = rint(x * sc) + 0x8080808080 without an fp64 -> int64 conversion: fma(x, sc, 1.5 * 2^52) rounds the
 // exact product (|x sc| < 2^45) to an integer in one step (ties to even, like __double2ll_rn), and the
 // bit pattern minus that of 1.5 * 2^52 is the integer
@@ -638,7 +641,16 @@ __device__ void oz_slice(const double (*T)[B + 1], uint8_t *dst, int *dexp, int 
     // balanced digits q_5..q_1 (q = u - 128), and U >> 40 is q_0 (|q_0| <= 33).  Four consecutive t are
     // transposed byte-wise (PRMT) into the digit planes.
     for (int it = tid; it < B * 8; it += 256) {
-        const int c = it & (B - 1), tc = it >> 7;  // consecutive threads: consecutive columns (conflict-free)
+        // KFAC_OZ_SLICE_LANES consecutive lanes cut the consecutive 16-row chunks tc of one column, so a
+        // warp's 16-byte stores cover 32 / LANES lines (LANES = 1: every lane its own column, 32 lines,
+        // conflict-free shared reads; LANES = 2: 16 lines, still conflict-free for 8-byte reads)
+        const int lane = it & 31, wi = it >> 5;  // warp item 0..31
+        const int c = (KFAC_OZ_SLICE_LANES == 1) ? (it & (B - 1))
+                                                 : (32 / KFAC_OZ_SLICE_LANES) * (wi % (B * KFAC_OZ_SLICE_LANES / 32)) +
+                                                       lane % (32 / KFAC_OZ_SLICE_LANES);
+        const int tc = (KFAC_OZ_SLICE_LANES == 1) ? (it >> 7)
+                                                  : KFAC_OZ_SLICE_LANES * (wi / (B * KFAC_OZ_SLICE_LANES / 32)) +
+                                                        lane / (32 / KFAC_OZ_SLICE_LANES);
         const double sc = __longlong_as_double((long long)(1023 + kOzBits - sexp[c]) << 52);
         uint32_t wd[kOzD][4];
 #pragma unroll
@@ -1153,6 +1165,7 @@ __device__ int oz_update(const InvParams &P, const MatDesc &m, int k, int ns, in
     }
     if (piv) {
         WSYNC();
+        TRACE(if (threadIdx.x == 0) g_trace_sub[blockIdx.x][2] = gtime();)
         if (last >= 1 && threadIdx.x == 0) {  // its slot held P_{last-1}: step last-1's panels must be done
             int vv;
             do {
@@ -1162,11 +1175,13 @@ __device__ int oz_update(const InvParams &P, const MatDesc &m, int k, int ns, in
         }
         WSYNC();
         TRACE(if (threadIdx.x == 0) g_trace_sub[blockIdx.x][1] = gtime();)
-        const int f = pivot_block(W, ld, i0, bi, pivot_slot(m, last + 1), dyn, true);
+        const int f = pivot_block(W, ld, i0, bi, nullptr, dyn, true);  // the panels read P's digits only
+        TRACE(WSYNC(); if (threadIdx.x == 0) g_trace_sub[blockIdx.x][3] = gtime();)
         if (!f) {  // P_{last+1}'s digits (S = -P, upper storage) for the next step's panel products
             WSYNC();
             oz_slice<2>(reinterpret_cast<const double(*)[B + 1]>(dyn), oz_pivdig(m, last + 1), oz_pivexp(m, last + 1), o.sexp, bi);
         }
+        TRACE(WSYNC(); if (threadIdx.x == 0) g_trace_sub[blockIdx.x][4] = gtime();)
         return f;
     }
     deferred = true;
@@ -1354,7 +1369,7 @@ __global__ void __launch_bounds__(256, 1) pivot_kernel(const __grid_constant__ I
     const MatDesc &m = P.m[blockIdx.x];
     if (*m.status != 0) return;
     extern __shared__ double dyn[];
-    const int f = pivot_block(m.work, m.ld, 0, min(B, m.n), pivot_slot(m, 0), dyn);
+    const int f = pivot_block(m.work, m.ld, 0, min(B, m.n), P.ozflag[blockIdx.x] ? nullptr : pivot_slot(m, 0), dyn);
     if (f && threadIdx.x == 0) *m.status = f;
     if (!f && P.ozflag[blockIdx.x]) {  // P_0's digits for step 0's int8 panel products
         __shared__ __align__(16) int sexp[3 * B];

@@ -41,6 +41,14 @@ if sub:
     ph = [(r[11] - r[7], r[9] - r[11], r[10] - r[9], r[12] - r[10], r[13] - r[12], r[8] - r[13]) for r in sub]
     names = ["stage R_J", "slice R_J", "passes", "stage Wp_J", "slice Wp_J", "W tile + flags"]
     print("kind 0 detail: " + ", ".join(f"{nm} {sum(p[i] for p in ph) / n / 1e3:.1f} us" for i, nm in enumerate(names)) + f" (n={n})")
+# chain (kind 5) epilogue: passes end (sub0 is the panel's) ... sub2 RMW done, sub1 pflag wait done,
+# sub3 pivot done, sub4 P digits done, end
+sub = [r for r in rows if r[2] == 5 and len(r) >= 15 and r[11] <= r[10] <= r[12] <= r[13] <= r[8]]
+if sub:
+    n = len(sub)
+    ph = [(r[10] - r[11], r[12] - r[10], r[13] - r[12], r[8] - r[13]) for r in sub]
+    names = ["pflag wait", "pivot 128^2", "P digits", "flags"]
+    print("kind 5 epilogue detail: " + ", ".join(f"{nm} {sum(p[i] for p in ph) / n / 1e3:.1f} us" for i, nm in enumerate(names)) + f" (n={n})")
 # utilisation over time: fraction of CTAs busy (work phase) per 5% of the kernel
 T = max(r[8] for r in rows) - t0
 bins = [0.0] * 20
