@@ -600,6 +600,7 @@ template <int MODE>
 __device__ __forceinline__ double oz_x(const double (*T)[B + 1], int t, int c, int bk) {
     if (MODE == 0) return T[t][c];
     if (MODE == 1) return T[c][t];
+    if (MODE == 3) return (t < bk && c < bk) ? -T[t][c] : 0.0;  // the pivot after pivot_fill_lower
     return (t < bk && c < bk) ? -T[min(t, c)][max(t, c)] : 0.0;
 }
 #ifndef KFAC_OZ_SLICE_LANES
@@ -610,6 +611,14 @@ __device__ __forceinline__ double oz_x(const double (*T)[B + 1], int t, int c, i
 // bit pattern minus that of 1.5 * 2^52 is the integer
 __device__ __forceinline__ long long oz_round_bias(double x, double sc) {
     return __double_as_longlong(fma(x, sc, 6755399441055744.0)) - (0x4338000000000000LL - 0x8080808080LL);
+}
+// the swept pivot block lives in upper storage; mirror it into the lower triangle so that its digit cut
+// reads rows (MODE 3) instead of the min / max gather of MODE 2
+__device__ __forceinline__ void pivot_fill_lower(double (*S)[B + 1]) {
+    for (int e = threadIdx.x; e < B * B; e += kWorkers) {
+        const int i = e >> 7, j = e & (B - 1);
+        if (j < i) S[i][j] = S[j][i];
+    }
 }
 template <int MODE>
 __device__ void oz_slice(const double (*T)[B + 1], uint8_t *dst, int *dexp, int *sexp, int bk = B) {
@@ -968,16 +977,21 @@ __device__ void oz_panel(const MatDesc &m, int k, int J, double *dyn, OzState &o
     TRACE(if (threadIdx.x == 0) g_trace_sub[blockIdx.x][3] = gtime();)
     oz_slice<0>(T, oz_slices(m, k, J, 1), oz_exps(m, k, 1) + j0, sexp);  // Wp_J's digits
     TRACE(WSYNC(); if (threadIdx.x == 0) g_trace_sub[blockIdx.x][4] = gtime();)
-    for (int e = threadIdx.x; e < bk * B; e += 256) {  // the step-k value of tile (K, J)
-        const int t = e >> 7, j = e & (B - 1);
-        if (j >= bjp || trans) continue;
-        m.work[(int64_t)(k0 + t) * ld + j0 + j] = T[t][j];
-    }
-    if (trans)  // M_JK <- Wp_J^T: row j of tile (J, K), consecutive threads along t
-        for (int e = threadIdx.x; e < bj * B; e += 256) {
-            const int j = e >> 7, t = e & (B - 1);
-            if (t < bk) m.work[(int64_t)(j0 + j) * ld + k0 + t] = T[t][j];
+    // the step-k value of tile (K, J), 16-byte stores (W rows and tile columns are 16-byte aligned)
+    if (!trans) {
+        for (int e = threadIdx.x; e < bk * (B / 2); e += 256) {
+            const int t = e >> 6, j = 2 * (e & (B / 2 - 1));
+            if (j < bjp)  // bjp is a multiple of 16
+                *reinterpret_cast<double2 *>(m.work + (int64_t)(k0 + t) * ld + j0 + j) = make_double2(T[t][j], T[t][j + 1]);
         }
+    } else {  // M_JK <- Wp_J^T: row j of tile (J, K), consecutive threads along t
+        for (int e = threadIdx.x; e < bj * (B / 2); e += 256) {
+            const int j = e >> 6, t = 2 * (e & (B / 2 - 1));
+            double *dst = m.work + (int64_t)(j0 + j) * ld + k0 + t;
+            if (t + 1 < bk) *reinterpret_cast<double2 *>(dst) = make_double2(T[t][j], T[t + 1][j]);
+            else if (t < bk) *dst = T[t][j];
+        }
+    }
 }
 
 // pass order of an update task: quarter-major (both steps of quarter q, then quarter q+1), so that a
@@ -1179,7 +1193,9 @@ __device__ int oz_update(const InvParams &P, const MatDesc &m, int k, int ns, in
         TRACE(WSYNC(); if (threadIdx.x == 0) g_trace_sub[blockIdx.x][3] = gtime();)
         if (!f) {  // P_{last+1}'s digits (S = -P, upper storage) for the next step's panel products
             WSYNC();
-            oz_slice<2>(reinterpret_cast<const double(*)[B + 1]>(dyn), oz_pivdig(m, last + 1), oz_pivexp(m, last + 1), o.sexp, bi);
+            pivot_fill_lower(reinterpret_cast<double(*)[B + 1]>(dyn));
+            WSYNC();
+            oz_slice<3>(reinterpret_cast<const double(*)[B + 1]>(dyn), oz_pivdig(m, last + 1), oz_pivexp(m, last + 1), o.sexp, bi);
         }
         TRACE(WSYNC(); if (threadIdx.x == 0) g_trace_sub[blockIdx.x][4] = gtime();)
         return f;
@@ -1374,7 +1390,9 @@ __global__ void __launch_bounds__(256, 1) pivot_kernel(const __grid_constant__ I
     if (!f && P.ozflag[blockIdx.x]) {  // P_0's digits for step 0's int8 panel products
         __shared__ __align__(16) int sexp[3 * B];
         WSYNC();
-        oz_slice<2>(reinterpret_cast<const double(*)[B + 1]>(dyn), oz_pivdig(m, 0), oz_pivexp(m, 0), sexp, min(B, m.n));
+        pivot_fill_lower(reinterpret_cast<double(*)[B + 1]>(dyn));
+        WSYNC();
+        oz_slice<3>(reinterpret_cast<const double(*)[B + 1]>(dyn), oz_pivdig(m, 0), oz_pivexp(m, 0), sexp, min(B, m.n));
     }
 }
 
