@@ -269,10 +269,15 @@ __device__ __forceinline__ int block_sweep32(const double (*S)[B + 1], int s0, d
     return 0;
 }
 
-#ifdef PIVOT_DBG
+#ifdef PIVOT_DBG  // cycles per pivot phase, summed over every pivot (kfac_debug_pclk)
 __device__ int g_pivot_dbg;
-__device__ long long g_pclk[64];
-#define PCLK(k) if (threadIdx.x == 0) g_pclk[k] = clock64();
+__device__ unsigned long long g_pacc[32];
+#define PCLK(k)                                                                          \
+    if (threadIdx.x == 0) {                                                              \
+        const long long now_ = clock64();                                                \
+        atomicAdd(&g_pacc[k], (unsigned long long)(now_ - pclk_last));                   \
+        pclk_last = now_;                                                                \
+    }
 #else
 #define PCLK(k)
 #endif
@@ -280,6 +285,9 @@ __device__ long long g_pclk[64];
 // the value the sweep gives that tile at step K (no later task has to read the pivot slot for it)
 __device__ int pivot_block(double *__restrict__ W, int64_t ld, int k0, int bk, double *__restrict__ Pout,
                            double *smem, bool preloaded = false) {
+#ifdef PIVOT_DBG
+    long long pclk_last = clock64();
+#endif
     double(*S)[B + 1] = reinterpret_cast<double(*)[B + 1]>(smem);
     double *O = smem + B * (B + 1);       // [S2][SLD] old block row
     double *Wr = O + S2 * SLD;            // [S2][SLD] Q * O
@@ -401,6 +409,7 @@ __device__ int pivot_block(double *__restrict__ W, int64_t ld, int k0, int bk, d
         if (Pout) Pout[e] = in ? -S[min(i, j)][max(i, j)] : 0.0;  // (int8 matrices: their panels read P's digits)
         if (in && j >= i) W[(int64_t)(k0 + i) * ld + k0 + j] = S[i][j];
     }
+    PCLK(21)
     return 0;
 }
 
@@ -871,7 +880,7 @@ __device__ __forceinline__ void oz_drain6(uint32_t tacc, double (&acc)[16], cons
 constexpr int kOzPRing = kOzD * kOzQBytes;  // 24 KB
 constexpr int kOzPanelSmem = 133120 + 3 * kOzPRing + 1024;
 static_assert(kOzPanelSmem <= kUpdSmem, "the int8 panel fits the update kernel's shared memory");
-__device__ void oz_panel(const MatDesc &m, int k, int J, double *dyn, OzState &o, int *sexp, int *eP) {
+__device__ void oz_panel(const MatDesc &m, int k, int J, double *dyn, OzState &o, int *sexp, int *eP, const int *pivflag) {
     const int n = m.n, k0 = k * B, K = k;
     const int64_t ld = m.ld;
     const int j0 = J * B;
@@ -888,6 +897,16 @@ __device__ void oz_panel(const MatDesc &m, int k, int J, double *dyn, OzState &o
             tma_load_4d(ring + (q % 3) * kOzPRing, m.tmaps + OZ_MAP_R6, o.bar + OZ_R + q % 3, 0, kOzQ * q, 0, oz_set(m, k, J, 0));
         };
         oz_wait(o, OZ_RD);  // the workers are done with T and R_J's digits are in global memory
+        // P_k only now: R_J's staging and digits do not need it, so they overlap the pivot's tail
+        // (the task waited for everything else at its start)
+        if (k >= 1) {
+            int v;
+            for (;;) {
+                asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(pivflag) : "memory");
+                if (v >= k + 1) break;
+                __nanosleep(64);
+            }
+        }
         asm volatile("fence.proxy.async;" ::: "memory");
         asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(m.tmaps + OZ_MAP_R6) : "memory");
         cbar_expect(o.bar + OZ_A, kOzSet + B * 4);
@@ -1207,9 +1226,10 @@ __device__ int oz_update(const InvParams &P, const MatDesc &m, int k, int ns, in
 // ---- panel task (m, k, J): R_J = block row K (from upper storage), Wp_J = P_k R_J.  The task also
 // gives tile (K, J) its step-k value Wp_J (M_KJ <- Wp_J, or M_JK <- Wp_J^T left of the diagonal):
 // nothing else reads that tile at step k, so the row / column K "copy" updates have no work left.
-__device__ void panel_task(const MatDesc &m, int k, int J, double *dyn, Ring &ring, bool oz, OzState &ozs) {
+__device__ void panel_task(const MatDesc &m, int k, int J, double *dyn, Ring &ring, bool oz, OzState &ozs,
+                           const int *pivflag) {
     if (oz) {
-        oz_panel(m, k, J, dyn, ozs, ozs.sexp, ozs.eP);
+        oz_panel(m, k, J, dyn, ozs, ozs.sexp, ozs.eP, pivflag);
         return;
     }
     const int n = m.n, k0 = k * B, K = k;
@@ -1526,7 +1546,7 @@ __global__ void __launch_bounds__(kThreads, 1) inverse_kernel(const __grid_const
                 const int lane = threadIdx.x;
                 if (lane == 0 && k >= 1)
                     wait_ge(P.tileflag + m.tile_begin + (J >= k ? upper_index(k, J, nt) : upper_index(J, k, nt)), k);
-                if (lane == 1 && k >= 1) wait_ge(P.pivflag + mi, k + 1);
+                if (lane == 1 && k >= 1 && !oz) wait_ge(P.pivflag + mi, k + 1);  // int8 panels: inside, before P's digits
                 if (lane == 2 && k >= kPanelBufs)  // its buffer's previous user: all updates of step k - kPanelBufs
                     wait_ge(P.tiles_done + m.col_begin + k - kPanelBufs, nt * (nt + 1) / 2);
                 if (lane == 3 && task.y == 3 && k >= 1) wait_ge(P.tileflag + m.tile_begin + upper_index(J, J, nt), k);
@@ -1536,7 +1556,7 @@ __global__ void __launch_bounds__(kThreads, 1) inverse_kernel(const __grid_const
             __syncthreads();
             TRACE(tr1 = gtime(); trJ = J; trkind = task.y == 3 ? 5 : 0;)
             const bool live = next == 0;
-            if (live && J != k && (oz || !producer)) panel_task(m, k, J, dyn, ring, oz, ozs);  // R_K / P R_K are never read
+            if (live && J != k && (oz || !producer)) panel_task(m, k, J, dyn, ring, oz, ozs, P.pivflag + mi);  // R_K / P R_K are never read
             TRACE(if (task.y == 3 && threadIdx.x == 0) g_trace_sub[blockIdx.x][0] = gtime();)
             __threadfence();
             __syncthreads();
@@ -1694,6 +1714,11 @@ extern "C" __attribute__((visibility("default"))) int kfac_debug_inverse_trace(v
 }
 #endif
 
+#ifdef PIVOT_DBG
+extern "C" __attribute__((visibility("default"))) int kfac_debug_pclk(void *host) {
+    return (int)cudaMemcpyFromSymbol(host, g_pacc, sizeof(g_pacc));
+}
+#endif
 int64_t inverse_ld(int n) { return (n + 15) / 16 * 16; }
 static int64_t pair_doubles(int npairs) { return ((8 * (int64_t)npairs + 15) / 16) * 16; }
 static int64_t state_ints(int npairs, int64_t sum_nt, int64_t sum_tiles) {
