@@ -247,7 +247,9 @@ __device__ __forceinline__ int block_sweep32(const double (*S)[B + 1], int s0, d
         const int l = 4 * w + r;  // upper storage
         x[r] = S[s0 + min(l, lane)][s0 + max(l, lane)];
     }
-#pragma unroll
+    // unrolled by 4 only: the pivot runs once per step per matrix, and a fully unrolled body (32 copies)
+    // misses the instruction cache on every call; t & 3 stays a compile-time index
+#pragma unroll 4
     for (int t = 0; t < S2_; t++) {
         double *rb = rowbuf + (t & 1) * 32;
         if (w == (t >> 2)) rb[lane] = x[t & 3];
