@@ -285,8 +285,14 @@ __device__ unsigned long long g_pacc[32];
 #endif
 // P = (S)^-1 into Pout (B x B, zero outside bk); -P also goes straight into the upper tile (K, K) of W,
 // the value the sweep gives that tile at step K (no later task has to read the pivot slot for it)
+__device__ __forceinline__ void pivot_write_w(const double (*S)[B + 1], double *__restrict__ W, int64_t ld, int k0, int bk) {
+    for (int e = threadIdx.x; e < B * B; e += kWorkers) {  // W_KK = -P (upper storage)
+        const int i = e >> 7, j = e & (B - 1);
+        if (i < bk && j < bk && j >= i) W[(int64_t)(k0 + i) * ld + k0 + j] = S[i][j];
+    }
+}
 __device__ int pivot_block(double *__restrict__ W, int64_t ld, int k0, int bk, double *__restrict__ Pout,
-                           double *smem, bool preloaded = false) {
+                           double *smem, bool preloaded = false, bool write_w = true) {
 #ifdef PIVOT_DBG
     long long pclk_last = clock64();
 #endif
@@ -409,7 +415,7 @@ __device__ int pivot_block(double *__restrict__ W, int64_t ld, int k0, int bk, d
         const int i = e >> 7, j = e & (B - 1);
         const bool in = i < bk && j < bk;
         if (Pout) Pout[e] = in ? -S[min(i, j)][max(i, j)] : 0.0;  // (int8 matrices: their panels read P's digits)
-        if (in && j >= i) W[(int64_t)(k0 + i) * ld + k0 + j] = S[i][j];
+        if (write_w && in && j >= i) W[(int64_t)(k0 + i) * ld + k0 + j] = S[i][j];
     }
     PCLK(21)
     return 0;
@@ -1027,7 +1033,7 @@ __host__ __device__ constexpr int oz_pass_st(int p, int ns) { return ns == 2 ? p
 // shared memory to a coalesced C read-modify-write (the C tile was prefetched into L2 at the task
 // start).  Same contract as update_task's DMMA path.
 __device__ int oz_update(const InvParams &P, const MatDesc &m, int k, int ns, int I, int J, double *dyn, const int *pflag,
-                         OzState &o, bool &deferred) {
+                         OzState &o, bool &deferred, int *pivf) {
     const int n = m.n, i0 = I * B, j0 = J * B, bi = min(B, n - i0);
     const int64_t ld = m.ld;
     double *W = m.work;
@@ -1210,15 +1216,22 @@ __device__ int oz_update(const InvParams &P, const MatDesc &m, int k, int ns, in
         }
         WSYNC();
         TRACE(if (threadIdx.x == 0) g_trace_sub[blockIdx.x][1] = gtime();)
-        const int f = pivot_block(W, ld, i0, bi, nullptr, dyn, true);  // the panels read P's digits only
+        // the panels read P's digits only (no fp64 pivot slot); W_KK is written after P's release
+        const int f = pivot_block(W, ld, i0, bi, nullptr, dyn, true, false);
         TRACE(WSYNC(); if (threadIdx.x == 0) g_trace_sub[blockIdx.x][3] = gtime();)
         if (!f) {  // P_{last+1}'s digits (S = -P, upper storage) for the next step's panel products
             WSYNC();
             pivot_fill_lower(reinterpret_cast<double(*)[B + 1]>(dyn));
             WSYNC();
             oz_slice<3>(reinterpret_cast<const double(*)[B + 1]>(dyn), oz_pivdig(m, last + 1), oz_pivexp(m, last + 1), o.sexp, bi);
+            // release P_{last+1} now: the next step's panels need only its digits (the task's end
+            // repeats the same release after the tile stamp)
+            __threadfence();
+            WSYNC();
+            if (threadIdx.x == 0) asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(pivf), "r"(last + 2) : "memory");
         }
         TRACE(WSYNC(); if (threadIdx.x == 0) g_trace_sub[blockIdx.x][4] = gtime();)
+        pivot_write_w(reinterpret_cast<const double(*)[B + 1]>(dyn), W, ld, i0, bi);  // fenced by the task's end
         return f;
     }
     deferred = true;
@@ -1302,7 +1315,7 @@ __device__ void panel_task(const MatDesc &m, int k, int J, double *dyn, Ring &ri
 // nsteps = 2: the merged update for steps k and k+1 (I, J not in {k, k+1}).
 __device__ int update_task(const InvParams &P, const MatDesc &m, int k, int nsteps, int I, int J, double *dyn,
                            const int *pflag, uint64_t *cbar, uint32_t &cph, Ring &ring, bool &deferred, bool oz,
-                           OzState &ozs) {
+                           OzState &ozs, int *pivf) {
     const int n = m.n, k0 = k * B, K = k;
     const int64_t ld = m.ld;
     const int bk = min(B, n - k0);
@@ -1312,7 +1325,7 @@ __device__ int update_task(const InvParams &P, const MatDesc &m, int k, int nste
     double *W = m.work;
     if (I == K && J == K) return 0;  // M_KK <- -P_K: written by the pivot itself (pivot_block)
     if (I == K || J == K) return 0;  // M_KJ <- Wp_J / M_IK <- Wp_I^T: written by the panel tasks
-    if (oz) return oz_update(P, m, k, nsteps, I, J, dyn, pflag, ozs, deferred);
+    if (oz) return oz_update(P, m, k, nsteps, I, J, dyn, pflag, ozs, deferred, pivf);
     double acc[8][8];
 #pragma unroll
     for (int p = 0; p < 8; p++)
@@ -1571,7 +1584,7 @@ __global__ void __launch_bounds__(kThreads, 1) inverse_kernel(const __grid_const
                 bool deferred = false;  // stays false: the pivot path writes W itself
                 if (live && (oz || !producer))
                     f = update_task(P, m, k, 1, J, J, dyn, P.panels_done + m.col_begin + (k >= 1 ? k - 1 : 0), &cbar, cph,
-                                    ring, deferred, oz, ozs);
+                                    ring, deferred, oz, ozs, P.pivflag + mi);
                 if (f && threadIdx.x == 0) *m.status = f;
                 __threadfence();
                 __syncthreads();
@@ -1603,7 +1616,7 @@ __global__ void __launch_bounds__(kThreads, 1) inverse_kernel(const __grid_const
             bool deferred = false;
             if (next == 0 && (oz || !producer))
                 f = update_task(P, m, k, ns, I, J, dyn, P.panels_done + m.col_begin + (last >= 1 ? last - 1 : 0), &cbar,
-                                cph, ring, deferred, oz, ozs);
+                                cph, ring, deferred, oz, ozs, P.pivflag + mi);
             if (deferred) {  // tile stores still draining: release at the next task's start
                 pend = true;
                 pend_tile = P.tileflag + m.tile_begin + upper_index(I, J, nt);
