@@ -1695,21 +1695,45 @@ __global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ I
             T[r][tx] = (i < n && j < n) ? m.work[(int64_t)i * ld + j] : 0.0;
         }
         __syncthreads();
-#pragma unroll 4
-        for (int k = 0; k < kFinT / RG; k++) {
-            const int r = ty + RG * k;
-            const int i = bi * kFinT + r, j = bj * kFinT + tx;
-            if (i < n && j < n) {
-                const float v = (float)(-((bi < bj || r <= tx) ? T[r][tx] : T[tx][r]));
-                m.inv[(int64_t)i * n + j] = v;
-                if (m.split) split_store(m.split, n, kp, i, j, v);
-            }
-            if (bi < bj) {
-                const int i2 = bj * kFinT + r, j2 = bi * kFinT + tx;
-                if (i2 < n && j2 < n) {
-                    const float v = (float)(-T[tx][r]);
-                    m.inv[(int64_t)i2 * n + j2] = v;
-                    if (m.split) split_store(m.split, n, kp, i2, j2, v);
+        // writes: 16 threads x 4 consecutive columns per row (16-byte stores of the inverse when n is a
+        // multiple of 4, and of both split planes: kp is), 16 rows per pass
+        const int tq = threadIdx.x & 15, rq = threadIdx.x >> 4;
+#pragma unroll 2
+        for (int k = 0; k < kFinT / 16; k++) {
+            const int r = rq + 16 * k;
+#pragma unroll
+            for (int side = 0; side < 2; side++) {
+                if (side == 1 && bi == bj) break;
+                // side 0: block (bi, bj), element (r, c); side 1: block (bj, bi), element (r, c) = -T[c][r]
+                const int i = (side ? bj : bi) * kFinT + r, j = (side ? bi : bj) * kFinT + 4 * tq;
+                if (i >= n || j >= n) continue;
+                float v[4];
+#pragma unroll
+                for (int c = 0; c < 4; c++) {
+                    const int cc = 4 * tq + c;
+                    v[c] = (float)(-(side ? T[cc][r] : ((bi < bj || r <= cc) ? T[r][cc] : T[cc][r])));
+                }
+                float *dst = m.inv + (int64_t)i * n + j;
+                if ((n & 3) == 0 && j + 3 < n) {
+                    *reinterpret_cast<float4 *>(dst) = make_float4(v[0], v[1], v[2], v[3]);
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 4; c++)
+                        if (j + c < n) dst[c] = v[c];
+                }
+                if (m.split) {
+                    float hi[4], lo[4];
+#pragma unroll
+                    for (int c = 0; c < 4; c++) {
+                        hi[c] = tf32_rn_inv(v[c]);
+                        lo[c] = tf32_rn_inv(v[c] - hi[c]);
+                        if (j + c >= n) hi[c] = lo[c] = 0.f;  // the padding columns (kp > n) stay zero
+                    }
+                    float *sh = m.split + (int64_t)i * kp + j, *sl = sh + (int64_t)n * kp;
+                    if (j + 3 < kp) {  // kp is a multiple of 4 and j of 4: always true
+                        *reinterpret_cast<float4 *>(sh) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+                        *reinterpret_cast<float4 *>(sl) = make_float4(lo[0], lo[1], lo[2], lo[3]);
+                    }
                 }
             }
         }
