@@ -202,13 +202,20 @@ __global__ void unpack_damp_kernel(const __grid_constant__ InvParams P) {
     const double add = P.pair_scratch[8 * m.pair + (m.is_A ? 1 : 2)];
     const int64_t i0 = (int64_t)(blockIdx.x - P.unp_begin[r]) * kUnpRows;
     for (int64_t i = i0; i < min(n, i0 + kUnpRows); i++) {
-        const float *src = m.packed + poff(i, i, n);
+        const float *src = m.packed + poff(i, i, n) - i;  // src[j] = packed (i, j)
         double *dst = m.work + i * m.ld;
+        // 16-byte stores of element pairs (j even; the work rows are 128-byte aligned), an odd first
+        // or last element alone
+        const int64_t j0 = i + (i & 1);
+        if (threadIdx.x == 0) {
+            if (i & 1) dst[i] = (double)src[i] + add;
+            if ((n - j0) & 1) dst[n - 1] = (double)src[n - 1] + (n - 1 == i ? add : 0.0);
+        }
 #pragma unroll 4
-        for (int64_t j = i + threadIdx.x; j < n; j += blockDim.x) {
-            double v = (double)src[j - i];
-            if (j == i) v += add;
-            dst[j] = v;
+        for (int64_t j = j0 + 2 * threadIdx.x; j + 1 < n; j += 2 * blockDim.x) {
+            double a = (double)src[j];
+            if (j == i) a += add;
+            *reinterpret_cast<double2 *>(dst + j) = make_double2(a, (double)src[j + 1]);
         }
     }
 }
