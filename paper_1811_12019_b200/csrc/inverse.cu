@@ -840,23 +840,20 @@ __device__ __forceinline__ void oz_drain(uint32_t tacc, double (&acc)[16], const
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t tb = tacc + ((uint32_t)(32 * (w & 3)) << 16) + 16 * (w >> 2);
     const int ea = eA[32 * (w & 3) + lane] - 42 + 1023;
+    // all five diagonals' 16 columns in flight at once, one wait (a wait covers every earlier load)
+    uint32_t a[kOzS][16];
 #pragma unroll
-    for (int h = 0; h < 2; h++) {
-        uint32_t a[kOzS][8];
+    for (int d = 0; d < kOzS; d++) tmem_ld_32x32b_x16(tb + kOzQ * d, a[d]);
+    tmem_ld_wait();
 #pragma unroll
-        for (int d = 0; d < kOzS; d++) tmem_ld_x8(tb + kOzQ * d + 8 * h, a[d]);
-        tmem_ld_wait();
+    for (int d = 0; d < kOzS; d++) tmem_regs_ready(a[d]);
 #pragma unroll
-        for (int d = 0; d < kOzS; d++) tmem_regs_ready(a[d]);
-#pragma unroll
-        for (int c = 0; c < 8; c++) {
-            // Horner in int32 while it fits (|Acc_0 2^8 + Acc_1| < 2^26), then 64-bit
-            const int v01 = (int)a[0][c] * 256 + (int)a[1][c];
-            const long long V = ((long long)v01 * 256 + (int)a[2][c]) * 65536LL + ((long long)(int)a[3][c] * 256 + (int)a[4][c]);
-            const double v = __longlong_as_double(V + 0x4338000000000000LL) - 6755399441055744.0;  // exact, |V| < 2^51
-            const int ex = max(ea + eB[16 * (w >> 2) + 8 * h + c], 0);
-            acc[8 * h + c] = fma(v, __longlong_as_double((long long)ex << 52), acc[8 * h + c]);
-        }
+    for (int c = 0; c < 16; c++) {
+        const int v01 = (int)a[0][c] * 256 + (int)a[1][c];
+        const long long V = ((long long)v01 * 256 + (int)a[2][c]) * 65536LL + ((long long)(int)a[3][c] * 256 + (int)a[4][c]);
+        const double v = __longlong_as_double(V + 0x4338000000000000LL) - 6755399441055744.0;  // exact, |V| < 2^51
+        const int ex = max(ea + eB[16 * (w >> 2) + c], 0);
+        acc[c] = fma(v, __longlong_as_double((long long)ex << 52), acc[c]);
     }
 }
 
