@@ -2,6 +2,7 @@
 // argument validation, marshalling into the grouped kernel launchers, and the
 // NCCL collectives.  Every step of the path runs in this library's kernels or
 // in NCCL; nothing here computes on the host.
+#include <nvtx3/nvToolsExt.h>
 #include <dlfcn.h>
 
 #include <cmath>
@@ -13,6 +14,15 @@
 #include "kfac_plan.hpp"
 
 using namespace kfac;
+
+// NVTX ranges around the stage entry points (SURVEY §5 tracing): header-only NVTX 3, a no-op unless a
+// profiler injects its collector (nsys / ncu --nvtx)
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
+};
 
 struct kfac_comm {
     ncclComm_t comm = nullptr;
@@ -104,6 +114,7 @@ kfac_status kfac_factor_ws_bytes(const kfac_layer_desc *layer, int32_t n, int32_
 
 kfac_status kfac_factor_all(kfac_plan_t p, const void *const *xs, const void *const *gys, kfac_dtype dt,
                             const float *alphaA, const float *alphaG, float *rs_send, void *ws, void *stream) {
+    const NvtxRange nvtx_("kfac.factor_all");
     if (p && p->stale && rs_send) return replicate_dw(p, rs_send, stream);
     if (!p || (!xs && !p->g_only) || !gys || !rs_send) return set_error(KFAC_ERR_ARG, "kfac_factor_all: NULL argument");
     if (dt != KFAC_BF16 && dt != KFAC_FP16) return set_error(KFAC_ERR_ARG, "kfac_factor_all: dtype");
@@ -178,6 +189,7 @@ kfac_status kfac_factor_all(kfac_plan_t p, const void *const *xs, const void *co
 // ------------------------------------------------------------------ stale Fisher (NEXT-1)
 kfac_status kfac_factor_diff(kfac_plan_t p, int32_t rank, const float *recv_cur, const float *recv_prev, double *diff,
                              void *ws, void *stream) {
+    const NvtxRange nvtx_("kfac.factor_diff");
     if (!p || !recv_cur || !recv_prev || !diff || !ws) return set_error(KFAC_ERR_ARG, "kfac_factor_diff: NULL argument");
     if (p->stale || p->g_only) return set_error(KFAC_ERR_STATE, "kfac_factor_diff: needs the full plan's recv chunks");
     if (rank < 0 || rank >= p->world) return set_error(KFAC_ERR_STATE, "kfac_factor_diff: rank out of range");
@@ -279,6 +291,7 @@ kfac_status kfac_reduce_scatter_factors(kfac_comm_t c, kfac_plan_t p, const floa
 
 kfac_status kfac_reduce_scatter_factors_ws(kfac_comm_t c, kfac_plan_t p, const float *send, float *recv, void *ws,
                                            void *stream) {
+    const NvtxRange nvtx_("kfac.reduce_scatter");
     if (!p || !send || !recv) return set_error(KFAC_ERR_ARG, "kfac_reduce_scatter_factors: NULL argument");
     if (p->world > 1 && (!c || c->world != p->world))
         return set_error(KFAC_ERR_STATE, "kfac_reduce_scatter_factors: comm/plan world mismatch");
@@ -313,6 +326,7 @@ kfac_status kfac_reduce_scatter_factors_ws(kfac_comm_t c, kfac_plan_t p, const f
 // ------------------------------------------------------------------ stage 4
 kfac_status kfac_damped_inverse(kfac_plan_t p, int32_t rank, const float *recv, float gamma, float *inv_ws,
                                 int32_t *dev_status, float *pi_out, void *ws, void *stream) {
+    const NvtxRange nvtx_("kfac.damped_inverse");
     if (!p || !recv || !inv_ws || !dev_status || !ws) return set_error(KFAC_ERR_ARG, "kfac_damped_inverse: NULL argument");
     if (p->stale) return set_error(KFAC_ERR_STATE, "kfac_damped_inverse: a stale plan carries no factors (reuse the cached inverses)");
     if (!(gamma > 0.f)) return set_error(KFAC_ERR_ARG, "kfac_damped_inverse: gamma must be > 0");
@@ -375,6 +389,7 @@ kfac_status kfac_inverse_report(kfac_plan_t p, int32_t rank, const void *ws, dou
 // ------------------------------------------------------------------ stage 5
 kfac_status kfac_precondition(kfac_plan_t p, int32_t rank, const float *recv, float *inv_ws, float *ag_buf,
                               void *ws, void *stream) {
+    const NvtxRange nvtx_("kfac.precondition");
     if (!p || !recv || !inv_ws || !ag_buf || !ws) return set_error(KFAC_ERR_ARG, "kfac_precondition: NULL argument");
     if (rank < 0 || rank >= p->world) return set_error(KFAC_ERR_STATE, "kfac_precondition: rank out of range");
     const auto &ow = p->owned[rank];
@@ -411,6 +426,7 @@ kfac_status kfac_precondition(kfac_plan_t p, int32_t rank, const float *recv, fl
 // ------------------------------------------------------------------ NEXT-3: the update after stage 6
 kfac_status kfac_update(kfac_plan_t p, const float *ag_buf, float *const *w, float *const *w_prev, float lr,
                         float momentum, int32_t rescale, float eps, void *ws, void *stream) {
+    const NvtxRange nvtx_("kfac.update");
     if (!p || !ag_buf || !w || !w_prev || !ws) return set_error(KFAC_ERR_ARG, "kfac_update: NULL argument");
     if (!(eps >= 0.f) || !std::isfinite(lr) || !std::isfinite(momentum))
         return set_error(KFAC_ERR_ARG, "kfac_update: lr, momentum finite and eps >= 0");
@@ -433,6 +449,7 @@ kfac_status kfac_update(kfac_plan_t p, const float *ag_buf, float *const *w, flo
 // ------------------------------------------------------------------ NEXT-2: Batch Normalization Fisher
 kfac_status kfac_bn_grads(int32_t nl, const int32_t *c, const int32_t *hw, const void *const *xhat,
                           const void *const *gy, kfac_dtype dt, int32_t n, float *const *Sv, void *stream) {
+    const NvtxRange nvtx_("kfac.bn_grads");
     if (nl < 1 || !c || !hw || !xhat || !gy || !Sv) return set_error(KFAC_ERR_ARG, "kfac_bn_grads: NULL argument / nl < 1");
     if (n < 1) return set_error(KFAC_ERR_ARG, "kfac_bn_grads: n >= 1 (empty capture)");
     if (dt != KFAC_BF16 && dt != KFAC_FP16) return set_error(KFAC_ERR_ARG, "kfac_bn_grads: dtype");
@@ -455,6 +472,7 @@ kfac_status kfac_bn_grads(int32_t nl, const int32_t *c, const int32_t *hw, const
 
 kfac_status kfac_bn_exchange(kfac_comm_t cm, int32_t nl, const int32_t *c, int32_t n_local, const float *const *S_local,
                              float *const *S_all, float *const *grad, void *stream) {
+    const NvtxRange nvtx_("kfac.bn_exchange");
     if (!cm || nl < 1 || !c || !S_local || !S_all || !grad || n_local < 1)
         return set_error(KFAC_ERR_ARG, "kfac_bn_exchange: NULL argument / nl, n_local < 1");
     for (int l = 0; l < nl; l++)
@@ -487,6 +505,7 @@ kfac_status kfac_bn_ws_bytes(int32_t nl, const int32_t *c, int32_t n, int64_t *b
 kfac_status kfac_bn_precondition(int32_t nl, const int32_t *c, int32_t n, const float *const *Sv,
                                  const float *const *grad, float gamma_bn, int32_t full, float *const *out,
                                  void *ws, int64_t ws_bytes, void *stream) {
+    const NvtxRange nvtx_("kfac.bn_precondition");
     if (nl < 1 || !c || !Sv || !grad || !out) return set_error(KFAC_ERR_ARG, "kfac_bn_precondition: NULL argument / nl < 1");
     if (!(gamma_bn > 0.f)) return set_error(KFAC_ERR_ARG, "kfac_bn_precondition: gamma_bn must be > 0");
     if (n < 1) return set_error(KFAC_ERR_ARG, "kfac_bn_precondition: n >= 1");
@@ -508,6 +527,7 @@ kfac_status kfac_bn_precondition(int32_t nl, const int32_t *c, int32_t n, const 
 
 // ------------------------------------------------------------------ stage 6
 kfac_status kfac_allgather_precond(kfac_comm_t c, kfac_plan_t p, float *ag_buf, void *stream) {
+    const NvtxRange nvtx_("kfac.allgather");
     if (!p || !ag_buf) return set_error(KFAC_ERR_ARG, "kfac_allgather_precond: NULL argument");
     if (p->world == 1) return KFAC_OK;
     if (!c || c->world != p->world) return set_error(KFAC_ERR_STATE, "kfac_allgather_precond: comm/plan world mismatch");
