@@ -1059,13 +1059,16 @@ __device__ int oz_update(const InvParams &P, const MatDesc &m, int k, int ns, in
             tma_load_4d(ring + (p % 3) * kOzRBytes, m.tmaps + OZ_MAP_R5, o.bar + OZ_R + p % 3, 0, kOzQ * oz_pass_q(p, ns), 0,
                         oz_set(m, k + oz_pass_st(p, ns), J, 1));
         };
+        // in the order the passes consume them: step st's A digits, then pass st's B quarter (pass 0
+        // starts after 100 KB instead of waiting behind step 1's A as well)
         for (int st = 0; st < ns; st++) {
             cbar_expect(o.bar + OZ_A + st, kOzABytes + 2 * B * 4);
             tma_load_4d(sm + st * kOzABytes, m.tmaps + OZ_MAP_A, o.bar + OZ_A + st, 0, 0, 0, oz_set(m, k + st, I, 0));
             bulk_row(eA + st * B, oz_exps(m, k + st, 0) + i0, B * 4, o.bar + OZ_A + st);
             bulk_row(eB + st * B, oz_exps(m, k + st, 1) + j0, B * 4, o.bar + OZ_A + st);
+            load_ring(st);
         }
-        for (int p = 0; p < 3 && p < Q; p++) load_ring(p);
+        for (int p = ns; p < 3 && p < Q; p++) load_ring(p);
         TRACE(const bool rec = Q == 8 && g_ozcnt[blockIdx.x] == 20;)
         for (int p = 0; p < Q; p++) {
             const int st = oz_pass_st(p, ns);
